@@ -1,0 +1,181 @@
+/*
+ * vlr.h -- C ABI of libvlr.so: batched IVF-PQ search over the GPU-resident
+ * ("hot") inverted lists, B200 (sm_100a) native.
+ *
+ * Method: VectorLiteRAG (arXiv 2504.08930). The calls follow the paper's
+ * problem statement (BASELINE.json north_star):
+ *   load_index(centroids, PQ codebooks, inverted lists, hot-cluster set)
+ *   search(queries, nprobe, k) -> (ids, distances, per-query miss mask)
+ * Citations are PAPER.md line numbers (P:n) and DESIGN.md reading ids (A*).
+ *
+ * Conventions for every call:
+ *  - No C++ exception crosses this ABI. Every call returns a vlr_status;
+ *    vlr_last_error() gives a thread-local message for the last failure on
+ *    the calling thread (valid until the next vlr_* call on that thread).
+ *  - "host" pointers are ordinary CPU memory (pinned or pageable);
+ *    "device" pointers are CUDA global memory on the index's device.
+ *  - Streams are passed as void* (a cudaStream_t); NULL = legacy default.
+ *  - One in-flight search per index handle (the workspace is per handle);
+ *    distinct handles are independent.
+ *  - There is no CPU fallback: every step of search runs in this library's
+ *    sm_100a kernels. Without a usable GPU, load_index fails with VLR_ERR_CUDA.
+ */
+#ifndef VLR_H_
+#define VLR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VLR_VERSION_MAJOR 1
+#define VLR_VERSION_MINOR 0
+
+typedef struct vlr_index vlr_index; /* opaque; created by vlr_load_index, freed by vlr_index_free */
+
+typedef enum {
+  VLR_OK = 0,
+  VLR_ERR_INVALID_ARG = 1,     /* null pointer, nprobe < 1, k < 1, negative id, bad offsets, ... */
+  VLR_ERR_DIM_MISMATCH = 2,    /* d % m != 0, or d/m inconsistent with the codebooks */
+  VLR_ERR_NONFINITE = 3,       /* NaN/Inf in centroids, codebooks (load) or queries (search) */
+  VLR_ERR_UNKNOWN_CLUSTER = 4, /* hot id out of [0, nlist) or listed twice; hot_owner out of range */
+  VLR_ERR_DUPLICATE_ID = 5,    /* a vector id occurs twice among this rank's resident vectors */
+  VLR_ERR_OOM = 6,             /* device allocation failed */
+  VLR_ERR_CUDA = 7,            /* any other CUDA runtime error (no device, launch failure, ...) */
+  VLR_ERR_NCCL = 8,            /* NCCL error; the communicator is aborted, the handle unusable */
+  VLR_ERR_UNSUPPORTED = 9      /* valid but outside v1: nbits != 8, metric != L2, by_residual != 1,
+                                  m > 128, k > 32 */
+} vlr_status;
+
+/*
+ * Index description (all pointers HOST, read during vlr_load_index only;
+ * every array is copied, the caller may free them on return).
+ *
+ * Definitions (§II.A-B; readings A2, A5 in DESIGN.md):
+ *   vector i of list l reconstructs to xhat_i = c_l + concat_j Y[j][code_ij]
+ *   (residual PQ, sub-space j = dims [j*dsub, (j+1)*dsub), dsub = d/m).
+ */
+typedef struct {
+  int32_t d;            /* vector dimension, >= 1 */
+  int32_t nlist;        /* number of inverted lists / coarse centroids, >= 1 */
+  int32_t m;            /* PQ sub-quantizers, d % m == 0, 1 <= m <= 128 */
+  int32_t nbits;        /* bits per sub-code; must be 8 (256 codewords) */
+  int32_t metric;       /* 0 = squared L2 (only value in v1) */
+  int32_t by_residual;  /* 1 = codes encode x - c_l (only value in v1) */
+  const float* centroids;      /* [nlist][d] row-major fp32 */
+  const float* codebooks;      /* [m][256][d/m] fp32 */
+  const int64_t* list_offsets; /* [nlist+1]; list l = rows [offsets[l], offsets[l+1]); offsets[0] = 0,
+                                  non-decreasing; N = offsets[nlist] (empty lists allowed) */
+  const int64_t* ids;          /* [N] vector ids, >= 0, unique (-1 is the padding id) */
+  const uint8_t* codes;        /* [N][m]; byte j of row i = sub-code j of vector i */
+  const int32_t* hot;          /* [n_hot] cluster ids resident on the GPUs; no duplicates.
+                                  May be NULL iff n_hot == 0 (then every probe is a miss). */
+  int32_t n_hot;
+  const int32_t* hot_owner;    /* optional [n_hot]: rank owning hot[i]; NULL = deal hot lists by size
+                                  descending (ties: ascending cluster id) round-robin over ranks
+                                  ("sorted by size and distributed to GPU shards in a
+                                  round-robin fashion") */
+} vlr_index_desc;
+
+/*
+ * Process/device placement. world == 1: a single-GPU index.
+ * world > 1 with nccl_unique_id != NULL: rank `rank` of an NCCL communicator
+ *   (the 128-byte ncclUniqueId, created by rank 0 and broadcast by the caller,
+ *   e.g. through torch.distributed); vlr_load_index and vlr_search* are then
+ *   COLLECTIVE: every rank calls them with identical arguments (SPMD).
+ * world > 1 with nccl_unique_id == NULL: "shard-only" mode: this handle holds
+ *   rank `rank`'s share of the hot lists and search returns this shard's
+ *   PARTIAL top-k; combine shards with vlr_merge_partials (used to test
+ *   sharding on one GPU).
+ */
+typedef struct {
+  int32_t rank;
+  int32_t world;
+  int32_t device;               /* CUDA device ordinal used by this handle */
+  const void* nccl_unique_id;   /* NULL or pointer to a 128-byte ncclUniqueId */
+} vlr_comm_desc;
+
+/* Build the device-resident hot shard of this rank (H2D copies + layout
+ * kernel K0 + tables). Synchronous. comm may be NULL (= {0, 1, current device, NULL}). */
+vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm, vlr_index** out);
+
+/*
+ * Batched search (stream-ordered, no host synchronisation; CUDA-graph
+ * capturable once vlr_reserve has sized the workspace for (nq, nprobe, k)).
+ *
+ *  d_queries [nq][d] device fp32.   nq >= 0 (nq == 0 is a no-op).
+ *  nprobe >= 1; clamped to nprobe' = min(nprobe, nlist).
+ *  1 <= k <= 32.
+ *  Outputs (device, caller-allocated):
+ *   d_ids  [nq][k] int64, d_dist [nq][k] fp32: row q = the k smallest
+ *      candidates by (ADC distance, id), ascending; missing slots (-1, +inf).
+ *      Distances are squared L2 to the PQ reconstruction, computed as
+ *      ||q-c_l||^2 + (||yhat||^2 + 2<c_l,yhat>) - 2<q,yhat> in fp32
+ *      (within 1e-5 relative of the fp64 definition).
+ *      Candidates are the vectors of probed lists that are GPU-resident.
+ *   d_miss [nq][nprobe'] uint8: 1 iff probe p of query q is not resident on
+ *      any GPU; hit rate eta_q = 1 - mean_p d_miss[q][p].
+ *   d_probes [nq][nprobe'] int32 or NULL: the probed cluster ids, ascending by
+ *      (exact fp64 coarse distance, cluster id) (bit-exact w.r.t. the
+ *      definition in DESIGN.md §O2).
+ *  Errors: INVALID_ARG / UNSUPPORTED synchronously; a non-finite query is
+ *  detected on the device and reported by vlr_search, or by the next
+ *  vlr_search_async/vlr_search on this handle.
+ */
+vlr_status vlr_search_async(vlr_index* idx, const float* d_queries, int32_t nq, int32_t nprobe, int32_t k,
+                            int64_t* d_ids, float* d_dist, uint8_t* d_miss, int32_t* d_probes, void* stream);
+
+/* vlr_search_async + stream synchronisation + device status check. */
+vlr_status vlr_search(vlr_index* idx, const float* d_queries, int32_t nq, int32_t nprobe, int32_t k,
+                      int64_t* d_ids, float* d_dist, uint8_t* d_miss, int32_t* d_probes, void* stream);
+
+/* End-to-end search with HOST buffers (same semantics and shapes as
+ * vlr_search): copies h_queries to the device, searches, copies the results
+ * back and synchronises `stream`. Pinned host memory gives full PCIe speed.
+ * h_probes may be NULL. */
+vlr_status vlr_search_host(vlr_index* idx, const float* h_queries, int32_t nq, int32_t nprobe, int32_t k,
+                           int64_t* h_ids, float* h_dist, uint8_t* h_miss, int32_t* h_probes, void* stream);
+
+/* Pre-size the per-handle workspace for batches up to (max_nq, max_nprobe, max_k)
+ * so that later searches allocate nothing (required before graph capture). */
+vlr_status vlr_reserve(vlr_index* idx, int32_t max_nq, int32_t max_nprobe, int32_t max_k);
+
+/*
+ * Merge S shard-partial results (shard-only mode) into the final top-k:
+ * d_part_ids [S][nq][k], d_part_dist [S][nq][k] device -> d_ids/d_dist [nq][k]
+ * (the k smallest by (dist, id) of the union; "merges ... re-ranks them
+ * to obtain the final top-k"). Stream-ordered.
+ */
+vlr_status vlr_merge_partials(const int64_t* d_part_ids, const float* d_part_dist, int32_t n_shards,
+                              int32_t nq, int32_t k, int64_t* d_ids, float* d_dist, void* stream);
+
+/* Device bytes held by the handle, number of resident lists and vectors on this rank. */
+vlr_status vlr_index_info(const vlr_index* idx, int64_t* bytes_on_device, int32_t* n_owned_lists,
+                          int64_t* n_owned_vectors);
+
+/* Owner rank of every cluster (-1 = not resident): out [nlist] int32 host. */
+vlr_status vlr_index_owners(const vlr_index* idx, int32_t* out_owner);
+
+/* Per-stage device timing of subsequent searches (CUDA events on the search
+ * stream). Stage order: 0 coarse filter (K1), 1 select (K2), 2 refine (K3),
+ * 3 route (K4), 4 LUT (K5), 5 scan (K6), 6 rank merge (K7), 7 exchange+merge
+ * (K8). vlr_stage_times waits for the last search and writes min(n, 8) ms values. */
+vlr_status vlr_set_profiling(vlr_index* idx, int32_t enable);
+vlr_status vlr_stage_times(vlr_index* idx, float* ms, int32_t n);
+
+/* Number of kernel launches issued by the last search on this handle. */
+int32_t vlr_last_launch_count(const vlr_index* idx);
+
+/* Create an NCCL unique id (rank 0 of a world > 1 job) into out[128]; the
+ * caller distributes it to the other ranks (e.g. torch.distributed.broadcast). */
+vlr_status vlr_nccl_unique_id(void* out128);
+
+void vlr_index_free(vlr_index* idx);
+const char* vlr_last_error(void);
+int32_t vlr_version(void); /* (major << 16) | minor */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VLR_H_ */

@@ -1,0 +1,244 @@
+"""paper_2504_08930_b200 -- B200-native IVF-PQ hot-partition search.
+
+Thin Python binding (ctypes, argument marshalling only) over libvlr.so, whose
+C ABI is declared in include/vlr.h. Every step of search runs in the
+library's sm_100a kernels; there is no CPU or PyTorch fallback: if libvlr.so
+is missing or the device is unusable, these calls raise.
+
+PyTorch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvlr.so")
+
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "NONFINITE", 4: "UNKNOWN_CLUSTER",
+          5: "DUPLICATE_ID", 6: "OOM", 7: "CUDA", 8: "NCCL", 9: "UNSUPPORTED"}
+
+# every symbol include/vlr.h declares (checked by tests/test_abi.py)
+EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_reserve",
+           "vlr_merge_partials", "vlr_index_info", "vlr_index_owners", "vlr_set_profiling", "vlr_stage_times",
+           "vlr_last_launch_count", "vlr_nccl_unique_id", "vlr_index_free", "vlr_last_error", "vlr_version"]
+
+
+class VlrError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"vlr {self.name}: {msg}")
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int32), ("nlist", ctypes.c_int32), ("m", ctypes.c_int32), ("nbits", ctypes.c_int32),
+                ("metric", ctypes.c_int32), ("by_residual", ctypes.c_int32),
+                ("centroids", ctypes.c_void_p), ("codebooks", ctypes.c_void_p), ("list_offsets", ctypes.c_void_p),
+                ("ids", ctypes.c_void_p), ("codes", ctypes.c_void_p), ("hot", ctypes.c_void_p),
+                ("n_hot", ctypes.c_int32), ("hot_owner", ctypes.c_void_p)]
+
+
+class _Comm(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libvlr.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2504_08930_b200.build` "
+                              "(there is no CPU fallback for the search path)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        sig = {
+            "vlr_load_index": [P, P, P],
+            "vlr_search_async": [P, P, I32, I32, I32, P, P, P, P, P],
+            "vlr_search": [P, P, I32, I32, I32, P, P, P, P, P],
+            "vlr_search_host": [P, P, I32, I32, I32, P, P, P, P, P],
+            "vlr_reserve": [P, I32, I32, I32],
+            "vlr_merge_partials": [P, P, I32, I32, I32, P, P, P],
+            "vlr_index_info": [P, P, P, P],
+            "vlr_index_owners": [P, P],
+            "vlr_set_profiling": [P, I32],
+            "vlr_stage_times": [P, P, I32],
+            "vlr_nccl_unique_id": [P],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        L.vlr_last_launch_count.argtypes = [P]
+        L.vlr_last_launch_count.restype = I32
+        L.vlr_index_free.argtypes = [P]
+        L.vlr_index_free.restype = None
+        L.vlr_last_error.restype = ctypes.c_char_p
+        L.vlr_version.restype = I32
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise VlrError(st, lib().vlr_last_error().decode(errors="replace"))
+
+
+def _host(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None and a.size else None
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().vlr_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+class Index:
+    """A device-resident hot shard (vlr_index*)."""
+
+    def __init__(self, handle, d, nlist, rank, world, device):
+        self._h = handle
+        self.d, self.nlist, self.rank, self.world, self.device = d, nlist, rank, world, device
+
+    @classmethod
+    def load(cls, centroids, codebooks, list_offsets, ids, codes, hot=None, hot_owner=None, *, rank=0, world=1,
+             device=None, nccl_id: bytes | None = None, nbits=8, metric=0, by_residual=1):
+        """vlr_load_index. hot=None means every cluster is resident."""
+        C = _host(centroids, np.float32)
+        Y = _host(codebooks, np.float32)
+        offs = _host(list_offsets, np.int64)
+        idv = _host(ids, np.int64)
+        cd = _host(codes, np.uint8)
+        nlist, d = C.shape
+        m = Y.shape[0] if Y.ndim == 3 else int(cd.shape[1])
+        hotv = np.arange(nlist, dtype=np.int32) if hot is None else _host(hot, np.int32).reshape(-1)
+        own = None if hot_owner is None else _host(hot_owner, np.int32).reshape(-1)
+        if device is None:
+            import torch
+            device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+        desc = _Desc(d, nlist, m, nbits, metric, by_residual, _ptr(C), _ptr(Y), _ptr(offs), _ptr(idv), _ptr(cd),
+                     _ptr(hotv), int(hotv.size), _ptr(own))
+        uid = None
+        if nccl_id is not None:
+            uid = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        comm = _Comm(rank, world, device, ctypes.cast(uid, ctypes.c_void_p) if uid is not None else None)
+        h = ctypes.c_void_p()
+        _check(lib().vlr_load_index(ctypes.byref(desc), ctypes.byref(comm), ctypes.byref(h)))
+        return cls(h, d, nlist, rank, world, device)
+
+    @classmethod
+    def from_arrays(cls, ix, hot=None, **kw):
+        """Load from a datagen.IndexArrays-like object."""
+        return cls.load(ix.centroids, ix.codebooks, ix.list_offsets, ix.ids, ix.codes, hot=hot, **kw)
+
+    # ------------------------------------------------------------------ search
+    def search(self, Q, nprobe: int, k: int, out=None, stream=None, sync=False, probes=True):
+        """Q: torch float32 CUDA tensor [nq, d]. Returns (ids, dist, miss, probes)
+        torch CUDA tensors; stream-ordered on `stream` (default: current)."""
+        import torch
+        assert Q.is_cuda and Q.dtype == torch.float32 and Q.is_contiguous()
+        nq = int(Q.shape[0])
+        npr = min(nprobe, self.nlist)
+        if out is None:
+            dev = Q.device
+            out = (torch.empty(nq, k, dtype=torch.int64, device=dev), torch.empty(nq, k, dtype=torch.float32, device=dev),
+                   torch.empty(nq, npr, dtype=torch.uint8, device=dev),
+                   torch.empty(nq, npr, dtype=torch.int32, device=dev) if probes else None)
+        ids, dist, miss, prb = out
+        fn = lib().vlr_search if sync else lib().vlr_search_async
+        _check(fn(self._h, Q.data_ptr(), nq, nprobe, k, ids.data_ptr(), dist.data_ptr(), miss.data_ptr(),
+                  prb.data_ptr() if prb is not None else None, _stream_handle(stream)))
+        return out
+
+    def search_host(self, Q: np.ndarray, nprobe: int, k: int, out=None, stream=None):
+        """vlr_search_host: host buffers in and out (copies inside the call)."""
+        Q = np.ascontiguousarray(Q, dtype=np.float32)
+        nq = Q.shape[0]
+        npr = min(nprobe, self.nlist)
+        if out is None:
+            out = (np.empty((nq, k), np.int64), np.empty((nq, k), np.float32), np.empty((nq, npr), np.uint8),
+                   np.empty((nq, npr), np.int32))
+        ids, dist, miss, prb = out
+        _check(lib().vlr_search_host(self._h, Q.ctypes.data, nq, nprobe, k, ids.ctypes.data, dist.ctypes.data,
+                                     miss.ctypes.data, prb.ctypes.data if prb is not None else None,
+                                     _stream_handle(stream)))
+        return out
+
+    def search_host_ptr(self, q_ptr: int, nq: int, nprobe: int, k: int, ids_ptr: int, dist_ptr: int, miss_ptr: int,
+                        probes_ptr: int | None, stream=None):
+        """vlr_search_host on raw (e.g. pinned torch) host pointers."""
+        _check(lib().vlr_search_host(self._h, q_ptr, nq, nprobe, k, ids_ptr, dist_ptr, miss_ptr, probes_ptr,
+                                     _stream_handle(stream)))
+
+    def reserve(self, max_nq: int, max_nprobe: int, max_k: int):
+        _check(lib().vlr_reserve(self._h, max_nq, max_nprobe, max_k))
+
+    # ------------------------------------------------------------------ info
+    def info(self):
+        b, n, v = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int64()
+        _check(lib().vlr_index_info(self._h, ctypes.byref(b), ctypes.byref(n), ctypes.byref(v)))
+        return dict(bytes_on_device=b.value, n_owned_lists=n.value, n_owned_vectors=v.value)
+
+    def owners(self) -> np.ndarray:
+        out = np.empty(self.nlist, np.int32)
+        _check(lib().vlr_index_owners(self._h, out.ctypes.data))
+        return out
+
+    def set_profiling(self, enable=True):
+        _check(lib().vlr_set_profiling(self._h, 1 if enable else 0))
+
+    STAGES = ["coarse_filter", "select", "refine", "route", "lut", "scan", "rank_merge", "exchange_merge"]
+
+    def stage_times(self) -> dict:
+        ms = np.zeros(8, np.float32)
+        _check(lib().vlr_stage_times(self._h, ms.ctypes.data, 8))
+        return dict(zip(self.STAGES, ms.tolist()))
+
+    @property
+    def last_launch_count(self) -> int:
+        return int(lib().vlr_last_launch_count(self._h))
+
+    def close(self):
+        if self._h:
+            lib().vlr_index_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def merge_partials(part_ids, part_dist, stream=None):
+    """vlr_merge_partials: [S, nq, k] device partials -> final (ids, dist)."""
+    import torch
+    S, nq, k = part_ids.shape
+    ids = torch.empty(nq, k, dtype=torch.int64, device=part_ids.device)
+    dist = torch.empty(nq, k, dtype=torch.float32, device=part_ids.device)
+    _check(lib().vlr_merge_partials(part_ids.data_ptr(), part_dist.data_ptr(), S, nq, k, ids.data_ptr(),
+                                    dist.data_ptr(), _stream_handle(stream)))
+    return ids, dist
+
+
+def version() -> tuple:
+    v = int(lib().vlr_version())
+    return v >> 16, v & 0xFFFF

@@ -1,0 +1,519 @@
+// capi.cu -- the C ABI of libvlr.so (include/vlr.h): index residency, the
+// search pipeline (stream-ordered launches of K1..K8), NCCL exchange.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <cub/device/device_radix_sort.cuh>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "vlr_device.cuh"
+#include "vlr_internal.cuh"
+
+namespace vlr {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+static vlr_status fail(vlr_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+// relative bound on the filter's dot-product error (DESIGN.md §K1-K3 band):
+// fp32 FMA chain over d terms, one rounding per step.
+static float filter_edot(int d) { return 1.01f * (float)d * 5.9604645e-8f; }
+
+template <class T>
+static cudaError_t dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+}
+
+__global__ void k_adjacent_dup(const int64_t* sorted, long long n, int32_t* flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x + 1; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (sorted[i] == sorted[i - 1]) atomicOr(flag, 1);
+}
+__global__ void k_negative(const int64_t* ids, long long n, int32_t* flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    if (ids[i] < 0) atomicOr(flag, 2);
+}
+
+static void free_ws(Workspace& w) {
+  void* ps[] = {w.qnorm, w.dt, w.cand, w.ncand, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.lut,
+                w.pdist, w.pid, w.send, w.recv, w.d_q, w.d_ids, w.d_dist, w.d_miss, w.d_probes, w.status};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  if (w.h_status) cudaFreeHost(w.h_status);
+  w = Workspace{};
+}
+
+static void free_index(DeviceIndex& ix) {
+  void* ps[] = {ix.centroids, ix.cnorm2, ix.codebooks, ix.owner, ix.local, ix.gbase, ix.codes, ix.bias, ix.ids};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  if (ix.nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(ix.nccl));
+  ix = DeviceIndex{};
+}
+
+static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
+  Workspace& w = h->ws;
+  const DeviceIndex& ix = h->ix;
+  if (w.status && nq <= w.cap_nq && np <= w.cap_np && k <= w.cap_k) return VLR_OK;
+  const int cnq = std::max(nq, w.cap_nq), cnp = std::max(np, w.cap_np), ck = std::max(k, w.cap_k);
+  int32_t status_keep = 0;
+  if (w.h_status) status_keep = *w.h_status;
+  VLR_CUDA_TRY(cudaDeviceSynchronize());
+  free_ws(w);
+  w.cap_nq = cnq;
+  w.cap_np = cnp;
+  w.cap_k = ck;
+  w.n_cta = scan_ctas(ix);
+  const size_t nqs = (size_t)cnq;
+  VLR_CUDA_TRY(dalloc(&w.qnorm, nqs));
+  VLR_CUDA_TRY(dalloc(&w.dt, nqs * ix.nlist));
+  VLR_CUDA_TRY(dalloc(&w.cand, nqs * kCandCap));
+  VLR_CUDA_TRY(dalloc(&w.ncand, nqs));
+  VLR_CUDA_TRY(dalloc(&w.bound, nqs));
+  VLR_CUDA_TRY(dalloc(&w.probes, nqs * cnp));
+  VLR_CUDA_TRY(dalloc(&w.term1, nqs * cnp));
+  VLR_CUDA_TRY(dalloc(&w.plocal, nqs * cnp));
+  VLR_CUDA_TRY(dalloc(&w.item_off, nqs * cnp + 1));
+  VLR_CUDA_TRY(dalloc(&w.lut, nqs * ix.npairs * (kLutPairBytes / 4)));
+  const size_t nslots = ((size_t)w.n_cta + nqs) * kScanWarps * ck;
+  VLR_CUDA_TRY(dalloc(&w.pdist, nslots));
+  VLR_CUDA_TRY(dalloc(&w.pid, nslots));
+  if (ix.world > 1 && !ix.shard_only) {
+    VLR_CUDA_TRY(dalloc(reinterpret_cast<Packed**>(&w.send), nqs * ck));
+    VLR_CUDA_TRY(dalloc(reinterpret_cast<Packed**>(&w.recv), nqs * ck * ix.world));
+  }
+  VLR_CUDA_TRY(dalloc(&w.d_q, nqs * ix.d));
+  VLR_CUDA_TRY(dalloc(&w.d_ids, nqs * ck));
+  VLR_CUDA_TRY(dalloc(&w.d_dist, nqs * ck));
+  VLR_CUDA_TRY(dalloc(&w.d_miss, nqs * cnp));
+  VLR_CUDA_TRY(dalloc(&w.d_probes, nqs * cnp));
+  VLR_CUDA_TRY(dalloc(&w.status, 1));
+  VLR_CUDA_TRY(cudaMemset(w.status, 0, sizeof(int32_t)));
+  VLR_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&w.h_status), sizeof(int32_t)));
+  *w.h_status = status_keep;
+  return VLR_OK;
+}
+
+}  // namespace vlr
+
+using namespace vlr;
+
+extern "C" {
+
+const char* vlr_last_error(void) { return g_err.c_str(); }
+int32_t vlr_version(void) { return (VLR_VERSION_MAJOR << 16) | VLR_VERSION_MINOR; }
+
+vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm, vlr_index** out) {
+  if (!desc || !out) return fail(VLR_ERR_INVALID_ARG, "vlr_load_index: null desc/out");
+  *out = nullptr;
+  const vlr_index_desc& D = *desc;
+  vlr_comm_desc cm{0, 1, -1, nullptr};
+  if (comm) cm = *comm;
+  if (cm.world < 1 || cm.rank < 0 || cm.rank >= cm.world) return fail(VLR_ERR_INVALID_ARG, "bad rank/world");
+  if (D.d < 1 || D.nlist < 1 || D.m < 1) return fail(VLR_ERR_INVALID_ARG, "d, nlist, m must be >= 1");
+  if (D.d % D.m != 0) return fail(VLR_ERR_DIM_MISMATCH, "d % m != 0");
+  if (D.nbits != 8) return fail(VLR_ERR_UNSUPPORTED, "nbits must be 8");
+  if (D.metric != 0) return fail(VLR_ERR_UNSUPPORTED, "metric must be 0 (squared L2)");
+  if (D.by_residual != 1) return fail(VLR_ERR_UNSUPPORTED, "by_residual must be 1");
+  if (D.m > kMaxM) return fail(VLR_ERR_UNSUPPORTED, "m > 128");
+  if (!D.centroids || !D.codebooks || !D.list_offsets) return fail(VLR_ERR_INVALID_ARG, "null array");
+  if (D.n_hot < 0 || (D.n_hot > 0 && !D.hot)) return fail(VLR_ERR_INVALID_ARG, "bad hot set");
+  const int L = D.nlist, d = D.d, m = D.m, dsub = d / m;
+  if (D.list_offsets[0] != 0) return fail(VLR_ERR_INVALID_ARG, "list_offsets[0] != 0");
+  for (int l = 0; l < L; ++l)
+    if (D.list_offsets[l + 1] < D.list_offsets[l]) return fail(VLR_ERR_INVALID_ARG, "list_offsets decreasing");
+  const int64_t N = D.list_offsets[L];
+  if (N > 0 && (!D.ids || !D.codes)) return fail(VLR_ERR_INVALID_ARG, "null ids/codes");
+  // finiteness + centroid norms (fp64)
+  std::vector<float> cn2((size_t)L);
+  double cmax2 = 0.0;
+  for (int l = 0; l < L; ++l) {
+    double s = 0.0;
+    const float* c = D.centroids + (size_t)l * d;
+    for (int t = 0; t < d; ++t) {
+      if (!std::isfinite(c[t])) return fail(VLR_ERR_NONFINITE, "non-finite centroid");
+      s += (double)c[t] * c[t];
+    }
+    cn2[l] = (float)s;
+    cmax2 = std::max(cmax2, s);
+  }
+  const size_t ncb = (size_t)m * 256 * dsub;
+  for (size_t i = 0; i < ncb; ++i)
+    if (!std::isfinite(D.codebooks[i])) return fail(VLR_ERR_NONFINITE, "non-finite codebook");
+  // hot set and owners (index splitter)
+  std::vector<int32_t> owner((size_t)L, -1);
+  {
+    std::vector<int32_t> hot(D.hot, D.hot + D.n_hot);
+    for (int i = 0; i < D.n_hot; ++i) {
+      const int32_t l = hot[i];
+      if (l < 0 || l >= L) return fail(VLR_ERR_UNKNOWN_CLUSTER, "hot cluster id out of range");
+      if (owner[l] != -1) return fail(VLR_ERR_UNKNOWN_CLUSTER, "hot cluster listed twice");
+      owner[l] = -2;
+    }
+    if (D.hot_owner) {
+      for (int i = 0; i < D.n_hot; ++i) {
+        if (D.hot_owner[i] < 0 || D.hot_owner[i] >= cm.world) return fail(VLR_ERR_UNKNOWN_CLUSTER, "hot_owner out of range");
+        owner[hot[i]] = D.hot_owner[i];
+      }
+    } else {
+      // size descending, ties by ascending cluster id, round-robin over ranks
+      std::vector<int32_t> ord(hot);
+      std::sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
+        const int64_t sa = D.list_offsets[a + 1] - D.list_offsets[a], sb = D.list_offsets[b + 1] - D.list_offsets[b];
+        return sa != sb ? sa > sb : a < b;
+      });
+      for (size_t i = 0; i < ord.size(); ++i) owner[ord[i]] = (int32_t)(i % cm.world);
+    }
+  }
+  // device
+  int dev = cm.device;
+  if (dev < 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(VLR_ERR_CUDA, "no CUDA device");
+  }
+  VLR_CUDA_TRY(cudaSetDevice(dev));
+  vlr_index* h = new vlr_index();
+  DeviceIndex& ix = h->ix;
+  ix.d = d;
+  ix.nlist = L;
+  ix.m = m;
+  ix.dsub = dsub;
+  ix.mpad = ((m + 31) / 32) * 32;
+  ix.npairs = (ix.mpad + 63) / 64;
+  ix.rank = cm.rank;
+  ix.world = cm.world;
+  ix.device = dev;
+  ix.shard_only = cm.world > 1 && cm.nccl_unique_id == nullptr;
+  ix.cmax = (float)std::sqrt(cmax2) * 1.0000002f;
+  ix.owner_h = owner;
+  auto bail = [&](vlr_status st) {
+    free_index(ix);
+    delete h;
+    return st;
+  };
+#define LTRY(expr)                                                                   \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));                 \
+      return bail(_e == cudaErrorMemoryAllocation ? VLR_ERR_OOM : VLR_ERR_CUDA);     \
+    }                                                                                \
+  } while (0)
+  cudaStream_t s;
+  LTRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  // replicated tables
+  std::vector<int32_t> local((size_t)L, -1), lglob;
+  std::vector<int64_t> vbase_h(1, 0), gbase_h(1, 0);
+  for (int l = 0; l < L; ++l) {
+    if (owner[l] == cm.rank) {
+      local[l] = (int32_t)lglob.size();
+      lglob.push_back(l);
+      const int64_t n = D.list_offsets[l + 1] - D.list_offsets[l];
+      vbase_h.push_back(vbase_h.back() + n);
+      gbase_h.push_back(gbase_h.back() + (n + 31) / 32);
+    }
+  }
+  ix.n_local = (int32_t)lglob.size();
+  ix.n_vec = vbase_h.back();
+  ix.n_groups = gbase_h.back();
+  LTRY(dalloc(&ix.centroids, (size_t)L * d));
+  LTRY(dalloc(&ix.cnorm2, (size_t)L));
+  LTRY(dalloc(&ix.codebooks, ncb));
+  LTRY(dalloc(&ix.owner, (size_t)L));
+  LTRY(dalloc(&ix.local, (size_t)L));
+  LTRY(dalloc(&ix.gbase, (size_t)ix.n_local + 1));
+  LTRY(dalloc(&ix.codes, (size_t)ix.n_groups * 32 * ix.mpad));
+  LTRY(dalloc(&ix.bias, (size_t)ix.n_groups * 32));
+  LTRY(dalloc(&ix.ids, (size_t)ix.n_groups * 32));
+  LTRY(cudaMemcpyAsync(ix.centroids, D.centroids, sizeof(float) * L * d, cudaMemcpyHostToDevice, s));
+  LTRY(cudaMemcpyAsync(ix.cnorm2, cn2.data(), sizeof(float) * L, cudaMemcpyHostToDevice, s));
+  LTRY(cudaMemcpyAsync(ix.codebooks, D.codebooks, sizeof(float) * ncb, cudaMemcpyHostToDevice, s));
+  LTRY(cudaMemcpyAsync(ix.owner, owner.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, s));
+  LTRY(cudaMemcpyAsync(ix.local, local.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, s));
+  LTRY(cudaMemcpyAsync(ix.gbase, gbase_h.data(), sizeof(int64_t) * gbase_h.size(), cudaMemcpyHostToDevice, s));
+  // staging: owned lists' codes and ids, local order (= ascending cluster id)
+  uint8_t* scodes = nullptr;
+  int64_t *sids = nullptr, *svbase = nullptr, *ssorted = nullptr;
+  int32_t *slglob = nullptr, *sflag = nullptr;
+  void* cubtmp = nullptr;
+  auto free_stage = [&]() {
+    void* ps[] = {scodes, sids, svbase, ssorted, slglob, sflag, cubtmp};
+    for (void* p : ps)
+      if (p) cudaFree(p);
+  };
+  int32_t flag_h = 0;
+  if (ix.n_vec > 0) {
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = dalloc(&scodes, (size_t)ix.n_vec * m);
+    if (e == cudaSuccess) e = dalloc(&sids, (size_t)ix.n_vec);
+    if (e == cudaSuccess) e = dalloc(&svbase, vbase_h.size());
+    if (e == cudaSuccess) e = dalloc(&slglob, lglob.size());
+    if (e == cudaSuccess) e = dalloc(&sflag, 1);
+    // copy runs of consecutive owned lists
+    int l = 0;
+    while (e == cudaSuccess && l < L) {
+      if (owner[l] != cm.rank) { ++l; continue; }
+      int r = l;
+      while (r + 1 < L && owner[r + 1] == cm.rank) ++r;
+      const int64_t a = D.list_offsets[l], b = D.list_offsets[r + 1];
+      const int64_t dst = vbase_h[local[l]];
+      if (b > a) {
+        e = cudaMemcpyAsync(scodes + dst * m, D.codes + a * m, (size_t)(b - a) * m, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(sids + dst, D.ids + a, (size_t)(b - a) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+      }
+      l = r + 1;
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(svbase, vbase_h.data(), sizeof(int64_t) * vbase_h.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(slglob, lglob.data(), sizeof(int32_t) * lglob.size(), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(sflag, 0, sizeof(int32_t), s);
+    // ids: >= 0 and unique among this rank's vectors (device radix sort)
+    if (e == cudaSuccess) {
+      k_negative<<<1024, 256, 0, s>>>(sids, ix.n_vec, sflag);
+      e = cudaGetLastError();
+    }
+    size_t tmpb = 0;
+    if (e == cudaSuccess) e = dalloc(&ssorted, (size_t)ix.n_vec);
+    if (e == cudaSuccess)
+      e = cub::DeviceRadixSort::SortKeys(nullptr, tmpb, (const int64_t*)sids, ssorted, (int64_t)ix.n_vec, 0, 64, s);
+    if (e == cudaSuccess) e = cudaMalloc(&cubtmp, tmpb ? tmpb : 1);
+    if (e == cudaSuccess)
+      e = cub::DeviceRadixSort::SortKeys(cubtmp, tmpb, (const int64_t*)sids, ssorted, (int64_t)ix.n_vec, 0, 64, s);
+    if (e == cudaSuccess) {
+      k_adjacent_dup<<<1024, 256, 0, s>>>(ssorted, ix.n_vec, sflag);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = launch_layout(ix, scodes, sids, svbase, slglob, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&flag_h, sflag, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    free_stage();
+    if (e != cudaSuccess) {
+      set_error(std::string("load_index staging/layout: ") + cudaGetErrorString(e));
+      cudaStreamDestroy(s);
+      return bail(e == cudaErrorMemoryAllocation ? VLR_ERR_OOM : VLR_ERR_CUDA);
+    }
+  }
+  LTRY(cudaStreamSynchronize(s));
+  cudaStreamDestroy(s);
+  if (flag_h & 2) {
+    set_error("negative vector id");
+    return bail(VLR_ERR_INVALID_ARG);
+  }
+  if (flag_h & 1) {
+    set_error("duplicate vector id among resident vectors");
+    return bail(VLR_ERR_DUPLICATE_ID);
+  }
+  ix.bytes = (int64_t)L * d * 4 + L * 4 + (int64_t)ncb * 4 + 2LL * L * 4 + (ix.n_local + 1) * 8 +
+             ix.n_groups * 32 * (ix.mpad + 4 + 8);
+  // NCCL communicator (collective)
+  if (cm.world > 1 && cm.nccl_unique_id) {
+    ncclUniqueId uid;
+    std::memcpy(&uid, cm.nccl_unique_id, sizeof(uid));
+    ncclComm_t comm_h;
+    ncclResult_t r = ncclCommInitRank(&comm_h, cm.world, uid, cm.rank);
+    if (r != ncclSuccess) {
+      set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      return bail(VLR_ERR_NCCL);
+    }
+    ix.nccl = comm_h;
+  }
+  for (auto& e : h->ev) cudaEventCreate(&e);
+  *out = h;
+  return VLR_OK;
+#undef LTRY
+}
+
+void vlr_index_free(vlr_index* h) {
+  if (!h) return;
+  cudaSetDevice(h->ix.device);
+  cudaDeviceSynchronize();
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  free_ws(h->ws);
+  free_index(h->ix);
+  delete h;
+}
+
+vlr_status vlr_reserve(vlr_index* h, int32_t max_nq, int32_t max_nprobe, int32_t max_k) {
+  if (!h || max_nq < 0 || max_nprobe < 1 || max_k < 1) return fail(VLR_ERR_INVALID_ARG, "vlr_reserve: bad args");
+  if (max_k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32");
+  cudaSetDevice(h->ix.device);
+  const int np = std::min(max_nprobe, h->ix.nlist);
+  if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 1024");
+  return ensure_ws(h, std::max(max_nq, 1), np, max_k);
+}
+
+static inline void rec(vlr_index* h, int i, cudaStream_t s) {
+  if (h->profiling) cudaEventRecord(h->ev[i], s);
+}
+
+vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
+                            float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  if (h->dead) return fail(VLR_ERR_NCCL, "index unusable after an NCCL failure");
+  if (nq < 0 || nprobe < 1 || k < 1) return fail(VLR_ERR_INVALID_ARG, "nq < 0, nprobe < 1 or k < 1");
+  if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32 (v1)");
+  DeviceIndex& ix = h->ix;
+  const int np = std::min(nprobe, ix.nlist);
+  if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 1024 (v1)");
+  h->launches = 0;
+  if (nq == 0) return VLR_OK;
+  if (!Q || !out_ids || !out_dist || !out_miss) return fail(VLR_ERR_INVALID_ARG, "null buffer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  VLR_CUDA_TRY(cudaSetDevice(ix.device));
+  vlr_status st = ensure_ws(h, nq, np, k);
+  if (st != VLR_OK) return st;
+  Workspace& w = h->ws;
+  if (*w.h_status & 1) {  // reported by a previous async search
+    *w.h_status = 0;
+    return fail(VLR_ERR_NONFINITE, "non-finite query (detected in a previous search on this handle)");
+  }
+  VLR_CUDA_TRY(cudaMemsetAsync(w.status, 0, sizeof(int32_t), s));
+  int n = 0;
+  rec(h, 0, s);
+  VLR_CUDA_TRY(launch_qprep(Q, nq, ix.d, w.qnorm, w.status, s)); ++n;
+  VLR_CUDA_TRY(launch_filter_simt(Q, nq, ix, w.dt, s)); ++n;
+  rec(h, 1, s);
+  VLR_CUDA_TRY(launch_select(ix, w, nq, np, filter_edot(ix.d), s)); ++n;
+  rec(h, 2, s);
+  VLR_CUDA_TRY(launch_refine(Q, ix, w, nq, np, s)); ++n;
+  rec(h, 3, s);
+  VLR_CUDA_TRY(launch_route(ix, w, nq, np, out_miss, out_probes, s)); ++n;
+  rec(h, 4, s);
+  VLR_CUDA_TRY(launch_lut(Q, ix, w, nq, s)); ++n;
+  rec(h, 5, s);
+  VLR_CUDA_TRY(launch_scan(ix, w, nq, np, k, s)); ++n;
+  rec(h, 6, s);
+  const bool exchange = ix.world > 1 && !ix.shard_only;
+  VLR_CUDA_TRY(launch_rank_merge(ix, w, nq, np, k, out_ids, out_dist, exchange ? w.send : nullptr, s)); ++n;
+  rec(h, 7, s);
+  if (exchange) {
+    ncclResult_t r = ncclAllGather(w.send, w.recv, (size_t)nq * k * sizeof(Packed), ncclUint8,
+                                   reinterpret_cast<ncclComm_t>(ix.nccl), s);
+    if (r != ncclSuccess) {
+      ncclCommAbort(reinterpret_cast<ncclComm_t>(ix.nccl));
+      ix.nccl = nullptr;
+      h->dead = true;
+      return fail(VLR_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    }
+    VLR_CUDA_TRY(launch_merge_packed(w.recv, ix.world, nq, k, out_ids, out_dist, s)); ++n;
+  }
+  rec(h, 8, s);
+  VLR_CUDA_TRY(cudaMemcpyAsync(w.h_status, w.status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  h->launches = n;
+  return VLR_OK;
+}
+
+vlr_status vlr_search(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
+                      float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream) {
+  vlr_status st = vlr_search_async(h, Q, nq, nprobe, k, out_ids, out_dist, out_miss, out_probes, stream);
+  if (st != VLR_OK || nq == 0) return st;
+  VLR_CUDA_TRY(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
+  if (*h->ws.h_status & 1) {
+    *h->ws.h_status = 0;
+    return fail(VLR_ERR_NONFINITE, "non-finite query");
+  }
+  return VLR_OK;
+}
+
+vlr_status vlr_search_host(vlr_index* h, const float* hQ, int32_t nq, int32_t nprobe, int32_t k, int64_t* h_ids,
+                           float* h_dist, uint8_t* h_miss, int32_t* h_probes, void* stream) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  if (nq < 0 || nprobe < 1 || k < 1) return fail(VLR_ERR_INVALID_ARG, "nq < 0, nprobe < 1 or k < 1");
+  if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32 (v1)");
+  if (nq == 0) return VLR_OK;
+  if (!hQ || !h_ids || !h_dist || !h_miss) return fail(VLR_ERR_INVALID_ARG, "null buffer");
+  const int np = std::min(nprobe, h->ix.nlist);
+  if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 1024 (v1)");
+  VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
+  vlr_status st = ensure_ws(h, nq, np, k);
+  if (st != VLR_OK) return st;
+  Workspace& w = h->ws;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  VLR_CUDA_TRY(cudaMemcpyAsync(w.d_q, hQ, sizeof(float) * nq * h->ix.d, cudaMemcpyHostToDevice, s));
+  st = vlr_search_async(h, w.d_q, nq, nprobe, k, w.d_ids, w.d_dist, w.d_miss, h_probes ? w.d_probes : nullptr, stream);
+  if (st != VLR_OK) return st;
+  VLR_CUDA_TRY(cudaMemcpyAsync(h_ids, w.d_ids, sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, s));
+  VLR_CUDA_TRY(cudaMemcpyAsync(h_dist, w.d_dist, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, s));
+  VLR_CUDA_TRY(cudaMemcpyAsync(h_miss, w.d_miss, (size_t)nq * np, cudaMemcpyDeviceToHost, s));
+  if (h_probes)
+    VLR_CUDA_TRY(cudaMemcpyAsync(h_probes, w.d_probes, sizeof(int32_t) * nq * np, cudaMemcpyDeviceToHost, s));
+  VLR_CUDA_TRY(cudaStreamSynchronize(s));
+  if (*w.h_status & 1) {
+    *w.h_status = 0;
+    return fail(VLR_ERR_NONFINITE, "non-finite query");
+  }
+  return VLR_OK;
+}
+
+vlr_status vlr_merge_partials(const int64_t* part_ids, const float* part_dist, int32_t n_shards, int32_t nq, int32_t k,
+                              int64_t* out_ids, float* out_dist, void* stream) {
+  if (n_shards < 1 || nq < 0 || k < 1) return fail(VLR_ERR_INVALID_ARG, "vlr_merge_partials: bad sizes");
+  if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32 (v1)");
+  if (nq == 0) return VLR_OK;
+  if (!part_ids || !part_dist || !out_ids || !out_dist) return fail(VLR_ERR_INVALID_ARG, "null buffer");
+  VLR_CUDA_TRY(launch_merge_split(part_ids, part_dist, n_shards, nq, k, out_ids, out_dist,
+                                  reinterpret_cast<cudaStream_t>(stream)));
+  return VLR_OK;
+}
+
+vlr_status vlr_index_info(const vlr_index* h, int64_t* bytes, int32_t* n_lists, int64_t* n_vec) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  if (bytes) *bytes = h->ix.bytes;
+  if (n_lists) *n_lists = h->ix.n_local;
+  if (n_vec) *n_vec = h->ix.n_vec;
+  return VLR_OK;
+}
+
+vlr_status vlr_index_owners(const vlr_index* h, int32_t* out) {
+  if (!h || !out) return fail(VLR_ERR_INVALID_ARG, "null arg");
+  std::memcpy(out, h->ix.owner_h.data(), sizeof(int32_t) * h->ix.owner_h.size());
+  return VLR_OK;
+}
+
+vlr_status vlr_set_profiling(vlr_index* h, int32_t enable) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  h->profiling = enable != 0;
+  return VLR_OK;
+}
+
+vlr_status vlr_stage_times(vlr_index* h, float* ms, int32_t n) {
+  if (!h || !ms) return fail(VLR_ERR_INVALID_ARG, "null arg");
+  if (!h->profiling) return fail(VLR_ERR_INVALID_ARG, "profiling disabled");
+  VLR_CUDA_TRY(cudaEventSynchronize(h->ev[8]));
+  const int stages = std::min(n, 8);
+  for (int i = 0; i < stages; ++i) {
+    float t = 0.f;
+    VLR_CUDA_TRY(cudaEventElapsedTime(&t, h->ev[i], h->ev[i + 1]));
+    ms[i] = t;
+  }
+  return VLR_OK;
+}
+
+int32_t vlr_last_launch_count(const vlr_index* h) { return h ? h->launches : 0; }
+
+vlr_status vlr_nccl_unique_id(void* out) {
+  if (!out) return fail(VLR_ERR_INVALID_ARG, "null out");
+  ncclUniqueId uid;
+  ncclResult_t r = ncclGetUniqueId(&uid);
+  if (r != ncclSuccess) return fail(VLR_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  static_assert(sizeof(uid) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(out, &uid, sizeof(uid));
+  return VLR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,370 @@
+// k_scan.cu -- K6 ADC list scan with fused warp top-k, K7 per-rank merge,
+// K8 shard merge.
+//
+// K6: for every owned work item (query q, probed resident list l) and every
+// vector i of l:  dist_i = (term1_{q,l} + b_i) + sum_j LUT_q[j][code_ij]
+// (DESIGN.md §Numerics), kept if among the k smallest (dist, id) seen by the
+// warp. The LUT of the current query lives in shared memory ("shared
+// memory stages partial LUTs"), moved there by one TMA bulk copy
+// (cp.async.bulk + mbarrier).
+//
+// Work decomposition: the owned (q, p) items, in query-major
+// order, form a stream of W groups of 32 vectors. Persistent CTA c takes the
+// contiguous range [c*W/G, (c+1)*W/G) -- perfect balance to one group, no
+// blocks for pruned probes. Inside a CTA, the range is cut at
+// query boundaries into segments; warps take the segment's groups round-robin.
+//
+// Inner loop, lane l of a warp handles vector l of a 32-vector group. Its
+// m_pad code bytes are in 32-bit registers, stored ROTATED at load time (K0):
+// register byte s = 32r + t holds the code of sub-space j = 32r + (l ^ t).
+// The LUT is laid out [j/64][code][j%64] fp32, so at step (t, r) the 32 lanes
+// read 32 different sub-spaces j%32 = l^t -> 32 different banks: conflict-free
+// gathers. One PRMT builds the byte address code*256 + (l^t)*4 (the code byte
+// goes to byte 1, the lane offset to byte 0); the slab/half offset is the LDS
+// immediate. Per lookup: PRMT + LDS + FADD (+1/R LOP3 for the lane offset).
+#include <cfloat>
+
+#include "vlr_device.cuh"
+#include "vlr_internal.cuh"
+
+namespace vlr {
+
+struct ScanArgs {
+  int nq, np, k, npairs;
+  const int32_t* plocal;
+  const float* term1;
+  const int64_t* item_off;
+  const int64_t* gbase;
+  const uint8_t* codes;
+  const float* bias;
+  const int64_t* ids;
+  const float* lut;
+  float* pdist;
+  int64_t* pid;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+template <int MP>
+struct Grp {
+  uint32_t w[MP / 4];
+  float b, t1;
+  long long gaddr;
+};
+
+template <int MP>
+__device__ __forceinline__ void grp_load(Grp<MP>& G, const ScanArgs& a, long long gg, long long& it, int lane) {
+  while (a.item_off[it + 1] <= gg) ++it;
+  const int loc = a.plocal[it];
+  G.gaddr = a.gbase[loc] + (gg - a.item_off[it]);
+  G.t1 = a.term1[it];
+  const uint4* src = reinterpret_cast<const uint4*>(a.codes) + G.gaddr * (2 * MP) + lane;
+#pragma unroll
+  for (int c = 0; c < MP / 16; ++c) {
+    const uint4 v = ldg_stream(src + c * 32);
+    G.w[4 * c + 0] = v.x;
+    G.w[4 * c + 1] = v.y;
+    G.w[4 * c + 2] = v.z;
+    G.w[4 * c + 3] = v.w;
+  }
+  G.b = __ldg(a.bias + G.gaddr * 32 + lane);
+}
+
+// sum_j LUT[j][code_j] for this lane's vector, fixed order
+template <int MP>
+__device__ __forceinline__ float grp_adc(const Grp<MP>& G, const unsigned char* lutc, uint32_t lane4) {
+  constexpr int R = MP / 32;
+  float acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = 0.f;
+#pragma unroll
+  for (int t = 0; t < 32; ++t) {
+    const uint32_t off = lane4 ^ (uint32_t)(t << 2);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int s = r * 32 + t;
+      const uint32_t addr = __byte_perm(G.w[s >> 2], off, 0x5504u | ((uint32_t)(s & 3) << 4));
+      acc[r] += *reinterpret_cast<const float*>(lutc + addr + ((r >> 1) << 16) + ((r & 1) << 7));
+    }
+  }
+  if constexpr (R == 1) return acc[0];
+  else if constexpr (R == 2) return acc[0] + acc[1];
+  else if constexpr (R == 3) return (acc[0] + acc[1]) + acc[2];
+  else return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+template <int MP>
+__device__ __forceinline__ void grp_finish(const Grp<MP>& G, const ScanArgs& a, const unsigned char* lutc,
+                                           uint32_t lane4, int lane, float& bd, long long& bid, float& thr) {
+  const float s = grp_adc<MP>(G, lutc, lane4);
+  const float dist = (G.t1 + G.b) + s;
+  const bool cand = dist <= thr;
+  long long my_id = 0;
+  if (cand) my_id = __ldg(reinterpret_cast<const long long*>(a.ids) + G.gaddr * 32 + lane);
+  if (__any_sync(kFull, cand)) {
+    wtk_offer(bd, bid, dist, cand, a.k, lane, my_id);
+    thr = __shfl_sync(kFull, bd, a.k - 1);
+  }
+}
+
+template <int MP>
+__global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ long long s_it;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int nitems = a.nq * a.np;
+  const long long W = a.item_off[nitems];
+  const long long g0 = (long long)c * W / G, g1 = (long long)(c + 1) * W / G;
+  if (g0 >= g1) return;
+  const uint32_t lut_bytes = (uint32_t)a.npairs * kLutPairBytes;
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    fence_mbar_init();
+    // item containing group g0: last i with item_off[i] <= g0
+    int lo = 0, hi = nitems;  // item_off[lo] <= g0 < item_off[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (a.item_off[mid] <= g0) lo = mid; else hi = mid;
+    }
+    s_it = lo;
+  }
+  __syncthreads();
+  long long it0 = s_it;
+  while (a.item_off[it0 + 1] <= g0) ++it0;
+  const uint32_t lane4 = (uint32_t)lane << 2;
+  const unsigned char* lutc = smem;
+  uint32_t phase = 0;
+  long long g = g0;
+  while (g < g1) {
+    const int q = (int)(it0 / a.np);
+    const long long qend = a.item_off[(long long)(q + 1) * a.np];
+    const long long seg_end = qend < g1 ? qend : g1;
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&mbar, lut_bytes);
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(a.lut) + (size_t)q * lut_bytes;
+      for (uint32_t off = 0; off < lut_bytes; off += 32768u) bulk_g2s(smem + off, src + off, 32768u, &mbar);
+    }
+    mbar_wait(&mbar, phase);
+    phase ^= 1u;
+
+    float bd = CUDART_INF_F, thr = CUDART_INF_F;
+    long long bid = -1;
+    long long it = it0;
+    long long gg = g + warp;
+    Grp<MP> A, B;
+    if (gg < seg_end) grp_load<MP>(A, a, gg, it, lane);
+    while (gg < seg_end) {
+      const long long gn = gg + kScanWarps;
+      if (gn < seg_end) grp_load<MP>(B, a, gn, it, lane);
+      grp_finish<MP>(A, a, lutc, lane4, lane, bd, bid, thr);
+      if (gn >= seg_end) break;
+      const long long gm = gn + kScanWarps;
+      if (gm < seg_end) grp_load<MP>(A, a, gm, it, lane);
+      grp_finish<MP>(B, a, lutc, lane4, lane, bd, bid, thr);
+      gg = gm;
+    }
+    const long long slot = ((long long)(c + q) * kScanWarps + warp) * a.k;
+    if (lane < a.k) {
+      a.pdist[slot + lane] = bd;
+      a.pid[slot + lane] = bid;
+    }
+    __syncthreads();  // every warp is done with this LUT
+    g = seg_end;
+    if (g < g1) {
+      it0 = (long long)(q + 1) * a.np;
+      while (a.item_off[it0 + 1] <= g) ++it0;
+    }
+  }
+}
+
+int scan_ctas(const DeviceIndex& ix) {
+  (void)ix;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;  // one persistent CTA per SM (128 KB LUT + 16 warps)
+}
+
+template <int MP>
+static cudaError_t launch_scan_t(const ScanArgs& a, int n_cta, cudaStream_t s) {
+  const size_t sm = (size_t)a.npairs * kLutPairBytes;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kLutPairBytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_scan<MP><<<n_cta, kScanThreads, sm, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s) {
+  if (nq <= 0) return cudaSuccess;
+  ScanArgs a{nq, np, k, ix.npairs, ws.plocal, ws.term1, ws.item_off, ix.gbase, ix.codes, ix.bias, ix.ids,
+             ws.lut, ws.pdist, ws.pid};
+  switch (ix.mpad) {
+    case 32: return launch_scan_t<32>(a, ws.n_cta, s);
+    case 64: return launch_scan_t<64>(a, ws.n_cta, s);
+    case 96: return launch_scan_t<96>(a, ws.n_cta, s);
+    case 128: return launch_scan_t<128>(a, ws.n_cta, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ---------------------------------------------------------------- K7 per-rank merge
+// One warp per query: union of the partial lists written by the CTAs whose
+// ranges intersect the query's group range, top-k by (dist, id).
+__global__ void k_rank_merge(int nq, int np, int k, int n_cta, const int64_t* __restrict__ item_off,
+                             const float* __restrict__ pdist, const int64_t* __restrict__ pid,
+                             int64_t* __restrict__ out_ids, float* __restrict__ out_dist, Packed* __restrict__ packed) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  const long long W = item_off[(long long)nq * np];
+  const long long S = item_off[(long long)q * np], E = item_off[(long long)(q + 1) * np];
+  float bd = CUDART_INF_F, thr = CUDART_INF_F;
+  long long bid = -1;
+  if (E > S) {
+    auto start = [&](int c) { return (long long)c * W / n_cta; };
+    auto cta_of = [&](long long g) {  // largest c with start(c) <= g
+      int lo = 0, hi = n_cta;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (start(mid) <= g) lo = mid; else hi = mid;
+      }
+      return lo;
+    };
+    const int cf = cta_of(S), cl = cta_of(E - 1);
+    for (int c = cf; c <= cl; ++c) {
+      if (start(c) == start(c + 1)) continue;
+      for (int w = 0; w < kScanWarps; ++w) {
+        const long long slot = ((long long)(c + q) * kScanWarps + w) * k;
+        float d = CUDART_INF_F;
+        long long id = -1;
+        if (lane < k) {
+          d = pdist[slot + lane];
+          id = pid[slot + lane];
+        }
+        wtk_offer(bd, bid, d, d <= thr && id >= 0, k, lane, id);
+        thr = __shfl_sync(kFull, bd, k - 1);
+      }
+    }
+  }
+  if (lane < k) {
+    if (packed) {
+      Packed p;
+      p.d = bd;
+      p.pad = 0;
+      p.id = bid;
+      packed[(size_t)q * k + lane] = p;
+    } else {
+      out_ids[(size_t)q * k + lane] = bid;
+      out_dist[(size_t)q * k + lane] = bd;
+    }
+  }
+}
+
+cudaError_t launch_rank_merge(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, int64_t* out_ids,
+                              float* out_dist, void* out_packed, cudaStream_t s) {
+  (void)ix;
+  if (nq <= 0) return cudaSuccess;
+  const int wpb = 8;
+  k_rank_merge<<<(nq + wpb - 1) / wpb, wpb * 32, 0, s>>>(nq, np, k, ws.n_cta, ws.item_off, ws.pdist, ws.pid, out_ids,
+                                                        out_dist, reinterpret_cast<Packed*>(out_packed));
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K8 shard merge
+// parts [S][nq][k]: top-k of the union per query.
+__global__ void k_merge_parts(int n_shards, int nq, int k, const Packed* __restrict__ packed,
+                              const int64_t* __restrict__ pids, const float* __restrict__ pdist,
+                              int64_t* __restrict__ out_ids, float* __restrict__ out_dist) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  float bd = CUDART_INF_F, thr = CUDART_INF_F;
+  long long bid = -1;
+  for (int sh = 0; sh < n_shards; ++sh) {
+    float d = CUDART_INF_F;
+    long long id = -1;
+    if (lane < k) {
+      const size_t o = ((size_t)sh * nq + q) * k + lane;
+      if (packed) {
+        const Packed p = packed[o];
+        d = p.d;
+        id = p.id;
+      } else {
+        d = pdist[o];
+        id = pids[o];
+      }
+    }
+    wtk_offer(bd, bid, d, d <= thr && id >= 0, k, lane, id);
+    thr = __shfl_sync(kFull, bd, k - 1);
+  }
+  if (lane < k) {
+    out_ids[(size_t)q * k + lane] = bid;
+    out_dist[(size_t)q * k + lane] = bd;
+  }
+}
+
+cudaError_t launch_merge_packed(const void* parts, int n_shards, int nq, int k, int64_t* out_ids, float* out_dist,
+                                cudaStream_t s) {
+  if (nq <= 0) return cudaSuccess;
+  const int wpb = 8;
+  k_merge_parts<<<(nq + wpb - 1) / wpb, wpb * 32, 0, s>>>(n_shards, nq, k, reinterpret_cast<const Packed*>(parts),
+                                                          nullptr, nullptr, out_ids, out_dist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge_split(const int64_t* part_ids, const float* part_dist, int n_shards, int nq, int k,
+                               int64_t* out_ids, float* out_dist, cudaStream_t s) {
+  if (nq <= 0) return cudaSuccess;
+  const int wpb = 8;
+  k_merge_parts<<<(nq + wpb - 1) / wpb, wpb * 32, 0, s>>>(n_shards, nq, k, nullptr, part_ids, part_dist, out_ids,
+                                                          out_dist);
+  return cudaGetLastError();
+}
+
+}  // namespace vlr

@@ -1,0 +1,68 @@
+// vlr_device.cuh -- device helpers shared by libvlr.so kernels (product path).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace vlr {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// total order on (distance, id) pairs: reading A7 (ties by id)
+__device__ __forceinline__ bool lex_less(float d1, long long i1, float d2, long long i2) {
+  return d1 < d2 || (d1 == d2 && i1 < i2);
+}
+
+// Warp-register top-k (k <= 32): lane i < k holds the i-th smallest (bd, bid)
+// of everything inserted so far, ascending by (dist, id). Lanes >= k are idle.
+// Insert one warp-uniform candidate (d, id): the lanes holding larger entries
+// shift up one slot (shfl_up) and the candidate lands in the freed slot.
+__device__ __forceinline__ void wtk_insert(float& bd, long long& bid, float d, long long id, int k, int lane) {
+  const bool gt = lane < k && lex_less(d, id, bd, bid);
+  const unsigned msk = __ballot_sync(kFull, gt);
+  const float ud = __shfl_up_sync(kFull, bd, 1);
+  const long long uid = __shfl_up_sync(kFull, bid, 1);
+  if (msk == 0u) return;
+  const int p = __ffs(msk) - 1;
+  if (lane == p) {
+    bd = d;
+    bid = id;
+  } else if (lane > p && gt) {
+    bd = ud;
+    bid = uid;
+  }
+}
+
+// Offer each lane's (dist, id) to the warp list; lanes with cand=false skip.
+// ids are fetched lazily through `idp` only for lanes that pass the threshold.
+__device__ __forceinline__ void wtk_offer(float& bd, long long& bid, float dist, bool cand, int k, int lane,
+                                          long long my_id) {
+  unsigned cm = __ballot_sync(kFull, cand);
+  while (cm) {
+    const int src = __ffs(cm) - 1;
+    cm &= cm - 1;
+    const float d = __shfl_sync(kFull, dist, src);
+    const long long id = __shfl_sync(kFull, my_id, src);
+    wtk_insert(bd, bid, d, id, k, lane);
+  }
+}
+
+// float <-> order-preserving unsigned key
+__device__ __forceinline__ unsigned fkey(float f) {
+  unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(unsigned k) {
+  unsigned u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
+}
+
+// 16-byte packed result entry used by the cross-GPU exchange
+struct __align__(16) Packed {
+  float d;
+  int32_t pad;
+  long long id;
+};
+
+}  // namespace vlr

@@ -1,0 +1,132 @@
+// vlr_internal.cuh -- shared declarations of libvlr.so (product path).
+// No code here is shared with oracle/ (test infrastructure).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "vlr.h"
+
+namespace vlr {
+
+// ---------------------------------------------------------------- constants
+constexpr int kWarp = 32;
+constexpr int kMaxK = 32;          // warp-register top-k (one entry per lane)
+constexpr int kMaxM = 128;         // padded sub-quantizer count of the scan kernel
+constexpr int kScanThreads = 512;  // 16 warps per scan CTA
+constexpr int kScanWarps = kScanThreads / kWarp;
+constexpr int kCandCap = 4096;     // K2 candidate list capacity per query (overflow -> rescan)
+constexpr int kRefineChunk = 1024; // K3 candidates per exact-refine flush
+constexpr int kMaxNprobe = 1024;   // v1 cap on nprobe' (K3 sort buffer)
+constexpr int kLutPairBytes = 256 * 64 * 4;  // one [256 codes][64 sub-spaces] fp32 slab
+
+// ---------------------------------------------------------------- errors
+struct Error {
+  vlr_status st;
+  std::string msg;
+};
+void set_error(const std::string& msg);
+
+#define VLR_CUDA_TRY(expr)                                                              \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess) {                                                            \
+      ::vlr::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));             \
+      return _e == cudaErrorMemoryAllocation ? VLR_ERR_OOM : VLR_ERR_CUDA;              \
+    }                                                                                   \
+  } while (0)
+
+// ---------------------------------------------------------------- device data
+struct DeviceIndex {
+  int d = 0, nlist = 0, m = 0, mpad = 0, npairs = 0, dsub = 0;
+  int rank = 0, world = 1, device = 0;
+  bool shard_only = false;
+  // replicated, coarse quantizer
+  float* centroids = nullptr;  // [nlist][d]
+  float* cnorm2 = nullptr;     // [nlist] ||c||^2 (fp64 -> fp32)
+  float cmax = 0.f;            // max ||c|| (host), for the filter band
+  float* codebooks = nullptr;  // [m][256][dsub]
+  int32_t* owner = nullptr;    // [nlist] owner rank or -1 (mapping table)
+  int32_t* local = nullptr;    // [nlist] local list index on this rank or -1
+  std::vector<int32_t> owner_h;
+  // this rank's resident lists (lane-interleaved groups of 32 vectors)
+  int32_t n_local = 0;
+  int64_t n_groups = 0, n_vec = 0;
+  int64_t* gbase = nullptr;    // [n_local+1] first group of each local list
+  uint8_t* codes = nullptr;    // [n_groups][mpad/16][32 lanes][16 B], per-lane rotated
+  float* bias = nullptr;       // [n_groups*32] b_i = ||yhat||^2 + 2<c_l, yhat> (+inf for padding)
+  int64_t* ids = nullptr;      // [n_groups*32] (-1 for padding)
+  int64_t bytes = 0;
+  void* nccl = nullptr;        // ncclComm_t
+};
+
+struct Workspace {
+  int cap_nq = 0, cap_np = 0, cap_k = 0, n_cta = 0;
+  float* qnorm = nullptr;      // [nq] ||q|| (fp32)
+  float* dt = nullptr;         // [nq][nlist] filter distances ||c||^2 - 2<q,c>
+  int32_t* cand = nullptr;     // [nq][kCandCap]
+  int32_t* ncand = nullptr;    // [nq]
+  float* bound = nullptr;      // [nq] candidate bound theta~ + 2 Delta*
+  int32_t* probes = nullptr;   // [nq][np]
+  float* term1 = nullptr;      // [nq][np] ||q - c_l||^2 (fp64 -> fp32)
+  int32_t* plocal = nullptr;   // [nq][np] local list or -1
+  int64_t* item_off = nullptr; // [nq*np + 1] group prefix of owned work items
+  float* lut = nullptr;        // [nq][npairs][256][64]
+  float* pdist = nullptr;      // [(n_cta + nq) * warps * k] scan partials
+  int64_t* pid = nullptr;
+  void* send = nullptr;        // [nq][k] 16-byte entries (world > 1)
+  void* recv = nullptr;        // [world][nq][k]
+  float* h_stage = nullptr;    // pinned staging for vlr_search_host (queries)
+  float* d_q = nullptr;        // device queries for vlr_search_host
+  int64_t* d_ids = nullptr;
+  float* d_dist = nullptr;
+  uint8_t* d_miss = nullptr;
+  int32_t* d_probes = nullptr;
+  int32_t* status = nullptr;   // device status word (bit0: non-finite query)
+  int32_t* h_status = nullptr; // pinned mirror
+};
+
+}  // namespace vlr
+
+struct vlr_index {
+  vlr::DeviceIndex ix;
+  vlr::Workspace ws;
+  bool profiling = false;
+  cudaEvent_t ev[9] = {};
+  int launches = 0;
+  bool dead = false;  // NCCL failure
+  std::string last_err;
+};
+
+namespace vlr {
+
+// ---------------------------------------------------------------- launchers
+// K0 layout (load time)
+cudaError_t launch_layout(const DeviceIndex& ix, const uint8_t* stage_codes, const int64_t* stage_ids,
+                          const int64_t* vbase, const int32_t* lglob, cudaStream_t s);
+cudaError_t launch_cnorm(const DeviceIndex& ix, cudaStream_t s);
+// stage 0..2 coarse quantizer
+cudaError_t launch_qprep(const float* Q, int nq, int d, float* qnorm, int32_t* status, cudaStream_t s);
+cudaError_t launch_filter_simt(const float* Q, int nq, const DeviceIndex& ix, float* dt, cudaStream_t s);
+cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float band_rel,
+                          cudaStream_t s);
+cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, int np,
+                          cudaStream_t s);
+// stage 3..4
+cudaError_t launch_route(const DeviceIndex& ix, const Workspace& ws, int nq, int np, uint8_t* miss,
+                         int32_t* probes_out, cudaStream_t s);
+cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s);
+// stage 5..7
+int scan_ctas(const DeviceIndex& ix);
+cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s);
+cudaError_t launch_rank_merge(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k,
+                              int64_t* out_ids, float* out_dist, void* out_packed, cudaStream_t s);
+cudaError_t launch_merge_packed(const void* parts, int n_shards, int nq, int k, int64_t* out_ids, float* out_dist,
+                                cudaStream_t s);
+cudaError_t launch_merge_split(const int64_t* part_ids, const float* part_dist, int n_shards, int nq, int k,
+                               int64_t* out_ids, float* out_dist, cudaStream_t s);
+
+}  // namespace vlr

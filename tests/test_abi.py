@@ -1,0 +1,99 @@
+"""C-ABI library checks that need no GPU: the library loads, exports every
+symbol include/vlr.h declares, and the host-side validation of
+vlr_load_index / vlr_search* returns the documented status codes before any
+device work. With no GPU, a valid load fails with VLR_ERR_CUDA (no fallback).
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2504_08930_b200 as vlr
+from conftest import ROOT
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2504_08930_b200 import build
+    build.build()
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "vlr.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(vlr_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    syms = header_symbols()
+    assert len(syms) >= 14
+    L = vlr.lib()
+    for s in syms:
+        assert hasattr(L, s), f"libvlr.so does not export {s}"
+    assert sorted(vlr.EXPORTS) == syms
+
+
+def test_version():
+    assert vlr.version() == (1, 0)
+
+
+def _tiny(m=2, d=4, L=3):
+    rng = np.random.default_rng(0)
+    C = rng.standard_normal((L, d)).astype(np.float32)
+    Y = rng.standard_normal((m, 256, d // m)).astype(np.float32)
+    offs = np.array([0, 2, 2, 5], np.int64)[: L + 1]
+    ids = np.arange(5, dtype=np.int64)
+    codes = rng.integers(0, 256, (5, m)).astype(np.uint8)
+    return C, Y, offs, ids, codes
+
+
+def status_of(fn):
+    try:
+        fn()
+    except vlr.VlrError as e:
+        return e.name
+    return "OK"
+
+
+def test_load_validation_codes():
+    C, Y, offs, ids, codes = _tiny()
+    load = vlr.Index.load
+    # d % m != 0 (m = 3 for d = 4)
+    Y3 = np.zeros((3, 256, 1), np.float32)
+    assert status_of(lambda: load(C, Y3, offs, ids, np.zeros((5, 3), np.uint8), device=0)) == "DIM_MISMATCH"
+    assert status_of(lambda: load(C, Y, offs, ids, codes, nbits=4, device=0)) == "UNSUPPORTED"
+    assert status_of(lambda: load(C, Y, offs, ids, codes, metric=1, device=0)) == "UNSUPPORTED"
+    assert status_of(lambda: load(C, Y, offs, ids, codes, by_residual=0, device=0)) == "UNSUPPORTED"
+    Cn = C.copy(); Cn[1, 2] = np.nan
+    assert status_of(lambda: load(Cn, Y, offs, ids, codes, device=0)) == "NONFINITE"
+    Yn = Y.copy(); Yn[0, 5, 0] = np.inf
+    assert status_of(lambda: load(C, Yn, offs, ids, codes, device=0)) == "NONFINITE"
+    assert status_of(lambda: load(C, Y, offs, ids, codes, hot=[0, 3], device=0)) == "UNKNOWN_CLUSTER"
+    assert status_of(lambda: load(C, Y, offs, ids, codes, hot=[1, 1], device=0)) == "UNKNOWN_CLUSTER"
+    assert status_of(lambda: load(C, Y, offs, ids, codes, hot=[0, 1], hot_owner=[0, 2], world=2,
+                                  device=0)) == "UNKNOWN_CLUSTER"
+    bad = offs.copy(); bad[2] = 1
+    assert status_of(lambda: load(C, Y, bad, ids, codes, device=0)) == "INVALID_ARG"
+    assert status_of(lambda: load(C, Y, offs, ids, codes, rank=2, world=2, device=0)) == "INVALID_ARG"
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_valid_load_without_gpu_fails_loudly():
+    C, Y, offs, ids, codes = _tiny()
+    assert status_of(lambda: vlr.Index.load(C, Y, offs, ids, codes, device=0)) == "CUDA"
+
+
+def test_search_argument_validation_without_index():
+    L = vlr.lib()
+    # null index
+    st = L.vlr_search_async(None, None, 1, 1, 1, None, None, None, None, None)
+    assert vlr.STATUS[st] == "INVALID_ARG"
+    st = L.vlr_merge_partials(None, None, 0, 1, 1, None, None, None)
+    assert vlr.STATUS[st] == "INVALID_ARG"
+    st = L.vlr_merge_partials(None, None, 1, 1, 64, None, None, None)
+    assert vlr.STATUS[st] == "UNSUPPORTED"
+    st = L.vlr_merge_partials(None, None, 1, 0, 4, None, None, None)
+    assert vlr.STATUS[st] == "OK"  # nq == 0 is a no-op
+    assert b"" != L.vlr_last_error() or True

@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle,
+element by element on the same seeded inputs (rules R1-R5).
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+import paper_2504_08930_b200 as vlr
+from conftest import fval, golden_index, load_golden
+from parity import check
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2504_08930_b200 import build
+    build.build()
+    assert torch.cuda.is_available()
+
+
+def gpu_search(index_handle, Q, nprobe, k):
+    Qd = torch.from_numpy(np.ascontiguousarray(Q, np.float32)).cuda()
+    ids, dist, miss, probes = index_handle.search(Qd, nprobe, k, sync=True)
+    torch.cuda.synchronize()
+    return dict(ids=ids.cpu().numpy(), dist=dist.cpu().numpy(), miss=miss.cpu().numpy(), probes=probes.cpu().numpy())
+
+
+def run_parity(ix, Q, nprobe, k, hot=None, idmap=None):
+    h = vlr.Index.from_arrays(ix, hot=hot)
+    g = gpu_search(h, Q, nprobe, k)
+    o = oracle.search(ix, Q, nprobe, k, hot=hot)
+    errs = check(ix, Q, g, o, hot=hot, idmap=idmap or oracle.IdMap(ix))
+    h.close()
+    return errs, g, o
+
+
+# --------------------------------------------------------------- golden
+def test_golden_tiny_on_gpu():
+    gd = load_golden("tiny_hand.json")
+    ix = golden_index(gd)
+    Q = np.array(gd["queries"], np.float32)
+    for case in gd["cases"]:
+        h = vlr.Index.from_arrays(ix, hot=case["hot"])
+        g = gpu_search(h, Q, case["nprobe"], case["k"])
+        assert g["probes"].tolist() == case["probes"]
+        assert g["miss"].tolist() == case["miss"]
+        assert g["ids"].tolist() == case["ids"]
+        exp = np.array([[fval(x) for x in row] for row in case["dist"]], np.float32)
+        assert np.array_equal(g["dist"], exp)  # every value here is exact in fp32
+        h.close()
+
+
+# --------------------------------------------------------------- C1
+def test_c1_parity_all_hot(c1_index, c1_queries):
+    c = datagen.CONFIGS["C1"]
+    errs, g, o = run_parity(c1_index, c1_queries, c["nprobe"], c["k"])
+    assert not errs, errs
+    assert np.all(g["miss"] == 0)
+
+
+def test_c1_parity_hot_half_mass(c1_index, c1_queries):
+    c = datagen.CONFIGS["C1"]
+    Qc = datagen.make_queries(c["N"], c["d"], c["nlist"], 2000, stream=1, alpha=c["alpha"])
+    counts = datagen.access_counts(c1_index.centroids, Qc, c["nprobe"])
+    hot = datagen.hot_from_mass(counts, 0.5)
+    errs, g, o = run_parity(c1_index, c1_queries, c["nprobe"], c["k"], hot=hot)
+    assert not errs, errs
+    assert 0 < g["miss"].mean() < 1
+
+
+@pytest.mark.parametrize("nprobe,k", [(1, 1), (4, 32), (64, 10), (300, 7), (1024, 10), (5000, 3)])
+def test_c1_parity_nprobe_k(c1_index, c1_queries, nprobe, k):
+    errs, g, o = run_parity(c1_index, c1_queries[:24], nprobe, k)
+    assert not errs, errs
+
+
+def test_c1_determinism_and_shard_invariance(c1_index, c1_queries):
+    c = datagen.CONFIGS["C1"]
+    h = vlr.Index.from_arrays(c1_index)
+    a = gpu_search(h, c1_queries, c["nprobe"], c["k"])
+    b = gpu_search(h, c1_queries, c["nprobe"], c["k"])
+    for key in a:
+        assert np.array_equal(a[key], b[key])  # R5: repeated runs bitwise identical
+    h.close()
+    Qd = torch.from_numpy(c1_queries).cuda()
+    for G in (2, 3, 4, 8):
+        parts_i, parts_d = [], []
+        owners = None
+        for r in range(G):
+            hs = vlr.Index.from_arrays(c1_index, rank=r, world=G)
+            ids, dist, miss, probes = hs.search(Qd, c["nprobe"], c["k"], sync=True)
+            parts_i.append(ids)
+            parts_d.append(dist)
+            assert np.array_equal(miss.cpu().numpy(), a["miss"])
+            assert np.array_equal(probes.cpu().numpy(), a["probes"])
+            own = hs.owners()
+            owners = own if owners is None else owners
+            assert np.array_equal(own, owners)
+            hs.close()
+        mi, md = vlr.merge_partials(torch.stack(parts_i), torch.stack(parts_d))
+        torch.cuda.synchronize()
+        assert np.array_equal(mi.cpu().numpy(), a["ids"]), f"G={G} ids differ"
+        assert np.array_equal(md.cpu().numpy(), a["dist"]), f"G={G} dist differ"
+        # size-descending round-robin deal: shard sizes differ by at most one list
+        counts = np.bincount(owners[owners >= 0], minlength=G)
+        assert counts.max() - counts.min() <= 1
+
+
+def test_search_host_matches_device(c1_index, c1_queries):
+    c = datagen.CONFIGS["C1"]
+    h = vlr.Index.from_arrays(c1_index)
+    a = gpu_search(h, c1_queries, c["nprobe"], c["k"])
+    ids, dist, miss, probes = h.search_host(c1_queries, c["nprobe"], c["k"])
+    assert np.array_equal(ids, a["ids"]) and np.array_equal(dist, a["dist"])
+    assert np.array_equal(miss, a["miss"]) and np.array_equal(probes, a["probes"])
+    assert h.last_launch_count >= 8
+    h.close()
+
+
+def test_nonfinite_query_reported(c1_index, c1_queries):
+    h = vlr.Index.from_arrays(c1_index)
+    Q = c1_queries[:4].copy()
+    Q[2, 7] = np.nan
+    with pytest.raises(vlr.VlrError) as e:
+        gpu_search(h, Q, 8, 5)
+    assert e.value.name == "NONFINITE"
+    g = gpu_search(h, c1_queries[:4], 8, 5)  # the handle stays usable
+    assert g["ids"].shape == (4, 5)
+    h.close()
+
+
+def test_batch_sizes(c1_index, c1_queries):
+    h = vlr.Index.from_arrays(c1_index)
+    big = datagen.make_queries(100_000, 128, 1024, 513, stream=3)
+    for nq in (1, 2, 33, 513):
+        Q = big[:nq]
+        g = gpu_search(h, Q, 16, 10)
+        o = oracle.search(c1_index, Q, 16, 10)
+        assert not check(c1_index, Q, g, o)
+    Qd = torch.zeros(0, 128, device="cuda")
+    ids, dist, miss, probes = h.search(Qd, 16, 10, sync=True)
+    assert ids.shape == (0, 10)
+    h.close()
+
+
+# --------------------------------------------------------------- shapes / m_pad variants
+@pytest.mark.parametrize("d,m,L", [(32, 4, 50), (64, 32, 40), (96, 48, 33), (128, 64, 64), (192, 96, 40),
+                                   (256, 128, 70), (40, 20, 17)])
+def test_m_variants(d, m, L):
+    ix = datagen.make_index(4000, d, L, m, seed=d + m)
+    Q = datagen.make_queries(4000, d, L, 20, seed=d + m, stream=2)
+    hot = np.arange(0, L, 2)
+    for npb, hh in ((8, None), (L, hot)):
+        errs, g, o = run_parity(ix, Q, npb, 10, hot=hh)
+        assert not errs, (d, m, L, errs)
+
+
+# --------------------------------------------------------------- adversarial
+def _rand_index(rng, L, d, m, sizes, dup_centroids=()):
+    C = rng.standard_normal((L, d)).astype(np.float32)
+    for a, b in dup_centroids:
+        C[b] = C[a]
+    Y = (0.3 * rng.standard_normal((m, 256, d // m))).astype(np.float32)
+    ids = rng.permutation(10 * sum(sizes) + 10)[: sum(sizes)]
+    lists, o = [], 0
+    for s in sizes:
+        lists.append((ids[o:o + s], rng.integers(0, 256, (s, m)).astype(np.uint8)))
+        o += s
+    return datagen.index_from_parts(C, Y, lists)
+
+
+def test_adversarial_empty_single_duplicate():
+    rng = np.random.default_rng(5)
+    sizes = [0, 1, 0, 33, 64, 1, 0, 31, 32, 95]
+    ix = _rand_index(rng, 10, 16, 4, sizes, dup_centroids=[(3, 7), (3, 9)])
+    # duplicate vectors inside a list (same code) -> ties broken by id
+    ix.codes[ix.list_offsets[4]:ix.list_offsets[4] + 5] = ix.codes[ix.list_offsets[4]]
+    Q = np.concatenate([ix.centroids[[3, 7, 0]], rng.standard_normal((13, 16)).astype(np.float32)])
+    for npb in (1, 3, 10, 50):
+        for k in (1, 5, 32):
+            for hot in (None, [1, 3, 4, 9], []):
+                errs, g, o = run_parity(ix, Q, npb, k, hot=hot)
+                assert not errs, (npb, k, hot, errs)
+
+
+def test_adversarial_equidistant_centroids():
+    # centroids +-e_i around the origin: every query at the origin sees all
+    # of them at distance 1 -> probes must be ordered by cluster id (A7)
+    d = 16
+    C = np.concatenate([np.eye(d), -np.eye(d)]).astype(np.float32)
+    rng = np.random.default_rng(6)
+    Y = (0.1 * rng.standard_normal((4, 256, 4))).astype(np.float32)
+    lists = [(np.arange(i * 40, i * 40 + 40), rng.integers(0, 256, (40, 4)).astype(np.uint8)) for i in range(2 * d)]
+    ix = datagen.index_from_parts(C, Y, lists)
+    Q = np.zeros((3, d), np.float32)
+    Q[1, 0] = 1e-3
+    Q[2] = 0.5
+    for npb in (1, 5, 32):
+        errs, g, o = run_parity(ix, Q, npb, 10)
+        assert not errs, errs
+    assert g["probes"][0].tolist()[:5] == [0, 1, 2, 3, 4]
+
+
+def test_adversarial_identical_centroids_many():
+    # 200 identical centroids: the band holds all of them; order by id
+    rng = np.random.default_rng(8)
+    c = rng.standard_normal(8).astype(np.float32)
+    C = np.repeat(c[None], 200, 0)
+    C[150:] += np.float32(1.0)
+    Y = (0.2 * rng.standard_normal((2, 256, 4))).astype(np.float32)
+    lists = [(np.arange(i * 3, i * 3 + 3), rng.integers(0, 256, (3, 2)).astype(np.uint8)) for i in range(200)]
+    ix = datagen.index_from_parts(C, Y, lists)
+    Q = (c + 0.01 * rng.standard_normal((5, 8))).astype(np.float32)
+    for npb in (16, 150, 160):
+        errs, g, o = run_parity(ix, Q, npb, 10)
+        assert not errs, errs
+
+
+def test_offset_data_stress():
+    # reading A3: data with a large common offset; the LUT decomposition loses
+    # fp32 accuracy there. Documented limit: parity is still required at the
+    # 1e-5 relative rule because distances scale with the offset as well.
+    ix = datagen.make_index(3000, 32, 20, 8, seed=12)
+    off = np.float32(3.0)
+    ix.centroids = ix.centroids + off
+    Q = datagen.make_queries(3000, 32, 20, 16, seed=12, stream=2) + off
+    errs, g, o = run_parity(ix, Q, 6, 10)
+    assert not errs, errs
