@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""bench.py -- batched IVF-PQ hot-partition search throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl vlr|reference]
+
+One step = one batch search (coarse quantizer K1-K3, route K4, LUT K5, ADC
+scan K6, merges K7/K8) over `batch` synthetic queries of BASELINE.json's
+128M-vector config (C4 by default), inputs resident in HBM. N > 1: launched
+by torchrun, one rank per GPU; hot lists dealt over the ranks, every rank
+runs the SPMD search and the partial top-k are merged over NCCL (strong
+scaling: the index and the batch are fixed). Rank 0 prints ONE JSON line.
+--impl reference times the CPU oracle (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "IVF-PQ search queries/s (batch 256, nprobe 128, k 10)"
+UNIT = "queries/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=40)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="vlr", choices=["vlr", "reference"])
+    p.add_argument("--config", default="C4")
+    p.add_argument("--N", type=int, default=None, help="override vector count (testing only)")
+    p.add_argument("--batch", type=int, default=None)
+    p.add_argument("--nprobe", type=int, default=None)
+    p.add_argument("--k", type=int, default=None)
+    p.add_argument("--hot-mass", type=float, default=1.0)
+    p.add_argument("--alpha", type=float, default=None)
+    p.add_argument("--seed", type=int, default=2504_08930)
+    p.add_argument("--no-oracle", action="store_true")
+    p.add_argument("--oracle-seconds", type=float, default=15.0)
+    p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--ncu", action="store_true", help="short run for ncu: no e2e/oracle/clocks")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- helpers
+def cfg_of(a):
+    import datagen
+    c = dict(datagen.CONFIGS[a.config])
+    for key in ("N", "batch", "nprobe", "k", "alpha"):
+        v = getattr(a, key)
+        if v is not None:
+            c[key] = v
+    c["hot_mass"] = a.hot_mass
+    return c
+
+
+def workload_name(c, name):
+    hot = "all lists resident" if c["hot_mass"] >= 1 else f"hot set = {c['hot_mass']:.0%} of access mass"
+    return (f"{name}: {c['N'] / 1e6:g}M x d{c['d']}, IVF{c['nlist']}, PQ{c['m']}x8, nprobe {c['nprobe']}, "
+            f"k {c['k']}, batch {c['batch']}, Zipf alpha {c['alpha']}, {hot}")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        rows = [r for r in self.rows if len(r) == 7]
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def allmax(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def gen_index(c, seed, rank, world, hot=None):
+    """Generate this rank's shard of the synthetic index on the GPU (TOOLING)."""
+    import datagen
+    sizes = datagen.list_sizes(c["N"], c["nlist"], seed)
+    owned = None
+    if world > 1:
+        own = datagen.deal_owners(sizes, np.arange(c["nlist"]) if hot is None else hot, world)
+        owned = own == rank
+    t = time.time()
+    ix = datagen.make_index(c["N"], c["d"], c["nlist"], c["m"], seed=seed, device="cuda", owned=owned)
+    return ix, time.time() - t
+
+
+def calib_hot(c, seed):
+    """Hot set from a calibration stream (seed stream 1, disjoint from the test
+    stream): shortest prefix of the access ranking holding
+    hot_mass of the accesses (TOOLING)."""
+    import datagen
+    if c["hot_mass"] >= 1.0:
+        return None, None
+    ncal = 10_000
+    C = datagen.gen.Generator(c["N"], c["d"], c["nlist"], 1, seed=seed, device="cuda").centroids().cpu().numpy()
+    Qc = datagen.make_queries(c["N"], c["d"], c["nlist"], ncal, seed=seed, stream=1, alpha=c["alpha"], device="cuda")
+    counts = datagen.access_counts(C, Qc, c["nprobe"], device="cuda")
+    return datagen.hot_from_mass(counts, c["hot_mass"]), counts
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(a):
+    """The oracle, as it stands, on host cores: each step a bounded sample of
+    the workload (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    import datagen
+    import oracle
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    c = cfg_of(a)
+    oracle.build()
+    hot, _ = calib_hot(c, a.seed)
+    ix, gen_s = gen_index(c, a.seed, 0, 1, hot=hot)
+    B = c["batch"]
+    pool = datagen.make_queries(c["N"], c["d"], c["nlist"], (a.warmup + a.steps) * B, seed=a.seed, stream=2,
+                                alpha=c["alpha"], device="cuda")
+    cores = oracle.default_threads()
+    # sample size per step: ~1 s of oracle work on the host cores
+    t = time.time()
+    oracle.search(ix, pool[:cores], c["nprobe"], c["k"], hot=hot, nthreads=cores)
+    per_q = (time.time() - t) / cores
+    S = int(max(1, min(B, round(max(1.0, 2.0 * cores * per_q) / per_q))))
+    S = max(cores, (S // cores) * cores) if S >= cores else S
+    times = []
+    for i in range(a.warmup + a.steps):
+        Q = pool[i * B:i * B + S]
+        t = time.time()
+        oracle.search(ix, Q, c["nprobe"], c["k"], hot=hot, nthreads=cores)
+        if i >= a.warmup:
+            times.append(time.time() - t)
+    tot = sum(times)
+    val = a.steps * S / tot
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": 1, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded clustered embeddings, Zipf queries)",
+            "config": {"workload": workload_name(c, a.config), "seed": a.seed, "sample_queries_per_step": S},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{S} of the {B} queries of each step's batch, oracle/oracle.c fp64, OpenMP"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gen_s": gen_s}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import datagen
+    import paper_2504_08930_b200 as vlr
+    from paper_2504_08930_b200 import build as vbuild
+
+    rank, world, local = dist_setup()
+    if world != a.gpus and rank == 0:
+        print(f"warning: --gpus {a.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if rank == 0:
+        vbuild.build()
+    barrier(world)
+    c = cfg_of(a)
+    B, NP, K = c["batch"], min(c["nprobe"], c["nlist"]), c["k"]
+    # ---- index (tooling), shard residency (vlr_load_index)
+    t0 = time.time()
+    hot, counts = calib_hot(c, a.seed)
+    ix, gen_s = gen_index(c, a.seed, rank, world, hot=hot)
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [vlr.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    t1 = time.time()
+    h = vlr.Index.from_arrays(ix, hot=hot, rank=rank, world=world, device=local, nccl_id=nccl_id)
+    load_s = time.time() - t1
+    owners = h.owners()
+    exp_own = datagen.deal_owners(ix.list_sizes, np.arange(c["nlist"]) if hot is None else hot, world)
+    assert np.array_equal(owners, exp_own), "owner table differs from the documented deal"
+    info = h.info()
+    # ---- queries (test stream), resident in HBM
+    pool = datagen.make_queries(c["N"], c["d"], c["nlist"], (a.warmup + a.steps) * B, seed=a.seed, stream=2,
+                                alpha=c["alpha"], device="cuda")
+    Qdev = torch.from_numpy(pool).cuda().reshape(a.warmup + a.steps, B, c["d"])
+    h.reserve(B, NP, K)
+    outs = [(torch.empty(B, K, dtype=torch.int64, device="cuda"), torch.empty(B, K, device="cuda"),
+             torch.empty(B, NP, dtype=torch.uint8, device="cuda"), torch.empty(B, NP, dtype=torch.int32, device="cuda"))
+            for _ in range(a.steps)]
+    stream = torch.cuda.current_stream()
+    for i in range(a.warmup):
+        h.search(Qdev[i], c["nprobe"], K, out=outs[0], stream=stream)
+    torch.cuda.synchronize()
+    h.set_profiling(True)
+    launches = h.last_launch_count
+    clocks = Clocks(local)
+    if not a.ncu:
+        clocks.start()
+        time.sleep(0.3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(a.steps):
+        ev[i][0].record(stream)
+        h.search(Qdev[a.warmup + i], c["nprobe"], K, out=outs[i], stream=stream)
+        ev[i][1].record(stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop() if not a.ncu else None
+    h.set_profiling(False)
+    ms_total = allmax(e0.elapsed_time(e1), world)
+    lat = np.array([s.elapsed_time(e) for s, e in ev])
+    nrec = min(a.steps, 64)
+    stages = [h.stage_times(back=j) for j in range(nrec)]
+    stage_mean = {k2: float(np.mean([s[k2] for s in stages])) for k2 in stages[0]}
+    scan_ms = np.array([s["scan"] for s in stages[::-1]])  # oldest first -> steps a.steps-nrec .. a.steps-1
+    # ---- algorithmic scan bytes: sum over owned hot probes of n_l * (m + 4)
+    sizes = ix.list_sizes
+    per_vec = c["m"] + 4
+    step_bytes, hit = [], []
+    for i in range(a.steps):
+        prb = outs[i][3].cpu().numpy()
+        miss = outs[i][2].cpu().numpy()
+        own = owners[prb] == rank
+        step_bytes.append(float((sizes[prb] * own).sum()) * per_vec)
+        hit.append(1.0 - miss.mean(axis=1))
+    step_bytes = np.array(step_bytes)
+    bytes_rec = step_bytes[a.steps - nrec:]
+    achieved = float(bytes_rec.sum() / (scan_ms.sum() * 1e-3) / 1e9)
+    peak, peak_src = peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_scan_latest.json")) as f:
+            tj = json.load(f)
+        if tj.get("config") == a.config and tj.get("batch") == B:
+            traffic = tj.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    # ---- e2e through the C-ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not a.ncu:
+        ne = a.e2e_steps or a.steps
+        hq = torch.from_numpy(pool[: B * ne].reshape(ne, B, c["d"]).copy()).pin_memory()
+        hid = torch.empty(B, K, dtype=torch.int64).pin_memory()
+        hd = torch.empty(B, K, dtype=torch.float32).pin_memory()
+        hm = torch.empty(B, NP, dtype=torch.uint8).pin_memory()
+        for i in range(min(3, ne)):
+            h.search_host_ptr(hq[i].data_ptr(), B, c["nprobe"], K, hid.data_ptr(), hd.data_ptr(), hm.data_ptr(), None)
+        barrier(world)
+        t = time.perf_counter()
+        for i in range(ne):
+            h.search_host_ptr(hq[i].data_ptr(), B, c["nprobe"], K, hid.data_ptr(), hd.data_ptr(), hm.data_ptr(), None)
+        el = allmax(time.perf_counter() - t, world)
+        e2e = {"value": ne * B / el, "unit": UNIT, "h2d_bytes_per_step": B * c["d"] * 4,
+               "d2h_bytes_per_step": B * K * 12 + B * NP}
+    # ---- oracle: cpu_baseline + sampled full-size parity (rank 0, N = 1)
+    cpu = None
+    par = None
+    if rank == 0 and world == 1 and not a.no_oracle and not a.ncu:
+        cpu, par = oracle_leg(a, c, ix, hot, pool, outs)
+    value = a.steps * B / (ms_total * 1e-3)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms_total / a.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded clustered embeddings, Zipf-skewed queries; generated on the GPU)",
+            "config": {"workload": workload_name(c, a.config), "N": c["N"], "d": c["d"], "nlist": c["nlist"], "m": c["m"],
+                       "nprobe": c["nprobe"], "k": K, "batch": B, "alpha": c["alpha"], "hot_mass": c["hot_mass"],
+                       "seed": a.seed, "parallelism": f"hot-list shards x{world}, NCCL partial top-k merge",
+                       "l2": "inputs larger than L2 (index %.1f GB/GPU, %.2f GB scanned per batch)" % (
+                           info["bytes_on_device"] / 1e9, float(step_bytes.mean()) / 1e9)},
+            "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+            "gpu_launches": int(launches * a.steps),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "kernel": "k_scan (K6 ADC scan)", "peak_source": peak_src,
+                         "bytes_per_launch": float(bytes_rec.mean()), "ms_per_launch": float(scan_ms.mean())},
+            "stage_ms": stage_mean,
+            "hit_rate_mean": float(np.mean(np.concatenate(hit))),
+            "e2e": e2e, "clocks": clk, "cpu_baseline": cpu, "parity_sample": par,
+            "gen_s": round(gen_s, 1), "load_s": round(load_s, 1),
+        }
+        if counts is not None:
+            line["top20_share"] = datagen.topk_share(counts)
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def oracle_leg(a, c, ix, hot, pool, outs):
+    import oracle
+    from parity import check
+    oracle.build()
+    cores = oracle.default_threads()
+    B = c["batch"]
+    first = pool[a.warmup * B:(a.warmup + 1) * B]  # the first timed batch
+    # size the sample to ~oracle_seconds of CPU work
+    t = time.time()
+    o = oracle.search(ix, first[:cores], c["nprobe"], c["k"], hot=hot, nthreads=cores)
+    dt = time.time() - t
+    S = int(min(B, max(cores, cores * math.floor(a.oracle_seconds / max(dt, 1e-3)))))
+    t = time.time()
+    o = oracle.search(ix, first[:S], c["nprobe"], c["k"], hot=hot, nthreads=cores)
+    el = time.time() - t
+    cpu = {"value": S / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"first {S} queries of the first timed batch (same index and queries), oracle/oracle.c fp64"}
+    g = outs[0]
+    gpu = dict(ids=g[0].cpu().numpy()[:S], dist=g[1].cpu().numpy()[:S], miss=g[2].cpu().numpy()[:S],
+               probes=g[3].cpu().numpy()[:S])
+    errs = check(ix, first, gpu, o, hot=hot, idmap=oracle.IdMap(ix) if ix.N <= 200_000_000 else None,
+                 qsel=np.arange(S))
+    par = {"queries": S, "rules": "R1 probes+mask bit-exact, R2 dist 1e-5 rel, R3 id sets, R4 order/padding",
+           "pass": not errs, "errors": errs[:3]}
+    return cpu, par
+
+
+if __name__ == "__main__":
+    main()

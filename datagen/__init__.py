@@ -18,4 +18,6 @@ from .gen import (  # noqa: F401
     coverage_mean_hitrate,
     topk_share,
     index_from_parts,
+    list_sizes,
+    deal_owners,
 )

@@ -157,12 +157,14 @@ vlr_status vlr_index_info(const vlr_index* idx, int64_t* bytes_on_device, int32_
 /* Owner rank of every cluster (-1 = not resident): out [nlist] int32 host. */
 vlr_status vlr_index_owners(const vlr_index* idx, int32_t* out_owner);
 
-/* Per-stage device timing of subsequent searches (CUDA events on the search
- * stream). Stage order: 0 coarse filter (K1), 1 select (K2), 2 refine (K3),
- * 3 route (K4), 4 LUT (K5), 5 scan (K6), 6 rank merge (K7), 7 exchange+merge
- * (K8). vlr_stage_times waits for the last search and writes min(n, 8) ms values. */
+/* Per-stage device timing of subsequent searches (CUDA events recorded on the
+ * search stream into a ring of the last 64 searches). Stage order: 0 coarse
+ * filter (qprep + K1), 1 select (K2), 2 refine (K3), 3 route (K4), 4 LUT (K5),
+ * 5 scan (K6), 6 rank merge (K7), 7 exchange + merge (K8).
+ * vlr_stage_times waits for search number `back` before the last one
+ * (back = 0: the last search; back < 64) and writes min(n, 8) ms values. */
 vlr_status vlr_set_profiling(vlr_index* idx, int32_t enable);
-vlr_status vlr_stage_times(vlr_index* idx, float* ms, int32_t n);
+vlr_status vlr_stage_times(vlr_index* idx, int32_t back, float* ms, int32_t n);
 
 /* Number of kernel launches issued by the last search on this handle. */
 int32_t vlr_last_launch_count(const vlr_index* idx);

@@ -68,7 +68,7 @@ def lib():
             "vlr_index_info": [P, P, P, P],
             "vlr_index_owners": [P, P],
             "vlr_set_profiling": [P, I32],
-            "vlr_stage_times": [P, P, I32],
+            "vlr_stage_times": [P, I32, P, I32],
             "vlr_nccl_unique_id": [P],
         }
         for name, args in sig.items():
@@ -207,9 +207,10 @@ class Index:
 
     STAGES = ["coarse_filter", "select", "refine", "route", "lut", "scan", "rank_merge", "exchange_merge"]
 
-    def stage_times(self) -> dict:
+    def stage_times(self, back: int = 0) -> dict:
+        """Per-stage ms of the search `back` searches ago (0 = last)."""
         ms = np.zeros(8, np.float32)
-        _check(lib().vlr_stage_times(self._h, ms.ctypes.data, 8))
+        _check(lib().vlr_stage_times(self._h, back, ms.ctypes.data, 8))
         return dict(zip(self.STAGES, ms.tolist()))
 
     @property

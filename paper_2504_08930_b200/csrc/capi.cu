@@ -24,9 +24,11 @@ static vlr_status fail(vlr_status st, const std::string& msg) {
   return st;
 }
 
-// relative bound on the filter's dot-product error (DESIGN.md §K1-K3 band):
-// fp32 FMA chain over d terms, one rounding per step.
-static float filter_edot(int d) { return 1.01f * (float)d * 5.9604645e-8f; }
+// relative bound on the filter's dot-product error (DESIGN.md §5 band proof):
+// operands pre-rounded to TF32 with cvt.rna (relative error <= 2^-11 each,
+// products exact in fp32), fp32 accumulation over d terms in the tensor core
+// bounded conservatively by d * 2^-23 (order and rounding mode unspecified).
+static float filter_edot(int d) { return 2.0f * 4.8828125e-4f + 2.3841858e-7f + 1.01f * (float)d * 1.1920929e-7f; }
 
 template <class T>
 static cudaError_t dalloc(T** p, size_t n) {
@@ -45,7 +47,7 @@ __global__ void k_negative(const int64_t* ids, long long n, int32_t* flag) {
 }
 
 static void free_ws(Workspace& w) {
-  void* ps[] = {w.qnorm, w.dt, w.cand, w.ncand, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.lut,
+  void* ps[] = {w.qnorm, w.qtf32, w.dt, w.cand, w.ncand, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.lut,
                 w.pdist, w.pid, w.send, w.recv, w.d_q, w.d_ids, w.d_dist, w.d_miss, w.d_probes, w.status};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -54,7 +56,7 @@ static void free_ws(Workspace& w) {
 }
 
 static void free_index(DeviceIndex& ix) {
-  void* ps[] = {ix.centroids, ix.cnorm2, ix.codebooks, ix.owner, ix.local, ix.gbase, ix.codes, ix.bias, ix.ids};
+  void* ps[] = {ix.centroids, ix.ctf32, ix.cnorm2, ix.codebooks, ix.owner, ix.local, ix.gbase, ix.codes, ix.bias, ix.ids};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (ix.nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(ix.nccl));
@@ -76,6 +78,7 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   w.n_cta = scan_ctas(ix);
   const size_t nqs = (size_t)cnq;
   VLR_CUDA_TRY(dalloc(&w.qnorm, nqs));
+  VLR_CUDA_TRY(dalloc(&w.qtf32, nqs * ix.d4));
   VLR_CUDA_TRY(dalloc(&w.dt, nqs * ix.nlist));
   VLR_CUDA_TRY(dalloc(&w.cand, nqs * kCandCap));
   VLR_CUDA_TRY(dalloc(&w.ncand, nqs));
@@ -189,6 +192,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   vlr_index* h = new vlr_index();
   DeviceIndex& ix = h->ix;
   ix.d = d;
+  ix.d4 = (d + 3) / 4 * 4;
   ix.nlist = L;
   ix.m = m;
   ix.dsub = dsub;
@@ -232,6 +236,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   ix.n_groups = gbase_h.back();
   LTRY(dalloc(&ix.centroids, (size_t)L * d));
   LTRY(dalloc(&ix.cnorm2, (size_t)L));
+  LTRY(dalloc(&ix.ctf32, (size_t)L * ix.d4));
   LTRY(dalloc(&ix.codebooks, ncb));
   LTRY(dalloc(&ix.owner, (size_t)L));
   LTRY(dalloc(&ix.local, (size_t)L));
@@ -241,6 +246,8 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   LTRY(dalloc(&ix.ids, (size_t)ix.n_groups * 32));
   LTRY(cudaMemcpyAsync(ix.centroids, D.centroids, sizeof(float) * L * d, cudaMemcpyHostToDevice, s));
   LTRY(cudaMemcpyAsync(ix.cnorm2, cn2.data(), sizeof(float) * L, cudaMemcpyHostToDevice, s));
+  LTRY(launch_round_tf32(ix.centroids, L, d, ix.d4, ix.ctf32, s));
+  LTRY(make_tmap_2d(ix.tmapA, ix.ctf32, L, ix.d4, 128));
   LTRY(cudaMemcpyAsync(ix.codebooks, D.codebooks, sizeof(float) * ncb, cudaMemcpyHostToDevice, s));
   LTRY(cudaMemcpyAsync(ix.owner, owner.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, s));
   LTRY(cudaMemcpyAsync(ix.local, local.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, s));
@@ -317,7 +324,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
     set_error("duplicate vector id among resident vectors");
     return bail(VLR_ERR_DUPLICATE_ID);
   }
-  ix.bytes = (int64_t)L * d * 4 + L * 4 + (int64_t)ncb * 4 + 2LL * L * 4 + (ix.n_local + 1) * 8 +
+  ix.bytes = (int64_t)L * d * 4 + (int64_t)L * ix.d4 * 4 + L * 4 + (int64_t)ncb * 4 + 2LL * L * 4 + (ix.n_local + 1) * 8 +
              ix.n_groups * 32 * (ix.mpad + 4 + 8);
   // NCCL communicator (collective)
   if (cm.world > 1 && cm.nccl_unique_id) {
@@ -331,7 +338,6 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
     }
     ix.nccl = comm_h;
   }
-  for (auto& e : h->ev) cudaEventCreate(&e);
   *out = h;
   return VLR_OK;
 #undef LTRY
@@ -341,8 +347,9 @@ void vlr_index_free(vlr_index* h) {
   if (!h) return;
   cudaSetDevice(h->ix.device);
   cudaDeviceSynchronize();
-  for (auto& e : h->ev)
-    if (e) cudaEventDestroy(e);
+  for (auto& row : h->ev)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
   free_ws(h->ws);
   free_index(h->ix);
   delete h;
@@ -358,7 +365,7 @@ vlr_status vlr_reserve(vlr_index* h, int32_t max_nq, int32_t max_nprobe, int32_t
 }
 
 static inline void rec(vlr_index* h, int i, cudaStream_t s) {
-  if (h->profiling) cudaEventRecord(h->ev[i], s);
+  if (h->profiling) cudaEventRecord(h->ev[h->nsearch % vlr_index::kRing][i], s);
 }
 
 vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
@@ -385,8 +392,8 @@ vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t np
   VLR_CUDA_TRY(cudaMemsetAsync(w.status, 0, sizeof(int32_t), s));
   int n = 0;
   rec(h, 0, s);
-  VLR_CUDA_TRY(launch_qprep(Q, nq, ix.d, w.qnorm, w.status, s)); ++n;
-  VLR_CUDA_TRY(launch_filter_simt(Q, nq, ix, w.dt, s)); ++n;
+  VLR_CUDA_TRY(launch_qprep(Q, nq, ix.d, ix.d4, w.qnorm, w.qtf32, w.status, s)); ++n;
+  VLR_CUDA_TRY(launch_filter_tc(w.qtf32, nq, ix, w.dt, s)); ++n;
   rec(h, 1, s);
   VLR_CUDA_TRY(launch_select(ix, w, nq, np, filter_edot(ix.d), s)); ++n;
   rec(h, 2, s);
@@ -415,6 +422,7 @@ vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t np
   rec(h, 8, s);
   VLR_CUDA_TRY(cudaMemcpyAsync(w.h_status, w.status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   h->launches = n;
+  if (h->profiling) ++h->nsearch;
   return VLR_OK;
 }
 
@@ -487,18 +495,26 @@ vlr_status vlr_index_owners(const vlr_index* h, int32_t* out) {
 
 vlr_status vlr_set_profiling(vlr_index* h, int32_t enable) {
   if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  if (enable && !h->ev[0][0]) {
+    VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
+    for (auto& row : h->ev)
+      for (auto& e : row) VLR_CUDA_TRY(cudaEventCreate(&e));
+  }
   h->profiling = enable != 0;
   return VLR_OK;
 }
 
-vlr_status vlr_stage_times(vlr_index* h, float* ms, int32_t n) {
+vlr_status vlr_stage_times(vlr_index* h, int32_t back, float* ms, int32_t n) {
   if (!h || !ms) return fail(VLR_ERR_INVALID_ARG, "null arg");
-  if (!h->profiling) return fail(VLR_ERR_INVALID_ARG, "profiling disabled");
-  VLR_CUDA_TRY(cudaEventSynchronize(h->ev[8]));
+  if (!h->ev[0][0]) return fail(VLR_ERR_INVALID_ARG, "profiling never enabled");
+  if (back < 0 || back >= vlr_index::kRing || back >= h->nsearch)
+    return fail(VLR_ERR_INVALID_ARG, "no such recorded search");
+  cudaEvent_t* ev = h->ev[(h->nsearch - 1 - back) % vlr_index::kRing];
+  VLR_CUDA_TRY(cudaEventSynchronize(ev[8]));
   const int stages = std::min(n, 8);
   for (int i = 0; i < stages; ++i) {
     float t = 0.f;
-    VLR_CUDA_TRY(cudaEventElapsedTime(&t, h->ev[i], h->ev[i + 1]));
+    VLR_CUDA_TRY(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
     ms[i] = t;
   }
   return VLR_OK;

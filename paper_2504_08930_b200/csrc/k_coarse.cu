@@ -19,15 +19,19 @@
 namespace vlr {
 
 // ----------------------------------------------------------------- qprep
-__global__ void k_qprep(const float* __restrict__ Q, int d, float* __restrict__ qnorm, int32_t* status) {
+__global__ void k_qprep(const float* __restrict__ Q, int d, int d4, float* __restrict__ qnorm,
+                        float* __restrict__ qtf32, int32_t* status) {
   const int q = blockIdx.x;
   const float* row = Q + (size_t)q * d;
   double s = 0.0;
   bool bad = false;
-  for (int t = threadIdx.x; t < d; t += blockDim.x) {
-    float v = row[t];
+  for (int t = threadIdx.x; t < d4; t += blockDim.x) {
+    float v = t < d ? row[t] : 0.f;
     bad |= !isfinite(v);
     s += (double)v * (double)v;
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    qtf32[(size_t)q * d4 + t] = __uint_as_float(r);
   }
   __shared__ double red[32];
   __shared__ int sbad;
@@ -45,9 +49,10 @@ __global__ void k_qprep(const float* __restrict__ Q, int d, float* __restrict__ 
   }
 }
 
-cudaError_t launch_qprep(const float* Q, int nq, int d, float* qnorm, int32_t* status, cudaStream_t s) {
+cudaError_t launch_qprep(const float* Q, int nq, int d, int d4, float* qnorm, float* qtf32, int32_t* status,
+                         cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  k_qprep<<<nq, 256, 0, s>>>(Q, d, qnorm, status);
+  k_qprep<<<nq, 256, 0, s>>>(Q, d, d4, qnorm, qtf32, status);
   return cudaGetLastError();
 }
 

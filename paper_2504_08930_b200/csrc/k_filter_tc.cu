@@ -1,0 +1,274 @@
+// k_filter_tc.cu -- K1 coarse filter on the 5th-gen tensor cores (tcgen05).
+//
+// dt[q][l] = ||c_l||^2 - 2 <q~, c~_l>   (the coarse-quantizer contraction,
+// stage 1 of Fig. 2; ||q||^2 is constant per query)
+// with q~, c~ the operands rounded to TF32 (cvt.rna) beforehand, so the
+// tensor core's own input conversion is exact; fp32 accumulation in TMEM.
+//
+// Swap-AB: A = a 128-centroid tile (M = 128, K-major rows of the centroid
+// matrix), B = the query batch (N = up to 256 per accumulator, two
+// accumulators for up to 512 queries), so a small batch still fills the
+// 128-row MMA. Warp roles (192 threads): warp 0 = TMA producer (one elected
+// lane: cp.async.bulk.tensor 2D, SWIZZLE_128B, mbarrier complete_tx),
+// warp 1 = TMEM allocator + MMA issuer (one lane: tcgen05.mma.kind::tf32,
+// tcgen05.commit -> mbarriers), warps 2-5 = epilogue (tcgen05.ld 32x32b,
+// thread i <-> TMEM lane i <-> centroid m0+i; coalesced stores of dt).
+// The error of dt w.r.t. the exact D - ||q||^2 is bounded in DESIGN.md §5
+// (band proof); K2/K3 make the probes exact.
+#include <cuda.h>
+
+#include "vlr_device.cuh"
+#include "vlr_internal.cuh"
+
+namespace vlr {
+
+constexpr int kTcM = 128;        // centroids per tile (MMA M)
+constexpr int kTcBK = 32;        // fp32 elements per K block (128 B = one SW128 row)
+constexpr int kTcThreads = 192;  // 6 warps
+constexpr int kTcMaxStages = 6;
+
+__device__ __forceinline__ uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(b)), "r"(n));
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mb_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(s32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// bounded wait: a pipeline bug traps (CUDA error) instead of hanging the GPU
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  for (uint32_t i = 0; !mb_try(b, parity); ++i)
+    if (i > (1u << 26)) asm volatile("trap;");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          s32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(s32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  // UMMA shared-memory descriptor, K-major SWIZZLE_128B: start>>4, LBO = 1 (unused),
+  // SBO = 1024 B (8 rows x 128 B), version 1 (bits 46-47), layout type 2 (bits 61-63)
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(bar))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_filter_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int L, int nq,
+                int kblocks, int nN, int nacc, int stages, const float* __restrict__ cn2, float* __restrict__ dt) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * kTcM;
+  const int q0 = blockIdx.y * (nN * nacc);
+  const uint32_t bytesA = kTcM * 128, bytesB = (uint32_t)(nacc * nN * 128);
+  const uint32_t stage_bytes = bytesA + bytesB;
+  const int ncols_used = nN * nacc;
+  uint32_t ncols = 32;
+  while ((int)ncols < ncols_used) ncols <<= 1;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    mb_init(&tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tmem_base)), "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tbase = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % stages;
+        const uint32_t ph = (uint32_t)(kb / stages) & 1u;
+        mb_wait(&empty[s], ph ^ 1u);
+        uint8_t* sA = smem + (size_t)s * stage_bytes;
+        uint8_t* sB = sA + bytesA;
+        mb_expect_tx(&full[s], stage_bytes);
+        tma_2d(sA, &tmA, kb * kTcBK, m0, &full[s]);
+        for (int r = 0; r < nacc * nN; r += 256) {
+          tma_2d(sB + (size_t)r * 128, &tmB, kb * kTcBK, q0 + r, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // instruction descriptor: F32 accum, A/B TF32, K-major, N, M = 128
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(nN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % stages;
+        const uint32_t ph = (uint32_t)(kb / stages) & 1u;
+        mb_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t aaddr = s32(smem + (size_t)s * stage_bytes);
+        const uint32_t baddr = aaddr + bytesA;
+#pragma unroll
+        for (int kk = 0; kk < kTcBK / 8; ++kk) {  // K = 8 tf32 (32 B) per MMA
+          const uint64_t ad = sw128_desc(aaddr + kk * 32);
+          for (int acc = 0; acc < nacc; ++acc) {
+            const uint64_t bd = sw128_desc(baddr + (uint32_t)(acc * nN * 128) + kk * 32);
+            mma_tf32(tbase + (uint32_t)(acc * nN), ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+        }
+        mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+      }
+      mma_commit(&tfull);  // accumulator complete
+    }
+    __syncwarp();
+  } else {
+    // epilogue: warps 2..5 -> TMEM lane groups (warp % 4)
+    const int lg = warp & 3;
+    const int row = m0 + lg * 32 + lane;
+    const float cn = row < L ? cn2[row] : 0.f;
+    mb_wait(&tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    for (int c = 0; c < ncols_used; c += 16) {
+      uint32_t v[16];
+      const uint32_t taddr = tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)c;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < L) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int q = q0 + c + j;
+          if (q < nq) dt[(size_t)q * L + row] = cn - 2.f * __uint_as_float(v[j]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D fp32 tensor [rows][cols] (cols = d4, row stride d4*4 B), box {32, box_rows}, SW128
+cudaError_t make_tmap_2d(void* map_, const float* base, int rows, int cols, int box_rows) {
+  CUtensorMap* map = reinterpret_cast<CUtensorMap*>(map_);
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return cudaErrorNotSupported;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, float* dt, cudaStream_t s) {
+  if (nq <= 0) return cudaSuccess;
+  int nacc, nN;
+  if (nq <= 256) {
+    nacc = 1;
+    nN = ((nq + 15) / 16) * 16;
+  } else {
+    nacc = 2;
+    nN = 256;
+  }
+  const int box_rows_b = nN < 256 ? nN : 256;
+  CUtensorMap tmB;
+  cudaError_t e = make_tmap_2d(&tmB, Qt, nq, ix.d4, box_rows_b);
+  if (e != cudaSuccess) return e;
+  const uint32_t stage_bytes = kTcM * 128 + (uint32_t)(nacc * nN * 128);
+  int stages = (int)((200 * 1024) / stage_bytes);
+  if (stages > kTcMaxStages) stages = kTcMaxStages;
+  if (stages < 2) stages = 2;
+  const size_t smem = (size_t)stages * stage_bytes + 1024;
+  static size_t configured = 0;
+  if (smem > configured) {
+    e = cudaFuncSetAttribute(k_filter_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  const int kblocks = (ix.d4 + kTcBK - 1) / kTcBK;
+  dim3 grid((ix.nlist + kTcM - 1) / kTcM, (nq + nN * nacc - 1) / (nN * nacc));
+  k_filter_tc<<<grid, kTcThreads, smem, s>>>(*reinterpret_cast<const CUtensorMap*>(ix.tmapA), tmB, ix.nlist, nq,
+                                              kblocks, nN, nacc, stages, ix.cnorm2, dt);
+  return cudaGetLastError();
+}
+
+// TF32 rounding (round to nearest, ties away: cvt.rna) into a d4-padded copy
+__global__ void k_round_tf32(const float* __restrict__ src, int rows, int d, int d4, float* __restrict__ dst) {
+  const long long n = (long long)rows * d4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / d4;
+    const int c = (int)(i - r * d4);
+    float v = 0.f;
+    if (c < d) {
+      uint32_t t;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(src[r * d + c]));
+      v = __uint_as_float(t);
+    }
+    dst[i] = v;
+  }
+}
+
+cudaError_t launch_round_tf32(const float* src, int rows, int d, int d4, float* dst, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  long long n = (long long)rows * d4;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_round_tf32<<<(int)blocks, 256, 0, s>>>(src, rows, d, d4, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace vlr

@@ -79,34 +79,70 @@ cudaError_t launch_route(const DeviceIndex& ix, const Workspace& ws, int nq, int
 }
 
 // ----------------------------------------------------------------- K5 LUT
-__global__ void __launch_bounds__(256) k_lut(const float* __restrict__ Q, int d, int m, int dsub,
+// grid (npairs * 4 code quarters, ceil(nq / kLutQB)); 256 threads = 4 codes x
+// 64 sub-spaces (jj fastest -> coalesced LUT rows). Each thread keeps its
+// codeword y_{j,c} in registers and reuses it for kLutQB queries, whose
+// sub-vectors sit in shared memory padded to dsub+1 per sub-space (bank-
+// conflict-free across the 64 sub-spaces of a warp).
+constexpr int kLutQB = 8;
+constexpr int kLutMaxDsub = 32;
+
+__global__ void __launch_bounds__(256) k_lut(const float* __restrict__ Q, int nq, int d, int m, int dsub,
                                              const float* __restrict__ Y, int npairs, float* __restrict__ lut) {
-  const int q = blockIdx.x, pair = blockIdx.y;
-  extern __shared__ float qs[];
-  for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = Q[(size_t)q * d + t];
-  __syncthreads();
-  float* out = lut + ((size_t)q * npairs + pair) * (256 * 64);
-  const int jj = threadIdx.x & 63;
+  extern __shared__ float qs[];  // [kLutQB][64 * (dsub + 1)]
+  const int pair = blockIdx.x >> 2, cq = blockIdx.x & 3;
+  const int q0 = blockIdx.y * kLutQB;
+  const int jj = threadIdx.x & 63, cs = threadIdx.x >> 6;
   const int j = pair * 64 + jj;
-  for (int c = threadIdx.x >> 6; c < 256; c += 4) {
+  const int jv = min(64, m - pair * 64);  // valid sub-spaces of this pair (>= 1)
+  const int row = jv * (dsub + 1);
+  for (int i = threadIdx.x; i < kLutQB * jv * dsub; i += blockDim.x) {
+    const int qq = i / (jv * dsub), r = i - qq * jv * dsub;
+    const int jl = r / dsub, u = r - jl * dsub;
+    const int jg = pair * 64 + jl;
     float v = 0.f;
+    if (q0 + qq < nq) v = Q[(size_t)(q0 + qq) * d + jg * dsub + u];
+    qs[qq * row + jl * (dsub + 1) + u] = v;
+  }
+  __syncthreads();
+  const int nqb = min(kLutQB, nq - q0);
+  for (int c = cq * 64 + cs; c < cq * 64 + 64; c += 4) {
+    float acc[kLutQB];
+#pragma unroll
+    for (int qq = 0; qq < kLutQB; ++qq) acc[qq] = 0.f;
     if (j < m) {
       const float* y = Y + ((size_t)j * 256 + c) * dsub;
-      const float* qq = qs + j * dsub;
-      float dot = 0.f;
-      for (int u = 0; u < dsub; ++u) dot = fmaf(qq[u], __ldg(y + u), dot);
-      v = -2.f * dot;
+      for (int u0 = 0; u0 < dsub; u0 += kLutMaxDsub) {
+        float yr[kLutMaxDsub];
+#pragma unroll
+        for (int u = 0; u < kLutMaxDsub; ++u) yr[u] = (u0 + u < dsub) ? __ldg(y + u0 + u) : 0.f;
+#pragma unroll
+        for (int qq = 0; qq < kLutQB; ++qq) {
+          const float* qv = qs + qq * row + jj * (dsub + 1) + u0;
+          float a = acc[qq];
+#pragma unroll
+          for (int u = 0; u < kLutMaxDsub; ++u)
+            if (u0 + u < dsub) a = fmaf(qv[u], yr[u], a);
+          acc[qq] = a;
+        }
+      }
     }
-    out[c * 64 + jj] = v;
+    for (int qq = 0; qq < nqb; ++qq)
+      lut[(((size_t)(q0 + qq) * npairs + pair) * 256 + c) * 64 + jj] = -2.f * acc[qq];
   }
 }
 
 cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  dim3 grid(nq, ix.npairs);
-  const size_t sm = (size_t)ix.d * sizeof(float);
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_lut<<<grid, 256, sm, s>>>(Q, ix.d, ix.m, ix.dsub, ix.codebooks, ix.npairs, ws.lut);
+  dim3 grid(ix.npairs * 4, (nq + kLutQB - 1) / kLutQB);
+  const size_t sm = (size_t)kLutQB * (ix.m < 64 ? ix.m : 64) * (ix.dsub + 1) * sizeof(float);
+  static size_t configured = 0;
+  if (sm > 48 * 1024 && sm > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = sm;
+  }
+  k_lut<<<grid, 256, sm, s>>>(Q, nq, ix.d, ix.m, ix.dsub, ix.codebooks, ix.npairs, ws.lut);
   return cudaGetLastError();
 }
 

@@ -41,12 +41,14 @@ void set_error(const std::string& msg);
 
 // ---------------------------------------------------------------- device data
 struct DeviceIndex {
-  int d = 0, nlist = 0, m = 0, mpad = 0, npairs = 0, dsub = 0;
+  int d = 0, d4 = 0, nlist = 0, m = 0, mpad = 0, npairs = 0, dsub = 0;
   int rank = 0, world = 1, device = 0;
   bool shard_only = false;
   // replicated, coarse quantizer
   float* centroids = nullptr;  // [nlist][d]
   float* cnorm2 = nullptr;     // [nlist] ||c||^2 (fp64 -> fp32)
+  float* ctf32 = nullptr;      // [nlist][d4] centroids rounded to TF32 (cvt.rna), zero-padded to d4
+  alignas(64) unsigned char tmapA[128] = {};  // CUtensorMap of ctf32 (box 32 x 128, SWIZZLE_128B)
   float cmax = 0.f;            // max ||c|| (host), for the filter band
   float* codebooks = nullptr;  // [m][256][dsub]
   int32_t* owner = nullptr;    // [nlist] owner rank or -1 (mapping table)
@@ -66,6 +68,7 @@ struct DeviceIndex {
 struct Workspace {
   int cap_nq = 0, cap_np = 0, cap_k = 0, n_cta = 0;
   float* qnorm = nullptr;      // [nq] ||q|| (fp32)
+  float* qtf32 = nullptr;      // [nq][d4] queries rounded to TF32, zero-padded
   float* dt = nullptr;         // [nq][nlist] filter distances ||c||^2 - 2<q,c>
   int32_t* cand = nullptr;     // [nq][kCandCap]
   int32_t* ncand = nullptr;    // [nq]
@@ -95,7 +98,9 @@ struct vlr_index {
   vlr::DeviceIndex ix;
   vlr::Workspace ws;
   bool profiling = false;
-  cudaEvent_t ev[9] = {};
+  static constexpr int kRing = 64;
+  cudaEvent_t ev[kRing][9] = {};
+  int64_t nsearch = 0;       // searches recorded while profiling
   int launches = 0;
   bool dead = false;  // NCCL failure
   std::string last_err;
@@ -109,8 +114,12 @@ cudaError_t launch_layout(const DeviceIndex& ix, const uint8_t* stage_codes, con
                           const int64_t* vbase, const int32_t* lglob, cudaStream_t s);
 cudaError_t launch_cnorm(const DeviceIndex& ix, cudaStream_t s);
 // stage 0..2 coarse quantizer
-cudaError_t launch_qprep(const float* Q, int nq, int d, float* qnorm, int32_t* status, cudaStream_t s);
+cudaError_t launch_qprep(const float* Q, int nq, int d, int d4, float* qnorm, float* qtf32, int32_t* status,
+                         cudaStream_t s);
 cudaError_t launch_filter_simt(const float* Q, int nq, const DeviceIndex& ix, float* dt, cudaStream_t s);
+cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, float* dt, cudaStream_t s);
+cudaError_t launch_round_tf32(const float* src, int rows, int d, int d4, float* dst, cudaStream_t s);
+cudaError_t make_tmap_2d(void* map, const float* base, int rows, int cols, int box_rows);
 cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float band_rel,
                           cudaStream_t s);
 cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, int np,
