@@ -155,7 +155,9 @@ def barrier(world):
 
 
 def gen_index(c, seed, rank, world, hot=None):
-    """Generate this rank's shard of the synthetic index on the GPU (TOOLING)."""
+    """Generate this rank's shard of the synthetic index on the GPU (TOOLING).
+    VLR_GEN_CACHE=<dir> reuses arrays saved by an earlier process of the same
+    command sequence (never relied on for timing: only generation time)."""
     import datagen
     sizes = datagen.list_sizes(c["N"], c["nlist"], seed)
     owned = None
@@ -163,7 +165,22 @@ def gen_index(c, seed, rank, world, hot=None):
         own = datagen.deal_owners(sizes, np.arange(c["nlist"]) if hot is None else hot, world)
         owned = own == rank
     t = time.time()
+    cache = os.environ.get("VLR_GEN_CACHE")
+    key = f"{c['N']}_{c['d']}_{c['nlist']}_{c['m']}_{seed}_{world}_{rank}_{'all' if hot is None else len(hot)}"
+    if cache:
+        path = os.path.join(cache, key)
+        if os.path.exists(os.path.join(path, "done")):
+            f = {n: np.load(os.path.join(path, n + ".npy"), mmap_mode="r") for n in
+                 ("centroids", "codebooks", "list_offsets", "ids", "codes")}
+            ix = datagen.IndexArrays(d=c["d"], nlist=c["nlist"], m=c["m"], seed=seed,
+                                     **{n: np.ascontiguousarray(v) for n, v in f.items()})
+            return ix, time.time() - t
     ix = datagen.make_index(c["N"], c["d"], c["nlist"], c["m"], seed=seed, device="cuda", owned=owned)
+    if cache:
+        os.makedirs(path, exist_ok=True)
+        for n in ("centroids", "codebooks", "list_offsets", "ids", "codes"):
+            np.save(os.path.join(path, n + ".npy"), getattr(ix, n))
+        open(os.path.join(path, "done"), "w").close()
     return ix, time.time() - t
 
 

@@ -47,7 +47,7 @@ __global__ void k_negative(const int64_t* ids, long long n, int32_t* flag) {
 }
 
 static void free_ws(Workspace& w) {
-  void* ps[] = {w.qnorm, w.qtf32, w.dt, w.cand, w.ncand, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.lut,
+  void* ps[] = {w.qnorm, w.qtf32, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.lut,
                 w.pdist, w.pid, w.send, w.recv, w.d_q, w.d_ids, w.d_dist, w.d_miss, w.d_probes, w.status};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -80,13 +80,17 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   VLR_CUDA_TRY(dalloc(&w.qnorm, nqs));
   VLR_CUDA_TRY(dalloc(&w.qtf32, nqs * ix.d4));
   VLR_CUDA_TRY(dalloc(&w.dt, nqs * ix.nlist));
+  VLR_CUDA_TRY(dalloc(&w.gmin, nqs * ((ix.nlist + 31) / 32)));
   VLR_CUDA_TRY(dalloc(&w.cand, nqs * kCandCap));
   VLR_CUDA_TRY(dalloc(&w.ncand, nqs));
+  VLR_CUDA_TRY(dalloc(&w.exact, nqs * kCandCap));
   VLR_CUDA_TRY(dalloc(&w.bound, nqs));
   VLR_CUDA_TRY(dalloc(&w.probes, nqs * cnp));
   VLR_CUDA_TRY(dalloc(&w.term1, nqs * cnp));
   VLR_CUDA_TRY(dalloc(&w.plocal, nqs * cnp));
   VLR_CUDA_TRY(dalloc(&w.item_off, nqs * cnp + 1));
+  VLR_CUDA_TRY(dalloc(&w.item_local, nqs * cnp));
+  VLR_CUDA_TRY(dalloc(&w.qtot, nqs));
   VLR_CUDA_TRY(dalloc(&w.lut, nqs * ix.npairs * (kLutPairBytes / 4)));
   const size_t nslots = ((size_t)w.n_cta + nqs) * kScanWarps * ck;
   VLR_CUDA_TRY(dalloc(&w.pdist, nslots));
@@ -393,13 +397,14 @@ vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t np
   int n = 0;
   rec(h, 0, s);
   VLR_CUDA_TRY(launch_qprep(Q, nq, ix.d, ix.d4, w.qnorm, w.qtf32, w.status, s)); ++n;
-  VLR_CUDA_TRY(launch_filter_tc(w.qtf32, nq, ix, w.dt, s)); ++n;
+  VLR_CUDA_TRY(launch_filter_tc(w.qtf32, nq, ix, w.dt, w.gmin, s)); ++n;
   rec(h, 1, s);
   VLR_CUDA_TRY(launch_select(ix, w, nq, np, filter_edot(ix.d), s)); ++n;
   rec(h, 2, s);
-  VLR_CUDA_TRY(launch_refine(Q, ix, w, nq, np, s)); ++n;
+  VLR_CUDA_TRY(launch_exact(Q, ix, w, nq, s)); ++n;
+  VLR_CUDA_TRY(launch_refine(Q, ix, w, nq, np, out_miss, out_probes, s)); ++n;
   rec(h, 3, s);
-  VLR_CUDA_TRY(launch_route(ix, w, nq, np, out_miss, out_probes, s)); ++n;
+  VLR_CUDA_TRY(launch_offsets(w, nq, np, s)); ++n;
   rec(h, 4, s);
   VLR_CUDA_TRY(launch_lut(Q, ix, w, nq, s)); ++n;
   rec(h, 5, s);

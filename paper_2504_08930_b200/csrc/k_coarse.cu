@@ -2,9 +2,8 @@
 // PAPER.md:117, :147): which nprobe clusters each query visits.
 //
 //  qprep   : ||q|| per query, non-finite check (status bit 0).
-//  K1 simt : filter distances dt[q][l] = ||c_l||^2 - 2<q, c_l> (fp32 FMA).
-//            (The tcgen05 TF32 filter in k_filter_tc.cu computes the same
-//            quantity on the tensor cores.)
+//  (K1, the filter dt[q][l] = ||c_l||^2 - 2<q~, c~_l> on the tcgen05 tensor
+//   cores, is in k_filter_tc.cu.)
 //  K2      : theta~ = nprobe'-th smallest dt (radix select), candidate set
 //            {l : dt <= theta~ + 2 Delta*} (DESIGN.md §K1-K3 band proof).
 //  K3      : exact fp64 D = sum_t (q_t - c_t)^2 in dimension order with
@@ -56,123 +55,77 @@ cudaError_t launch_qprep(const float* Q, int nq, int d, int d4, float* qnorm, fl
   return cudaGetLastError();
 }
 
-// ----------------------------------------------------------------- K1 (SIMT)
-// 64 queries x 64 centroids per CTA, 256 threads, 4x4 outputs each, BK = 16.
-constexpr int FB = 64, FK = 16;
-__global__ void __launch_bounds__(256) k_filter_simt(const float* __restrict__ Q, int nq, const float* __restrict__ C,
-                                                     const float* __restrict__ cn2, int L, int d,
-                                                     float* __restrict__ dt) {
-  __shared__ float sq[FK][FB + 4];
-  __shared__ float sc[FK][FB + 4];
-  const int q0 = blockIdx.y * FB, l0 = blockIdx.x * FB;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float acc[4][4] = {};
-  for (int k0 = 0; k0 < d; k0 += FK) {
-    for (int i = threadIdx.x; i < FB * FK; i += 256) {
-      int r = i / FK, c = i % FK;
-      int gq = q0 + r, gl = l0 + r, gk = k0 + c;
-      sq[c][r] = (gq < nq && gk < d) ? Q[(size_t)gq * d + gk] : 0.f;
-      sc[c][r] = (gl < L && gk < d) ? C[(size_t)gl * d + gk] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < FK; ++kk) {
-      float a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = sq[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = sc[kk][tx * 4 + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int gq = q0 + ty * 4 + i;
-    if (gq >= nq) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int gl = l0 + tx * 4 + j;
-      if (gl < L) dt[(size_t)gq * L + gl] = cn2[gl] - 2.f * acc[i][j];
-    }
-  }
-}
-
-cudaError_t launch_filter_simt(const float* Q, int nq, const DeviceIndex& ix, float* dt, cudaStream_t s) {
-  if (nq <= 0) return cudaSuccess;
-  dim3 grid((ix.nlist + FB - 1) / FB, (nq + FB - 1) / FB);
-  k_filter_simt<<<grid, 256, 0, s>>>(Q, nq, ix.centroids, ix.cnorm2, ix.nlist, ix.d, dt);
-  return cudaGetLastError();
-}
-
 // ----------------------------------------------------------------- K2 select
-// One CTA (1024 threads) per query. Radix select (4 x 8-bit digits) of the
-// np-th smallest order key, then the band bound and candidate compaction.
-__global__ void __launch_bounds__(1024) k_select(const float* __restrict__ dt, int L, int np,
-                                                 const float* __restrict__ qnorm, float cmax, float e_dot,
-                                                 int32_t* __restrict__ cand, int32_t* __restrict__ ncand,
-                                                 float* __restrict__ bound_out) {
+// One CTA per query. theta' = the np-th smallest of the 32-centroid group
+// minima written by K1 (a subset order statistic, so theta' >= theta~, the
+// np-th smallest filter value), found by a bitonic sort in
+// shared memory; if there are fewer groups than np, theta' = +inf (every
+// centroid is a candidate). Then one coalesced pass over the filter row
+// compacts {l : dt[l] <= theta' + 2 Delta*}.
+constexpr int kSelThreads = 1024;
+constexpr int kSelMaxGroups = 16384;  // nlist <= 512K for the sorted-minima path
+
+__global__ void __launch_bounds__(kSelThreads) k_select(const float* __restrict__ dt, const float* __restrict__ gmin,
+                                                        int L, int np, const float* __restrict__ qnorm, float cmax,
+                                                        float e_dot, int32_t* __restrict__ cand,
+                                                        int32_t* __restrict__ ncand, float* __restrict__ bound_out) {
+  extern __shared__ unsigned skeys[];
+  __shared__ unsigned s_cnt;
   const int q = blockIdx.x;
-  const float* row = dt + (size_t)q * L;
-  __shared__ unsigned hist[256];
-  __shared__ unsigned s_prefix, s_want, s_cnt;
-  unsigned prefix = 0u, mask = 0u, want = (unsigned)np;
   const int lane = threadIdx.x & 31;
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
-    __syncthreads();
-    for (int i0 = 0; i0 < L; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      bool act = false;
-      unsigned bin = 0u;
-      if (i < L) {
-        unsigned key = fkey(row[i]);
-        act = (key & mask) == prefix;
-        bin = (key >> shift) & 255u;
-      }
-      // warp-aggregated histogram update
-      const unsigned am = __ballot_sync(kFull, act);
-      if (act) {
-        const unsigned peers = __match_any_sync(am, bin);
-        if (lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned)__popc(peers));
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      // lane handles bins [8*lane, 8*lane+8): find the bin holding the want-th key
-      unsigned loc[8], tot = 0u;
-#pragma unroll
-      for (int b = 0; b < 8; ++b) { loc[b] = hist[lane * 8 + b]; tot += loc[b]; }
-      unsigned incl = tot;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        unsigned v = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const unsigned excl = incl - tot;
-      if (excl < want && want <= incl) {
-        unsigned c = excl;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          if (c < want && want <= c + loc[b]) {
-            s_prefix = prefix | ((unsigned)(lane * 8 + b) << shift);
-            s_want = want - c;
-          }
-          c += loc[b];
+  const int ng = (L + 31) / 32;
+  float theta = CUDART_INF_F;
+  if (ng >= np && ng <= kSelMaxGroups) {
+    // radix select (4 x 8-bit digits) of the np-th smallest group minimum
+    __shared__ unsigned hist[256];
+    __shared__ unsigned s_prefix, s_want;
+    for (int i = threadIdx.x; i < ng; i += blockDim.x) skeys[i] = fkey(gmin[(size_t)q * ng + i]);
+    unsigned prefix = 0u, mask = 0u, want = (unsigned)np;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
+      __syncthreads();
+      for (int i0 = 0; i0 < ng; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        const unsigned key = i < ng ? skeys[i] : 0u;
+        const bool act = i < ng && (key & mask) == prefix;
+        const unsigned bin = (key >> shift) & 255u;
+        const unsigned am = __ballot_sync(kFull, act);
+        if (act) {
+          const unsigned peers = __match_any_sync(am, bin);
+          if (lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned)__popc(peers));
         }
       }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        unsigned loc[8], tot = 0u;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) { loc[b] = hist[lane * 8 + b]; tot += loc[b]; }
+        unsigned incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned v = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const unsigned excl = incl - tot;
+        if (excl < want && want <= incl) {
+          unsigned c = excl;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            if (c < want && want <= c + loc[b]) {
+              s_prefix = prefix | ((unsigned)(lane * 8 + b) << shift);
+              s_want = want - c;
+            }
+            c += loc[b];
+          }
+        }
+      }
+      __syncthreads();
+      prefix = s_prefix;
+      want = s_want;
+      mask |= 255u << shift;
     }
-    __syncthreads();
-    prefix = s_prefix;
-    want = s_want;
-    mask |= 255u << shift;
-    __syncthreads();
+    theta = fkey_inv(prefix);
   }
-  const float theta = fkey_inv(prefix);
-  // band (Appendix A of SURVEY / DESIGN §K1-K3): Delta* bounds |dt - (D - ||q||^2)|
   const float qn = qnorm[q];
   const float u = 5.9604645e-8f;  // 2^-24
   const float delta = 2.0f * (2.0f * (e_dot + 2.0f * u) * qn * cmax + 4.0f * u * (cmax * cmax + qn * qn));
@@ -182,17 +135,35 @@ __global__ void __launch_bounds__(1024) k_select(const float* __restrict__ dt, i
     bound_out[q] = bnd;
   }
   __syncthreads();
+  const float* row = dt + (size_t)q * L;
   int32_t* out = cand + (size_t)q * kCandCap;
-  for (int i0 = 0; i0 < L; i0 += blockDim.x) {
-    const int i = i0 + threadIdx.x;
-    const bool keep = i < L && row[i] <= bnd;
+  auto emit = [&](bool keep, int i) {
     const unsigned km = __ballot_sync(kFull, keep);
+    if (km == 0u) return;
     unsigned base = 0u;
-    if (lane == 0 && km) base = atomicAdd(&s_cnt, (unsigned)__popc(km));
+    if (lane == 0) base = atomicAdd(&s_cnt, (unsigned)__popc(km));
     base = __shfl_sync(kFull, base, 0);
     if (keep) {
       const unsigned pos = base + __popc(km & ((1u << lane) - 1u));
       if (pos < (unsigned)kCandCap) out[pos] = i;
+    }
+  };
+  if ((L & 3) == 0) {
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    for (int i0 = 0; i0 < L / 4; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      const bool in = i < L / 4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (in) v = __ldg(r4 + i);
+      emit(in && v.x <= bnd, 4 * i);
+      emit(in && v.y <= bnd, 4 * i + 1);
+      emit(in && v.z <= bnd, 4 * i + 2);
+      emit(in && v.w <= bnd, 4 * i + 3);
+    }
+  } else {
+    for (int i0 = 0; i0 < L; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      emit(i < L && row[i] <= bnd, i);
     }
   }
   __syncthreads();
@@ -201,36 +172,33 @@ __global__ void __launch_bounds__(1024) k_select(const float* __restrict__ dt, i
 
 cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float e_dot, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  k_select<<<nq, 1024, 0, s>>>(ws.dt, ix.nlist, np, ws.qnorm, ix.cmax, e_dot, ws.cand, ws.ncand, ws.bound);
+  const int ng = (ix.nlist + 31) / 32;
+  int n2 = 1;
+  while (n2 < ng) n2 <<= 1;
+  const size_t sm = ng <= kSelMaxGroups ? (size_t)ng * sizeof(unsigned) : 0;
+  static size_t configured = 0;
+  if (sm > 48 * 1024 && sm > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = sm;
+  }
+  k_select<<<nq, kSelThreads, sm, s>>>(ws.dt, ws.gmin, ix.nlist, np, ws.qnorm, ix.cmax, e_dot, ws.cand, ws.ncand,
+                                       ws.bound);
   return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------- K3 refine
-constexpr int kRefineThreads = 256;
+// One CTA (16 warps) per query. Candidate ids are gathered in chunks of up to
+// kRefineChunk; a warp takes 32 candidates at a time (lane l <-> candidate l)
+// and streams their centroid rows through shared memory in 32-dimension tiles
+// (cp.async, double-buffered, 16-B chunks XOR-swizzled by row so the per-lane
+// LDS.128 of a row is conflict-free). Each lane then runs its candidate's
+// exact fp64 sum in dimension order; the chunk is merged with the running best
+// nprobe' by a bitonic sort on (D, l).
+constexpr int kRefineThreads = 512;
+constexpr int kRefineWarps = kRefineThreads / 32;
+constexpr int kRescanWarps = 8;  // warps computing exact distances on the (rare) overflow path
 constexpr int kSortCap = 2048;  // >= kMaxNprobe + kRefineChunk
-
-__device__ __forceinline__ double exact_coarse(const float* __restrict__ qs, const float* __restrict__ c, int d) {
-  // D = sum_{t=0}^{d-1} (q_t - c_t)^2, left to right, each op correctly rounded
-  double s = 0.0;
-  int t = 0;
-  if ((d & 3) == 0) {
-    const float4* c4 = reinterpret_cast<const float4*>(c);
-    for (; t < d; t += 4) {
-      const float4 v = __ldg(c4 + (t >> 2));
-      double e;
-      e = __dsub_rn((double)qs[t + 0], (double)v.x); s = __dadd_rn(s, __dmul_rn(e, e));
-      e = __dsub_rn((double)qs[t + 1], (double)v.y); s = __dadd_rn(s, __dmul_rn(e, e));
-      e = __dsub_rn((double)qs[t + 2], (double)v.z); s = __dadd_rn(s, __dmul_rn(e, e));
-      e = __dsub_rn((double)qs[t + 3], (double)v.w); s = __dadd_rn(s, __dmul_rn(e, e));
-    }
-  } else {
-    for (; t < d; ++t) {
-      const double e = __dsub_rn((double)qs[t], (double)__ldg(c + t));
-      s = __dadd_rn(s, __dmul_rn(e, e));
-    }
-  }
-  return s;
-}
 
 __device__ __forceinline__ bool key_less(double a, int ia, double b, int ib) {
   return a < b || (a == b && ia < ib);
@@ -258,26 +226,168 @@ __device__ void bitonic_sort(double* key, int* id, int n) {
   __syncthreads();
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// exact D for 32 candidates of a warp (lane <-> rows[lane]); buf = S x 32 x 32
+// floats. Tiles of 32 dimensions are streamed with cp.async S-1 tiles ahead;
+// the 16-B chunks of row r are XOR-swizzled by (r & 7) so that lane r's
+// LDS.128 of its own row are conflict-free.
+template <int S>
+__device__ double warp_exact(const double* __restrict__ qs, const float* __restrict__ C, int d, int row_id,
+                             float* buf, int lane) {
+  double s = 0.0;
+  const int ntile = d >> 5;  // full 32-dim tiles (d % 4 == 0 guaranteed by the caller for ntile > 0)
+  // this lane copies 8 of the tile's 256 16-byte chunks: (row r, chunk k) for
+  // idx = i*32 + lane; source pointers and swizzled destinations are fixed
+  // for the whole task, only the tile offset moves
+  const float* src[8];
+  uint32_t dst[8];
+  const uint32_t buf_s = (uint32_t)__cvta_generic_to_shared(buf);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int idx = i * 32 + lane;
+    const int r = idx >> 3, k = idx & 7;
+    src[i] = C + (size_t)__shfl_sync(kFull, row_id, r) * d + 4 * k;
+    dst[i] = buf_s + (uint32_t)(r * 32 + ((k ^ (r & 7)) << 2)) * 4u;
+  }
+  auto issue = [&](int tile) {
+    if (tile < ntile) {
+      const uint32_t so = (uint32_t)(tile % S) * 4096u;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst[i] + so), "l"(src[i] + tile * 32)
+                     : "memory");
+    }
+    cp_async_commit();  // (possibly empty) group keeps the wait count uniform
+  };
+#pragma unroll
+  for (int t = 0; t < S - 1; ++t) issue(t);
+  for (int tile = 0; tile < ntile; ++tile) {
+    issue(tile + S - 1);
+    cp_async_wait<S - 1>();
+    __syncwarp();
+    const float* rowp = buf + (tile % S) * 1024 + lane * 32;
+    const double2* qt = reinterpret_cast<const double2*>(qs + tile * 32);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 v = *reinterpret_cast<const float4*>(rowp + ((k ^ (lane & 7)) << 2));
+      const double2 qa = qt[2 * k], qb = qt[2 * k + 1];
+      double e;
+      e = __dsub_rn(qa.x, (double)v.x); s = __dadd_rn(s, __dmul_rn(e, e));
+      e = __dsub_rn(qa.y, (double)v.y); s = __dadd_rn(s, __dmul_rn(e, e));
+      e = __dsub_rn(qb.x, (double)v.z); s = __dadd_rn(s, __dmul_rn(e, e));
+      e = __dsub_rn(qb.y, (double)v.w); s = __dadd_rn(s, __dmul_rn(e, e));
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  for (int t = ntile * 32; t < d; ++t) {  // tail dimensions, still in order
+    const double e = __dsub_rn(qs[t], (double)__ldg(C + (size_t)row_id * d + t));
+    s = __dadd_rn(s, __dmul_rn(e, e));
+  }
+  return s;
+}
+
+__device__ __forceinline__ double scalar_exact(const double* __restrict__ qs, const float* __restrict__ C, int d,
+                                               int row_id) {
+  double s = 0.0;
+  for (int t = 0; t < d; ++t) {
+    const double e = __dsub_rn(qs[t], (double)__ldg(C + (size_t)row_id * d + t));
+    s = __dadd_rn(s, __dmul_rn(e, e));
+  }
+  return s;
+}
+
+// K3a: exact fp64 D of every listed candidate, 4 warps per CTA, warp <-> 32
+// candidates of one query; grid (nq, kCandCap / 128). CTAs past the query's
+// candidate count (or queries whose list overflowed) exit at once.
+constexpr int kExactWarps = 4;
+constexpr int kExactStages = 4;
+
+__global__ void __launch_bounds__(kExactWarps * 32) k_exact(const float* __restrict__ Q, const float* __restrict__ C,
+                                                            int d, const int32_t* __restrict__ cand,
+                                                            const int32_t* __restrict__ ncand,
+                                                            double* __restrict__ exact) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int q = blockIdx.x;
+  const int nc = ncand[q];
+  const int g0 = blockIdx.y * kExactWarps * 32;
+  if (nc > kCandCap || g0 >= nc) return;
+  double* qs = reinterpret_cast<double*>(sm);
+  float* tiles = reinterpret_cast<float*>(qs + ((d + 1) & ~1));
+  for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = (double)Q[(size_t)q * d + t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int32_t* lst = cand + (size_t)q * kCandCap;
+  // groups of 32 candidates: this warp takes g = g0 + 32*warp + stride*i
+  const int stride = gridDim.y * kExactWarps * 32;
+  for (int g = g0 + warp * 32; g < nc; g += stride) {
+    const int j = g + lane;
+    const int rid = lst[j < nc ? j : g];
+    double D;
+    if ((d & 3) == 0)
+      D = warp_exact<kExactStages>(qs, C, d, rid, tiles + warp * (kExactStages * 1024), lane);
+    else
+      D = scalar_exact(qs, C, d, rid);
+    if (j < nc) exact[(size_t)q * kCandCap + j] = D;
+  }
+}
+
+size_t exact_smem(int d) {
+  return (size_t)((d + 1) & ~1) * sizeof(double) + (size_t)kExactWarps * kExactStages * 1024 * sizeof(float);
+}
+
+cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
+  if (nq <= 0) return cudaSuccess;
+  const size_t sm = exact_smem(ix.d);
+  static size_t configured = 0;
+  if (sm > 48 * 1024 && sm > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = sm;
+  }
+  dim3 grid(nq, 8);  // 8 x 4 warps; queries with > 1024 candidates loop
+  k_exact<<<grid, kExactWarps * 32, sm, s>>>(Q, ix.centroids, ix.d, ws.cand, ws.ncand, ws.exact);
+  return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restrict__ Q, const float* __restrict__ C,
                                                            int d, int L, int np, const float* __restrict__ dt,
                                                            const int32_t* __restrict__ cand,
                                                            const int32_t* __restrict__ ncand,
                                                            const float* __restrict__ bound,
-                                                           int32_t* __restrict__ probes, float* __restrict__ term1) {
+                                                           const double* __restrict__ exact,
+                                                           int32_t* __restrict__ probes, float* __restrict__ term1,
+                                                           int rank, const int32_t* __restrict__ owner,
+                                                           const int32_t* __restrict__ local,
+                                                           const int64_t* __restrict__ gbase, uint8_t* __restrict__ miss,
+                                                           int32_t* __restrict__ probes_out,
+                                                           int32_t* __restrict__ plocal,
+                                                           int64_t* __restrict__ item_local,
+                                                           int64_t* __restrict__ qtot) {
   extern __shared__ __align__(16) unsigned char sm[];
-  double* key = reinterpret_cast<double*>(sm);             // [kSortCap]
-  int* id = reinterpret_cast<int*>(key + kSortCap);        // [kSortCap]
-  int* lbuf = id + kSortCap;                               // [kRefineChunk]
-  float* qs = reinterpret_cast<float*>(lbuf + kRefineChunk);  // [d]
+  float* tiles = reinterpret_cast<float*>(sm);                        // [kRescanWarps][2][32][32]
+  double* key = reinterpret_cast<double*>(tiles + kRescanWarps * 2048);  // [kSortCap]
+  int* id = reinterpret_cast<int*>(key + kSortCap);                   // [kSortCap]
+  int* lbuf = id + kSortCap;                                          // [kRefineChunk]
+  double* qs = reinterpret_cast<double*>(lbuf + kRefineChunk);        // [d]
   __shared__ int s_cnt;
   const int q = blockIdx.x;
-  for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = Q[(size_t)q * d + t];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = (double)Q[(size_t)q * d + t];
   const int nc = ncand[q];
   const bool listed = nc <= kCandCap;
   const int src_len = listed ? nc : L;
   const float bnd = bound[q];
   const int32_t* lst = cand + (size_t)q * kCandCap;
   const float* row = dt + (size_t)q * L;
+  const bool vec_ok = (d & 3) == 0;
   int nbest = 0;
   int pos = 0;
   __syncthreads();
@@ -301,11 +411,24 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
     }
     __syncthreads();
     const int cnt = s_cnt;
-    // exact distances
-    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-      const int l = lbuf[j];
-      key[nbest + j] = exact_coarse(qs, C + (size_t)l * d, d);
-      id[nbest + j] = l;
+    // exact distances: precomputed by K3a for listed candidates; the overflow
+    // (rescan) path computes them here, 32 candidates per warp pass
+    if (listed) {
+      const double* ex = exact + (size_t)q * kCandCap + (pos - cnt);
+      for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+        key[nbest + j] = ex[j];
+        id[nbest + j] = lbuf[j];
+      }
+    } else {
+      for (int g = warp * 32; warp < kRescanWarps && g < cnt; g += kRescanWarps * 32) {
+        const int j = g + lane;
+        const int rid = j < cnt ? lbuf[j] : lbuf[g];
+        const double dsum = vec_ok ? warp_exact<2>(qs, C, d, rid, tiles + warp * 2048, lane) : scalar_exact(qs, C, d, rid);
+        if (j < cnt) {
+          key[nbest + j] = dsum;
+          id[nbest + j] = rid;
+        }
+      }
     }
     const int tot = nbest + cnt;
     int n2 = 1;
@@ -317,29 +440,69 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
     bitonic_sort(key, id, n2);
     nbest = min(np, tot);
   }
-  for (int p = threadIdx.x; p < np; p += blockDim.x) {
-    // nbest == np whenever the candidate set holds >= np clusters (always: the band
-    // contains the np smallest); defensive -1 otherwise
-    probes[(size_t)q * np + p] = p < nbest ? id[p] : -1;
-    term1[(size_t)q * np + p] = p < nbest ? __double2float_rn(key[p]) : CUDART_INF_F;
+  // ---- router epilogue (K4 fused): mask, owned work items
+  // and their within-query prefix (groups of 32 vectors); K4b adds the
+  // query bases. Items p of this query are handled 2 per thread in order.
+  __shared__ long long s_wsum[kRefineWarps];
+  long long g2[2] = {0, 0};
+  const int p0 = 2 * threadIdx.x;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int p = p0 + h;
+    if (p < np) {
+      // nbest == np whenever the candidate set holds >= np clusters (always: the
+      // band contains the np smallest)
+      const int l = p < nbest ? id[p] : -1;
+      const size_t o = (size_t)q * np + p;
+      probes[o] = l;
+      term1[o] = p < nbest ? __double2float_rn(key[p]) : CUDART_INF_F;
+      const int own = l >= 0 ? owner[l] : -1;
+      miss[o] = own < 0 ? 1 : 0;
+      if (probes_out) probes_out[o] = l;
+      const int loc = (own == rank) ? local[l] : -1;
+      plocal[o] = loc;
+      if (loc >= 0) g2[h] = gbase[loc + 1] - gbase[loc];
+    }
   }
+  const long long mine = g2[0] + g2[1];
+  long long incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long v = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  long long wbase = 0, total = 0;
+  for (int w = 0; w < kRefineWarps; ++w) {
+    const long long v = s_wsum[w];
+    if (w < warp) wbase += v;
+    total += v;
+  }
+  const long long ex = wbase + incl - mine;
+  if (p0 < np) item_local[(size_t)q * np + p0] = ex;
+  if (p0 + 1 < np) item_local[(size_t)q * np + p0 + 1] = ex + g2[0];
+  if (threadIdx.x == 0) qtot[q] = total;
 }
 
 size_t refine_smem(int d) {
-  return (size_t)kSortCap * (sizeof(double) + sizeof(int)) + kRefineChunk * sizeof(int) + (size_t)d * sizeof(float);
+  return (size_t)kRescanWarps * 2048 * sizeof(float) + (size_t)kSortCap * (sizeof(double) + sizeof(int)) +
+         kRefineChunk * sizeof(int) + (size_t)d * sizeof(double);
 }
 
-cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, int np, cudaStream_t s) {
+cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, int np, uint8_t* miss,
+                          int32_t* probes_out, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
   const size_t sm = refine_smem(ix.d);
-  static int configured_for = -1;
-  if (sm > 48 * 1024 && configured_for < (int)sm) {
+  static size_t configured = 0;
+  if (sm > 48 * 1024 && sm > configured) {
     cudaError_t e = cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    configured_for = (int)sm;
+    configured = sm;
   }
   k_refine<<<nq, kRefineThreads, sm, s>>>(Q, ix.centroids, ix.d, ix.nlist, np, ws.dt, ws.cand, ws.ncand, ws.bound,
-                                           ws.probes, ws.term1);
+                                           ws.exact, ws.probes, ws.term1, ix.rank, ix.owner, ix.local, ix.gbase, miss,
+                                           probes_out, ws.plocal, ws.item_local, ws.qtot);
   return cudaGetLastError();
 }
 

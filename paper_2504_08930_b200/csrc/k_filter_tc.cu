@@ -78,7 +78,8 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_filter_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int L, int nq,
-                int kblocks, int nN, int nacc, int stages, const float* __restrict__ cn2, float* __restrict__ dt) {
+                int kblocks, int nN, int nacc, int stages, const float* __restrict__ cn2, float* __restrict__ dt,
+                float* __restrict__ gmin, int ngroups) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull;
@@ -156,22 +157,49 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const float cn = row < L ? cn2[row] : 0.f;
     mb_wait(&tfull, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    for (int c = 0; c < ncols_used; c += 16) {
-      uint32_t v[16];
+    // 32 query columns at a time: dt stores (lanes = 32 consecutive centroids,
+    // coalesced) and the min over this warp's 32 centroids of each column
+    // (transpose-reduce: 31 shuffles leave column j's min in lane j).
+    const int grp = blockIdx.x * 4 + lg;
+    for (int c = 0; c < ncols_used; c += 32) {
+      uint32_t v[32];
       const uint32_t taddr = tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)c;
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
           : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
             "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
           : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < L) {
+      if (c + 16 < ncols_used) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr + 16u));
+      } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int q = q0 + c + j;
-          if (q < nq) dt[(size_t)q * L + row] = cn - 2.f * __uint_as_float(v[j]);
+        for (int j = 16; j < 32; ++j) v[j] = __float_as_uint(CUDART_INF_F);
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      float f[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        f[j] = row < L ? cn - 2.f * __uint_as_float(v[j]) : CUDART_INF_F;
+        const int q = q0 + c + j;
+        if (row < L && q < nq && c + j < ncols_used) dt[(size_t)q * L + row] = f[j];
+      }
+#pragma unroll
+      for (int w = 16; w >= 1; w >>= 1) {
+        const bool upper = (lane & w) != 0;
+#pragma unroll
+        for (int j = 0; j < w; ++j) {
+          const float send = upper ? f[j] : f[j + w];
+          const float keep = upper ? f[j + w] : f[j];
+          f[j] = fminf(keep, __shfl_xor_sync(kFull, send, w));
         }
       }
+      const int q = q0 + c + lane;
+      if (q < nq && c + lane < ncols_used && grp < ngroups) gmin[(size_t)q * ngroups + grp] = f[0];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -214,7 +242,7 @@ cudaError_t make_tmap_2d(void* map_, const float* base, int rows, int cols, int 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, float* dt, cudaStream_t s) {
+cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, float* dt, float* gmin, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
   int nacc, nN;
   if (nq <= 256) {
@@ -229,7 +257,9 @@ cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, flo
   cudaError_t e = make_tmap_2d(&tmB, Qt, nq, ix.d4, box_rows_b);
   if (e != cudaSuccess) return e;
   const uint32_t stage_bytes = kTcM * 128 + (uint32_t)(nacc * nN * 128);
-  int stages = (int)((200 * 1024) / stage_bytes);
+  // ~100 KB of stages so that two CTAs share an SM: one CTA's epilogue
+  // overlaps the other's TMA/MMA pipeline
+  int stages = (int)((100 * 1024) / stage_bytes);
   if (stages > kTcMaxStages) stages = kTcMaxStages;
   if (stages < 2) stages = 2;
   const size_t smem = (size_t)stages * stage_bytes + 1024;
@@ -242,7 +272,8 @@ cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, flo
   const int kblocks = (ix.d4 + kTcBK - 1) / kTcBK;
   dim3 grid((ix.nlist + kTcM - 1) / kTcM, (nq + nN * nacc - 1) / (nN * nacc));
   k_filter_tc<<<grid, kTcThreads, smem, s>>>(*reinterpret_cast<const CUtensorMap*>(ix.tmapA), tmB, ix.nlist, nq,
-                                              kblocks, nN, nacc, stages, ix.cnorm2, dt);
+                                              kblocks, nN, nacc, stages, ix.cnorm2, dt, gmin,
+                                              (ix.nlist + 31) / 32);
   return cudaGetLastError();
 }
 

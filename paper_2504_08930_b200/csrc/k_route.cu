@@ -1,11 +1,13 @@
 // k_route.cu -- K4 router and K5 LUT builder.
 //
-// K4 (§IV.B.1 Router): remap every probe through the
-// mapping tables (owner, local id), emit the miss mask for probes that
-// are not GPU-resident and keep only this rank's probes ("effective
-// nprobe per shard") as work items. Items are (query, probe) pairs in
-// query-major order; item i owns ngroups(list) groups of 32 vectors and
-// item_off is their exclusive prefix sum (item_off[n] = total groups W).
+// K4 (§IV.B.1 Router): every probe is remapped through the
+// mapping tables (owner, local id), the miss mask marks probes that are
+// not GPU-resident and only this rank's probes ("effective nprobe per
+// shard") become work items -- done in the epilogue of K3 (k_coarse.cu),
+// which also writes each item's within-query prefix of groups. Items are
+// (query, probe) pairs in query-major order; item i owns ngroups(list) groups
+// of 32 vectors; K4b (below) turns the per-query prefixes into the global
+// exclusive prefix item_off (item_off[n] = total groups W).
 //
 // K5 (stage 2 of Fig. 2): LUT_q[j][c] = -2 <q_j, y_{j,c}>, the
 // query-dependent part of the residual-PQ distance,
@@ -16,125 +18,180 @@
 
 namespace vlr {
 
-constexpr int kRouteThreads = 1024;
+// K4b: item_off[q*np + p] = sum_{q' < q} qtot[q'] + item_local[q*np + p];
+// item_off[nq*np] = W. Every block recomputes the (short) query prefix in
+// shared memory, so there is no serial pass over the items.
+constexpr int kOffThreads = 256;
 
-__global__ void __launch_bounds__(kRouteThreads) k_route(const int32_t* __restrict__ probes, int n, int rank,
-                                                         const int32_t* __restrict__ owner,
-                                                         const int32_t* __restrict__ local,
-                                                         const int64_t* __restrict__ gbase,
-                                                         uint8_t* __restrict__ miss, int32_t* __restrict__ probes_out,
-                                                         int32_t* __restrict__ plocal,
+__global__ void __launch_bounds__(kOffThreads) k_offsets(int nq, int np, const int64_t* __restrict__ qtot,
+                                                         const int64_t* __restrict__ item_local,
                                                          int64_t* __restrict__ item_off) {
-  __shared__ long long warp_sums[kRouteThreads / 32];
-  __shared__ long long s_carry;
-  if (threadIdx.x == 0) s_carry = 0;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int base = 0; base < n; base += kRouteThreads) {
-    const int i = base + threadIdx.x;
-    long long g = 0;
-    if (i < n) {
-      const int l = probes[i];
-      const int o = owner[l];
-      miss[i] = o < 0 ? 1 : 0;
-      if (probes_out) probes_out[i] = l;
-      const int loc = (o == rank) ? local[l] : -1;
-      plocal[i] = loc;
-      if (loc >= 0) g = gbase[loc + 1] - gbase[loc];
-    }
-    // block exclusive scan of g
-    long long incl = g;
+  extern __shared__ long long qbase[];  // [nq + 1]
+  __shared__ long long wsum[kOffThreads / 32];
+  __shared__ long long carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < nq; b0 += kOffThreads) {
+    const int i = b0 + threadIdx.x;
+    const long long v = i < nq ? qtot[i] : 0;
+    long long incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      long long v = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += v;
+      const long long t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
     }
-    if (lane == 31) warp_sums[wid] = incl;
+    if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    if (wid == 0) {
-      long long ws = warp_sums[lane];
-      long long wi = ws;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        long long v = __shfl_up_sync(kFull, wi, o);
-        if (lane >= o) wi += v;
-      }
-      warp_sums[lane] = wi - ws;  // exclusive prefix of warp totals
+    long long wb = 0, tot = 0;
+    for (int w = 0; w < kOffThreads / 32; ++w) {
+      if (w < warp) wb += wsum[w];
+      tot += wsum[w];
     }
+    const long long c0 = carry;
+    if (i < nq) qbase[i] = c0 + wb + incl - v;
     __syncthreads();
-    const long long carry = s_carry;
-    if (i < n) item_off[i] = carry + warp_sums[wid] + incl - g;
-    __syncthreads();
-    if (threadIdx.x == kRouteThreads - 1) s_carry = carry + warp_sums[wid] + incl;
+    if (threadIdx.x == 0) carry = c0 + tot;
     __syncthreads();
   }
-  if (threadIdx.x == 0) item_off[n] = s_carry;
+  if (threadIdx.x == 0) qbase[nq] = carry;
+  __syncthreads();
+  const long long n = (long long)nq * np;
+  for (long long i = blockIdx.x * (long long)kOffThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kOffThreads)
+    item_off[i] = qbase[i / np] + item_local[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) item_off[n] = qbase[nq];
 }
 
-cudaError_t launch_route(const DeviceIndex& ix, const Workspace& ws, int nq, int np, uint8_t* miss,
-                         int32_t* probes_out, cudaStream_t s) {
-  const int n = nq * np;
-  k_route<<<1, kRouteThreads, 0, s>>>(ws.probes, n, ix.rank, ix.owner, ix.local, ix.gbase, miss, probes_out, ws.plocal,
-                                      ws.item_off);
+cudaError_t launch_offsets(const Workspace& ws, int nq, int np, cudaStream_t s) {
+  const long long n = (long long)nq * np;
+  long long blocks = (n + kOffThreads - 1) / kOffThreads;
+  if (blocks > 148 * 4) blocks = 148 * 4;
+  if (blocks < 1) blocks = 1;
+  const size_t sm = (size_t)(nq + 1) * sizeof(long long);
+  static size_t configured = 0;
+  if (sm > 48 * 1024 && sm > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_offsets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    configured = sm;
+  }
+  k_offsets<<<(int)blocks, kOffThreads, sm, s>>>(nq, np, ws.qtot, ws.item_local, ws.item_off);
   return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------- K5 LUT
-// grid (npairs * 4 code quarters, ceil(nq / kLutQB)); 256 threads = 4 codes x
-// 64 sub-spaces (jj fastest -> coalesced LUT rows). Each thread keeps its
-// codeword y_{j,c} in registers and reuses it for kLutQB queries, whose
-// sub-vectors sit in shared memory padded to dsub+1 per sub-space (bank-
-// conflict-free across the 64 sub-spaces of a warp).
+// grid (npairs * 4 code quarters, ceil(nq / kLutQB)); 256 threads = 16 x 4
+// sub-spaces (jj4) x 16 code slots (cc). A thread computes 4 consecutive
+// sub-spaces x 4 codes x kLutQB queries: codewords stay in registers across
+// the queries, query sub-vectors come from shared memory (padded to dsub+1
+// per sub-space), and each (code, query) result is one 16-B store (the 16
+// jj4 lanes of a code write 256 contiguous bytes of the LUT row).
 constexpr int kLutQB = 8;
-constexpr int kLutMaxDsub = 32;
 
 __global__ void __launch_bounds__(256) k_lut(const float* __restrict__ Q, int nq, int d, int m, int dsub,
                                              const float* __restrict__ Y, int npairs, float* __restrict__ lut) {
-  extern __shared__ float qs[];  // [kLutQB][64 * (dsub + 1)]
+  extern __shared__ float qs[];  // [kLutQB][jv * (dsub + 1)]
   const int pair = blockIdx.x >> 2, cq = blockIdx.x & 3;
   const int q0 = blockIdx.y * kLutQB;
-  const int jj = threadIdx.x & 63, cs = threadIdx.x >> 6;
-  const int j = pair * 64 + jj;
+  const int jj4 = threadIdx.x & 15, cc = threadIdx.x >> 4;
   const int jv = min(64, m - pair * 64);  // valid sub-spaces of this pair (>= 1)
   const int row = jv * (dsub + 1);
   for (int i = threadIdx.x; i < kLutQB * jv * dsub; i += blockDim.x) {
     const int qq = i / (jv * dsub), r = i - qq * jv * dsub;
     const int jl = r / dsub, u = r - jl * dsub;
-    const int jg = pair * 64 + jl;
     float v = 0.f;
-    if (q0 + qq < nq) v = Q[(size_t)(q0 + qq) * d + jg * dsub + u];
+    if (q0 + qq < nq) v = Q[(size_t)(q0 + qq) * d + (pair * 64 + jl) * dsub + u];
     qs[qq * row + jl * (dsub + 1) + u] = v;
   }
   __syncthreads();
   const int nqb = min(kLutQB, nq - q0);
-  for (int c = cq * 64 + cs; c < cq * 64 + 64; c += 4) {
-    float acc[kLutQB];
+#pragma unroll 1
+  for (int ci = 0; ci < 4; ++ci) {
+    const int c = cq * 64 + cc + 16 * ci;
+    float acc[4][kLutQB];
 #pragma unroll
-    for (int qq = 0; qq < kLutQB; ++qq) acc[qq] = 0.f;
-    if (j < m) {
-      const float* y = Y + ((size_t)j * 256 + c) * dsub;
-      for (int u0 = 0; u0 < dsub; u0 += kLutMaxDsub) {
-        float yr[kLutMaxDsub];
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int u = 0; u < kLutMaxDsub; ++u) yr[u] = (u0 + u < dsub) ? __ldg(y + u0 + u) : 0.f;
+      for (int qq = 0; qq < kLutQB; ++qq) acc[a][qq] = 0.f;
+    for (int u0 = 0; u0 < dsub; u0 += 8) {
+      float yr[4][8];
 #pragma unroll
-        for (int qq = 0; qq < kLutQB; ++qq) {
-          const float* qv = qs + qq * row + jj * (dsub + 1) + u0;
-          float a = acc[qq];
+      for (int a = 0; a < 4; ++a) {
+        const int jl = 4 * jj4 + a;
+        const float* y = Y + ((size_t)(pair * 64 + jl) * 256 + c) * dsub + u0;
 #pragma unroll
-          for (int u = 0; u < kLutMaxDsub; ++u)
-            if (u0 + u < dsub) a = fmaf(qv[u], yr[u], a);
-          acc[qq] = a;
+        for (int u = 0; u < 8; ++u) yr[a][u] = (jl < jv && u0 + u < dsub) ? __ldg(y + u) : 0.f;
+      }
+#pragma unroll
+      for (int qq = 0; qq < kLutQB; ++qq) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int jl = min(4 * jj4 + a, jv - 1);
+          const float* qv = qs + qq * row + jl * (dsub + 1) + u0;
+          float t = acc[a][qq];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (u0 + u < dsub) t = fmaf(qv[u], yr[a][u], t);
+          acc[a][qq] = t;
         }
       }
     }
-    for (int qq = 0; qq < nqb; ++qq)
-      lut[(((size_t)(q0 + qq) * npairs + pair) * 256 + c) * 64 + jj] = -2.f * acc[qq];
+    for (int qq = 0; qq < nqb; ++qq) {
+      const float4 v = make_float4(-2.f * acc[0][qq], -2.f * acc[1][qq], -2.f * acc[2][qq], -2.f * acc[3][qq]);
+      *reinterpret_cast<float4*>(lut + (((size_t)(q0 + qq) * npairs + pair) * 256 + c) * 64 + 4 * jj4) = v;
+    }
+  }
+}
+
+// Fast path for dsub == 8 (every BASELINE config): thread (jj, cs) keeps the 8
+// queries' sub-vectors of sub-space jj in registers (64 floats) and walks 16
+// codes: per code 2 LDG.128 of the codeword, 64 FMA, 8 coalesced stores.
+__global__ void __launch_bounds__(256) k_lut8(const float* __restrict__ Q, int nq, int d, int m,
+                                              const float* __restrict__ Y, int npairs, float* __restrict__ lut) {
+  const int pair = blockIdx.x >> 2, cq = blockIdx.x & 3;
+  const int q0 = blockIdx.y * kLutQB;
+  const int jj = threadIdx.x & 63, cs = threadIdx.x >> 6;
+  const int j = pair * 64 + jj;
+  const int nqb = min(kLutQB, nq - q0);
+  float qv[kLutQB][8];
+#pragma unroll
+  for (int qq = 0; qq < kLutQB; ++qq) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (qq < nqb && j < m) {
+      const float4* src = reinterpret_cast<const float4*>(Q + (size_t)(q0 + qq) * d + j * 8);
+      a = __ldg(src);
+      b = __ldg(src + 1);
+    }
+    qv[qq][0] = a.x; qv[qq][1] = a.y; qv[qq][2] = a.z; qv[qq][3] = a.w;
+    qv[qq][4] = b.x; qv[qq][5] = b.y; qv[qq][6] = b.z; qv[qq][7] = b.w;
+  }
+#pragma unroll 2
+  for (int i = 0; i < 16; ++i) {
+    const int c = cq * 64 + cs + 4 * i;
+    float4 ya = make_float4(0.f, 0.f, 0.f, 0.f), yb = ya;
+    if (j < m) {
+      const float4* y = reinterpret_cast<const float4*>(Y + ((size_t)j * 256 + c) * 8);
+      ya = __ldg(y);
+      yb = __ldg(y + 1);
+    }
+#pragma unroll
+    for (int qq = 0; qq < kLutQB; ++qq) {
+      float t = 0.f;
+      t = fmaf(qv[qq][0], ya.x, t); t = fmaf(qv[qq][1], ya.y, t);
+      t = fmaf(qv[qq][2], ya.z, t); t = fmaf(qv[qq][3], ya.w, t);
+      t = fmaf(qv[qq][4], yb.x, t); t = fmaf(qv[qq][5], yb.y, t);
+      t = fmaf(qv[qq][6], yb.z, t); t = fmaf(qv[qq][7], yb.w, t);
+      if (qq < nqb) lut[(((size_t)(q0 + qq) * npairs + pair) * 256 + c) * 64 + jj] = -2.f * t;
+    }
   }
 }
 
 cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
   dim3 grid(ix.npairs * 4, (nq + kLutQB - 1) / kLutQB);
+  if (ix.dsub == 8 && (ix.d % 4) == 0) {
+    k_lut8<<<grid, 256, 0, s>>>(Q, nq, ix.d, ix.m, ix.codebooks, ix.npairs, ws.lut);
+    return cudaGetLastError();
+  }
   const size_t sm = (size_t)kLutQB * (ix.m < 64 ? ix.m : 64) * (ix.dsub + 1) * sizeof(float);
   static size_t configured = 0;
   if (sm > 48 * 1024 && sm > configured) {

@@ -29,6 +29,8 @@
 
 namespace vlr {
 
+constexpr int kPfDist = 2;  // L2 prefetch distance (in this warp's groups) beyond the register buffer
+
 struct ScanArgs {
   int nq, np, k, npairs;
   const int32_t* plocal;
@@ -93,6 +95,19 @@ struct Grp {
   float b, t1;
   long long gaddr;
 };
+
+// L2 prefetch of a whole group (codes + bias) by one lane: keeps DRAM
+// requests in flight beyond the register double buffer (K6).
+template <int MP>
+__device__ __forceinline__ void grp_prefetch(const ScanArgs& a, long long gg, long long& it, int lane) {
+  while (a.item_off[it + 1] <= gg) ++it;
+  if (lane == 0) {
+    const long long gaddr = a.gbase[a.plocal[it]] + (gg - a.item_off[it]);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.codes + gaddr * 32 * MP), "r"(32 * MP)
+                 : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.bias + gaddr * 32), "r"(128) : "memory");
+  }
+}
 
 template <int MP>
 __device__ __forceinline__ void grp_load(Grp<MP>& G, const ScanArgs& a, long long gg, long long& it, int lane) {
@@ -197,13 +212,20 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
     long long it = it0;
     long long gg = g + warp;
     Grp<MP> A, B;
-    if (gg < seg_end) grp_load<MP>(A, a, gg, it, lane);
+    long long itp = it0;  // prefetch cursor: kPfDist groups (of this warp) ahead of the loads
+    if (gg < seg_end) {
+      for (int p = 1; p <= kPfDist; ++p)
+        if (gg + p * kScanWarps < seg_end) grp_prefetch<MP>(a, gg + p * kScanWarps, itp, lane);
+      grp_load<MP>(A, a, gg, it, lane);
+    }
     while (gg < seg_end) {
       const long long gn = gg + kScanWarps;
+      if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP>(a, gn + kPfDist * kScanWarps, itp, lane);
       if (gn < seg_end) grp_load<MP>(B, a, gn, it, lane);
       grp_finish<MP>(A, a, lutc, lane4, lane, bd, bid, thr);
       if (gn >= seg_end) break;
       const long long gm = gn + kScanWarps;
+      if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP>(a, gm + kPfDist * kScanWarps, itp, lane);
       if (gm < seg_end) grp_load<MP>(A, a, gm, it, lane);
       grp_finish<MP>(B, a, lutc, lane4, lane, bd, bid, thr);
       gg = gm;
@@ -267,7 +289,7 @@ __global__ void k_rank_merge(int nq, int np, int k, int n_cta, const int64_t* __
   if (q >= nq) return;
   const long long W = item_off[(long long)nq * np];
   const long long S = item_off[(long long)q * np], E = item_off[(long long)(q + 1) * np];
-  float bd = CUDART_INF_F, thr = CUDART_INF_F;
+  float bd = CUDART_INF_F;
   long long bid = -1;
   if (E > S) {
     auto start = [&](int c) { return (long long)c * W / n_cta; };
@@ -280,20 +302,16 @@ __global__ void k_rank_merge(int nq, int np, int k, int n_cta, const int64_t* __
       return lo;
     };
     const int cf = cta_of(S), cl = cta_of(E - 1);
-    for (int c = cf; c <= cl; ++c) {
-      if (start(c) == start(c + 1)) continue;
-      for (int w = 0; w < kScanWarps; ++w) {
-        const long long slot = ((long long)(c + q) * kScanWarps + w) * k;
-        float d = CUDART_INF_F;
-        long long id = -1;
-        if (lane < k) {
-          d = pdist[slot + lane];
-          id = pid[slot + lane];
-        }
-        wtk_offer(bd, bid, d, d <= thr && id >= 0, k, lane, id);
-        thr = __shfl_sync(kFull, bd, k - 1);
-      }
-    }
+    const int per = kScanWarps * k;  // entries per (CTA, query) partial
+    const int n = (cl - cf + 1) * per;
+    const bool maybe_empty = W < n_cta;  // otherwise every CTA owns >= 1 group
+    warp_select_merge<8>(bd, bid, k, lane, n, [&](int i, float& d, long long& id) {
+      const int c = cf + i / per;
+      if (maybe_empty && start(c) == start(c + 1)) return;  // CTA without work wrote nothing
+      const long long slot = (long long)(c + q) * per + (i % per);
+      d = pdist[slot];
+      id = pid[slot];
+    });
   }
   if (lane < k) {
     if (packed) {
@@ -327,25 +345,19 @@ __global__ void k_merge_parts(int n_shards, int nq, int k, const Packed* __restr
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
-  float bd = CUDART_INF_F, thr = CUDART_INF_F;
+  float bd = CUDART_INF_F;
   long long bid = -1;
-  for (int sh = 0; sh < n_shards; ++sh) {
-    float d = CUDART_INF_F;
-    long long id = -1;
-    if (lane < k) {
-      const size_t o = ((size_t)sh * nq + q) * k + lane;
-      if (packed) {
-        const Packed p = packed[o];
-        d = p.d;
-        id = p.id;
-      } else {
-        d = pdist[o];
-        id = pids[o];
-      }
+  warp_select_merge<4>(bd, bid, k, lane, n_shards * k, [&](int i, float& d, long long& id) {
+    const size_t o = ((size_t)(i / k) * nq + q) * k + (i % k);
+    if (packed) {
+      const Packed p = packed[o];
+      d = p.d;
+      id = p.id;
+    } else {
+      d = pdist[o];
+      id = pids[o];
     }
-    wtk_offer(bd, bid, d, d <= thr && id >= 0, k, lane, id);
-    thr = __shfl_sync(kFull, bd, k - 1);
-  }
+  });
   if (lane < k) {
     out_ids[(size_t)q * k + lane] = bid;
     out_dist[(size_t)q * k + lane] = bd;

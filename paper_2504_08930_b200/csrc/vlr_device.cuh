@@ -48,6 +48,71 @@ __device__ __forceinline__ void wtk_offer(float& bd, long long& bid, float dist,
   }
 }
 
+// Warp-cooperative k-selection: the running list (lane i < k holds the i-th
+// smallest) is merged with n entries fetched as fetch(i) -> (dist, id), in
+// chunks of 32*E: k rounds of (lane-local min over E entries + list entry,
+// 5-step warp argmin by (dist, id)); the winner's slot is retired. Sorted
+// output, ties by id. Padding is (+inf, -1).
+template <int E, class F>
+__device__ __forceinline__ void warp_select_merge(float& bd, long long& bid, int k, int lane, int n, F fetch) {
+  for (int base = 0; base < n; base += 32 * E) {
+    float ed[E + 1];
+    long long eid[E + 1];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = base + e * 32 + lane;
+      ed[e] = CUDART_INF_F;
+      eid[e] = -1;
+      if (i < n) fetch(i, ed[e], eid[e]);
+    }
+    ed[E] = lane < k ? bd : CUDART_INF_F;
+    eid[E] = lane < k ? bid : -1;
+    float nd = CUDART_INF_F;
+    long long nid = -1;
+    for (int r = 0; r < k; ++r) {
+      float md = ed[0];
+      long long mid = eid[0];
+      int ms = 0;
+#pragma unroll
+      for (int e = 1; e <= E; ++e)
+        if (lex_less(ed[e], eid[e], md, mid)) {
+          md = ed[e];
+          mid = eid[e];
+          ms = e;
+        }
+      float wd = md;
+      long long wid = mid;
+      int wl = lane;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const float od = __shfl_xor_sync(kFull, wd, o);
+        const long long oid = __shfl_xor_sync(kFull, wid, o);
+        const int ol = __shfl_xor_sync(kFull, wl, o);
+        if (lex_less(od, oid, wd, wid) || (od == wd && oid == wid && ol < wl)) {
+          wd = od;
+          wid = oid;
+          wl = ol;
+        }
+      }
+      if (lane == r) {
+        nd = wd;
+        nid = wid;
+      }
+      if (wid < 0) break;  // only padding left (warp-uniform)
+      if (lane == wl) {
+#pragma unroll
+        for (int e = 0; e <= E; ++e)
+          if (e == ms) {
+            ed[e] = CUDART_INF_F;
+            eid[e] = -1;
+          }
+      }
+    }
+    bd = nd;
+    bid = nid;
+  }
+}
+
 // float <-> order-preserving unsigned key
 __device__ __forceinline__ unsigned fkey(float f) {
   unsigned u = __float_as_uint(f);

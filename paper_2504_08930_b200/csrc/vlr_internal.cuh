@@ -70,13 +70,17 @@ struct Workspace {
   float* qnorm = nullptr;      // [nq] ||q|| (fp32)
   float* qtf32 = nullptr;      // [nq][d4] queries rounded to TF32, zero-padded
   float* dt = nullptr;         // [nq][nlist] filter distances ||c||^2 - 2<q,c>
+  float* gmin = nullptr;       // [nq][ceil(nlist/32)] min of dt over each 32-centroid group
   int32_t* cand = nullptr;     // [nq][kCandCap]
   int32_t* ncand = nullptr;    // [nq]
+  double* exact = nullptr;     // [nq][kCandCap] exact fp64 D of listed candidates (K3a)
   float* bound = nullptr;      // [nq] candidate bound theta~ + 2 Delta*
   int32_t* probes = nullptr;   // [nq][np]
   float* term1 = nullptr;      // [nq][np] ||q - c_l||^2 (fp64 -> fp32)
   int32_t* plocal = nullptr;   // [nq][np] local list or -1
   int64_t* item_off = nullptr; // [nq*np + 1] group prefix of owned work items
+  int64_t* item_local = nullptr; // [nq*np] within-query group prefix
+  int64_t* qtot = nullptr;     // [nq] groups owned per query
   float* lut = nullptr;        // [nq][npairs][256][64]
   float* pdist = nullptr;      // [(n_cta + nq) * warps * k] scan partials
   int64_t* pid = nullptr;
@@ -112,21 +116,19 @@ namespace vlr {
 // K0 layout (load time)
 cudaError_t launch_layout(const DeviceIndex& ix, const uint8_t* stage_codes, const int64_t* stage_ids,
                           const int64_t* vbase, const int32_t* lglob, cudaStream_t s);
-cudaError_t launch_cnorm(const DeviceIndex& ix, cudaStream_t s);
 // stage 0..2 coarse quantizer
 cudaError_t launch_qprep(const float* Q, int nq, int d, int d4, float* qnorm, float* qtf32, int32_t* status,
                          cudaStream_t s);
-cudaError_t launch_filter_simt(const float* Q, int nq, const DeviceIndex& ix, float* dt, cudaStream_t s);
-cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, float* dt, cudaStream_t s);
+cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, float* dt, float* gmin, cudaStream_t s);
 cudaError_t launch_round_tf32(const float* src, int rows, int d, int d4, float* dst, cudaStream_t s);
 cudaError_t make_tmap_2d(void* map, const float* base, int rows, int cols, int box_rows);
 cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float band_rel,
                           cudaStream_t s);
-cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, int np,
-                          cudaStream_t s);
+cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s);
+cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, int np, uint8_t* miss,
+                          int32_t* probes_out, cudaStream_t s);
 // stage 3..4
-cudaError_t launch_route(const DeviceIndex& ix, const Workspace& ws, int nq, int np, uint8_t* miss,
-                         int32_t* probes_out, cudaStream_t s);
+cudaError_t launch_offsets(const Workspace& ws, int nq, int np, cudaStream_t s);
 cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s);
 // stage 5..7
 int scan_ctas(const DeviceIndex& ix);

@@ -148,12 +148,12 @@ def test_batch_sizes(c1_index, c1_queries):
 
 # --------------------------------------------------------------- shapes / m_pad variants
 @pytest.mark.parametrize("d,m,L", [(32, 4, 50), (64, 32, 40), (96, 48, 33), (128, 64, 64), (192, 96, 40),
-                                   (256, 128, 70), (40, 20, 17)])
+                                   (256, 128, 70), (40, 20, 17), (64, 16, 1030)])
 def test_m_variants(d, m, L):
     ix = datagen.make_index(4000, d, L, m, seed=d + m)
     Q = datagen.make_queries(4000, d, L, 20, seed=d + m, stream=2)
     hot = np.arange(0, L, 2)
-    for npb, hh in ((8, None), (L, hot)):
+    for npb, hh in ((8, None), (min(L, 1000), hot)):
         errs, g, o = run_parity(ix, Q, npb, 10, hot=hh)
         assert not errs, (d, m, L, errs)
 
@@ -229,3 +229,21 @@ def test_offset_data_stress():
     Q = datagen.make_queries(3000, 32, 20, 16, seed=12, stream=2) + off
     errs, g, o = run_parity(ix, Q, 6, 10)
     assert not errs, errs
+
+
+def test_candidate_overflow_rescan_path():
+    # 5000 identical centroids: every one lies inside the filter band, so the
+    # candidate list (capacity 4096) overflows and K3 takes the rescan path.
+    rng = np.random.default_rng(9)
+    L, d = 5000, 8
+    c = rng.standard_normal(d).astype(np.float32)
+    C = np.repeat(c[None], L, 0)
+    C[4990:] += np.float32(2.0)
+    Y = (0.2 * rng.standard_normal((2, 256, 4))).astype(np.float32)
+    lists = [(np.arange(i * 2, i * 2 + 2), rng.integers(0, 256, (2, 2)).astype(np.uint8)) for i in range(L)]
+    ix = datagen.index_from_parts(C, Y, lists)
+    Q = (c + 0.01 * rng.standard_normal((3, d))).astype(np.float32)
+    for npb in (8, 700):
+        errs, g, o = run_parity(ix, Q, npb, 10)
+        assert not errs, errs
+        assert g["probes"][0].tolist() == list(range(npb))  # equal distances -> ascending id
