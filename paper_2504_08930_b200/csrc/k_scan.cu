@@ -23,6 +23,7 @@
 // goes to byte 1, the lane offset to byte 0); the slab/half offset is the LDS
 // immediate. Per lookup: PRMT + LDS + FADD (+1/R LOP3 for the lane offset).
 #include <cfloat>
+#include <cstdlib>
 
 #include "vlr_device.cuh"
 #include "vlr_internal.cuh"
@@ -109,7 +110,7 @@ __device__ __forceinline__ void grp_prefetch(const ScanArgs& a, long long gg, lo
   }
 }
 
-template <int MP>
+template <int MP, int EXP = 0>
 __device__ __forceinline__ void grp_load(Grp<MP>& G, const ScanArgs& a, long long gg, long long& it, int lane) {
   while (a.item_off[it + 1] <= gg) ++it;
   const int loc = a.plocal[it];
@@ -118,7 +119,9 @@ __device__ __forceinline__ void grp_load(Grp<MP>& G, const ScanArgs& a, long lon
   const uint4* src = reinterpret_cast<const uint4*>(a.codes) + G.gaddr * (2 * MP) + lane;
 #pragma unroll
   for (int c = 0; c < MP / 16; ++c) {
-    const uint4 v = ldg_stream(src + c * 32);
+    uint4 v;
+    if constexpr (EXP == 2) v = make_uint4(gg * 2654435761u + c, gg * 40503u + lane, c * 7919u, lane * 104729u);
+    else v = ldg_stream(src + c * 32);
     G.w[4 * c + 0] = v.x;
     G.w[4 * c + 1] = v.y;
     G.w[4 * c + 2] = v.z;
@@ -127,33 +130,58 @@ __device__ __forceinline__ void grp_load(Grp<MP>& G, const ScanArgs& a, long lon
   G.b = __ldg(a.bias + G.gaddr * 32 + lane);
 }
 
-// sum_j LUT[j][code_j] for this lane's vector, fixed order
+// two independent fp32 accumulators in one 64-bit register pair: FADD2
+// (sm_100 packed fp32 add), elementwise identical to two FADDs
+__device__ __forceinline__ void fadd2(unsigned long long& acc, float a, float b) {
+  asm("{\n.reg .b64 t;\nmov.b64 t, {%1, %2};\nadd.rn.f32x2 %0, %0, t;\n}" : "+l"(acc) : "f"(a), "f"(b));
+}
+__device__ __forceinline__ float lo32(unsigned long long v) { return __uint_as_float((unsigned)v); }
+__device__ __forceinline__ float hi32(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
+
+// sum_j LUT[j][code_j] for this lane's vector, fixed order:
+// accumulator r collects sub-spaces 32r + (lane ^ t), t = 0..31 in order;
+// result ((acc0 + acc1) + (acc2 + acc3)).
 template <int MP>
 __device__ __forceinline__ float grp_adc(const Grp<MP>& G, const unsigned char* lutc, uint32_t lane4) {
   constexpr int R = MP / 32;
-  float acc[R];
+  auto look = [&](int t, int r, uint32_t off) -> float {
+    const int s = r * 32 + t;
+    const uint32_t addr = __byte_perm(G.w[s >> 2], off, 0x5504u | ((uint32_t)(s & 3) << 4));
+    return *reinterpret_cast<const float*>(lutc + addr + ((r >> 1) << 16) + ((r & 1) << 7));
+  };
+  if constexpr (R == 1) {
+    float acc = 0.f;
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = 0.f;
+    for (int t = 0; t < 32; ++t) acc += look(t, 0, lane4 ^ (uint32_t)(t << 2));
+    return acc;
+  } else {
+    unsigned long long a01 = 0ull, a23 = 0ull;
+    float a2 = 0.f;
 #pragma unroll
-  for (int t = 0; t < 32; ++t) {
-    const uint32_t off = lane4 ^ (uint32_t)(t << 2);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int s = r * 32 + t;
-      const uint32_t addr = __byte_perm(G.w[s >> 2], off, 0x5504u | ((uint32_t)(s & 3) << 4));
-      acc[r] += *reinterpret_cast<const float*>(lutc + addr + ((r >> 1) << 16) + ((r & 1) << 7));
+    for (int t = 0; t < 32; ++t) {
+      const uint32_t off = lane4 ^ (uint32_t)(t << 2);
+      fadd2(a01, look(t, 0, off), look(t, 1, off));
+      if constexpr (R == 3) a2 += look(t, 2, off);
+      if constexpr (R == 4) fadd2(a23, look(t, 2, off), look(t, 3, off));
     }
+    if constexpr (R == 2) return lo32(a01) + hi32(a01);
+    else if constexpr (R == 3) return (lo32(a01) + hi32(a01)) + a2;
+    else return (lo32(a01) + hi32(a01)) + (lo32(a23) + hi32(a23));
   }
-  if constexpr (R == 1) return acc[0];
-  else if constexpr (R == 2) return acc[0] + acc[1];
-  else if constexpr (R == 3) return (acc[0] + acc[1]) + acc[2];
-  else return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
-template <int MP>
+template <int MP, int EXP>
 __device__ __forceinline__ void grp_finish(const Grp<MP>& G, const ScanArgs& a, const unsigned char* lutc,
                                            uint32_t lane4, int lane, float& bd, long long& bid, float& thr) {
-  const float s = grp_adc<MP>(G, lutc, lane4);
+  float s;
+  if constexpr (EXP == 1) {  // timing experiment: no LUT gathers (ALU sum of code words)
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < MP / 4; ++i) x ^= G.w[i];
+    s = (float)(x & 0xffff) * 1e-9f;
+  } else {
+    s = grp_adc<MP>(G, lutc, lane4);
+  }
   const float dist = (G.t1 + G.b) + s;
   const bool cand = dist <= thr;
   long long my_id = 0;
@@ -164,7 +192,7 @@ __device__ __forceinline__ void grp_finish(const Grp<MP>& G, const ScanArgs& a, 
   }
 }
 
-template <int MP>
+template <int MP, int EXP>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
@@ -216,18 +244,18 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
     if (gg < seg_end) {
       for (int p = 1; p <= kPfDist; ++p)
         if (gg + p * kScanWarps < seg_end) grp_prefetch<MP>(a, gg + p * kScanWarps, itp, lane);
-      grp_load<MP>(A, a, gg, it, lane);
+      grp_load<MP, EXP>(A, a, gg, it, lane);
     }
     while (gg < seg_end) {
       const long long gn = gg + kScanWarps;
       if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP>(a, gn + kPfDist * kScanWarps, itp, lane);
-      if (gn < seg_end) grp_load<MP>(B, a, gn, it, lane);
-      grp_finish<MP>(A, a, lutc, lane4, lane, bd, bid, thr);
+      if (gn < seg_end) grp_load<MP, EXP>(B, a, gn, it, lane);
+      grp_finish<MP, EXP>(A, a, lutc, lane4, lane, bd, bid, thr);
       if (gn >= seg_end) break;
       const long long gm = gn + kScanWarps;
       if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP>(a, gm + kPfDist * kScanWarps, itp, lane);
-      if (gm < seg_end) grp_load<MP>(A, a, gm, it, lane);
-      grp_finish<MP>(B, a, lutc, lane4, lane, bd, bid, thr);
+      if (gm < seg_end) grp_load<MP, EXP>(A, a, gm, it, lane);
+      grp_finish<MP, EXP>(B, a, lutc, lane4, lane, bd, bid, thr);
       gg = gm;
     }
     const long long slot = ((long long)(c + q) * kScanWarps + warp) * a.k;
@@ -252,17 +280,38 @@ int scan_ctas(const DeviceIndex& ix) {
   return sms;  // one persistent CTA per SM (128 KB LUT + 16 warps)
 }
 
-template <int MP>
-static cudaError_t launch_scan_t(const ScanArgs& a, int n_cta, cudaStream_t s) {
+template <int MP, int EXP>
+static cudaError_t launch_scan_e(const ScanArgs& a, int n_cta, cudaStream_t s) {
   const size_t sm = (size_t)a.npairs * kLutPairBytes;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kLutPairBytes));
+    cudaError_t e = cudaFuncSetAttribute(k_scan<MP, EXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kLutPairBytes));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_scan<MP><<<n_cta, kScanThreads, sm, s>>>(a);
+  k_scan<MP, EXP><<<n_cta, kScanThreads, sm, s>>>(a);
   return cudaGetLastError();
+}
+
+// VLR_SCAN_EXPERIMENT=1|2 (timing experiments only; results are wrong):
+// 1 = no LUT gathers, 2 = no code loads.
+static int scan_experiment() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VLR_SCAN_EXPERIMENT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <int MP>
+static cudaError_t launch_scan_t(const ScanArgs& a, int n_cta, cudaStream_t s) {
+  if constexpr (MP == 128) {
+    const int x = scan_experiment();
+    if (x == 1) return launch_scan_e<MP, 1>(a, n_cta, s);
+    if (x == 2) return launch_scan_e<MP, 2>(a, n_cta, s);
+  }
+  return launch_scan_e<MP, 0>(a, n_cta, s);
 }
 
 cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s) {
