@@ -154,7 +154,7 @@ def barrier(world):
         dist.barrier()
 
 
-def gen_index(c, seed, rank, world, hot=None):
+def gen_index(c, seed, rank, world, hot=None, gt_queries=None):
     """Generate this rank's shard of the synthetic index on the GPU (TOOLING).
     VLR_GEN_CACHE=<dir> reuses arrays saved by an earlier process of the same
     command sequence (never relied on for timing: only generation time)."""
@@ -167,18 +167,24 @@ def gen_index(c, seed, rank, world, hot=None):
     t = time.time()
     cache = os.environ.get("VLR_GEN_CACHE")
     key = f"{c['N']}_{c['d']}_{c['nlist']}_{c['m']}_{seed}_{world}_{rank}_{'all' if hot is None else len(hot)}"
+    if gt_queries is not None:
+        import hashlib
+        key += f"_gt{len(gt_queries)}_{hashlib.md5(gt_queries.tobytes()).hexdigest()[:10]}"
+    names = ["centroids", "codebooks", "list_offsets", "ids", "codes"] + (["gt_ids"] if gt_queries is not None else [])
     if cache:
         path = os.path.join(cache, key)
         if os.path.exists(os.path.join(path, "done")):
-            f = {n: np.load(os.path.join(path, n + ".npy"), mmap_mode="r") for n in
-                 ("centroids", "codebooks", "list_offsets", "ids", "codes")}
-            ix = datagen.IndexArrays(d=c["d"], nlist=c["nlist"], m=c["m"], seed=seed,
-                                     **{n: np.ascontiguousarray(v) for n, v in f.items()})
+            f = {n: np.ascontiguousarray(np.load(os.path.join(path, n + ".npy"), mmap_mode="r")) for n in names}
+            gt = f.pop("gt_ids", None)
+            ix = datagen.IndexArrays(d=c["d"], nlist=c["nlist"], m=c["m"], seed=seed, **f)
+            if gt is not None:
+                ix.gt_ids = gt
             return ix, time.time() - t
-    ix = datagen.make_index(c["N"], c["d"], c["nlist"], c["m"], seed=seed, device="cuda", owned=owned)
+    ix = datagen.make_index(c["N"], c["d"], c["nlist"], c["m"], seed=seed, device="cuda", owned=owned,
+                            gt_queries=gt_queries)
     if cache:
         os.makedirs(path, exist_ok=True)
-        for n in ("centroids", "codebooks", "list_offsets", "ids", "codes"):
+        for n in names:
             np.save(os.path.join(path, n + ".npy"), getattr(ix, n))
         open(os.path.join(path, "done"), "w").close()
     return ix, time.time() - t
@@ -265,7 +271,12 @@ def main():
     # ---- index (tooling), shard residency (vlr_load_index)
     t0 = time.time()
     hot, counts = calib_hot(c, a.seed)
-    ix, gen_s = gen_index(c, a.seed, rank, world, hot=hot)
+    # query stream (test stream) first: ground truth of the first timed batch is
+    # accumulated while the index vectors are generated (N = 1 only)
+    pool = datagen.make_queries(c["N"], c["d"], c["nlist"], (a.warmup + a.steps) * B, seed=a.seed, stream=2,
+                                alpha=c["alpha"], device="cuda")
+    gtq = pool[a.warmup * B:(a.warmup + 1) * B] if (world == 1 and not a.ncu) else None
+    ix, gen_s = gen_index(c, a.seed, rank, world, hot=hot, gt_queries=gtq)
     nccl_id = None
     if world > 1:
         import torch.distributed as dist
@@ -280,8 +291,6 @@ def main():
     assert np.array_equal(owners, exp_own), "owner table differs from the documented deal"
     info = h.info()
     # ---- queries (test stream), resident in HBM
-    pool = datagen.make_queries(c["N"], c["d"], c["nlist"], (a.warmup + a.steps) * B, seed=a.seed, stream=2,
-                                alpha=c["alpha"], device="cuda")
     Qdev = torch.from_numpy(pool).cuda().reshape(a.warmup + a.steps, B, c["d"])
     h.reserve(B, NP, K)
     outs = [(torch.empty(B, K, dtype=torch.int64, device="cuda"), torch.empty(B, K, device="cuda"),
@@ -361,6 +370,14 @@ def main():
     par = None
     if rank == 0 and world == 1 and not a.no_oracle and not a.ncu:
         cpu, par = oracle_leg(a, c, ix, hot, pool, outs)
+    recall = None
+    if getattr(ix, "gt_ids", None) is not None:
+        got = outs[0][0].cpu().numpy()
+        kk = min(10, K)
+        r = [len(set(g[:kk].tolist()) & set(t[:kk].tolist())) / kk for g, t in zip(got, ix.gt_ids)]
+        recall = {"recall_at_10": float(np.mean(r)), "queries": len(r),
+                  "ground_truth": "exact fp32 flat search over all N float vectors (regenerated during index "
+                                  "generation), first timed batch; results are bitwise identical at any G (R5)"}
     value = a.steps * B / (ms_total * 1e-3)
     if rank == 0:
         line = {
@@ -379,7 +396,7 @@ def main():
                          "bytes_per_launch": float(bytes_rec.mean()), "ms_per_launch": float(scan_ms.mean())},
             "stage_ms": stage_mean,
             "hit_rate_mean": float(np.mean(np.concatenate(hit))),
-            "e2e": e2e, "clocks": clk, "cpu_baseline": cpu, "parity_sample": par,
+            "e2e": e2e, "clocks": clk, "cpu_baseline": cpu, "parity_sample": par, "recall": recall,
             "gen_s": round(gen_s, 1), "load_s": round(load_s, 1),
         }
         if counts is not None:

@@ -48,8 +48,9 @@ __device__ __forceinline__ bool mb_try(uint64_t* b, uint32_t parity) {
 }
 // bounded wait: a pipeline bug traps (CUDA error) instead of hanging the GPU
 __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  const unsigned long long t0 = globaltimer_ns();
   for (uint32_t i = 0; !mb_try(b, parity); ++i)
-    if (i > (1u << 26)) asm volatile("trap;");
+    if ((i & 1023u) == 1023u && globaltimer_ns() - t0 > 4000000000ull) asm volatile("trap;");
 }
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(

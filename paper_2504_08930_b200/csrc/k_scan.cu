@@ -69,6 +69,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const unsigned long long t0 = globaltimer_ns();
   for (uint32_t i = 0;; ++i) {
     uint32_t ok;
     asm volatile(
@@ -79,7 +80,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
     if (ok) break;
-    if (i > (1u << 26)) asm volatile("trap;");  // bounded: never hang the GPU
+    if ((i & 1023u) == 1023u && globaltimer_ns() - t0 > 4000000000ull) asm volatile("trap;");  // bounded: never hang the GPU
   }
 }
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {

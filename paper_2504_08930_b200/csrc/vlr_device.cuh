@@ -9,6 +9,13 @@ namespace vlr {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// bounded mbarrier waits trap (CUDA error) after 4 s instead of hanging the GPU
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // total order on (distance, id) pairs: reading A7 (ties by id)
 __device__ __forceinline__ bool lex_less(float d1, long long i1, float d2, long long i2) {
   return d1 < d2 || (d1 == d2 && i1 < i2);
