@@ -247,3 +247,27 @@ def test_candidate_overflow_rescan_path():
         errs, g, o = run_parity(ix, Q, npb, 10)
         assert not errs, errs
         assert g["probes"][0].tolist() == list(range(npb))  # equal distances -> ascending id
+
+
+# --------------------------------------------------------------- full-size sampled parity
+@pytest.mark.parametrize("cfg,hot_mass,nq", [("C2", 1.0, 24), ("C3", 0.5, 16)])
+def test_full_size_sampled_parity(cfg, hot_mass, nq):
+    """BASELINE configs at full size (generated on the GPU), the batch and launch
+    configuration bench.py uses; the oracle checks a sample of queries."""
+    c = datagen.CONFIGS[cfg]
+    ix = datagen.make_index(c["N"], c["d"], c["nlist"], c["m"], device="cuda")
+    Q = datagen.make_queries(c["N"], c["d"], c["nlist"], c["batch"], stream=2, alpha=c["alpha"], device="cuda")
+    hot = None
+    if hot_mass < 1.0:
+        Qc = datagen.make_queries(c["N"], c["d"], c["nlist"], 10_000, stream=1, alpha=c["alpha"], device="cuda")
+        hot = datagen.hot_from_mass(datagen.access_counts(ix.centroids, Qc, c["nprobe"], device="cuda"), hot_mass)
+    h = vlr.Index.from_arrays(ix, hot=hot)
+    g = gpu_search(h, Q, c["nprobe"], c["k"])  # the full batch, as timed by bench.py
+    h.close()
+    sel = np.linspace(0, len(Q) - 1, nq).astype(np.int64)
+    o = oracle.search(ix, Q[sel], c["nprobe"], c["k"], hot=hot)
+    gs = {key: v[sel] for key, v in g.items()}
+    errs = check(ix, Q, gs, o, hot=hot, idmap=oracle.IdMap(ix), qsel=sel)
+    assert not errs, errs
+    if hot is not None:
+        assert 0.0 < g["miss"].mean() < 1.0
