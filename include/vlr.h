@@ -150,6 +150,14 @@ vlr_status vlr_reserve(vlr_index* idx, int32_t max_nq, int32_t max_nprobe, int32
 vlr_status vlr_merge_partials(const int64_t* d_part_ids, const float* d_part_dist, int32_t n_shards,
                               int32_t nq, int32_t k, int64_t* d_ids, float* d_dist, void* stream);
 
+/* Cluster access profile (NEXT-2; P:254 access-frequency profiling, P:419
+ * runtime monitoring): d_counts[l] += number of entries of d_probes[0..n)
+ * equal to l (entries < 0 or >= nlist are ignored). d_probes is the device
+ * probe output of vlr_search* (any n = nq * nprobe'); d_counts is a device
+ * int64 [nlist] array the caller zeroes. Stream-ordered. */
+vlr_status vlr_access_counts(const vlr_index* idx, const int32_t* d_probes, int64_t n, int64_t* d_counts,
+                             void* stream);
+
 /* Device bytes held by the handle, number of resident lists and vectors on this rank. */
 vlr_status vlr_index_info(const vlr_index* idx, int64_t* bytes_on_device, int32_t* n_owned_lists,
                           int64_t* n_owned_vectors);

@@ -22,7 +22,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "NONFINITE", 4: "UNKN
 
 # every symbol include/vlr.h declares (checked by tests/test_abi.py)
 EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_reserve",
-           "vlr_merge_partials", "vlr_index_info", "vlr_index_owners", "vlr_set_profiling", "vlr_stage_times",
+           "vlr_merge_partials", "vlr_access_counts", "vlr_index_info", "vlr_index_owners", "vlr_set_profiling", "vlr_stage_times",
            "vlr_last_launch_count", "vlr_nccl_unique_id", "vlr_index_free", "vlr_last_error", "vlr_version"]
 
 
@@ -66,6 +66,7 @@ def lib():
             "vlr_reserve": [P, I32, I32, I32],
             "vlr_merge_partials": [P, P, I32, I32, I32, P, P, P],
             "vlr_index_info": [P, P, P, P],
+            "vlr_access_counts": [P, P, I64, P, P],
             "vlr_index_owners": [P, P],
             "vlr_set_profiling": [P, I32],
             "vlr_stage_times": [P, I32, P, I32],
@@ -190,6 +191,16 @@ class Index:
 
     def reserve(self, max_nq: int, max_nprobe: int, max_k: int):
         _check(lib().vlr_reserve(self._h, max_nq, max_nprobe, max_k))
+
+    def access_counts(self, probes, counts=None, stream=None):
+        """vlr_access_counts: accumulate per-cluster probe counts (torch int32
+        CUDA probes of any shape) into an int64 [nlist] CUDA tensor."""
+        import torch
+        if counts is None:
+            counts = torch.zeros(self.nlist, dtype=torch.int64, device=probes.device)
+        _check(lib().vlr_access_counts(self._h, probes.data_ptr(), probes.numel(), counts.data_ptr(),
+                                       _stream_handle(stream)))
+        return counts
 
     # ------------------------------------------------------------------ info
     def info(self):

@@ -484,6 +484,14 @@ vlr_status vlr_merge_partials(const int64_t* part_ids, const float* part_dist, i
   return VLR_OK;
 }
 
+vlr_status vlr_access_counts(const vlr_index* h, const int32_t* d_probes, int64_t n, int64_t* d_counts,
+                             void* stream) {
+  if (!h || n < 0 || (n > 0 && (!d_probes || !d_counts))) return fail(VLR_ERR_INVALID_ARG, "vlr_access_counts: bad args");
+  VLR_CUDA_TRY(launch_access_hist(d_probes, n, h->ix.nlist, reinterpret_cast<unsigned long long*>(d_counts),
+                                  reinterpret_cast<cudaStream_t>(stream)));
+  return VLR_OK;
+}
+
 vlr_status vlr_index_info(const vlr_index* h, int64_t* bytes, int32_t* n_lists, int64_t* n_vec) {
   if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
   if (bytes) *bytes = h->ix.bytes;

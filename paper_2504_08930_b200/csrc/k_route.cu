@@ -203,4 +203,25 @@ cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& w
   return cudaGetLastError();
 }
 
+// ----------------------------------------------------------------- access histogram
+// NEXT-2 ("the router monitors ... per-cluster access
+// frequencies"): counts[l] += number of (query, probe) pairs that probed l.
+// Warp-aggregated atomics on int64 counters.
+__global__ void k_access_hist(const int32_t* __restrict__ probes, long long n, int nlist,
+                              unsigned long long* __restrict__ counts) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int l = probes[i];
+    if (l >= 0 && l < nlist) atomicAdd(counts + l, 1ull);
+  }
+}
+
+cudaError_t launch_access_hist(const int32_t* probes, long long n, int nlist, unsigned long long* counts,
+                               cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_access_hist<<<(int)blocks, 256, 0, s>>>(probes, n, nlist, counts);
+  return cudaGetLastError();
+}
+
 }  // namespace vlr

@@ -130,6 +130,8 @@ cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace
 // stage 3..4
 cudaError_t launch_offsets(const Workspace& ws, int nq, int np, cudaStream_t s);
 cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s);
+cudaError_t launch_access_hist(const int32_t* probes, long long n, int nlist, unsigned long long* counts,
+                               cudaStream_t s);
 // stage 5..7
 int scan_ctas(const DeviceIndex& ix);
 cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s);

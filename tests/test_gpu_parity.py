@@ -271,3 +271,48 @@ def test_full_size_sampled_parity(cfg, hot_mass, nq):
     assert not errs, errs
     if hot is not None:
         assert 0.0 < g["miss"].mean() < 1.0
+
+
+def test_hybrid_hot_gpu_plus_cold_cpu_equals_monolithic(c1_index, c1_queries):
+    """NEXT-1 / S:473: the GPU result over the hot lists merged (on the
+    GPU, vlr_merge_partials) with a cold-tier result over the remaining lists
+    equals the search over all lists. The cold tier here is the oracle (the
+    paper's CPU path)."""
+    c = datagen.CONFIGS["C1"]
+    ix, Q = c1_index, c1_queries
+    rng = np.random.default_rng(11)
+    hot = np.sort(rng.choice(ix.nlist, ix.nlist // 2, replace=False))
+    cold = np.setdiff1d(np.arange(ix.nlist), hot)
+    h = vlr.Index.from_arrays(ix, hot=hot)
+    g = gpu_search(h, Q, c["nprobe"], c["k"])
+    h.close()
+    oc = oracle.search(ix, Q, c["nprobe"], c["k"], hot=cold)
+    # cold-tier partial in the GPU's fp32 distance type
+    parts_i = torch.from_numpy(np.stack([g["ids"], oc["ids"]])).cuda()
+    parts_d = torch.from_numpy(np.stack([g["dist"], oc["dist"].astype(np.float32)])).cuda()
+    mi, md = vlr.merge_partials(parts_i, parts_d)
+    merged = dict(ids=mi.cpu().numpy(), dist=md.cpu().numpy(), miss=np.zeros_like(g["miss"]), probes=g["probes"])
+    full = oracle.search(ix, Q, c["nprobe"], c["k"])
+    errs = check(ix, Q, merged, full, idmap=oracle.IdMap(ix))
+    assert not errs, errs
+    assert np.array_equal(g["miss"], np.isin(g["probes"], cold).astype(np.uint8))
+
+
+def test_access_counts_and_hot_set(c1_index):
+    """NEXT-2: the GPU access profile of a calibration stream equals the count
+    of the oracle's probes; the hot set chosen from it covers the target mass
+    and its measured mean hit rate equals the coverage eta-bar."""
+    c = datagen.CONFIGS["C1"]
+    Qc = datagen.make_queries(c["N"], c["d"], c["nlist"], 1500, stream=1, alpha=1.2)
+    h = vlr.Index.from_arrays(c1_index)
+    g = gpu_search(h, Qc, c["nprobe"], 1)
+    cnt = h.access_counts(torch.from_numpy(g["probes"]).cuda()).cpu().numpy()
+    po, _ = oracle.coarse(Qc, c1_index.centroids, c["nprobe"])
+    assert np.array_equal(cnt, np.bincount(po.reshape(-1), minlength=c1_index.nlist))
+    hot = datagen.hot_from_mass(cnt, 0.5)
+    h.close()
+    h2 = vlr.Index.from_arrays(c1_index, hot=hot)
+    g2 = gpu_search(h2, Qc, c["nprobe"], 1)
+    h2.close()
+    eta = 1.0 - g2["miss"].mean(axis=1)
+    assert abs(eta.mean() - datagen.coverage_mean_hitrate(cnt, hot)) < 1e-12
