@@ -98,17 +98,16 @@ struct Grp {
   long long gaddr;
 };
 
-// L2 prefetch of a whole group (codes + bias) by one lane: keeps DRAM
-// requests in flight beyond the register double buffer (K6).
+// L2 prefetch of a whole group's codes: each lane prefetches one 128-B line
+// (LSU prefetch, no data return; a 4 KB TMA bulk prefetch per group costs
+// ~0.3 us of TMA issue time, tools/tma_issue.cu): keeps DRAM requests in
+// flight beyond the register double buffer (K6).
 template <int MP>
 __device__ __forceinline__ void grp_prefetch(const ScanArgs& a, long long gg, long long& it, int lane) {
   while (a.item_off[it + 1] <= gg) ++it;
-  if (lane == 0) {
-    const long long gaddr = a.gbase[a.plocal[it]] + (gg - a.item_off[it]);
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.codes + gaddr * 32 * MP), "r"(32 * MP)
-                 : "memory");
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.bias + gaddr * 32), "r"(128) : "memory");
-  }
+  const long long gaddr = a.gbase[a.plocal[it]] + (gg - a.item_off[it]);
+  if (lane < MP / 4)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.codes + gaddr * 32 * MP + lane * 128) : "memory");
 }
 
 template <int MP, int EXP = 0>
