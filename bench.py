@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--oracle-seconds", type=float, default=15.0)
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--ncu", action="store_true", help="short run for ncu: no e2e/oracle/clocks")
+    p.add_argument("--sweep-out", default=None,
+                   help="also run the C5 batch x nprobe sweep on the same index and write JSON lines here")
     return p.parse_args()
 
 
@@ -69,6 +71,16 @@ def workload_name(c, name):
     hot = "all lists resident" if c["hot_mass"] >= 1 else f"hot set = {c['hot_mass']:.0%} of access mass"
     return (f"{name}: {c['N'] / 1e6:g}M x d{c['d']}, IVF{c['nlist']}, PQ{c['m']}x8, nprobe {c['nprobe']}, "
             f"k {c['k']}, batch {c['batch']}, Zipf alpha {c['alpha']}, {hot}")
+
+
+def tf32_peak():
+    """Dense TF32 tensor peak: measured bf16 (MEASURED_PEAKS.json) x the guide's nominal tf32/bf16 ratio 1.1/2.25."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["bf16_tflops"]) * 1.1 / 2.25, "measured bf16_tflops x 1.1/2.25 (B200_PROFILING.md nominal ratio)"
+    except Exception:
+        return 1100.0, "fallback (B200_PROFILING.md tf32 1.1 PFLOP/s dense)"
 
 
 def peaks():
@@ -378,6 +390,19 @@ def main():
         recall = {"recall_at_10": float(np.mean(r)), "queries": len(r),
                   "ground_truth": "exact fp32 flat search over all N float vectors (regenerated during index "
                                   "generation), first timed batch; results are bitwise identical at any G (R5)"}
+    # ---- coarse contraction (K1, tcgen05 TF32): 2*B*L*d flops per launch; the stage
+    # also holds the tiny q-prep kernel, so this understates K1's own rate slightly
+    cf_ms = float(stage_mean["coarse_filter"]) if stage_mean else None
+    coarse_roof = None
+    if cf_ms:
+        tp, tp_src = tf32_peak()
+        fl = 2.0 * B * c["nlist"] * c["d"]
+        tfs = fl / (cf_ms * 1e-3) / 1e12
+        cbytes = c["nlist"] * c["d"] * 4 + B * c["nlist"] * 4
+        coarse_roof = {"bound": "tensor", "dtype": "tf32", "achieved": tfs, "peak": tp, "unit": "TFLOP/s",
+                       "frac": tfs / tp, "peak_source": tp_src, "flops_per_launch": fl,
+                       "ms_per_launch": cf_ms, "hbm_gbs": cbytes / (cf_ms * 1e-3) / 1e9,
+                       "kernel": "k_qprep + k_filter_tc (K1)"}
     value = a.steps * B / (ms_total * 1e-3)
     if rank == 0:
         line = {
@@ -394,6 +419,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "k_scan (K6 ADC scan)", "peak_source": peak_src,
                          "bytes_per_launch": float(bytes_rec.mean()), "ms_per_launch": float(scan_ms.mean())},
+            "coarse_roofline": coarse_roof,
             "stage_ms": stage_mean,
             "hit_rate_mean": float(np.mean(np.concatenate(hit))),
             "e2e": e2e, "clocks": clk, "cpu_baseline": cpu, "parity_sample": par, "recall": recall,
@@ -402,10 +428,53 @@ def main():
         if counts is not None:
             line["top20_share"] = datagen.topk_share(counts)
         print(json.dumps(line), flush=True)
+    if a.sweep_out:
+        sweep(a, c, h, pool, world, rank)
     h.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def sweep(a, c, h, pool, world, rank):
+    """C5: batch x nprobe sweep on the loaded index (device-timed, CUDA events,
+    max over ranks); one JSON line per point in --sweep-out."""
+    import torch
+    K = c["k"]
+    batches = [1, 2, 4, 8, 16, 32, 64, 128, 256, 512]
+    nprobes = [16, 32, 64, 128, 256, 512]
+    qd = torch.from_numpy(pool).cuda()
+    lines = []
+    for npb in nprobes:
+        for B in batches:
+            if B > len(pool):
+                continue
+            NP = min(npb, c["nlist"])
+            h.reserve(B, NP, K)
+            out = (torch.empty(B, K, dtype=torch.int64, device="cuda"), torch.empty(B, K, device="cuda"),
+                   torch.empty(B, NP, dtype=torch.uint8, device="cuda"), None)
+            steps = max(10, min(200, int(2000 / max(B, 1))))
+            nb = len(pool) // B
+            for i in range(3):
+                h.search(qd[(i % nb) * B:(i % nb + 1) * B], npb, K, out=out)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            barrier(world)
+            torch.cuda.synchronize()
+            for i in range(steps):
+                ev[i][0].record()
+                h.search(qd[(i % nb) * B:(i % nb + 1) * B], npb, K, out=out)
+                ev[i][1].record()
+            torch.cuda.synchronize()
+            lat = np.array([e0.elapsed_time(e1) for e0, e1 in ev])
+            tot = allmax(float(lat.sum()), world)
+            if rank == 0:
+                lines.append({"batch": B, "nprobe": npb, "k": K, "n_gpus": world, "qps": steps * B / (tot * 1e-3),
+                              "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+                              "steps": steps})
+    if rank == 0:
+        with open(a.sweep_out, "w") as f:
+            for ln in lines:
+                f.write(json.dumps(ln) + "\n")
 
 
 def oracle_leg(a, c, ix, hot, pool, outs):

@@ -328,17 +328,27 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
 }
 
 // ---------------------------------------------------------------- K7 per-rank merge
-// One warp per query: union of the partial lists written by the CTAs whose
-// ranges intersect the query's group range, top-k by (dist, id).
+// One CTA of nw warps per query: union of the partial lists written by the
+// CTAs whose ranges intersect the query's group range, top-k by (dist, id).
+// Each warp streams a strided slice of the partial entries (8 coalesced
+// chunks of 32 in flight per lane) and offers only the entries at or below its
+// running k-th distance to its warp-register list (wtk_offer), so the cost is
+// ~ one ballot per 32 entries plus O(k log n) insertions. The nw warp lists
+// meet in shared memory and warp 0 reduces them the same way. Small batches
+// (one query spans all 148 CTAs x 16 warps = 23,680 entries at k = 10) get up
+// to 32 warps; large batches (a query spans 1-2 CTAs) get one.
+constexpr int kMergeMaxWarps = 32;
+
 __global__ void k_rank_merge(int nq, int np, int k, int n_cta, const int64_t* __restrict__ item_off,
                              const float* __restrict__ pdist, const int64_t* __restrict__ pid,
                              int64_t* __restrict__ out_ids, float* __restrict__ out_dist, Packed* __restrict__ packed) {
-  const int lane = threadIdx.x & 31;
-  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (q >= nq) return;
+  __shared__ float s_d[kMergeMaxWarps * 32];
+  __shared__ long long s_id[kMergeMaxWarps * 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int q = blockIdx.x;
   const long long W = item_off[(long long)nq * np];
   const long long S = item_off[(long long)q * np], E = item_off[(long long)(q + 1) * np];
-  float bd = CUDART_INF_F;
+  float bd = CUDART_INF_F, thr = CUDART_INF_F;
   long long bid = -1;
   if (E > S) {
     auto start = [&](int c) { return (long long)c * W / n_cta; };
@@ -354,13 +364,49 @@ __global__ void k_rank_merge(int nq, int np, int k, int n_cta, const int64_t* __
     const int per = kScanWarps * k;  // entries per (CTA, query) partial
     const int n = (cl - cf + 1) * per;
     const bool maybe_empty = W < n_cta;  // otherwise every CTA owns >= 1 group
-    warp_select_merge<8>(bd, bid, k, lane, n, [&](int i, float& d, long long& id) {
-      const int c = cf + i / per;
-      if (maybe_empty && start(c) == start(c + 1)) return;  // CTA without work wrote nothing
-      const long long slot = (long long)(c + q) * per + (i % per);
-      d = pdist[slot];
-      id = pid[slot];
-    });
+    const long long base = (long long)(cf + q) * per;  // partials of CTAs cf..cl are contiguous
+    constexpr int U = 8;
+    for (int i0 = warp * 32 * U; i0 < n; i0 += nw * 32 * U) {
+      float d[U];
+      long long id[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * 32 + lane;
+        d[u] = CUDART_INF_F;
+        id[u] = -1;
+        if (i < n) {
+          bool ok = true;
+          if (maybe_empty) {
+            const int c = cf + i / per;
+            ok = start(c) != start(c + 1);  // a CTA without work wrote nothing
+          }
+          if (ok) d[u] = __ldg(pdist + base + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool cand = d[u] < CUDART_INF_F && d[u] <= thr;  // (+inf, -1) slots never enter
+        if (__any_sync(kFull, cand)) {
+          const long long my = cand ? __ldg(reinterpret_cast<const long long*>(pid) + base + i0 + u * 32 + lane) : -1;
+          wtk_offer(bd, bid, d[u], cand, k, lane, my);
+          thr = __shfl_sync(kFull, bd, k - 1);
+        }
+      }
+    }
+  }
+  if (nw > 1) {
+    s_d[warp * 32 + lane] = lane < k ? bd : CUDART_INF_F;
+    s_id[warp * 32 + lane] = lane < k ? bid : -1;
+    __syncthreads();
+    if (warp != 0) return;
+    for (int w = 1; w < nw; ++w) {
+      const float d = s_d[w * 32 + lane];
+      const bool cand = lane < k && d <= thr;
+      if (__any_sync(kFull, cand)) {
+        wtk_offer(bd, bid, d, cand, k, lane, s_id[w * 32 + lane]);
+        thr = __shfl_sync(kFull, bd, k - 1);
+      }
+    }
   }
   if (lane < k) {
     if (packed) {
@@ -380,9 +426,12 @@ cudaError_t launch_rank_merge(const DeviceIndex& ix, const Workspace& ws, int nq
                               float* out_dist, void* out_packed, cudaStream_t s) {
   (void)ix;
   if (nq <= 0) return cudaSuccess;
-  const int wpb = 8;
-  k_rank_merge<<<(nq + wpb - 1) / wpb, wpb * 32, 0, s>>>(nq, np, k, ws.n_cta, ws.item_off, ws.pdist, ws.pid, out_ids,
-                                                        out_dist, reinterpret_cast<Packed*>(out_packed));
+  // expected partial entries per query: (CTAs spanned) x warps x k
+  const long long per_q = ((long long)ws.n_cta / nq + 2) * kScanWarps * k;
+  int nw = 1;
+  while (nw < kMergeMaxWarps && (long long)nw * 512 < per_q) nw <<= 1;
+  k_rank_merge<<<nq, nw * 32, 0, s>>>(nq, np, k, ws.n_cta, ws.item_off, ws.pdist, ws.pid, out_ids, out_dist,
+                                      reinterpret_cast<Packed*>(out_packed));
   return cudaGetLastError();
 }
 
