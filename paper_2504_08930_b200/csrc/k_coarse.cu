@@ -65,7 +65,7 @@ cudaError_t launch_qprep(const float* Q, int nq, int d, int d4, float* qnorm, fl
 constexpr int kSelThreads = 1024;
 constexpr int kSelMaxGroups = 16384;  // nlist <= 512K for the sorted-minima path
 
-__global__ void __launch_bounds__(kSelThreads) k_select(const float* __restrict__ dt, const float* __restrict__ gmin,
+__global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restrict__ dt, const float* __restrict__ gmin,
                                                         int L, int np, const float* __restrict__ qnorm, float cmax,
                                                         float e_dot, int32_t* __restrict__ cand,
                                                         int32_t* __restrict__ ncand, float* __restrict__ bound_out) {
@@ -150,15 +150,23 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const float* __restrict_
   };
   if ((L & 3) == 0) {
     const float4* r4 = reinterpret_cast<const float4*>(row);
-    for (int i0 = 0; i0 < L / 4; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      const bool in = i < L / 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (in) v = __ldg(r4 + i);
-      emit(in && v.x <= bnd, 4 * i);
-      emit(in && v.y <= bnd, 4 * i + 1);
-      emit(in && v.z <= bnd, 4 * i + 2);
-      emit(in && v.w <= bnd, 4 * i + 3);
+    constexpr int U = 2;  // loads in flight per thread before any emit (32 regs: 2 CTAs per SM)
+    for (int i0 = 0; i0 < L / 4; i0 += U * blockDim.x) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * blockDim.x + threadIdx.x;
+        v[u] = i < L / 4 ? __ldg(r4 + i) : make_float4(CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * blockDim.x + threadIdx.x;
+        const bool in = i < L / 4;
+        emit(in && v[u].x <= bnd, 4 * i);
+        emit(in && v[u].y <= bnd, 4 * i + 1);
+        emit(in && v[u].z <= bnd, 4 * i + 2);
+        emit(in && v[u].w <= bnd, 4 * i + 3);
+      }
     }
   } else {
     for (int i0 = 0; i0 < L; i0 += blockDim.x) {

@@ -170,6 +170,24 @@ __device__ __forceinline__ float grp_adc(const Grp<MP>& G, const unsigned char* 
   }
 }
 
+// offer the lanes' (d, id) with cand set to the warp list (k entries); thr is
+// the list's k-th distance
+__device__ __forceinline__ void offer32(float& bd, long long& bid, float& thr, float d, long long id, bool cand, int k,
+                                        int lane) {
+  const unsigned cm = __ballot_sync(kFull, cand);
+  if (cm) {
+    if (__popc(cm) > 6) wtk_merge32(bd, bid, cand ? d : CUDART_INF_F, cand ? id : -1, k, lane);
+    else wtk_offer(bd, bid, d, cand, k, lane, id);
+    thr = __shfl_sync(kFull, bd, k - 1);
+  }
+}
+
+// offer a list held by lanes < k (padding (+inf, -1) elsewhere) to the warp list
+__device__ __forceinline__ void list_offer(float& bd, long long& bid, float& thr, float d, long long id, int k,
+                                           int lane) {
+  offer32(bd, bid, thr, d, id, lane < k && d < CUDART_INF_F && d <= thr, k, lane);
+}
+
 template <int MP, int EXP>
 __device__ __forceinline__ void grp_finish(const Grp<MP>& G, const ScanArgs& a, const unsigned char* lutc,
                                            uint32_t lane4, int lane, float& bd, long long& bid, float& thr) {
@@ -186,8 +204,10 @@ __device__ __forceinline__ void grp_finish(const Grp<MP>& G, const ScanArgs& a, 
   const bool cand = dist <= thr;
   long long my_id = 0;
   if (cand) my_id = __ldg(reinterpret_cast<const long long*>(a.ids) + G.gaddr * 32 + lane);
-  if (__any_sync(kFull, cand)) {
-    wtk_offer(bd, bid, dist, cand, a.k, lane, my_id);
+  const unsigned cm = __ballot_sync(kFull, cand);
+  if (cm) {
+    if (__popc(cm) > 6) wtk_merge32(bd, bid, cand ? dist : CUDART_INF_F, cand ? my_id : -1, a.k, lane);
+    else wtk_offer(bd, bid, dist, cand, a.k, lane, my_id);
     thr = __shfl_sync(kFull, bd, a.k - 1);
   }
 }
@@ -328,85 +348,188 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
 }
 
 // ---------------------------------------------------------------- K7 per-rank merge
-// One CTA of nw warps per query: union of the partial lists written by the
-// CTAs whose ranges intersect the query's group range, top-k by (dist, id).
-// Each warp streams a strided slice of the partial entries (8 coalesced
-// chunks of 32 in flight per lane) and offers only the entries at or below its
-// running k-th distance to its warp-register list (wtk_offer), so the cost is
-// ~ one ballot per 32 entries plus O(k log n) insertions. The nw warp lists
-// meet in shared memory and warp 0 reduces them the same way. Small batches
-// (one query spans all 148 CTAs x 16 warps = 23,680 entries at k = 10) get up
-// to 32 warps; large batches (a query spans 1-2 CTAs) get one.
-constexpr int kMergeMaxWarps = 32;
+// Top-k by (dist, id) of the union of the partial lists the scan wrote for a
+// query: every scan CTA whose range intersects the query's groups holds
+// kScanWarps warp lists of k, each SORTED ascending (padding (+inf, -1) last).
+// One CTA of nw warps per query, three phases:
+//  A. the k smallest list HEADS (minima) are found (lanes hold one list head
+//     each; warp lists + a pairwise tree). Their k-th distance T0 bounds the
+//     answer: k distinct entries are <= T0, so the final k-th <= T0, and a
+//     list whose head is > T0 cannot contribute. At most k lists (plus ties)
+//     pass.
+//  B. the indices of the lists with head <= T0 are compacted into shared
+//     memory.
+//  C. warp 0 stages those lists (k coalesced entries each, 32 lists at a
+//     time) in shared memory and k-way merges them: k rounds of a 5-step
+//     warp argmin over the 32 list heads.
+// Batch 1 (148 CTAs x 16 lists) reads 2,368 heads and ~k whole lists instead
+// of 23,680 entries; batch 256 (~32 lists per query) needs one warp.
+constexpr int kMergeMaxWarps = 16;
+constexpr int kMergeMaxLists = 4096;  // >= (scan CTAs) x kScanWarps (checked at launch)
 
-__global__ void k_rank_merge(int nq, int np, int k, int n_cta, const int64_t* __restrict__ item_off,
-                             const float* __restrict__ pdist, const int64_t* __restrict__ pid,
-                             int64_t* __restrict__ out_ids, float* __restrict__ out_dist, Packed* __restrict__ packed) {
+// pairwise tree over the CTA's warp lists; warp 0 ends with the CTA list.
+// Level `stride` reads slots = stride (mod 2 stride) and writes slots = 0
+// (mod 2 stride): one barrier per level.
+__device__ __forceinline__ void cta_tree(float& bd, long long& bid, float& thr, int k, int lane, int warp, int nw,
+                                         float* s_d, long long* s_id) {
+  if (nw == 1) return;
+  s_d[warp * 32 + lane] = lane < k ? bd : CUDART_INF_F;
+  s_id[warp * 32 + lane] = lane < k ? bid : -1;
+  __syncthreads();
+  for (int stride = 1; stride < nw; stride <<= 1) {
+    if ((warp & (2 * stride - 1)) == 0 && warp + stride < nw) {
+      list_offer(bd, bid, thr, s_d[(warp + stride) * 32 + lane], s_id[(warp + stride) * 32 + lane], k, lane);
+      s_d[warp * 32 + lane] = lane < k ? bd : CUDART_INF_F;
+      s_id[warp * 32 + lane] = lane < k ? bid : -1;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kMergeMaxWarps * 32) k_rank_merge(
+    int nq, int np, int k, int n_cta, const int64_t* __restrict__ item_off, const float* __restrict__ pdist,
+    const int64_t* __restrict__ pid, int64_t* __restrict__ out_ids, float* __restrict__ out_dist,
+    Packed* __restrict__ packed) {
   __shared__ float s_d[kMergeMaxWarps * 32];
   __shared__ long long s_id[kMergeMaxWarps * 32];
+  __shared__ float s_t0;
+  __shared__ int s_nrel;
+  __shared__ int s_rel[kMergeMaxLists];        // relevant list indices
+  __shared__ float s_ld[32 * 33];              // staged lists (phase C)
+  __shared__ long long s_lid[32 * 33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int q = blockIdx.x;
   const long long W = item_off[(long long)nq * np];
   const long long S = item_off[(long long)q * np], E = item_off[(long long)(q + 1) * np];
+  const long long* pidl = reinterpret_cast<const long long*>(pid);
   float bd = CUDART_INF_F, thr = CUDART_INF_F;
   long long bid = -1;
+  int cf = 0, nl = 0;  // lists of CTAs cf.. : nl = (#CTAs) x kScanWarps
+  bool maybe_empty = false;
+  auto start = [&](int c) { return (long long)c * W / n_cta; };
   if (E > S) {
-    auto start = [&](int c) { return (long long)c * W / n_cta; };
-    auto cta_of = [&](long long g) {  // largest c with start(c) <= g
-      int lo = 0, hi = n_cta;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (start(mid) <= g) lo = mid; else hi = mid;
-      }
-      return lo;
+    // largest c with start(c) = floor(c W / G) <= g  <=>  c W < (g + 1) G
+    auto cta_of = [&](long long g) {
+      const long long c = ((g + 1) * n_cta - 1) / W;
+      return (int)(c < n_cta - 1 ? c : n_cta - 1);
     };
-    const int cf = cta_of(S), cl = cta_of(E - 1);
-    const int per = kScanWarps * k;  // entries per (CTA, query) partial
-    const int n = (cl - cf + 1) * per;
-    const bool maybe_empty = W < n_cta;  // otherwise every CTA owns >= 1 group
-    const long long base = (long long)(cf + q) * per;  // partials of CTAs cf..cl are contiguous
-    constexpr int U = 8;
-    for (int i0 = warp * 32 * U; i0 < n; i0 += nw * 32 * U) {
-      float d[U];
-      long long id[U];
+    cf = cta_of(S);
+    nl = (cta_of(E - 1) - cf + 1) * kScanWarps;
+    maybe_empty = W < n_cta;  // otherwise every CTA owns >= 1 group
+  }
+  const long long base = (long long)(cf + q) * kScanWarps * k;  // list li starts at base + li * k
+  auto head_ok = [&](int li) { return !maybe_empty || start(cf + li / kScanWarps) != start(cf + li / kScanWarps + 1); };
+  // ---- phase A: k smallest heads
+  constexpr int U = 4;
+  for (int l0 = warp * 32 * U; l0 < nl; l0 += nw * 32 * U) {
+    float d[U];
+    long long id[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * 32 + lane;
-        d[u] = CUDART_INF_F;
-        id[u] = -1;
-        if (i < n) {
-          bool ok = true;
-          if (maybe_empty) {
-            const int c = cf + i / per;
-            ok = start(c) != start(c + 1);  // a CTA without work wrote nothing
-          }
-          if (ok) d[u] = __ldg(pdist + base + i);
-        }
+    for (int u = 0; u < U; ++u) {
+      const int li = l0 + u * 32 + lane;
+      d[u] = CUDART_INF_F;
+      id[u] = -1;
+      if (li < nl && head_ok(li)) {
+        d[u] = __ldg(pdist + base + (long long)li * k);
+        id[u] = __ldg(pidl + base + (long long)li * k);
       }
+    }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool cand = d[u] < CUDART_INF_F && d[u] <= thr;  // (+inf, -1) slots never enter
-        if (__any_sync(kFull, cand)) {
-          const long long my = cand ? __ldg(reinterpret_cast<const long long*>(pid) + base + i0 + u * 32 + lane) : -1;
-          wtk_offer(bd, bid, d[u], cand, k, lane, my);
-          thr = __shfl_sync(kFull, bd, k - 1);
-        }
-      }
+    for (int u = 0; u < U; ++u) offer32(bd, bid, thr, d[u], id[u], d[u] < CUDART_INF_F && d[u] <= thr, k, lane);
+  }
+  cta_tree(bd, bid, thr, k, lane, warp, nw, s_d, s_id);
+  if (warp == 0) {
+    const float t0 = __shfl_sync(kFull, bd, k - 1);
+    if (lane == 0) s_t0 = t0;
+  }
+  __syncthreads();
+  const float t0 = s_t0;
+  // ---- phase B: indices of the lists whose head <= T0 -> shared memory
+  if (threadIdx.x == 0) s_nrel = 0;
+  __syncthreads();
+  for (int l0 = warp * 32; l0 < nl; l0 += nw * 32) {
+    const int li = l0 + lane;
+    float h = CUDART_INF_F;
+    if (li < nl && head_ok(li)) h = __ldg(pdist + base + (long long)li * k);
+    const bool rel = h < CUDART_INF_F && h <= t0;
+    const unsigned rm = __ballot_sync(kFull, rel);
+    if (rm) {
+      int at = 0;
+      if (lane == 0) at = atomicAdd(&s_nrel, __popc(rm));
+      at = __shfl_sync(kFull, at, 0);
+      if (rel) s_rel[at + __popc(rm & ((1u << lane) - 1u))] = li;
     }
   }
-  if (nw > 1) {
-    s_d[warp * 32 + lane] = lane < k ? bd : CUDART_INF_F;
-    s_id[warp * 32 + lane] = lane < k ? bid : -1;
-    __syncthreads();
-    if (warp != 0) return;
-    for (int w = 1; w < nw; ++w) {
-      const float d = s_d[w * 32 + lane];
-      const bool cand = lane < k && d <= thr;
-      if (__any_sync(kFull, cand)) {
-        wtk_offer(bd, bid, d, cand, k, lane, s_id[w * 32 + lane]);
-        thr = __shfl_sync(kFull, bd, k - 1);
+  __syncthreads();
+  if (warp != 0) return;
+  // ---- phase C (warp 0): k-way merge of the relevant sorted lists, 32 at a
+  // time (lane r owns list r of the batch, staged in shared memory)
+  const int nrel = s_nrel;
+  bd = CUDART_INF_F;
+  bid = -1;
+  for (int r0 = 0; r0 < nrel; r0 += 32) {
+    const int nb = nrel - r0 < 32 ? nrel - r0 : 32;
+    for (int r1 = 0; r1 < nb; r1 += 8) {  // stage: k coalesced entries per list, 8 lists' loads in flight
+      float sd[8];
+      long long sid[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int r = r1 + v;
+        if (r < nb && lane < k) {
+          const long long o = base + (long long)s_rel[r0 + r] * k + lane;
+          sd[v] = __ldg(pdist + o);
+          sid[v] = __ldg(pidl + o);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int r = r1 + v;
+        if (r < nb && lane < k) {
+          s_ld[r * 33 + lane] = sd[v];
+          s_lid[r * 33 + lane] = sid[v];
+        }
       }
     }
+    __syncwarp();
+    int p = 0;
+    float hd = lane < nb ? s_ld[lane * 33] : CUDART_INF_F;
+    long long hid = lane < nb ? s_lid[lane * 33] : -1;
+    float od = CUDART_INF_F;
+    long long oid = -1;
+    for (int t = 0; t < k; ++t) {
+      float wd = hd;
+      long long wid = hid;
+      int wl = lane;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const float xd = __shfl_xor_sync(kFull, wd, o);
+        const long long xid = __shfl_xor_sync(kFull, wid, o);
+        const int xl = __shfl_xor_sync(kFull, wl, o);
+        if (lex_less(xd, xid, wd, wid) || (xd == wd && xid == wid && xl < wl)) {
+          wd = xd;
+          wid = xid;
+          wl = xl;
+        }
+      }
+      if (!(wd < CUDART_INF_F)) break;  // only padding left (warp-uniform)
+      if (lane == t) {
+        od = wd;
+        oid = wid;
+      }
+      if (lane == wl) {
+        ++p;
+        hd = p < k ? s_ld[lane * 33 + p] : CUDART_INF_F;
+        hid = p < k ? s_lid[lane * 33 + p] : -1;
+      }
+    }
+    __syncwarp();
+    if (r0 == 0) {
+      bd = od;
+      bid = oid;
+    } else {
+      list_offer(bd, bid, thr, od, oid, k, lane);
+    }
+    thr = __shfl_sync(kFull, bd, k - 1);
   }
   if (lane < k) {
     if (packed) {
@@ -426,10 +549,11 @@ cudaError_t launch_rank_merge(const DeviceIndex& ix, const Workspace& ws, int nq
                               float* out_dist, void* out_packed, cudaStream_t s) {
   (void)ix;
   if (nq <= 0) return cudaSuccess;
-  // expected partial entries per query: (CTAs spanned) x warps x k
-  const long long per_q = ((long long)ws.n_cta / nq + 2) * kScanWarps * k;
+  // expected lists per query: (scan CTAs spanned) x warps
+  const long long lists = ((long long)ws.n_cta / nq + 2) * kScanWarps;
   int nw = 1;
-  while (nw < kMergeMaxWarps && (long long)nw * 512 < per_q) nw <<= 1;
+  while (nw < kMergeMaxWarps && (long long)nw * 128 < lists) nw <<= 1;
+  if ((long long)ws.n_cta * kScanWarps > kMergeMaxLists) return cudaErrorInvalidConfiguration;
   k_rank_merge<<<nq, nw * 32, 0, s>>>(nq, np, k, ws.n_cta, ws.item_off, ws.pdist, ws.pid, out_ids, out_dist,
                                       reinterpret_cast<Packed*>(out_packed));
   return cudaGetLastError();

@@ -55,6 +55,46 @@ __device__ __forceinline__ void wtk_offer(float& bd, long long& bid, float dist,
   }
 }
 
+// Merge one (dist, id) candidate per lane into the warp list with a bitonic
+// network: sort the 32 candidates ascending (15 compare-exchange steps), take
+// the element-wise min with the list reversed (a bitonic sequence holding the
+// 32 smallest of the union), then a 5-step bitonic merge. Lanes without a
+// candidate pass (+inf, -1). ~21 shuffle steps in total: cheaper than
+// wtk_offer once more than ~6 lanes carry candidates.
+__device__ __forceinline__ void wtk_cmpx(float& d, long long& id, int lane, int stride, bool up) {
+  const float od = __shfl_xor_sync(kFull, d, stride);
+  const long long oid = __shfl_xor_sync(kFull, id, stride);
+  const bool lower = (lane & stride) == 0;
+  const bool take_min = lower == up;
+  const bool o_less = lex_less(od, oid, d, id);
+  if (take_min ? o_less : lex_less(d, id, od, oid)) {
+    d = od;
+    id = oid;
+  }
+}
+
+__device__ __forceinline__ void wtk_merge32(float& bd, long long& bid, float d, long long id, int k, int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1)
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) wtk_cmpx(d, id, lane, stride, (lane & size) == 0 || size == 32);
+  // d ascending across lanes; pair list[lane] with cand[31 - lane]
+  const float rd = __shfl_sync(kFull, d, 31 - lane);
+  const long long rid = __shfl_sync(kFull, id, 31 - lane);
+  float ld = lane < k ? bd : CUDART_INF_F;
+  long long lid = lane < k ? bid : -1;
+  if (lex_less(rd, rid, ld, lid)) {
+    ld = rd;
+    lid = rid;
+  }
+#pragma unroll
+  for (int stride = 16; stride > 0; stride >>= 1) wtk_cmpx(ld, lid, lane, stride, true);
+  if (lane < k) {
+    bd = ld;
+    bid = lid;
+  }
+}
+
 // Warp-cooperative k-selection: the running list (lane i < k holds the i-th
 // smallest) is merged with n entries fetched as fetch(i) -> (dist, id), in
 // chunks of 32*E: k rounds of (lane-local min over E entries + list entry,

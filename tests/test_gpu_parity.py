@@ -146,6 +146,20 @@ def test_batch_sizes(c1_index, c1_queries):
     h.close()
 
 
+def test_small_batch_wide_merge():
+    """Batches 1-8 over long lists: one query spans all scan CTAs, so K7 runs
+    its multi-warp path (up to 32 warps, sort-merge and insertion offers)."""
+    ix = datagen.make_index(2_000_000, 128, 1024, 16, device="cuda")
+    h = vlr.Index.from_arrays(ix)
+    Qa = datagen.make_queries(2_000_000, 128, 1024, 16, stream=2)
+    for nq, k in ((1, 10), (1, 32), (1, 1), (3, 10), (8, 32)):
+        Q = Qa[:nq]
+        g = gpu_search(h, Q, 64, k)
+        o = oracle.search(ix, Q, 64, k)
+        assert not check(ix, Q, g, o), (nq, k)
+    h.close()
+
+
 # --------------------------------------------------------------- shapes / m_pad variants
 @pytest.mark.parametrize("d,m,L", [(32, 4, 50), (64, 32, 40), (96, 48, 33), (128, 64, 64), (192, 96, 40),
                                    (256, 128, 70), (40, 20, 17), (64, 16, 1030)])
