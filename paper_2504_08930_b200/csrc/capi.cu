@@ -47,7 +47,7 @@ __global__ void k_negative(const int64_t* ids, long long n, int32_t* flag) {
 }
 
 static void free_ws(Workspace& w) {
-  void* ps[] = {w.qnorm, w.qtf32, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.lut,
+  void* ps[] = {w.qnorm, w.qf16, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.lut,
                 w.pdist, w.pid, w.send, w.recv, w.d_q, w.d_ids, w.d_dist, w.d_miss, w.d_probes, w.status};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -56,7 +56,7 @@ static void free_ws(Workspace& w) {
 }
 
 static void free_index(DeviceIndex& ix) {
-  void* ps[] = {ix.centroids, ix.ctf32, ix.cnorm2, ix.codebooks, ix.owner, ix.local, ix.gbase, ix.codes, ix.bias, ix.ids};
+  void* ps[] = {ix.centroids, ix.cf16, ix.cnorm2, ix.codebooks, ix.owner, ix.local, ix.gbase, ix.codes, ix.bias, ix.ids};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (ix.nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(ix.nccl));
@@ -78,7 +78,8 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   w.n_cta = scan_ctas(ix);
   const size_t nqs = (size_t)cnq;
   VLR_CUDA_TRY(dalloc(&w.qnorm, nqs));
-  VLR_CUDA_TRY(dalloc(&w.qtf32, nqs * ix.d4));
+  VLR_CUDA_TRY(dalloc(&w.qf16, nqs * ix.d8));
+  VLR_CUDA_TRY(dalloc(&w.qinv, nqs));
   VLR_CUDA_TRY(dalloc(&w.dt, nqs * ix.nlist));
   VLR_CUDA_TRY(dalloc(&w.gmin, nqs * ((ix.nlist + 31) / 32)));
   VLR_CUDA_TRY(dalloc(&w.cand, nqs * kCandCap));
@@ -144,12 +145,14 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   // finiteness + centroid norms (fp64)
   std::vector<float> cn2((size_t)L);
   double cmax2 = 0.0;
+  float cabs = 0.f;
   for (int l = 0; l < L; ++l) {
     double s = 0.0;
     const float* c = D.centroids + (size_t)l * d;
     for (int t = 0; t < d; ++t) {
       if (!std::isfinite(c[t])) return fail(VLR_ERR_NONFINITE, "non-finite centroid");
       s += (double)c[t] * c[t];
+      cabs = std::max(cabs, std::fabs(c[t]));
     }
     cn2[l] = (float)s;
     cmax2 = std::max(cmax2, s);
@@ -196,7 +199,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   vlr_index* h = new vlr_index();
   DeviceIndex& ix = h->ix;
   ix.d = d;
-  ix.d4 = (d + 3) / 4 * 4;
+  ix.d8 = (d + 7) / 8 * 8;
   ix.nlist = L;
   ix.m = m;
   ix.dsub = dsub;
@@ -207,6 +210,15 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   ix.device = dev;
   ix.shard_only = cm.world > 1 && cm.nccl_unique_id == nullptr;
   ix.cmax = (float)std::sqrt(cmax2) * 1.0000002f;
+  {  // power-of-two filter scale: max |c| 2^c_exp in [2^13, 2^14) (fp16 range), exponent clamped
+    int e = 0;
+    if (cabs > 0.f) {
+      std::frexp(cabs, &e);  // cabs < 2^e
+      e = std::min(60, std::max(-60, 14 - e));
+    }
+    ix.c_exp = e;
+    ix.c_inv = std::ldexp(1.0f, -e);
+  }
   ix.owner_h = owner;
   auto bail = [&](vlr_status st) {
     free_index(ix);
@@ -240,7 +252,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   ix.n_groups = gbase_h.back();
   LTRY(dalloc(&ix.centroids, (size_t)L * d));
   LTRY(dalloc(&ix.cnorm2, (size_t)L));
-  LTRY(dalloc(&ix.ctf32, (size_t)L * ix.d4));
+  LTRY(dalloc(&ix.cf16, (size_t)L * ix.d8));
   LTRY(dalloc(&ix.codebooks, ncb));
   LTRY(dalloc(&ix.owner, (size_t)L));
   LTRY(dalloc(&ix.local, (size_t)L));
@@ -250,8 +262,8 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   LTRY(dalloc(&ix.ids, (size_t)ix.n_groups * 32));
   LTRY(cudaMemcpyAsync(ix.centroids, D.centroids, sizeof(float) * L * d, cudaMemcpyHostToDevice, s));
   LTRY(cudaMemcpyAsync(ix.cnorm2, cn2.data(), sizeof(float) * L, cudaMemcpyHostToDevice, s));
-  LTRY(launch_round_tf32(ix.centroids, L, d, ix.d4, ix.ctf32, s));
-  LTRY(make_tmap_2d(ix.tmapA, ix.ctf32, L, ix.d4, 128));
+  LTRY(launch_round_f16(ix.centroids, L, d, ix.d8, std::ldexp(1.0f, ix.c_exp), ix.cf16, s));
+  LTRY(make_tmap_2d(ix.tmapA, ix.cf16, L, ix.d8, 128));
   LTRY(cudaMemcpyAsync(ix.codebooks, D.codebooks, sizeof(float) * ncb, cudaMemcpyHostToDevice, s));
   LTRY(cudaMemcpyAsync(ix.owner, owner.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, s));
   LTRY(cudaMemcpyAsync(ix.local, local.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, s));
@@ -328,7 +340,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
     set_error("duplicate vector id among resident vectors");
     return bail(VLR_ERR_DUPLICATE_ID);
   }
-  ix.bytes = (int64_t)L * d * 4 + (int64_t)L * ix.d4 * 4 + L * 4 + (int64_t)ncb * 4 + 2LL * L * 4 + (ix.n_local + 1) * 8 +
+  ix.bytes = (int64_t)L * d * 4 + (int64_t)L * ix.d8 * 2 + L * 4 + (int64_t)ncb * 4 + 2LL * L * 4 + (ix.n_local + 1) * 8 +
              ix.n_groups * 32 * (ix.mpad + 4 + 8);
   // NCCL communicator (collective)
   if (cm.world > 1 && cm.nccl_unique_id) {
@@ -396,8 +408,8 @@ vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t np
   VLR_CUDA_TRY(cudaMemsetAsync(w.status, 0, sizeof(int32_t), s));
   int n = 0;
   rec(h, 0, s);
-  VLR_CUDA_TRY(launch_qprep(Q, nq, ix.d, ix.d4, w.qnorm, w.qtf32, w.status, s)); ++n;
-  VLR_CUDA_TRY(launch_filter_tc(w.qtf32, nq, ix, w.dt, w.gmin, s)); ++n;
+  VLR_CUDA_TRY(launch_qprep(Q, nq, ix.d, ix.d8, w.qnorm, w.qf16, w.qinv, w.status, s)); ++n;
+  VLR_CUDA_TRY(launch_filter_tc(w.qf16, w.qinv, nq, ix, w.dt, w.gmin, s)); ++n;
   rec(h, 1, s);
   VLR_CUDA_TRY(launch_select(ix, w, nq, np, filter_edot(ix.d), s)); ++n;
   rec(h, 2, s);

@@ -12,46 +12,77 @@
 //            Bit-identical to the definition.
 #include <cfloat>
 
+#include <cuda_fp16.h>
+
 #include "vlr_device.cuh"
 #include "vlr_internal.cuh"
 
 namespace vlr {
 
 // ----------------------------------------------------------------- qprep
-__global__ void k_qprep(const float* __restrict__ Q, int d, int d4, float* __restrict__ qnorm,
-                        float* __restrict__ qtf32, int32_t* status) {
+// ||q|| (fp64 sum, rounded up), non-finite check, and the filter operand
+// fp16(q 2^e_q) with 2^e_q the power of two putting max |q_t| 2^e_q in
+// [2^13, 2^14) (exponent clamped to [-60, 60]; DESIGN.md §5 bounds the
+// subnormal flush that clamping can cause).
+__global__ void k_qprep(const float* __restrict__ Q, int d, int d8, float* __restrict__ qnorm,
+                        uint16_t* __restrict__ qf16, float* __restrict__ qinv, int32_t* status) {
   const int q = blockIdx.x;
   const float* row = Q + (size_t)q * d;
   double s = 0.0;
+  float mx = 0.f;
   bool bad = false;
-  for (int t = threadIdx.x; t < d4; t += blockDim.x) {
-    float v = t < d ? row[t] : 0.f;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) {
+    const float v = row[t];
     bad |= !isfinite(v);
     s += (double)v * (double)v;
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
-    qtf32[(size_t)q * d4 + t] = __uint_as_float(r);
+    mx = fmaxf(mx, fabsf(v));
   }
   __shared__ double red[32];
+  __shared__ float redm[32];
   __shared__ int sbad;
+  __shared__ float s_scale;
   if (threadIdx.x == 0) sbad = 0;
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(kFull, s, o);
+    mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+  }
   __syncthreads();
   if (bad) atomicOr(&sbad, 1);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = s;
+    redm[threadIdx.x >> 5] = mx;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    float m = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      t += red[w];
+      m = fmaxf(m, redm[w]);
+    }
     qnorm[q] = (float)sqrt(t) * 1.0000002f;
+    int e = 0;
+    if (m > 0.f && isfinite(m)) {
+      frexpf(m, &e);  // m < 2^e
+      e = 14 - e;
+      e = e < -60 ? -60 : (e > 60 ? 60 : e);
+    }
+    s_scale = ldexpf(1.f, e);
+    qinv[q] = ldexpf(1.f, -e);
     if (sbad) atomicOr(status, 1);
+  }
+  __syncthreads();
+  const float sc = s_scale;
+  for (int t = threadIdx.x; t < d8; t += blockDim.x) {
+    const float v = t < d ? row[t] * sc : 0.f;
+    qf16[(size_t)q * d8 + t] = __half_as_ushort(__float2half_rn(v));
   }
 }
 
-cudaError_t launch_qprep(const float* Q, int nq, int d, int d4, float* qnorm, float* qtf32, int32_t* status,
-                         cudaStream_t s) {
+cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, uint16_t* qf16, float* qinv,
+                         int32_t* status, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  k_qprep<<<nq, 256, 0, s>>>(Q, d, d4, qnorm, qtf32, status);
+  k_qprep<<<nq, 256, 0, s>>>(Q, d, d8, qnorm, qf16, qinv, status);
   return cudaGetLastError();
 }
 
@@ -67,7 +98,8 @@ constexpr int kSelMaxGroups = 16384;  // nlist <= 512K for the sorted-minima pat
 
 __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restrict__ dt, const float* __restrict__ gmin,
                                                         int L, int np, const float* __restrict__ qnorm, float cmax,
-                                                        float e_dot, int32_t* __restrict__ cand,
+                                                        float e_dot, float e_abs, const float* __restrict__ qinv,
+                                                        float c_inv, int32_t* __restrict__ cand,
                                                         int32_t* __restrict__ ncand, float* __restrict__ bound_out) {
   extern __shared__ unsigned skeys[];
   __shared__ unsigned s_cnt;
@@ -128,7 +160,13 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
   }
   const float qn = qnorm[q];
   const float u = 5.9604645e-8f;  // 2^-24
-  const float delta = 2.0f * (2.0f * (e_dot + 2.0f * u) * qn * cmax + 4.0f * u * (cmax * cmax + qn * qn));
+  // fp16 subnormal flush of the scaled operands (absolute):
+  // A = sqrt(d) 2^-25 (||q|| c_inv + c_max q_inv)(1 + 2^-11) + d 2^-50 c_inv q_inv,
+  // e_abs = sqrt(d) 2^-25 (1 + 2^-11), d 2^-50 = e_abs^2 / (1 + 2^-11)^2 <= e_abs^2
+  const float qi = qinv[q];
+  const float abs_dot = e_abs * (qn * c_inv + cmax * qi) + e_abs * e_abs * (c_inv * qi) + 1.2e-38f;
+  const float delta = 2.0f * (2.0f * (e_dot + 2.0f * u) * qn * cmax + 4.0f * u * (cmax * cmax + qn * qn) +
+                              2.0f * abs_dot);
   const float bnd = theta + 2.0f * delta;
   if (threadIdx.x == 0) {
     s_cnt = 0u;
@@ -190,8 +228,9 @@ cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, in
     if (e != cudaSuccess) return e;
     configured = sm;
   }
-  k_select<<<nq, kSelThreads, sm, s>>>(ws.dt, ws.gmin, ix.nlist, np, ws.qnorm, ix.cmax, e_dot, ws.cand, ws.ncand,
-                                       ws.bound);
+  const float e_abs = sqrtf((float)ix.d) * 2.9802322e-8f * 1.00049f * 1.0001f;  // sqrt(d) 2^-25 (1 + 2^-11), rounded up
+  k_select<<<nq, kSelThreads, sm, s>>>(ws.dt, ws.gmin, ix.nlist, np, ws.qnorm, ix.cmax, e_dot, e_abs, ws.qinv,
+                                       ix.c_inv, ws.cand, ws.ncand, ws.bound);
   return cudaGetLastError();
 }
 

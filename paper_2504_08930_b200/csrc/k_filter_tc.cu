@@ -2,20 +2,24 @@
 //
 // dt[q][l] = ||c_l||^2 - 2 <q~, c~_l>   (the coarse-quantizer contraction,
 // stage 1 of Fig. 2; ||q||^2 is constant per query)
-// with q~, c~ the operands rounded to TF32 (cvt.rna) beforehand, so the
-// tensor core's own input conversion is exact; fp32 accumulation in TMEM.
+// with q~ = fp16(q 2^e_q) 2^-e_q and c~ = fp16(c 2^e_c) 2^-e_c: operands
+// scaled by powers of two (max |x 2^e| < 2^14, so no fp16 overflow) and
+// rounded to fp16 (RN, 11-bit significand: the same relative precision as
+// TF32 at half the bytes and twice the MMA rate); products exact, fp32
+// accumulation in TMEM; the epilogue multiplies by 2^-(e_q + e_c) exactly.
 //
 // Swap-AB: A = a 128-centroid tile (M = 128, K-major rows of the centroid
 // matrix), B = the query batch (N = up to 256 per accumulator, two
 // accumulators for up to 512 queries), so a small batch still fills the
 // 128-row MMA. Warp roles (192 threads): warp 0 = TMA producer (one elected
 // lane: cp.async.bulk.tensor 2D, SWIZZLE_128B, mbarrier complete_tx),
-// warp 1 = TMEM allocator + MMA issuer (one lane: tcgen05.mma.kind::tf32,
+// warp 1 = TMEM allocator + MMA issuer (one lane: tcgen05.mma.kind::f16,
 // tcgen05.commit -> mbarriers), warps 2-5 = epilogue (tcgen05.ld 32x32b,
 // thread i <-> TMEM lane i <-> centroid m0+i; coalesced stores of dt).
 // The error of dt w.r.t. the exact D - ||q||^2 is bounded in DESIGN.md §5
 // (band proof); K2/K3 make the probes exact.
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "vlr_device.cuh"
 #include "vlr_internal.cuh"
@@ -23,7 +27,7 @@
 namespace vlr {
 
 constexpr int kTcM = 128;        // centroids per tile (MMA M)
-constexpr int kTcBK = 32;        // fp32 elements per K block (128 B = one SW128 row)
+constexpr int kTcBK = 64;        // fp16 elements per K block (128 B = one SW128 row)
 constexpr int kTcThreads = 192;  // 6 warps
 constexpr int kTcMaxStages = 6;
 
@@ -65,11 +69,11 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-__device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
+__device__ __forceinline__ void mma_f16(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -79,12 +83,14 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_filter_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int L, int nq,
-                int kblocks, int nN, int nacc, int stages, const float* __restrict__ cn2, float* __restrict__ dt,
-                float* __restrict__ gmin, int ngroups) {
+                int kblocks, int nN, int nacc, int stages, const float* __restrict__ cn2,
+                const float* __restrict__ qinv, float c_inv, float* __restrict__ dt, float* __restrict__ gmin,
+                int ngroups) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull;
   __shared__ uint32_t tmem_base;
+  __shared__ float s_inv[512];  // per query column: 2^-(e_q + e_c)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * kTcM;
   const int q0 = blockIdx.y * (nN * nacc);
@@ -129,8 +135,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // instruction descriptor: F32 accum, A/B TF32, K-major, N, M = 128
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(nN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+      // instruction descriptor: F32 accum, A/B F16, K-major, N, M = 128
+      const uint32_t idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(nN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
       for (int kb = 0; kb < kblocks; ++kb) {
         const int s = kb % stages;
         const uint32_t ph = (uint32_t)(kb / stages) & 1u;
@@ -139,11 +145,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t aaddr = s32(smem + (size_t)s * stage_bytes);
         const uint32_t baddr = aaddr + bytesA;
 #pragma unroll
-        for (int kk = 0; kk < kTcBK / 8; ++kk) {  // K = 8 tf32 (32 B) per MMA
+        for (int kk = 0; kk < kTcBK / 16; ++kk) {  // K = 16 fp16 (32 B) per MMA
           const uint64_t ad = sw128_desc(aaddr + kk * 32);
           for (int acc = 0; acc < nacc; ++acc) {
             const uint64_t bd = sw128_desc(baddr + (uint32_t)(acc * nN * 128) + kk * 32);
-            mma_tf32(tbase + (uint32_t)(acc * nN), ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            mma_f16(tbase + (uint32_t)(acc * nN), ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
         }
         mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
@@ -156,6 +162,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int lg = warp & 3;
     const int row = m0 + lg * 32 + lane;
     const float cn = row < L ? cn2[row] : 0.f;
+    for (int j = threadIdx.x - 64; j < ncols_used; j += 128) {
+      const int q = q0 + j;
+      s_inv[j] = q < nq ? qinv[q] * c_inv : 0.f;  // product of powers of two >= 2^-120: exact
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
     mb_wait(&tfull, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
     // 32 query columns at a time: dt stores (lanes = 32 consecutive centroids,
@@ -185,7 +196,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       float f[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        f[j] = row < L ? cn - 2.f * __uint_as_float(v[j]) : CUDART_INF_F;
+        f[j] = row < L ? cn - 2.f * (__uint_as_float(v[j]) * s_inv[c + j]) : CUDART_INF_F;
         const int q = q0 + c + j;
         if (row < L && q < nq && c + j < ncols_used) dt[(size_t)q * L + row] = f[j];
       }
@@ -228,22 +239,23 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2-D fp32 tensor [rows][cols] (cols = d4, row stride d4*4 B), box {32, box_rows}, SW128
-cudaError_t make_tmap_2d(void* map_, const float* base, int rows, int cols, int box_rows) {
+// 2-D fp16 tensor [rows][cols] (cols = d8, row stride d8*2 B), box {64, box_rows}, SW128
+cudaError_t make_tmap_2d(void* map_, const uint16_t* base, int rows, int cols, int box_rows) {
   CUtensorMap* map = reinterpret_cast<CUtensorMap*>(map_);
   EncodeTiledFn fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(uint16_t)};
   cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<uint16_t*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, float* dt, float* gmin, cudaStream_t s) {
+cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, float* dt, float* gmin,
+                             cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
   int nacc, nN;
   if (nq <= 256) {
@@ -255,7 +267,7 @@ cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, flo
   }
   const int box_rows_b = nN < 256 ? nN : 256;
   CUtensorMap tmB;
-  cudaError_t e = make_tmap_2d(&tmB, Qt, nq, ix.d4, box_rows_b);
+  cudaError_t e = make_tmap_2d(&tmB, Qh, nq, ix.d8, box_rows_b);
   if (e != cudaSuccess) return e;
   const uint32_t stage_bytes = kTcM * 128 + (uint32_t)(nacc * nN * 128);
   // ~100 KB of stages so that two CTAs share an SM: one CTA's epilogue
@@ -270,36 +282,32 @@ cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, flo
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  const int kblocks = (ix.d4 + kTcBK - 1) / kTcBK;
+  const int kblocks = (ix.d8 + kTcBK - 1) / kTcBK;
   dim3 grid((ix.nlist + kTcM - 1) / kTcM, (nq + nN * nacc - 1) / (nN * nacc));
   k_filter_tc<<<grid, kTcThreads, smem, s>>>(*reinterpret_cast<const CUtensorMap*>(ix.tmapA), tmB, ix.nlist, nq,
-                                              kblocks, nN, nacc, stages, ix.cnorm2, dt, gmin,
+                                              kblocks, nN, nacc, stages, ix.cnorm2, qinv, ix.c_inv, dt, gmin,
                                               (ix.nlist + 31) / 32);
   return cudaGetLastError();
 }
 
-// TF32 rounding (round to nearest, ties away: cvt.rna) into a d4-padded copy
-__global__ void k_round_tf32(const float* __restrict__ src, int rows, int d, int d4, float* __restrict__ dst) {
-  const long long n = (long long)rows * d4;
+// fp16(c * scale) (round to nearest even) into a d8-padded copy; scale is a power of two
+__global__ void k_round_f16(const float* __restrict__ src, int rows, int d, int d8, float scale,
+                            uint16_t* __restrict__ dst) {
+  const long long n = (long long)rows * d8;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / d4;
-    const int c = (int)(i - r * d4);
-    float v = 0.f;
-    if (c < d) {
-      uint32_t t;
-      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(src[r * d + c]));
-      v = __uint_as_float(t);
-    }
-    dst[i] = v;
+    const long long r = i / d8;
+    const int c = (int)(i - r * d8);
+    const float v = c < d ? src[r * d + c] * scale : 0.f;
+    dst[i] = __half_as_ushort(__float2half_rn(v));
   }
 }
 
-cudaError_t launch_round_tf32(const float* src, int rows, int d, int d4, float* dst, cudaStream_t s) {
+cudaError_t launch_round_f16(const float* src, int rows, int d, int d8, float scale, uint16_t* dst, cudaStream_t s) {
   if (rows <= 0) return cudaSuccess;
-  long long n = (long long)rows * d4;
+  long long n = (long long)rows * d8;
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  k_round_tf32<<<(int)blocks, 256, 0, s>>>(src, rows, d, d4, dst);
+  k_round_f16<<<(int)blocks, 256, 0, s>>>(src, rows, d, d8, scale, dst);
   return cudaGetLastError();
 }
 

@@ -41,14 +41,16 @@ void set_error(const std::string& msg);
 
 // ---------------------------------------------------------------- device data
 struct DeviceIndex {
-  int d = 0, d4 = 0, nlist = 0, m = 0, mpad = 0, npairs = 0, dsub = 0;
+  int d = 0, d8 = 0, nlist = 0, m = 0, mpad = 0, npairs = 0, dsub = 0;
   int rank = 0, world = 1, device = 0;
   bool shard_only = false;
   // replicated, coarse quantizer
   float* centroids = nullptr;  // [nlist][d]
   float* cnorm2 = nullptr;     // [nlist] ||c||^2 (fp64 -> fp32)
-  float* ctf32 = nullptr;      // [nlist][d4] centroids rounded to TF32 (cvt.rna), zero-padded to d4
-  alignas(64) unsigned char tmapA[128] = {};  // CUtensorMap of ctf32 (box 32 x 128, SWIZZLE_128B)
+  uint16_t* cf16 = nullptr;    // [nlist][d8] fp16(c * 2^c_exp) (RN), zero-padded to d8 (filter operand A)
+  int c_exp = 0;               // power-of-two centroid scale: max |c * 2^c_exp| < 2^14
+  float c_inv = 1.f;           // 2^-c_exp
+  alignas(64) unsigned char tmapA[128] = {};  // CUtensorMap of cf16 (box 64 x 128, SWIZZLE_128B)
   float cmax = 0.f;            // max ||c|| (host), for the filter band
   float* codebooks = nullptr;  // [m][256][dsub]
   int32_t* owner = nullptr;    // [nlist] owner rank or -1 (mapping table)
@@ -68,7 +70,8 @@ struct DeviceIndex {
 struct Workspace {
   int cap_nq = 0, cap_np = 0, cap_k = 0, n_cta = 0;
   float* qnorm = nullptr;      // [nq] ||q|| (fp32)
-  float* qtf32 = nullptr;      // [nq][d4] queries rounded to TF32, zero-padded
+  uint16_t* qf16 = nullptr;    // [nq][d8] fp16(q * 2^e_q) (RN), zero-padded (filter operand B)
+  float* qinv = nullptr;       // [nq] 2^-e_q
   float* dt = nullptr;         // [nq][nlist] filter distances ||c||^2 - 2<q,c>
   float* gmin = nullptr;       // [nq][ceil(nlist/32)] min of dt over each 32-centroid group
   int32_t* cand = nullptr;     // [nq][kCandCap]
@@ -117,11 +120,12 @@ namespace vlr {
 cudaError_t launch_layout(const DeviceIndex& ix, const uint8_t* stage_codes, const int64_t* stage_ids,
                           const int64_t* vbase, const int32_t* lglob, cudaStream_t s);
 // stage 0..2 coarse quantizer
-cudaError_t launch_qprep(const float* Q, int nq, int d, int d4, float* qnorm, float* qtf32, int32_t* status,
+cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, uint16_t* qf16, float* qinv, int32_t* status,
                          cudaStream_t s);
-cudaError_t launch_filter_tc(const float* Qt, int nq, const DeviceIndex& ix, float* dt, float* gmin, cudaStream_t s);
-cudaError_t launch_round_tf32(const float* src, int rows, int d, int d4, float* dst, cudaStream_t s);
-cudaError_t make_tmap_2d(void* map, const float* base, int rows, int cols, int box_rows);
+cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, float* dt, float* gmin,
+                             cudaStream_t s);
+cudaError_t launch_round_f16(const float* src, int rows, int d, int d8, float scale, uint16_t* dst, cudaStream_t s);
+cudaError_t make_tmap_2d(void* map, const uint16_t* base, int rows, int cols, int box_rows);
 cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float band_rel,
                           cudaStream_t s);
 cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s);
