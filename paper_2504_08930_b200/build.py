@@ -40,15 +40,20 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile every csrc/*.cu for sm_100a and link libvlr.so. `out`/`defines`
+    build a tuning variant elsewhere (tools/variants.py); the product library
+    is always LIB with no extra defines."""
+    lib_path = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
     nd = nccl_dir()
     objs = []
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
               f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}", f"-I{os.path.join(nd, 'include')}",
               "--expt-relaxed-constexpr"]
-    bdir = os.path.join(HERE, "_build")
+    common += [f"-D{d}" for d in defines]
+    bdir = os.path.join(HERE, "_build") if out is None else out + ".objs"
     os.makedirs(bdir, exist_ok=True)
     procs = []
     for src in sources():
@@ -66,12 +71,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stdout.write(f"nvcc failed: {src}\n")
     if failed:
         raise RuntimeError("libvlr build failed")
-    tmp = LIB + ".tmp"
+    tmp = lib_path + ".tmp"
     link = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, f"-L{os.path.join(nd, 'lib')}", "-l:libnccl.so.2",
             f"-Xlinker", f"-rpath={os.path.join(nd, 'lib')}"]
     subprocess.run(link, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":

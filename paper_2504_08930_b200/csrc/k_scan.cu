@@ -30,7 +30,10 @@
 
 namespace vlr {
 
-constexpr int kPfDist = 2;  // L2 prefetch distance (in this warp's groups) beyond the register buffer
+#ifndef VLR_PF_DIST
+#define VLR_PF_DIST 2
+#endif
+constexpr int kPfDist = VLR_PF_DIST;  // L2 prefetch distance (in this warp's groups) beyond the register buffer
 
 struct ScanArgs {
   int nq, np, k, npairs;

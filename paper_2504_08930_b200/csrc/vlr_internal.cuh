@@ -16,7 +16,10 @@ namespace vlr {
 constexpr int kWarp = 32;
 constexpr int kMaxK = 32;          // warp-register top-k (one entry per lane)
 constexpr int kMaxM = 128;         // padded sub-quantizer count of the scan kernel
-constexpr int kScanThreads = 512;  // 16 warps per scan CTA
+#ifndef VLR_SCAN_THREADS
+#define VLR_SCAN_THREADS 512
+#endif
+constexpr int kScanThreads = VLR_SCAN_THREADS;  // 16 warps per scan CTA (tuning variants: tools/variants.py)
 constexpr int kScanWarps = kScanThreads / kWarp;
 constexpr int kCandCap = 4096;     // K2 candidate list capacity per query (overflow -> rescan)
 constexpr int kRefineChunk = 1024; // K3 candidates per exact-refine flush
