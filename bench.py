@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--oracle-seconds", type=float, default=15.0)
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--ncu", action="store_true", help="short run for ncu: no e2e/oracle/clocks")
+    p.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampling")
+    p.add_argument("--dump-lat", default=None, help="diagnostics: write per-step latencies (ms) and scan times here")
     p.add_argument("--sweep-out", default=None,
                    help="also run the C5 batch x nprobe sweep on the same index and write JSON lines here")
     return p.parse_args()
@@ -133,8 +135,10 @@ class Clocks:
         mx = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(rows), "power_w_median": float(np.median(pw)) if pw else None,
+                "power_w_max": max(pw) if pw else None}
 
 
 def dist_setup():
@@ -312,10 +316,10 @@ def main():
     for i in range(a.warmup):
         h.search(Qdev[i], c["nprobe"], K, out=outs[0], stream=stream)
     torch.cuda.synchronize()
-    h.set_profiling(True)
+    h.set_profiling(2)  # timed region: only the two events around the scan (roofline), nothing else
     launches = h.last_launch_count
     clocks = Clocks(local)
-    if not a.ncu:
+    if not a.ncu and not a.no_clocks:
         clocks.start()
         time.sleep(0.3)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
@@ -330,14 +334,23 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
-    clk = clocks.stop() if not a.ncu else None
-    h.set_profiling(False)
+    clk = clocks.stop() if not a.ncu and not a.no_clocks else None
     ms_total = allmax(e0.elapsed_time(e1), world)
     lat = np.array([s.elapsed_time(e) for s, e in ev])
     nrec = min(a.steps, 64)
-    stages = [h.stage_times(back=j) for j in range(nrec)]
+    scan_ms = np.array([h.stage_times(back=j)["scan"] for j in range(nrec)][::-1])  # oldest first
+    if a.dump_lat and rank == 0:
+        with open(a.dump_lat, "w") as f:
+            json.dump({"lat_ms": lat.tolist(), "scan_ms_last64": scan_ms.tolist()}, f)
+    # ---- stage breakdown: a separate, untimed pass with events at every stage boundary
+    h.set_profiling(1)
+    nprof = min(a.steps, 16)
+    for i in range(nprof):
+        h.search(Qdev[a.warmup + i], c["nprobe"], K, out=outs[i], stream=stream)
+    torch.cuda.synchronize()
+    h.set_profiling(False)
+    stages = [h.stage_times(back=j) for j in range(nprof)]
     stage_mean = {k2: float(np.mean([s[k2] for s in stages])) for k2 in stages[0]}
-    scan_ms = np.array([s["scan"] for s in stages[::-1]])  # oldest first -> steps a.steps-nrec .. a.steps-1
     # ---- algorithmic scan bytes: sum over owned hot probes of n_l * (m + 4)
     sizes = ix.list_sizes
     per_vec = c["m"] + 4
@@ -415,12 +428,15 @@ def main():
                        "l2": "inputs larger than L2 (index %.1f GB/GPU, %.2f GB scanned per batch)" % (
                            info["bytes_on_device"] / 1e9, float(step_bytes.mean()) / 1e9)},
             "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+            "lat_ms_top5": [round(float(x), 4) for x in np.sort(lat)[::-1][:5]],
             "gpu_launches": int(launches * a.steps),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "k_scan (K6 ADC scan)", "peak_source": peak_src,
                          "bytes_per_launch": float(bytes_rec.mean()), "ms_per_launch": float(scan_ms.mean())},
             "coarse_roofline": coarse_roof,
             "stage_ms": stage_mean,
+            "stage_ms_source": "separate untimed pass (16 searches) with CUDA events at every stage boundary; "
+                               "the timed region records only the two events around the scan",
             "hit_rate_mean": float(np.mean(np.concatenate(hit))),
             "e2e": e2e, "clocks": clk, "cpu_baseline": cpu, "parity_sample": par, "recall": recall,
             "gen_s": round(gen_s, 1), "load_s": round(load_s, 1),
@@ -470,6 +486,7 @@ def sweep(a, c, h, pool, world, rank):
             if rank == 0:
                 lines.append({"batch": B, "nprobe": npb, "k": K, "n_gpus": world, "qps": steps * B / (tot * 1e-3),
                               "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+            "lat_ms_top5": [round(float(x), 4) for x in np.sort(lat)[::-1][:5]],
                               "steps": steps})
     if rank == 0:
         with open(a.sweep_out, "w") as f:

@@ -169,8 +169,11 @@ vlr_status vlr_index_owners(const vlr_index* idx, int32_t* out_owner);
  * search stream into a ring of the last 64 searches). Stage order: 0 coarse
  * filter (qprep + K1), 1 select (K2), 2 refine (K3), 3 route (K4), 4 LUT (K5),
  * 5 scan (K6), 6 rank merge (K7), 7 exchange + merge (K8).
- * vlr_stage_times waits for search number `back` before the last one
- * (back = 0: the last search; back < 64) and writes min(n, 8) ms values. */
+ * enable: 0 off, 1 every stage boundary (9 events per search), 2 only the
+ * two events around the scan (the bench's timed region: stage 5 valid, the
+ * others NaN). vlr_stage_times waits for search number `back` before the
+ * last one (back = 0: the last search; back < 64) and writes min(n, 8) ms
+ * values. INVALID_ARG for another mode or a search that was not recorded. */
 vlr_status vlr_set_profiling(vlr_index* idx, int32_t enable);
 vlr_status vlr_stage_times(vlr_index* idx, int32_t back, float* ms, int32_t n);
 

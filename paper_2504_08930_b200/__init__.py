@@ -214,7 +214,9 @@ class Index:
         return out
 
     def set_profiling(self, enable=True):
-        _check(lib().vlr_set_profiling(self._h, 1 if enable else 0))
+        """True/1: events at every stage boundary; 2: only around the scan; False/0: off."""
+        mode = int(enable) if not isinstance(enable, bool) else (1 if enable else 0)
+        _check(lib().vlr_set_profiling(self._h, mode))
 
     STAGES = ["coarse_filter", "select", "refine", "route", "lut", "scan", "rank_merge", "exchange_merge"]
 

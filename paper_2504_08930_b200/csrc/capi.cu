@@ -3,6 +3,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <limits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -381,7 +382,9 @@ vlr_status vlr_reserve(vlr_index* h, int32_t max_nq, int32_t max_nprobe, int32_t
 }
 
 static inline void rec(vlr_index* h, int i, cudaStream_t s) {
-  if (h->profiling) cudaEventRecord(h->ev[h->nsearch % vlr_index::kRing][i], s);
+  // mode 1: every stage boundary; mode 2: only around the scan (events 5, 6)
+  if (h->profiling == 1 || (h->profiling == 2 && (i == 5 || i == 6)))
+    cudaEventRecord(h->ev[h->nsearch % vlr_index::kRing][i], s);
 }
 
 vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
@@ -439,7 +442,7 @@ vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t np
   rec(h, 8, s);
   VLR_CUDA_TRY(cudaMemcpyAsync(w.h_status, w.status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   h->launches = n;
-  if (h->profiling) ++h->nsearch;
+  if (h->profiling) h->prof_mode[h->nsearch++ % vlr_index::kRing] = h->profiling;
   return VLR_OK;
 }
 
@@ -525,7 +528,8 @@ vlr_status vlr_set_profiling(vlr_index* h, int32_t enable) {
     for (auto& row : h->ev)
       for (auto& e : row) VLR_CUDA_TRY(cudaEventCreate(&e));
   }
-  h->profiling = enable != 0;
+  if (enable < 0 || enable > 2) return fail(VLR_ERR_INVALID_ARG, "profiling mode must be 0, 1 or 2");
+  h->profiling = enable;
   return VLR_OK;
 }
 
@@ -534,9 +538,16 @@ vlr_status vlr_stage_times(vlr_index* h, int32_t back, float* ms, int32_t n) {
   if (!h->ev[0][0]) return fail(VLR_ERR_INVALID_ARG, "profiling never enabled");
   if (back < 0 || back >= vlr_index::kRing || back >= h->nsearch)
     return fail(VLR_ERR_INVALID_ARG, "no such recorded search");
-  cudaEvent_t* ev = h->ev[(h->nsearch - 1 - back) % vlr_index::kRing];
-  VLR_CUDA_TRY(cudaEventSynchronize(ev[8]));
+  const int slot = (int)((h->nsearch - 1 - back) % vlr_index::kRing);
+  cudaEvent_t* ev = h->ev[slot];
   const int stages = std::min(n, 8);
+  if (h->prof_mode[slot] == 2) {  // scan only
+    VLR_CUDA_TRY(cudaEventSynchronize(ev[6]));
+    for (int i = 0; i < stages; ++i) ms[i] = std::numeric_limits<float>::quiet_NaN();
+    if (stages > 5) VLR_CUDA_TRY(cudaEventElapsedTime(&ms[5], ev[5], ev[6]));
+    return VLR_OK;
+  }
+  VLR_CUDA_TRY(cudaEventSynchronize(ev[8]));
   for (int i = 0; i < stages; ++i) {
     float t = 0.f;
     VLR_CUDA_TRY(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));

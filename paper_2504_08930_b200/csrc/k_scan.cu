@@ -30,10 +30,14 @@
 
 namespace vlr {
 
+// Optional per-lane L2 line prefetch kPfDist groups (of this warp) beyond the
+// register double buffer. Off by default: distances 1-4 measured no faster
+// than 0 at C4 (profiles/r01_summary.md), and the extra L2 requests cost power
+// under sustained load (tools/sustained.py: -0.8% mean step time without).
 #ifndef VLR_PF_DIST
-#define VLR_PF_DIST 2
+#define VLR_PF_DIST 0
 #endif
-constexpr int kPfDist = VLR_PF_DIST;  // L2 prefetch distance (in this warp's groups) beyond the register buffer
+constexpr int kPfDist = VLR_PF_DIST;
 
 struct ScanArgs {
   int nq, np, k, npairs;
@@ -271,12 +275,14 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
     }
     while (gg < seg_end) {
       const long long gn = gg + kScanWarps;
-      if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP>(a, gn + kPfDist * kScanWarps, itp, lane);
+      if constexpr (kPfDist > 0)
+        if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP>(a, gn + kPfDist * kScanWarps, itp, lane);
       if (gn < seg_end) grp_load<MP, EXP>(B, a, gn, it, lane);
       grp_finish<MP, EXP>(A, a, lutc, lane4, lane, bd, bid, thr);
       if (gn >= seg_end) break;
       const long long gm = gn + kScanWarps;
-      if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP>(a, gm + kPfDist * kScanWarps, itp, lane);
+      if constexpr (kPfDist > 0)
+        if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP>(a, gm + kPfDist * kScanWarps, itp, lane);
       if (gm < seg_end) grp_load<MP, EXP>(A, a, gm, it, lane);
       grp_finish<MP, EXP>(B, a, lutc, lane4, lane, bd, bid, thr);
       gg = gm;

@@ -107,9 +107,10 @@ struct Workspace {
 struct vlr_index {
   vlr::DeviceIndex ix;
   vlr::Workspace ws;
-  bool profiling = false;
+  int profiling = 0;  // 0 off, 1 every stage, 2 scan only
   static constexpr int kRing = 64;
   cudaEvent_t ev[kRing][9] = {};
+  int prof_mode[kRing] = {};
   int64_t nsearch = 0;       // searches recorded while profiling
   int launches = 0;
   bool dead = false;  // NCCL failure

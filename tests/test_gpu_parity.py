@@ -330,3 +330,29 @@ def test_access_counts_and_hot_set(c1_index):
     h2.close()
     eta = 1.0 - g2["miss"].mean(axis=1)
     assert abs(eta.mean() - datagen.coverage_mean_hitrate(cnt, hot)) < 1e-12
+
+
+def test_profiling_modes(c1_index, c1_queries):
+    """Stage timing: mode 1 = every stage boundary, mode 2 = scan only (the
+    bench's timed region); results do not depend on profiling."""
+    h = vlr.Index.from_arrays(c1_index)
+    Q = c1_queries[:64]
+    base = gpu_search(h, Q, 16, 10)
+    h.set_profiling(1)
+    g1 = gpu_search(h, Q, 16, 10)
+    st = h.stage_times()
+    assert all(np.isfinite(v) and v >= 0 for v in st.values()), st
+    assert st["scan"] > 0
+    h.set_profiling(2)
+    g2 = gpu_search(h, Q, 16, 10)
+    st2 = h.stage_times()
+    assert np.isfinite(st2["scan"]) and st2["scan"] > 0
+    assert all(np.isnan(v) for k2, v in st2.items() if k2 != "scan"), st2
+    assert h.stage_times(back=1)["select"] >= 0  # the mode-1 search is still in the ring
+    h.set_profiling(False)
+    with pytest.raises(vlr.VlrError):
+        h.set_profiling(3)
+    for g in (g1, g2):
+        for key in base:
+            assert np.array_equal(base[key], g[key]), key
+    h.close()
