@@ -416,6 +416,16 @@ def main():
                        "frac": tfs / tp, "peak_source": tp_src, "flops_per_launch": fl,
                        "ms_per_launch": cf_ms, "hbm_gbs": cbytes / (cf_ms * 1e-3) / 1e9,
                        "kernel": "k_qprep + k_filter_tc (K1)"}
+    # ---- residency (P:214 hit rate eta_q = 1 - sum_p miss / nprobe'; rho = resident share of the index)
+    hq = np.concatenate(hit)
+    sizes_all = ix.list_sizes
+    hot_ids = np.arange(c["nlist"]) if hot is None else np.asarray(hot)
+    residency = {"lists": float(len(hot_ids) / c["nlist"]),
+                 "vectors": float(sizes_all[hot_ids].sum() / max(1, sizes_all.sum())),
+                 "eta_q": {"mean": float(hq.mean()), "p10": float(np.percentile(hq, 10)),
+                           "p50": float(np.percentile(hq, 50)), "p90": float(np.percentile(hq, 90)),
+                           "all_hit_share": float((hq == 1.0).mean()), "all_miss_share": float((hq == 0.0).mean())},
+                 "calibration_mass": c["hot_mass"]}
     value = a.steps * B / (ms_total * 1e-3)
     if rank == 0:
         line = {
@@ -438,6 +448,7 @@ def main():
             "stage_ms_source": "separate untimed pass (16 searches) with CUDA events at every stage boundary; "
                                "the timed region records only the two events around the scan",
             "hit_rate_mean": float(np.mean(np.concatenate(hit))),
+            "residency": residency,
             "e2e": e2e, "clocks": clk, "cpu_baseline": cpu, "parity_sample": par, "recall": recall,
             "gen_s": round(gen_s, 1), "load_s": round(load_s, 1),
         }
