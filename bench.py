@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--hot-mass", type=float, default=1.0)
     p.add_argument("--alpha", type=float, default=None)
     p.add_argument("--seed", type=int, default=2504_08930)
+    p.add_argument("--metric", type=int, default=0, choices=[0, 1], help="0 squared L2, 1 inner product (NEXT-3)")
+    p.add_argument("--by-residual", type=int, default=1, choices=[0, 1], help="1 residual PQ codes (NEXT-3: 0)")
     p.add_argument("--no-oracle", action="store_true")
     p.add_argument("--oracle-seconds", type=float, default=15.0)
     p.add_argument("--e2e-steps", type=int, default=None)
@@ -66,23 +68,31 @@ def cfg_of(a):
         if v is not None:
             c[key] = v
     c["hot_mass"] = a.hot_mass
+    c["metric"] = a.metric
+    c["by_residual"] = a.by_residual
     return c
 
 
 def workload_name(c, name):
     hot = "all lists resident" if c["hot_mass"] >= 1 else f"hot set = {c['hot_mass']:.0%} of access mass"
+    var = ""
+    if c.get("metric", 0) == 1 or c.get("by_residual", 1) == 0:
+        var = ", " + ("inner product" if c.get("metric", 0) == 1 else "L2") + \
+              ("" if c.get("by_residual", 1) else ", non-residual PQ")
     return (f"{name}: {c['N'] / 1e6:g}M x d{c['d']}, IVF{c['nlist']}, PQ{c['m']}x8, nprobe {c['nprobe']}, "
-            f"k {c['k']}, batch {c['batch']}, Zipf alpha {c['alpha']}, {hot}")
+            f"k {c['k']}, batch {c['batch']}, Zipf alpha {c['alpha']}, {hot}{var}")
 
 
-def tf32_peak():
-    """Dense TF32 tensor peak: measured bf16 (MEASURED_PEAKS.json) x the guide's nominal tf32/bf16 ratio 1.1/2.25."""
+def f16_peak():
+    """Dense fp16 tensor peak (K1 runs kind::f16): the measured cuBLAS bf16 burst
+    figure (MEASURED_PEAKS.json; fp16 and bf16 share the nominal 2.25 PF/s rate,
+    B200_PROFILING.md), else the guide's fallback 1.59 PF/s."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             pk = json.load(f)
-        return float(pk["bf16_tflops"]) * 1.1 / 2.25, "measured bf16_tflops x 1.1/2.25 (B200_PROFILING.md nominal ratio)"
+        return float(pk["bf16_tflops"]), "of measured (MEASURED_PEAKS.json bf16_tflops; fp16 = bf16 nominal rate)"
     except Exception:
-        return 1100.0, "fallback (B200_PROFILING.md tf32 1.1 PFLOP/s dense)"
+        return 1590.0, "of fallback (B200_PROFILING.md 1.59 PFLOP/s bf16/fp16 burst)"
 
 
 def peaks():
@@ -183,6 +193,7 @@ def gen_index(c, seed, rank, world, hot=None, gt_queries=None):
     t = time.time()
     cache = os.environ.get("VLR_GEN_CACHE")
     key = f"{c['N']}_{c['d']}_{c['nlist']}_{c['m']}_{seed}_{world}_{rank}_{'all' if hot is None else len(hot)}"
+    key += f"_mt{c['metric']}_br{c['by_residual']}"
     if gt_queries is not None:
         import hashlib
         key += f"_gt{len(gt_queries)}_{hashlib.md5(gt_queries.tobytes()).hexdigest()[:10]}"
@@ -192,12 +203,13 @@ def gen_index(c, seed, rank, world, hot=None, gt_queries=None):
         if os.path.exists(os.path.join(path, "done")):
             f = {n: np.ascontiguousarray(np.load(os.path.join(path, n + ".npy"), mmap_mode="r")) for n in names}
             gt = f.pop("gt_ids", None)
-            ix = datagen.IndexArrays(d=c["d"], nlist=c["nlist"], m=c["m"], seed=seed, **f)
+            ix = datagen.IndexArrays(d=c["d"], nlist=c["nlist"], m=c["m"], seed=seed, metric=c["metric"],
+                                     by_residual=c["by_residual"], **f)
             if gt is not None:
                 ix.gt_ids = gt
             return ix, time.time() - t
     ix = datagen.make_index(c["N"], c["d"], c["nlist"], c["m"], seed=seed, device="cuda", owned=owned,
-                            gt_queries=gt_queries)
+                            gt_queries=gt_queries, metric=c["metric"], by_residual=c["by_residual"])
     if cache:
         os.makedirs(path, exist_ok=True)
         for n in names:
@@ -216,7 +228,7 @@ def calib_hot(c, seed):
     ncal = 10_000
     C = datagen.gen.Generator(c["N"], c["d"], c["nlist"], 1, seed=seed, device="cuda").centroids().cpu().numpy()
     Qc = datagen.make_queries(c["N"], c["d"], c["nlist"], ncal, seed=seed, stream=1, alpha=c["alpha"], device="cuda")
-    counts = datagen.access_counts(C, Qc, c["nprobe"], device="cuda")
+    counts = datagen.access_counts(C, Qc, c["nprobe"], device="cuda", metric=c["metric"])
     return datagen.hot_from_mass(counts, c["hot_mass"]), counts
 
 
@@ -403,16 +415,16 @@ def main():
         recall = {"recall_at_10": float(np.mean(r)), "queries": len(r),
                   "ground_truth": "exact fp32 flat search over all N float vectors (regenerated during index "
                                   "generation), first timed batch; results are bitwise identical at any G (R5)"}
-    # ---- coarse contraction (K1, tcgen05 TF32): 2*B*L*d flops per launch; the stage
+    # ---- coarse contraction (K1, tcgen05 kind::f16): 2*B*L*d flops per launch; the stage
     # also holds the tiny q-prep kernel, so this understates K1's own rate slightly
     cf_ms = float(stage_mean["coarse_filter"]) if stage_mean else None
     coarse_roof = None
     if cf_ms:
-        tp, tp_src = tf32_peak()
+        tp, tp_src = f16_peak()
         fl = 2.0 * B * c["nlist"] * c["d"]
         tfs = fl / (cf_ms * 1e-3) / 1e12
         cbytes = c["nlist"] * c["d"] * 4 + B * c["nlist"] * 4
-        coarse_roof = {"bound": "tensor", "dtype": "tf32", "achieved": tfs, "peak": tp, "unit": "TFLOP/s",
+        coarse_roof = {"bound": "tensor", "dtype": "f16 (power-of-two scaled operands, fp32 accumulate)", "achieved": tfs, "peak": tp, "unit": "TFLOP/s",
                        "frac": tfs / tp, "peak_source": tp_src, "flops_per_launch": fl,
                        "ms_per_launch": cf_ms, "hbm_gbs": cbytes / (cf_ms * 1e-3) / 1e9,
                        "kernel": "k_qprep + k_filter_tc (K1)"}

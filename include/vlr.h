@@ -30,7 +30,7 @@ extern "C" {
 #endif
 
 #define VLR_VERSION_MAJOR 1
-#define VLR_VERSION_MINOR 0
+#define VLR_VERSION_MINOR 1
 
 typedef struct vlr_index vlr_index; /* opaque; created by vlr_load_index, freed by vlr_index_free */
 
@@ -44,8 +44,8 @@ typedef enum {
   VLR_ERR_OOM = 6,             /* device allocation failed */
   VLR_ERR_CUDA = 7,            /* any other CUDA runtime error (no device, launch failure, ...) */
   VLR_ERR_NCCL = 8,            /* NCCL error; the communicator is aborted, the handle unusable */
-  VLR_ERR_UNSUPPORTED = 9      /* valid but outside v1: nbits != 8, metric != L2, by_residual != 1,
-                                  m > 128, k > 32 */
+  VLR_ERR_UNSUPPORTED = 9      /* valid but outside this version: nbits != 8, metric not in {0, 1},
+                                  m > 128, k > 32, nprobe' > 2048 */
 } vlr_status;
 
 /*
@@ -54,15 +54,20 @@ typedef enum {
  *
  * Definitions (§II.A-B; readings A2, A5 in DESIGN.md):
  *   vector i of list l reconstructs to xhat_i = c_l + concat_j Y[j][code_ij]
- *   (residual PQ, sub-space j = dims [j*dsub, (j+1)*dsub), dsub = d/m).
+ *   (residual PQ, sub-space j = dims [j*dsub, (j+1)*dsub), dsub = d/m);
+ *   with by_residual = 0, xhat_i = concat_j Y[j][code_ij].
+ *   metric 0: dist(q, x) = ||q - x||^2; metric 1 (inner product, "the
+ *   approach is independent of the distance metric"; reading A1' in
+ *   DESIGN.md): dist(q, x) = -<q, x>, so "ascending distance" is descending
+ *   similarity, and the coarse quantizer probes the largest <q, c_l>.
  */
 typedef struct {
   int32_t d;            /* vector dimension, >= 1 */
   int32_t nlist;        /* number of inverted lists / coarse centroids, >= 1 */
   int32_t m;            /* PQ sub-quantizers, d % m == 0, 1 <= m <= 128 */
   int32_t nbits;        /* bits per sub-code; must be 8 (256 codewords) */
-  int32_t metric;       /* 0 = squared L2 (only value in v1) */
-  int32_t by_residual;  /* 1 = codes encode x - c_l (only value in v1) */
+  int32_t metric;       /* 0 = squared L2, 1 = inner product (distance reported as -<q, x>) */
+  int32_t by_residual;  /* 1 = codes encode x - c_l, 0 = codes encode x */
   const float* centroids;      /* [nlist][d] row-major fp32 */
   const float* codebooks;      /* [m][256][d/m] fp32 */
   const int64_t* list_offsets; /* [nlist+1]; list l = rows [offsets[l], offsets[l+1]); offsets[0] = 0,
@@ -105,20 +110,23 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
  * capturable once vlr_reserve has sized the workspace for (nq, nprobe, k)).
  *
  *  d_queries [nq][d] device fp32.   nq >= 0 (nq == 0 is a no-op).
- *  nprobe >= 1; clamped to nprobe' = min(nprobe, nlist).
+ *  nprobe >= 1; clamped to nprobe' = min(nprobe, nlist); nprobe' <= 2048
+ *  (the paper's operating point), else VLR_ERR_UNSUPPORTED.
  *  1 <= k <= 32.
  *  Outputs (device, caller-allocated):
  *   d_ids  [nq][k] int64, d_dist [nq][k] fp32: row q = the k smallest
  *      candidates by (ADC distance, id), ascending; missing slots (-1, +inf).
- *      Distances are squared L2 to the PQ reconstruction, computed as
- *      ||q-c_l||^2 + (||yhat||^2 + 2<c_l,yhat>) - 2<q,yhat> in fp32
- *      (within 1e-5 relative of the fp64 definition).
+ *      Distances are dist(q, xhat) of the PQ reconstruction, computed as
+ *      ||q-c_l||^2 + (||yhat||^2 + 2<c_l,yhat>) - 2<q,yhat> in fp32 for the
+ *      default residual L2 index (the other variants drop the c_l terms or
+ *      use -<q,c_l> - <q,yhat>; within 1e-5 relative of
+ *      the fp64 definition).
  *      Candidates are the vectors of probed lists that are GPU-resident.
  *   d_miss [nq][nprobe'] uint8: 1 iff probe p of query q is not resident on
  *      any GPU; hit rate eta_q = 1 - mean_p d_miss[q][p].
  *   d_probes [nq][nprobe'] int32 or NULL: the probed cluster ids, ascending by
- *      (exact fp64 coarse distance, cluster id) (bit-exact w.r.t. the
- *      definition in DESIGN.md §O2).
+ *      (exact fp64 coarse distance dist(q, c_l), cluster id) (bit-exact
+ *      w.r.t. the definition in DESIGN.md §O2).
  *  Errors: INVALID_ARG / UNSUPPORTED synchronously; a non-finite query is
  *  detected on the device and reported by vlr_search, or by the next
  *  vlr_search_async/vlr_search on this handle.

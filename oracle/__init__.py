@@ -39,14 +39,18 @@ def lib():
         build()
         L = ctypes.CDLL(_LIB)
         P = ctypes.c_void_p
-        L.oracle_coarse.argtypes = [P, ctypes.c_int64, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P, ctypes.c_int32]
-        L.oracle_search.argtypes = [P, ctypes.c_int64, ctypes.c_int32, P, ctypes.c_int32, P, ctypes.c_int32,
-                                    P, P, P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, ctypes.c_int32]
-        L.oracle_dist_many.argtypes = [P, ctypes.c_int32, P, P, ctypes.c_int32, P, P, P, P, ctypes.c_int64, P, ctypes.c_int32]
+        I = ctypes.c_int32
+        L.oracle_coarse.argtypes = [P, ctypes.c_int64, P, I, I, I, P, P, I, I]
+        L.oracle_search.argtypes = [P, ctypes.c_int64, I, P, I, P, I, P, P, P, P, I, I, P, P, P, P, P, P, I, I, I]
+        L.oracle_dist_many.argtypes = [P, I, P, P, I, P, P, P, P, ctypes.c_int64, P, I, I, I]
         L.oracle_coarse_dist.argtypes = [P, P, ctypes.c_int32]
         L.oracle_coarse_dist.restype = ctypes.c_double
         L.oracle_adc_dist.argtypes = [P, P, P, P, ctypes.c_int32, ctypes.c_int32]
         L.oracle_adc_dist.restype = ctypes.c_double
+        L.oracle_coarse_ip.argtypes = [P, P, ctypes.c_int32]
+        L.oracle_coarse_ip.restype = ctypes.c_double
+        L.oracle_adc_dist_v.argtypes = [P, P, P, P, I, I, I, I]
+        L.oracle_adc_dist_v.restype = ctypes.c_double
         for f in (L.oracle_coarse, L.oracle_search, L.oracle_dist_many):
             f.restype = ctypes.c_int
         L.oracle_num_threads.restype = ctypes.c_int
@@ -66,15 +70,27 @@ def default_threads() -> int:
     return len(os.sched_getaffinity(0))
 
 
-def coarse(Q, centroids, nprobe, nthreads=0):
-    """O2/O3: (probes int32 [nq,nprobe'], fp64 distances [nq,nprobe'])."""
+def _variant(index, metric, by_residual):
+    """metric 0 = squared L2, 1 = inner product (reported as -<q, x>);
+    by_residual 1 = codes encode x - c_l. Defaults: the index's own."""
+    if metric is None:
+        metric = int(getattr(index, "metric", 0)) if index is not None else 0
+    if by_residual is None:
+        by_residual = int(getattr(index, "by_residual", 1)) if index is not None else 1
+    return int(metric), int(by_residual)
+
+
+def coarse(Q, centroids, nprobe, nthreads=0, metric=0):
+    """O2/O3: (probes int32 [nq,nprobe'], fp64 keys [nq,nprobe']): squared L2
+    distances (metric 0) or negated inner products (metric 1)."""
     Q = _c(Q, np.float32); C = _c(centroids, np.float32)
     nq, d = Q.shape
     L = C.shape[0]
     npr = min(nprobe, L)
     probes = np.empty((nq, npr), np.int32)
     dist = np.empty((nq, npr), np.float64)
-    rc = lib().oracle_coarse(_p(Q), nq, _p(C), L, d, nprobe, _p(probes), _p(dist), nthreads or default_threads())
+    rc = lib().oracle_coarse(_p(Q), nq, _p(C), L, d, nprobe, _p(probes), _p(dist), int(metric),
+                             nthreads or default_threads())
     if rc:
         raise ValueError("oracle_coarse: invalid arguments")
     return probes, dist
@@ -87,8 +103,9 @@ def hot_mask(nlist, hot) -> np.ndarray:
     return m
 
 
-def search(index, Q, nprobe, k, hot=None, nthreads=0):
+def search(index, Q, nprobe, k, hot=None, nthreads=0, metric=None, by_residual=None):
     """O2-O7. index: datagen.IndexArrays-like. hot=None means all lists hot.
+    metric / by_residual default to the index's attributes (0 / 1).
     Returns dict(ids int64 [nq,k], dist f64 [nq,k], miss u8, probes i32,
     kth1 f64 [nq], ncand i64 [nq])."""
     Q = _c(Q, np.float32)
@@ -106,7 +123,8 @@ def search(index, Q, nprobe, k, hot=None, nthreads=0):
                kth1=np.empty(nq, np.float64), ncand=np.empty(nq, np.int64))
     rc = lib().oracle_search(_p(Q), nq, d, _p(C), L, _p(Y), index.m, _p(offs), _p(ids), _p(codes), _p(isht),
                              nprobe, k, _p(out["ids"]), _p(out["dist"]), _p(out["miss"]), _p(out["probes"]),
-                             _p(out["kth1"]), _p(out["ncand"]), nthreads or default_threads())
+                             _p(out["kth1"]), _p(out["ncand"]), *_variant(index, metric, by_residual),
+                             nthreads or default_threads())
     if rc:
         raise ValueError("oracle_search: invalid arguments")
     return out
@@ -129,7 +147,7 @@ class IdMap:
         return ok, self.list_of_pos[pos], pos
 
 
-def dist_ref(index, Q, qidx, ids, idmap: IdMap | None = None, nthreads=0):
+def dist_ref(index, Q, qidx, ids, idmap: IdMap | None = None, nthreads=0, metric=None, by_residual=None):
     """O6 distance of each (query row qidx[i], vector id ids[i]); NaN for unknown ids."""
     idmap = idmap or IdMap(index)
     qidx = _c(qidx, np.int64).reshape(-1)
@@ -142,7 +160,7 @@ def dist_ref(index, Q, qidx, ids, idmap: IdMap | None = None, nthreads=0):
         lib().oracle_dist_many(_p(Q), index.d, _p(_c(index.centroids, np.float32)), _p(_c(index.codebooks, np.float32)),
                                index.m, _p(_c(index.codes, np.uint8)), _p(_c(qidx[sel], np.int64)),
                                _p(_c(lst[sel], np.int32)), _p(_c(pos[sel], np.int64)), len(sel), _p(tmp),
-                               nthreads or default_threads())
+                               *_variant(index, metric, by_residual), nthreads or default_threads())
         out[sel] = tmp
     return out
 

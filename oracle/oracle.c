@@ -26,6 +26,12 @@
  *       the LUT of stage 2/3 accumulates.
  *   O7  result: k smallest candidates by (dist, id), padded with (-1, +inf);
  *       also the (k+1)-th distance (for the tie rule R3).
+ * Variants (NEXT-3, readings A1'/A2' in DESIGN.md §2):
+ *   by_residual = 0: xhat_i = concat_j Y[j][code_ij] (no centroid term);
+ *   metric = 1 (inner product, "independent of the distance metric",
+ *       PAPER.md:243): coarse key D[q,l] = -<q, c_l> and dist_i = -<q, xhat_i>,
+ *       each summed sequentially in t-order; ranking ascending by these
+ *       negated inner products is ranking by descending similarity.
  * Pins: tests/test_oracle_pins.py (see DESIGN.md §Oracle pins).
  */
 #include <math.h>
@@ -47,6 +53,20 @@ double oracle_coarse_dist(const float* q, const float* c, int32_t d) {
     return s;
 }
 
+/* ---- O2 (metric = 1): exact negated inner product, sequential fp64 sum ---- */
+double oracle_coarse_ip(const float* q, const float* c, int32_t d) {
+    double s = 0.0;
+    for (int32_t t = 0; t < d; ++t) {
+        double pr = (double)q[t] * (double)c[t];
+        s = s + pr;
+    }
+    return -s;
+}
+
+static double coarse_key(const float* q, const float* c, int32_t d, int32_t metric) {
+    return metric == 1 ? oracle_coarse_ip(q, c, d) : oracle_coarse_dist(q, c, d);
+}
+
 typedef struct { double d; int64_t id; } pair_t;
 
 static int cmp_pair(const void* a, const void* b) {
@@ -61,8 +81,8 @@ static int cmp_pair(const void* a, const void* b) {
 
 /* ---- O3: probes = first nprobe' of sort by (D, l) ---- */
 int oracle_coarse(const float* Q, int64_t nq, const float* C, int32_t nlist, int32_t d,
-                  int32_t nprobe, int32_t* probes, double* probe_dist, int32_t nthreads) {
-    if (nprobe < 1 || nlist < 1 || d < 1) return 1;
+                  int32_t nprobe, int32_t* probes, double* probe_dist, int32_t metric, int32_t nthreads) {
+    if (nprobe < 1 || nlist < 1 || d < 1 || metric < 0 || metric > 1) return 1;
     int32_t np = nprobe < nlist ? nprobe : nlist;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -71,7 +91,7 @@ int oracle_coarse(const float* Q, int64_t nq, const float* C, int32_t nlist, int
     for (int64_t qi = 0; qi < nq; ++qi) {
         pair_t* all = (pair_t*)malloc(sizeof(pair_t) * (size_t)nlist);
         for (int32_t l = 0; l < nlist; ++l) {
-            all[l].d = oracle_coarse_dist(Q + qi * d, C + (int64_t)l * d, d);
+            all[l].d = coarse_key(Q + qi * d, C + (int64_t)l * d, d, metric);
             all[l].id = l;
         }
         qsort(all, (size_t)nlist, sizeof(pair_t), cmp_pair);
@@ -102,6 +122,30 @@ double oracle_adc_dist(const float* q, const float* c_l, const float* Y, const u
     return s;
 }
 
+/* ---- O6 variants: xhat = [c_l +] concat_j Y[j][code_j] (by_residual), and
+ * dist = sum_t (q_t - xhat_t)^2 (metric 0) or -sum_t q_t xhat_t (metric 1) ---- */
+double oracle_adc_dist_v(const float* q, const float* c_l, const float* Y, const uint8_t* code,
+                         int32_t d, int32_t m, int32_t metric, int32_t by_residual) {
+    if (metric == 0 && by_residual) return oracle_adc_dist(q, c_l, Y, code, d, m);
+    int32_t dsub = d / m;
+    double s = 0.0;
+    for (int32_t t = 0; t < d; ++t) {
+        int32_t j = t / dsub;
+        int32_t u = t - j * dsub;
+        double xh = (double)Y[((int64_t)j * 256 + code[j]) * dsub + u];
+        if (by_residual) xh = (double)c_l[t] + xh;
+        if (metric == 1) {
+            double pr = (double)q[t] * xh;
+            s = s + pr;
+        } else {
+            double diff = (double)q[t] - xh;
+            double sq = diff * diff;
+            s = s + sq;
+        }
+    }
+    return metric == 1 ? -s : s;
+}
+
 /* keep the kk smallest (dist,id) pairs in best[0..kk-1] (sorted) by insertion */
 static void insert_best(pair_t* best, int32_t kk, double dist, int64_t id) {
     pair_t v; v.d = dist; v.id = id;
@@ -122,8 +166,8 @@ int oracle_search(const float* Q, int64_t nq, int32_t d, const float* C, int32_t
                   const float* Y, int32_t m, const int64_t* offsets, const int64_t* ids,
                   const uint8_t* codes, const uint8_t* is_hot, int32_t nprobe, int32_t k,
                   int64_t* out_ids, double* out_dist, uint8_t* miss, int32_t* probes,
-                  double* kth1, int64_t* ncand, int32_t nthreads) {
-    if (nprobe < 1 || k < 1 || m < 1 || d % m != 0) return 1;
+                  double* kth1, int64_t* ncand, int32_t metric, int32_t by_residual, int32_t nthreads) {
+    if (nprobe < 1 || k < 1 || m < 1 || d % m != 0 || metric < 0 || metric > 1) return 1;
     int32_t np = nprobe < nlist ? nprobe : nlist;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -134,7 +178,7 @@ int oracle_search(const float* Q, int64_t nq, int32_t d, const float* C, int32_t
         /* O2 + O3 */
         pair_t* all = (pair_t*)malloc(sizeof(pair_t) * (size_t)nlist);
         for (int32_t l = 0; l < nlist; ++l) {
-            all[l].d = oracle_coarse_dist(q, C + (int64_t)l * d, d);
+            all[l].d = coarse_key(q, C + (int64_t)l * d, d, metric);
             all[l].id = l;
         }
         qsort(all, (size_t)nlist, sizeof(pair_t), cmp_pair);
@@ -150,7 +194,7 @@ int oracle_search(const float* Q, int64_t nq, int32_t d, const float* C, int32_t
             if (miss) miss[qi * np + p] = is_miss;
             if (is_miss) continue;
             for (int64_t i = offsets[l]; i < offsets[l + 1]; ++i) {
-                double dist = oracle_adc_dist(q, C + (int64_t)l * d, Y, codes + i * m, d, m);
+                double dist = oracle_adc_dist_v(q, C + (int64_t)l * d, Y, codes + i * m, d, m, metric, by_residual);
                 insert_best(best, kk, dist, ids[i]);
                 ++nc;
             }
@@ -173,13 +217,15 @@ int oracle_search(const float* Q, int64_t nq, int32_t d, const float* C, int32_t
  */
 int oracle_dist_many(const float* Q, int32_t d, const float* C, const float* Y, int32_t m,
                      const uint8_t* codes, const int64_t* qidx, const int32_t* list,
-                     const int64_t* pos, int64_t n, double* out, int32_t nthreads) {
+                     const int64_t* pos, int64_t n, double* out, int32_t metric, int32_t by_residual,
+                     int32_t nthreads) {
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
 #pragma omp parallel for schedule(static)
 #endif
     for (int64_t i = 0; i < n; ++i)
-        out[i] = oracle_adc_dist(Q + qidx[i] * d, C + (int64_t)list[i] * d, Y, codes + pos[i] * m, d, m);
+        out[i] = oracle_adc_dist_v(Q + qidx[i] * d, C + (int64_t)list[i] * d, Y, codes + pos[i] * m, d, m,
+                                   metric, by_residual);
     return 0;
 }
 

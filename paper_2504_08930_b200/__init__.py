@@ -147,7 +147,10 @@ class Index:
 
     @classmethod
     def from_arrays(cls, ix, hot=None, **kw):
-        """Load from a datagen.IndexArrays-like object."""
+        """Load from a datagen.IndexArrays-like object (its metric / by_residual
+        attributes, when present, select the variant)."""
+        kw.setdefault("metric", int(getattr(ix, "metric", 0)))
+        kw.setdefault("by_residual", int(getattr(ix, "by_residual", 1)))
         return cls.load(ix.centroids, ix.codebooks, ix.list_offsets, ix.ids, ix.codes, hot=hot, **kw)
 
     # ------------------------------------------------------------------ search

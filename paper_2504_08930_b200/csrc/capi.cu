@@ -48,7 +48,7 @@ __global__ void k_negative(const int64_t* ids, long long n, int32_t* flag) {
 }
 
 static void free_ws(Workspace& w) {
-  void* ps[] = {w.qnorm, w.qf16, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.lut,
+  void* ps[] = {w.qnorm, w.qsq, w.qf16, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.lut,
                 w.pdist, w.pid, w.send, w.recv, w.d_q, w.d_ids, w.d_dist, w.d_miss, w.d_probes, w.status};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -79,6 +79,7 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   w.n_cta = scan_ctas(ix);
   const size_t nqs = (size_t)cnq;
   VLR_CUDA_TRY(dalloc(&w.qnorm, nqs));
+  VLR_CUDA_TRY(dalloc(&w.qsq, nqs));
   VLR_CUDA_TRY(dalloc(&w.qf16, nqs * ix.d8));
   VLR_CUDA_TRY(dalloc(&w.qinv, nqs));
   VLR_CUDA_TRY(dalloc(&w.dt, nqs * ix.nlist));
@@ -132,8 +133,8 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   if (D.d < 1 || D.nlist < 1 || D.m < 1) return fail(VLR_ERR_INVALID_ARG, "d, nlist, m must be >= 1");
   if (D.d % D.m != 0) return fail(VLR_ERR_DIM_MISMATCH, "d % m != 0");
   if (D.nbits != 8) return fail(VLR_ERR_UNSUPPORTED, "nbits must be 8");
-  if (D.metric != 0) return fail(VLR_ERR_UNSUPPORTED, "metric must be 0 (squared L2)");
-  if (D.by_residual != 1) return fail(VLR_ERR_UNSUPPORTED, "by_residual must be 1");
+  if (D.metric != 0 && D.metric != 1) return fail(VLR_ERR_UNSUPPORTED, "metric must be 0 (squared L2) or 1 (inner product)");
+  if (D.by_residual != 0 && D.by_residual != 1) return fail(VLR_ERR_INVALID_ARG, "by_residual must be 0 or 1");
   if (D.m > kMaxM) return fail(VLR_ERR_UNSUPPORTED, "m > 128");
   if (!D.centroids || !D.codebooks || !D.list_offsets) return fail(VLR_ERR_INVALID_ARG, "null array");
   if (D.n_hot < 0 || (D.n_hot > 0 && !D.hot)) return fail(VLR_ERR_INVALID_ARG, "bad hot set");
@@ -155,7 +156,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
       s += (double)c[t] * c[t];
       cabs = std::max(cabs, std::fabs(c[t]));
     }
-    cn2[l] = (float)s;
+    cn2[l] = D.metric == 1 ? 0.f : (float)s;  // IP: the filter holds -2<q,c>
     cmax2 = std::max(cmax2, s);
   }
   const size_t ncb = (size_t)m * 256 * dsub;
@@ -208,6 +209,8 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   ix.npairs = (ix.mpad + 63) / 64;
   ix.rank = cm.rank;
   ix.world = cm.world;
+  ix.metric = D.metric;
+  ix.by_residual = D.by_residual;
   ix.device = dev;
   ix.shard_only = cm.world > 1 && cm.nccl_unique_id == nullptr;
   ix.cmax = (float)std::sqrt(cmax2) * 1.0000002f;
@@ -377,7 +380,7 @@ vlr_status vlr_reserve(vlr_index* h, int32_t max_nq, int32_t max_nprobe, int32_t
   if (max_k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32");
   cudaSetDevice(h->ix.device);
   const int np = std::min(max_nprobe, h->ix.nlist);
-  if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 1024");
+  if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 2048");
   return ensure_ws(h, std::max(max_nq, 1), np, max_k);
 }
 
@@ -395,7 +398,7 @@ vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t np
   if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32 (v1)");
   DeviceIndex& ix = h->ix;
   const int np = std::min(nprobe, ix.nlist);
-  if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 1024 (v1)");
+  if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 2048");
   h->launches = 0;
   if (nq == 0) return VLR_OK;
   if (!Q || !out_ids || !out_dist || !out_miss) return fail(VLR_ERR_INVALID_ARG, "null buffer");
@@ -411,7 +414,7 @@ vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t np
   VLR_CUDA_TRY(cudaMemsetAsync(w.status, 0, sizeof(int32_t), s));
   int n = 0;
   rec(h, 0, s);
-  VLR_CUDA_TRY(launch_qprep(Q, nq, ix.d, ix.d8, w.qnorm, w.qf16, w.qinv, w.status, s)); ++n;
+  VLR_CUDA_TRY(launch_qprep(Q, nq, ix.d, ix.d8, w.qnorm, w.qsq, w.qf16, w.qinv, w.status, s)); ++n;
   VLR_CUDA_TRY(launch_filter_tc(w.qf16, w.qinv, nq, ix, w.dt, w.gmin, s)); ++n;
   rec(h, 1, s);
   VLR_CUDA_TRY(launch_select(ix, w, nq, np, filter_edot(ix.d), s)); ++n;
@@ -466,7 +469,7 @@ vlr_status vlr_search_host(vlr_index* h, const float* hQ, int32_t nq, int32_t np
   if (nq == 0) return VLR_OK;
   if (!hQ || !h_ids || !h_dist || !h_miss) return fail(VLR_ERR_INVALID_ARG, "null buffer");
   const int np = std::min(nprobe, h->ix.nlist);
-  if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 1024 (v1)");
+  if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 2048");
   VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
   vlr_status st = ensure_ws(h, nq, np, k);
   if (st != VLR_OK) return st;

@@ -9,7 +9,10 @@
 //  K3      : exact fp64 D = sum_t (q_t - c_t)^2 in dimension order with
 //            correctly-rounded dsub/dmul/dadd (no FMA) for the candidates,
 //            sort by (D, l), keep nprobe' -> probes + term1 = (float)D.
-//            Bit-identical to the definition.
+//            Bit-identical to the definition. Inner-product
+//            metric (NEXT-3): D = -sum_t q_t c_t (products exact in fp64, the
+//            sum in dimension order); the filter then holds -2<q, c>
+//            (||c||^2 = 0 in K1), the same key scaled by 2.
 #include <cfloat>
 
 #include <cuda_fp16.h>
@@ -24,7 +27,7 @@ namespace vlr {
 // fp16(q 2^e_q) with 2^e_q the power of two putting max |q_t| 2^e_q in
 // [2^13, 2^14) (exponent clamped to [-60, 60]; DESIGN.md §5 bounds the
 // subnormal flush that clamping can cause).
-__global__ void k_qprep(const float* __restrict__ Q, int d, int d8, float* __restrict__ qnorm,
+__global__ void k_qprep(const float* __restrict__ Q, int d, int d8, float* __restrict__ qnorm, float* __restrict__ qsq,
                         uint16_t* __restrict__ qf16, float* __restrict__ qinv, int32_t* status) {
   const int q = blockIdx.x;
   const float* row = Q + (size_t)q * d;
@@ -61,6 +64,7 @@ __global__ void k_qprep(const float* __restrict__ Q, int d, int d8, float* __res
       m = fmaxf(m, redm[w]);
     }
     qnorm[q] = (float)sqrt(t) * 1.0000002f;
+    qsq[q] = (float)t;
     int e = 0;
     if (m > 0.f && isfinite(m)) {
       frexpf(m, &e);  // m < 2^e
@@ -79,10 +83,10 @@ __global__ void k_qprep(const float* __restrict__ Q, int d, int d8, float* __res
   }
 }
 
-cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, uint16_t* qf16, float* qinv,
+cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, float* qsq, uint16_t* qf16, float* qinv,
                          int32_t* status, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  k_qprep<<<nq, 256, 0, s>>>(Q, d, d8, qnorm, qf16, qinv, status);
+  k_qprep<<<nq, 256, 0, s>>>(Q, d, d8, qnorm, qsq, qf16, qinv, status);
   return cudaGetLastError();
 }
 
@@ -245,7 +249,16 @@ cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, in
 constexpr int kRefineThreads = 512;
 constexpr int kRefineWarps = kRefineThreads / 32;
 constexpr int kRescanWarps = 8;  // warps computing exact distances on the (rare) overflow path
-constexpr int kSortCap = 2048;  // >= kMaxNprobe + kRefineChunk
+constexpr int kSortCap = 4096;  // max sort buffer: >= kMaxNprobe + kRefineChunk (power of two)
+static_assert(kSortCap >= kMaxNprobe + kRefineChunk, "K3 sort buffer");
+// the launch sizes the buffer to next_pow2(np + kRefineChunk) (2048 for
+// np <= 1024: two K3b CTAs per SM stay resident)
+static int sort_cap(int np) {
+  int c = 1;
+  while (c < np + kRefineChunk) c <<= 1;
+  return c;
+}
+constexpr int kRefinePer = (kMaxNprobe + kRefineThreads - 1) / kRefineThreads;  // router items per thread
 
 __device__ __forceinline__ bool key_less(double a, int ia, double b, int ib) {
   return a < b || (a == b && ia < ib);
@@ -285,7 +298,18 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // floats. Tiles of 32 dimensions are streamed with cp.async S-1 tiles ahead;
 // the 16-B chunks of row r are XOR-swizzled by (r & 7) so that lane r's
 // LDS.128 of its own row are conflict-free.
-template <int S>
+// one dimension's term of the exact key, accumulated in t-order:
+// L2 s += (q - c)^2 (dsub, dmul, dadd), IP s += q c (dmul exact for fp32 inputs)
+template <int MET>
+__device__ __forceinline__ double key_term(double s, double q, double c) {
+  if constexpr (MET == 1) return __dadd_rn(s, __dmul_rn(q, c));
+  const double e = __dsub_rn(q, c);
+  return __dadd_rn(s, __dmul_rn(e, e));
+}
+template <int MET>
+__device__ __forceinline__ double key_final(double s) { return MET == 1 ? -s : s; }
+
+template <int S, int MET>
 __device__ double warp_exact(const double* __restrict__ qs, const float* __restrict__ C, int d, int row_id,
                              float* buf, int lane) {
   double s = 0.0;
@@ -325,30 +349,25 @@ __device__ double warp_exact(const double* __restrict__ qs, const float* __restr
     for (int k = 0; k < 8; ++k) {
       const float4 v = *reinterpret_cast<const float4*>(rowp + ((k ^ (lane & 7)) << 2));
       const double2 qa = qt[2 * k], qb = qt[2 * k + 1];
-      double e;
-      e = __dsub_rn(qa.x, (double)v.x); s = __dadd_rn(s, __dmul_rn(e, e));
-      e = __dsub_rn(qa.y, (double)v.y); s = __dadd_rn(s, __dmul_rn(e, e));
-      e = __dsub_rn(qb.x, (double)v.z); s = __dadd_rn(s, __dmul_rn(e, e));
-      e = __dsub_rn(qb.y, (double)v.w); s = __dadd_rn(s, __dmul_rn(e, e));
+      s = key_term<MET>(s, qa.x, (double)v.x);
+      s = key_term<MET>(s, qa.y, (double)v.y);
+      s = key_term<MET>(s, qb.x, (double)v.z);
+      s = key_term<MET>(s, qb.y, (double)v.w);
     }
     __syncwarp();
   }
   cp_async_wait<0>();
-  for (int t = ntile * 32; t < d; ++t) {  // tail dimensions, still in order
-    const double e = __dsub_rn(qs[t], (double)__ldg(C + (size_t)row_id * d + t));
-    s = __dadd_rn(s, __dmul_rn(e, e));
-  }
-  return s;
+  for (int t = ntile * 32; t < d; ++t)  // tail dimensions, still in order
+    s = key_term<MET>(s, qs[t], (double)__ldg(C + (size_t)row_id * d + t));
+  return key_final<MET>(s);
 }
 
+template <int MET>
 __device__ __forceinline__ double scalar_exact(const double* __restrict__ qs, const float* __restrict__ C, int d,
                                                int row_id) {
   double s = 0.0;
-  for (int t = 0; t < d; ++t) {
-    const double e = __dsub_rn(qs[t], (double)__ldg(C + (size_t)row_id * d + t));
-    s = __dadd_rn(s, __dmul_rn(e, e));
-  }
-  return s;
+  for (int t = 0; t < d; ++t) s = key_term<MET>(s, qs[t], (double)__ldg(C + (size_t)row_id * d + t));
+  return key_final<MET>(s);
 }
 
 // K3a: exact fp64 D of every listed candidate, 4 warps per CTA, warp <-> 32
@@ -357,6 +376,7 @@ __device__ __forceinline__ double scalar_exact(const double* __restrict__ qs, co
 constexpr int kExactWarps = 4;
 constexpr int kExactStages = 4;
 
+template <int MET>
 __global__ void __launch_bounds__(kExactWarps * 32) k_exact(const float* __restrict__ Q, const float* __restrict__ C,
                                                             int d, const int32_t* __restrict__ cand,
                                                             const int32_t* __restrict__ ncand,
@@ -379,9 +399,9 @@ __global__ void __launch_bounds__(kExactWarps * 32) k_exact(const float* __restr
     const int rid = lst[j < nc ? j : g];
     double D;
     if ((d & 3) == 0)
-      D = warp_exact<kExactStages>(qs, C, d, rid, tiles + warp * (kExactStages * 1024), lane);
+      D = warp_exact<kExactStages, MET>(qs, C, d, rid, tiles + warp * (kExactStages * 1024), lane);
     else
-      D = scalar_exact(qs, C, d, rid);
+      D = scalar_exact<MET>(qs, C, d, rid);
     if (j < nc) exact[(size_t)q * kCandCap + j] = D;
   }
 }
@@ -393,19 +413,22 @@ size_t exact_smem(int d) {
 cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
   const size_t sm = exact_smem(ix.d);
-  static size_t configured = 0;
-  if (sm > 48 * 1024 && sm > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  static size_t configured[2] = {0, 0};
+  auto fn = ix.metric == 1 ? k_exact<1> : k_exact<0>;
+  if (sm > 48 * 1024 && sm > configured[ix.metric]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    configured = sm;
+    configured[ix.metric] = sm;
   }
   dim3 grid(nq, 8);  // 8 x 4 warps; queries with > 1024 candidates loop
-  k_exact<<<grid, kExactWarps * 32, sm, s>>>(Q, ix.centroids, ix.d, ws.cand, ws.ncand, ws.exact);
+  fn<<<grid, kExactWarps * 32, sm, s>>>(Q, ix.centroids, ix.d, ws.cand, ws.ncand, ws.exact);
   return cudaGetLastError();
 }
 
+template <int MET>
 __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restrict__ Q, const float* __restrict__ C,
-                                                           int d, int L, int np, const float* __restrict__ dt,
+                                                           int d, int L, int np, int scap, int by_residual,
+                                                           const float* __restrict__ qsq, const float* __restrict__ dt,
                                                            const int32_t* __restrict__ cand,
                                                            const int32_t* __restrict__ ncand,
                                                            const float* __restrict__ bound,
@@ -420,9 +443,9 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
                                                            int64_t* __restrict__ qtot) {
   extern __shared__ __align__(16) unsigned char sm[];
   float* tiles = reinterpret_cast<float*>(sm);                        // [kRescanWarps][2][32][32]
-  double* key = reinterpret_cast<double*>(tiles + kRescanWarps * 2048);  // [kSortCap]
-  int* id = reinterpret_cast<int*>(key + kSortCap);                   // [kSortCap]
-  int* lbuf = id + kSortCap;                                          // [kRefineChunk]
+  double* key = reinterpret_cast<double*>(tiles + kRescanWarps * 2048);  // [scap]
+  int* id = reinterpret_cast<int*>(key + scap);                       // [scap]
+  int* lbuf = id + scap;                                              // [kRefineChunk]
   double* qs = reinterpret_cast<double*>(lbuf + kRefineChunk);        // [d]
   __shared__ int s_cnt;
   const int q = blockIdx.x;
@@ -470,7 +493,8 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
       for (int g = warp * 32; warp < kRescanWarps && g < cnt; g += kRescanWarps * 32) {
         const int j = g + lane;
         const int rid = j < cnt ? lbuf[j] : lbuf[g];
-        const double dsum = vec_ok ? warp_exact<2>(qs, C, d, rid, tiles + warp * 2048, lane) : scalar_exact(qs, C, d, rid);
+        const double dsum = vec_ok ? warp_exact<2, MET>(qs, C, d, rid, tiles + warp * 2048, lane)
+                                   : scalar_exact<MET>(qs, C, d, rid);
         if (j < cnt) {
           key[nbest + j] = dsum;
           id[nbest + j] = rid;
@@ -489,20 +513,24 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
   }
   // ---- router epilogue (K4 fused): mask, owned work items
   // and their within-query prefix (groups of 32 vectors); K4b adds the
-  // query bases. Items p of this query are handled 2 per thread in order.
+  // query bases. Items p of this query are handled kRefinePer per thread in order.
   __shared__ long long s_wsum[kRefineWarps];
-  long long g2[2] = {0, 0};
-  const int p0 = 2 * threadIdx.x;
+  long long g2[kRefinePer];
+  const int p0 = kRefinePer * threadIdx.x;
+  // term1: the key itself with residual codes (||q-c||^2
+  // or -<q,c>); without, ||q||^2 (L2) or 0 (IP)
+  const float t1c = by_residual ? 0.f : (MET == 1 ? 0.f : qsq[q]);
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < kRefinePer; ++h) {
     const int p = p0 + h;
+    g2[h] = 0;
     if (p < np) {
       // nbest == np whenever the candidate set holds >= np clusters (always: the
       // band contains the np smallest)
       const int l = p < nbest ? id[p] : -1;
       const size_t o = (size_t)q * np + p;
       probes[o] = l;
-      term1[o] = p < nbest ? __double2float_rn(key[p]) : CUDART_INF_F;
+      term1[o] = p < nbest ? (by_residual ? __double2float_rn(key[p]) : t1c) : CUDART_INF_F;
       const int own = l >= 0 ? owner[l] : -1;
       miss[o] = own < 0 ? 1 : 0;
       if (probes_out) probes_out[o] = l;
@@ -511,7 +539,9 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
       if (loc >= 0) g2[h] = gbase[loc + 1] - gbase[loc];
     }
   }
-  const long long mine = g2[0] + g2[1];
+  long long mine = 0;
+#pragma unroll
+  for (int h = 0; h < kRefinePer; ++h) mine += g2[h];
   long long incl = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -526,30 +556,35 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
     if (w < warp) wbase += v;
     total += v;
   }
-  const long long ex = wbase + incl - mine;
-  if (p0 < np) item_local[(size_t)q * np + p0] = ex;
-  if (p0 + 1 < np) item_local[(size_t)q * np + p0 + 1] = ex + g2[0];
+  long long ex = wbase + incl - mine;
+#pragma unroll
+  for (int h = 0; h < kRefinePer; ++h) {
+    if (p0 + h < np) item_local[(size_t)q * np + p0 + h] = ex;
+    ex += g2[h];
+  }
   if (threadIdx.x == 0) qtot[q] = total;
 }
 
-size_t refine_smem(int d) {
-  return (size_t)kRescanWarps * 2048 * sizeof(float) + (size_t)kSortCap * (sizeof(double) + sizeof(int)) +
+size_t refine_smem(int d, int scap) {
+  return (size_t)kRescanWarps * 2048 * sizeof(float) + (size_t)scap * (sizeof(double) + sizeof(int)) +
          kRefineChunk * sizeof(int) + (size_t)d * sizeof(double);
 }
 
 cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, int np, uint8_t* miss,
                           int32_t* probes_out, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  const size_t sm = refine_smem(ix.d);
-  static size_t configured = 0;
-  if (sm > 48 * 1024 && sm > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int scap = sort_cap(np);
+  const size_t sm = refine_smem(ix.d, scap);
+  static size_t configured[2] = {0, 0};
+  auto fn = ix.metric == 1 ? k_refine<1> : k_refine<0>;
+  if (sm > 48 * 1024 && sm > configured[ix.metric]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    configured = sm;
+    configured[ix.metric] = sm;
   }
-  k_refine<<<nq, kRefineThreads, sm, s>>>(Q, ix.centroids, ix.d, ix.nlist, np, ws.dt, ws.cand, ws.ncand, ws.bound,
-                                           ws.exact, ws.probes, ws.term1, ix.rank, ix.owner, ix.local, ix.gbase, miss,
-                                           probes_out, ws.plocal, ws.item_local, ws.qtot);
+  fn<<<nq, kRefineThreads, sm, s>>>(Q, ix.centroids, ix.d, ix.nlist, np, scap, ix.by_residual, ws.qsq, ws.dt, ws.cand,
+                                    ws.ncand, ws.bound, ws.exact, ws.probes, ws.term1, ix.rank, ix.owner, ix.local,
+                                    ix.gbase, miss, probes_out, ws.plocal, ws.item_local, ws.qtot);
   return cudaGetLastError();
 }
 

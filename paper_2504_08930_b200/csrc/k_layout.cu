@@ -9,7 +9,9 @@
 //          s = 32r + t holds sub-code j = 32r + (v ^ t) (0 for j >= m), the
 //          order the scan's conflict-free LUT gathers consume them in.
 //   bias:  b_v = ||yhat_v||^2 + 2 <c_l, yhat_v> computed in fp64, rounded to
-//          fp32 (+inf for padding slots, so they never enter a top-k).
+//          fp32 (+inf for padding slots, so they never enter a top-k);
+//          ||yhat_v||^2 without residual codes, 0 for the inner-product
+//          metric (NEXT-3).
 //   ids:   int64 id (-1 for padding).
 #include <cfloat>
 
@@ -18,7 +20,7 @@
 
 namespace vlr {
 
-__global__ void k_layout(int d, int m, int mpad, int dsub, int n_local, long long n_slots,
+__global__ void k_layout(int d, int m, int mpad, int dsub, int metric, int by_residual, int n_local, long long n_slots,
                          const int64_t* __restrict__ gbase, const int64_t* __restrict__ vbase,
                          const int32_t* __restrict__ lglob, const uint8_t* __restrict__ scodes,
                          const int64_t* __restrict__ sids, const float* __restrict__ C, const float* __restrict__ Y,
@@ -41,11 +43,13 @@ __global__ void k_layout(int d, int m, int mpad, int dsub, int n_local, long lon
       const uint8_t* src = scodes + v * m;
       const float* c = C + (size_t)lglob[list] * d;
       double b = 0.0;
-      for (int j = 0; j < m; ++j) {
-        const float* y = Y + ((size_t)j * 256 + src[j]) * dsub;
-        for (int u = 0; u < dsub; ++u) {
-          const double yy = (double)y[u];
-          b += yy * yy + 2.0 * (double)c[j * dsub + u] * yy;
+      if (metric == 0) {
+        for (int j = 0; j < m; ++j) {
+          const float* y = Y + ((size_t)j * 256 + src[j]) * dsub;
+          for (int u = 0; u < dsub; ++u) {
+            const double yy = (double)y[u];
+            b += yy * yy + (by_residual ? 2.0 * (double)c[j * dsub + u] * yy : 0.0);
+          }
         }
       }
       bias[slot] = (float)b;
@@ -79,7 +83,8 @@ cudaError_t launch_layout(const DeviceIndex& ix, const uint8_t* stage_codes, con
   const int threads = 256;
   long long blocks = (n_slots + threads - 1) / threads;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  k_layout<<<(int)blocks, threads, 0, s>>>(ix.d, ix.m, ix.mpad, ix.dsub, ix.n_local, n_slots, ix.gbase, vbase, lglob,
+  k_layout<<<(int)blocks, threads, 0, s>>>(ix.d, ix.m, ix.mpad, ix.dsub, ix.metric, ix.by_residual, ix.n_local, n_slots,
+                                           ix.gbase, vbase, lglob,
                                            stage_codes, stage_ids, ix.centroids, ix.codebooks, ix.codes, ix.bias,
                                            ix.ids);
   return cudaGetLastError();

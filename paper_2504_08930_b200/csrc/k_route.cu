@@ -10,7 +10,8 @@
 // exclusive prefix item_off (item_off[n] = total groups W).
 //
 // K5 (stage 2 of Fig. 2): LUT_q[j][c] = -2 <q_j, y_{j,c}>, the
-// query-dependent part of the residual-PQ distance,
+// query-dependent part of the residual-PQ distance;
+// -<q_j, y_{j,c}> for the inner-product metric (NEXT-3),
 // written in the scan's shared-memory layout [j/64][c][j%64] (padded
 // sub-spaces j >= m hold 0).
 #include "vlr_device.cuh"
@@ -88,7 +89,8 @@ cudaError_t launch_offsets(const Workspace& ws, int nq, int np, cudaStream_t s) 
 constexpr int kLutQB = 8;
 
 __global__ void __launch_bounds__(256) k_lut(const float* __restrict__ Q, int nq, int d, int m, int dsub,
-                                             const float* __restrict__ Y, int npairs, float* __restrict__ lut) {
+                                             const float* __restrict__ Y, int npairs, float scale,
+                                             float* __restrict__ lut) {
   extern __shared__ float qs[];  // [kLutQB][jv * (dsub + 1)]
   const int pair = blockIdx.x >> 2, cq = blockIdx.x & 3;
   const int q0 = blockIdx.y * kLutQB;
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(256) k_lut(const float* __restrict__ Q, int nq
       }
     }
     for (int qq = 0; qq < nqb; ++qq) {
-      const float4 v = make_float4(-2.f * acc[0][qq], -2.f * acc[1][qq], -2.f * acc[2][qq], -2.f * acc[3][qq]);
+      const float4 v = make_float4(scale * acc[0][qq], scale * acc[1][qq], scale * acc[2][qq], scale * acc[3][qq]);
       *reinterpret_cast<float4*>(lut + (((size_t)(q0 + qq) * npairs + pair) * 256 + c) * 64 + 4 * jj4) = v;
     }
   }
@@ -146,7 +148,8 @@ __global__ void __launch_bounds__(256) k_lut(const float* __restrict__ Q, int nq
 // queries' sub-vectors of sub-space jj in registers (64 floats) and walks 16
 // codes: per code 2 LDG.128 of the codeword, 64 FMA, 8 coalesced stores.
 __global__ void __launch_bounds__(256) k_lut8(const float* __restrict__ Q, int nq, int d, int m,
-                                              const float* __restrict__ Y, int npairs, float* __restrict__ lut) {
+                                              const float* __restrict__ Y, int npairs, float scale,
+                                              float* __restrict__ lut) {
   const int pair = blockIdx.x >> 2, cq = blockIdx.x & 3;
   const int q0 = blockIdx.y * kLutQB;
   const int jj = threadIdx.x & 63, cs = threadIdx.x >> 6;
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(256) k_lut8(const float* __restrict__ Q, int n
       t = fmaf(qv[qq][2], ya.z, t); t = fmaf(qv[qq][3], ya.w, t);
       t = fmaf(qv[qq][4], yb.x, t); t = fmaf(qv[qq][5], yb.y, t);
       t = fmaf(qv[qq][6], yb.z, t); t = fmaf(qv[qq][7], yb.w, t);
-      if (qq < nqb) lut[(((size_t)(q0 + qq) * npairs + pair) * 256 + c) * 64 + jj] = -2.f * t;
+      if (qq < nqb) lut[(((size_t)(q0 + qq) * npairs + pair) * 256 + c) * 64 + jj] = scale * t;
     }
   }
 }
@@ -188,8 +191,9 @@ __global__ void __launch_bounds__(256) k_lut8(const float* __restrict__ Q, int n
 cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
   dim3 grid(ix.npairs * 4, (nq + kLutQB - 1) / kLutQB);
+  const float scale = ix.metric == 1 ? -1.f : -2.f;  // exact power-of-two scaling of the fp32 dot
   if (ix.dsub == 8 && (ix.d % 4) == 0) {
-    k_lut8<<<grid, 256, 0, s>>>(Q, nq, ix.d, ix.m, ix.codebooks, ix.npairs, ws.lut);
+    k_lut8<<<grid, 256, 0, s>>>(Q, nq, ix.d, ix.m, ix.codebooks, ix.npairs, scale, ws.lut);
     return cudaGetLastError();
   }
   const size_t sm = (size_t)kLutQB * (ix.m < 64 ? ix.m : 64) * (ix.dsub + 1) * sizeof(float);
@@ -199,7 +203,7 @@ cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& w
     if (e != cudaSuccess) return e;
     configured = sm;
   }
-  k_lut<<<grid, 256, sm, s>>>(Q, nq, ix.d, ix.m, ix.dsub, ix.codebooks, ix.npairs, ws.lut);
+  k_lut<<<grid, 256, sm, s>>>(Q, nq, ix.d, ix.m, ix.dsub, ix.codebooks, ix.npairs, scale, ws.lut);
   return cudaGetLastError();
 }
 

@@ -21,9 +21,9 @@ constexpr int kMaxM = 128;         // padded sub-quantizer count of the scan ker
 #endif
 constexpr int kScanThreads = VLR_SCAN_THREADS;  // 16 warps per scan CTA (tuning variants: tools/variants.py)
 constexpr int kScanWarps = kScanThreads / kWarp;
-constexpr int kCandCap = 4096;     // K2 candidate list capacity per query (overflow -> rescan)
+constexpr int kCandCap = 8192;     // K2 candidate list capacity per query (overflow -> rescan)
 constexpr int kRefineChunk = 1024; // K3 candidates per exact-refine flush
-constexpr int kMaxNprobe = 1024;   // v1 cap on nprobe' (K3 sort buffer)
+constexpr int kMaxNprobe = 2048;   // cap on nprobe' (K3 sort buffer; the paper's operating point)
 constexpr int kLutPairBytes = 256 * 64 * 4;  // one [256 codes][64 sub-spaces] fp32 slab
 
 // ---------------------------------------------------------------- errors
@@ -46,10 +46,12 @@ void set_error(const std::string& msg);
 struct DeviceIndex {
   int d = 0, d8 = 0, nlist = 0, m = 0, mpad = 0, npairs = 0, dsub = 0;
   int rank = 0, world = 1, device = 0;
+  int metric = 0;              // 0 squared L2, 1 inner product (distance = -<q, x>)
+  int by_residual = 1;         // 1: codes encode x - c_l
   bool shard_only = false;
   // replicated, coarse quantizer
   float* centroids = nullptr;  // [nlist][d]
-  float* cnorm2 = nullptr;     // [nlist] ||c||^2 (fp64 -> fp32)
+  float* cnorm2 = nullptr;     // [nlist] ||c||^2 (fp64 -> fp32); zeros for metric 1 (filter = -2<q,c>)
   uint16_t* cf16 = nullptr;    // [nlist][d8] fp16(c * 2^c_exp) (RN), zero-padded to d8 (filter operand A)
   int c_exp = 0;               // power-of-two centroid scale: max |c * 2^c_exp| < 2^14
   float c_inv = 1.f;           // 2^-c_exp
@@ -72,7 +74,8 @@ struct DeviceIndex {
 
 struct Workspace {
   int cap_nq = 0, cap_np = 0, cap_k = 0, n_cta = 0;
-  float* qnorm = nullptr;      // [nq] ||q|| (fp32)
+  float* qnorm = nullptr;      // [nq] ||q|| (fp32, rounded up; filter band)
+  float* qsq = nullptr;        // [nq] ||q||^2 (fp64 sum -> fp32; term1 of L2 with by_residual = 0)
   uint16_t* qf16 = nullptr;    // [nq][d8] fp16(q * 2^e_q) (RN), zero-padded (filter operand B)
   float* qinv = nullptr;       // [nq] 2^-e_q
   float* dt = nullptr;         // [nq][nlist] filter distances ||c||^2 - 2<q,c>
@@ -82,7 +85,8 @@ struct Workspace {
   double* exact = nullptr;     // [nq][kCandCap] exact fp64 D of listed candidates (K3a)
   float* bound = nullptr;      // [nq] candidate bound theta~ + 2 Delta*
   int32_t* probes = nullptr;   // [nq][np]
-  float* term1 = nullptr;      // [nq][np] ||q - c_l||^2 (fp64 -> fp32)
+  float* term1 = nullptr;      // [nq][np] query-dependent constant of probe p (fp64 -> fp32): ||q - c_l||^2
+                               // (L2), -<q, c_l> (IP), ||q||^2 (L2, by_residual 0), 0 (IP, by_residual 0)
   int32_t* plocal = nullptr;   // [nq][np] local list or -1
   int64_t* item_off = nullptr; // [nq*np + 1] group prefix of owned work items
   int64_t* item_local = nullptr; // [nq*np] within-query group prefix
@@ -124,8 +128,8 @@ namespace vlr {
 cudaError_t launch_layout(const DeviceIndex& ix, const uint8_t* stage_codes, const int64_t* stage_ids,
                           const int64_t* vbase, const int32_t* lglob, cudaStream_t s);
 // stage 0..2 coarse quantizer
-cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, uint16_t* qf16, float* qinv, int32_t* status,
-                         cudaStream_t s);
+cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, float* qsq, uint16_t* qf16, float* qinv,
+                         int32_t* status, cudaStream_t s);
 cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, float* dt, float* gmin,
                              cudaStream_t s);
 cudaError_t launch_round_f16(const float* src, int rows, int d, int d8, float scale, uint16_t* dst, cudaStream_t s);

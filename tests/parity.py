@@ -14,7 +14,8 @@ FLOOR = 0.25     # absolute floor 1e-5 * 0.25 * ||q||^2 (DESIGN reading A11)
 
 
 def tol(ref, qn2):
-    return REL * np.maximum(ref, FLOOR * qn2)
+    # |ref|: inner-product distances (-<q, x>, NEXT-3) are negative
+    return REL * np.maximum(np.abs(ref), FLOOR * qn2)
 
 
 def check(index, Q, gpu, orc, hot=None, idmap=None, qsel=None, max_report=5):

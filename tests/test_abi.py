@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol():
 
 
 def test_version():
-    assert vlr.version() == (1, 0)
+    assert vlr.version() == (1, 1)
 
 
 def _tiny(m=2, d=4, L=3):
@@ -64,8 +64,8 @@ def test_load_validation_codes():
     Y3 = np.zeros((3, 256, 1), np.float32)
     assert status_of(lambda: load(C, Y3, offs, ids, np.zeros((5, 3), np.uint8), device=0)) == "DIM_MISMATCH"
     assert status_of(lambda: load(C, Y, offs, ids, codes, nbits=4, device=0)) == "UNSUPPORTED"
-    assert status_of(lambda: load(C, Y, offs, ids, codes, metric=1, device=0)) == "UNSUPPORTED"
-    assert status_of(lambda: load(C, Y, offs, ids, codes, by_residual=0, device=0)) == "UNSUPPORTED"
+    assert status_of(lambda: load(C, Y, offs, ids, codes, metric=2, device=0)) == "UNSUPPORTED"
+    assert status_of(lambda: load(C, Y, offs, ids, codes, by_residual=2, device=0)) == "INVALID_ARG"
     Cn = C.copy(); Cn[1, 2] = np.nan
     assert status_of(lambda: load(Cn, Y, offs, ids, codes, device=0)) == "NONFINITE"
     Yn = Y.copy(); Yn[0, 5, 0] = np.inf

@@ -246,18 +246,18 @@ def test_offset_data_stress():
 
 
 def test_candidate_overflow_rescan_path():
-    # 5000 identical centroids: every one lies inside the filter band, so the
-    # candidate list (capacity 4096) overflows and K3 takes the rescan path.
+    # 9000 identical centroids: every one lies inside the filter band, so the
+    # candidate list (capacity 8192) overflows and K3 takes the rescan path.
     rng = np.random.default_rng(9)
-    L, d = 5000, 8
+    L, d = 9000, 8
     c = rng.standard_normal(d).astype(np.float32)
     C = np.repeat(c[None], L, 0)
-    C[4990:] += np.float32(2.0)
+    C[8990:] += np.float32(2.0)
     Y = (0.2 * rng.standard_normal((2, 256, 4))).astype(np.float32)
     lists = [(np.arange(i * 2, i * 2 + 2), rng.integers(0, 256, (2, 2)).astype(np.uint8)) for i in range(L)]
     ix = datagen.index_from_parts(C, Y, lists)
     Q = (c + 0.01 * rng.standard_normal((3, d))).astype(np.float32)
-    for npb in (8, 700):
+    for npb in (8, 700, 2048):
         errs, g, o = run_parity(ix, Q, npb, 10)
         assert not errs, errs
         assert g["probes"][0].tolist() == list(range(npb))  # equal distances -> ascending id
@@ -356,3 +356,54 @@ def test_profiling_modes(c1_index, c1_queries):
         for key in base:
             assert np.array_equal(base[key], g[key]), key
     h.close()
+
+
+# --------------------------------------------------------------- NEXT-3 variants
+def test_golden_tiny_variants_on_gpu():
+    gv = load_golden("tiny_variants.json")
+    base = load_golden(gv["index"])
+    ix = golden_index(base)
+    Q = np.array(base["queries"], np.float32)
+    for case in gv["cases"]:
+        h = vlr.Index.from_arrays(ix, hot=case["hot"], metric=case["metric"], by_residual=case["by_residual"])
+        g = gpu_search(h, Q, case["nprobe"], case["k"])
+        h.close()
+        assert g["probes"].tolist() == case["probes"], case
+        assert g["miss"].tolist() == case["miss"], case
+        assert g["ids"].tolist() == case["ids"], case
+        exp = np.array([[fval(x) for x in row] for row in case["dist"]], np.float32)
+        assert np.array_equal(g["dist"], exp), case  # every value here is exact in fp32
+
+
+@pytest.fixture(scope="module")
+def c1_variant_indexes():
+    c = datagen.CONFIGS["C1"]
+    return {(mt, br): datagen.make_index(c["N"], c["d"], c["nlist"], c["m"], metric=mt, by_residual=br)
+            for mt, br in ((1, 1), (0, 0), (1, 0))}
+
+
+@pytest.mark.parametrize("metric,by_residual", [(1, 1), (0, 0), (1, 0)])
+def test_c1_variant_parity(c1_variant_indexes, c1_queries, metric, by_residual):
+    """Inner-product metric and plain (non-residual) PQ: probes and mask
+    bit-exact, distances within the R2 rule, id sets by R3 (DESIGN §2 A1', A2')."""
+    c = datagen.CONFIGS["C1"]
+    ix = c1_variant_indexes[(metric, by_residual)]
+    errs, g, o = run_parity(ix, c1_queries, c["nprobe"], c["k"])
+    assert not errs, errs
+    hot = np.arange(0, ix.nlist, 3)
+    for npb, k in ((1, 1), (64, 25), (1024, 10)):
+        errs, g, o = run_parity(ix, c1_queries[:24], npb, k, hot=hot)
+        assert not errs, (npb, k, errs)
+
+
+@pytest.mark.parametrize("metric", [0, 1])
+def test_paper_operating_point_nprobe_2048_k25(metric):
+    """The paper's operating point nprobe = 2048, k = 25 on an index
+    with nlist = 8192 > nprobe, so the coarse select keeps a strict subset."""
+    ix = datagen.make_index(600_000, 64, 8192, 16, seed=21, device="cuda", metric=metric)
+    Q = datagen.make_queries(600_000, 64, 8192, 40, seed=21, stream=2)
+    hot = np.arange(0, 8192, 2)
+    for hh in (None, hot):
+        errs, g, o = run_parity(ix, Q, 2048, 25, hot=hh)
+        assert not errs, errs
+        assert g["probes"].shape == (40, 2048)

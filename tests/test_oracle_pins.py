@@ -260,3 +260,113 @@ def test_zipf_stream_skew(small_index):
     cu = datagen.access_counts(ix.centroids, Qu, 1)
     assert datagen.topk_share(cz) > 0.5
     assert datagen.topk_share(cu) < 0.4
+
+
+# --- NEXT-3 variants: inner-product metric and by_residual = 0 -------------
+# ("independent of the distance metric"; DESIGN readings A1', A2')
+def test_golden_tiny_variants():
+    g = load_golden("tiny_variants.json")
+    ix = golden_index(load_golden(g["index"]))
+    Q = np.array(load_golden(g["index"])["queries"], np.float32)
+    for case in g["cases"]:
+        r = oracle.search(ix, Q, case["nprobe"], case["k"], hot=case["hot"], metric=case["metric"],
+                          by_residual=case["by_residual"])
+        assert r["probes"].tolist() == case["probes"], case
+        assert r["miss"].tolist() == case["miss"], case
+        assert r["ids"].tolist() == case["ids"], case
+        exp = np.array([[fval(x) for x in row] for row in case["dist"]])
+        assert np.array_equal(r["dist"], exp), case
+        if "coarse" in case:
+            p, dd = oracle.coarse(Q, ix.centroids, case["nprobe"], metric=case["metric"])
+            assert p.tolist() == case["probes"]
+            assert np.array_equal(dd, np.array(case["coarse"]))
+
+
+def test_ip_coarse_matches_numpy_ranking(small_index, small_queries):
+    # the IP coarse key is -<q, c>; against an fp64 numpy matmul + lexsort
+    C, Q = small_index.centroids, small_queries
+    p, dd = oracle.coarse(Q, C, C.shape[0], metric=1)
+    ref = -(Q.astype(np.float64) @ C.astype(np.float64).T)
+    for qi in range(len(Q)):
+        assert np.allclose(dd[qi], ref[qi, p[qi]], rtol=0, atol=1e-12)
+        o = np.lexsort((np.arange(C.shape[0]), ref[qi]))
+        gaps = np.diff(ref[qi, o])
+        clear = np.concatenate([[True], gaps > 1e-12]) & np.concatenate([gaps > 1e-12, [True]])
+        assert np.array_equal(p[qi][clear], o[clear])
+    # a query equal to a unit-norm centroid direction probes it first
+    u = C[7] / np.linalg.norm(C[7])
+    p1, _ = oracle.coarse((u * 3.0)[None, :].astype(np.float32), C / np.linalg.norm(C, axis=1, keepdims=True), 1,
+                          metric=1)
+    assert p1[0, 0] == 7
+
+
+def _flat_topk_variant(ix, Q, k, metric, by_residual):
+    c, y, _ = _recon(ix, np.arange(ix.N))
+    X = c + y if by_residual else y
+    Qd = Q.astype(np.float64)
+    if metric == 1:
+        D = -(Qd @ X.T)
+    else:
+        D = (Qd * Qd).sum(1)[:, None] + (X * X).sum(1)[None, :] - 2 * Qd @ X.T
+    out = []
+    for row in D:
+        o = np.lexsort((ix.ids, row))[:k]
+        out.append((ix.ids[o], row[o]))
+    return out
+
+
+@pytest.mark.parametrize("metric,by_residual", [(1, 1), (0, 0), (1, 0)])
+def test_variant_full_probe_equals_exhaustive(small_index, small_queries, metric, by_residual):
+    ix, Q = small_index, small_queries[:16]
+    k = 10
+    r = oracle.search(ix, Q, ix.nlist, k, metric=metric, by_residual=by_residual)
+    flat = _flat_topk_variant(ix, Q, k + 1, metric, by_residual)
+    for qi, (fid, fd) in enumerate(flat):
+        assert np.allclose(r["dist"][qi], fd[:k], rtol=1e-10, atol=1e-12)
+        if fd[k] - fd[k - 1] > 1e-9:
+            assert set(r["ids"][qi].tolist()) == set(fid[:k].tolist())
+
+
+def test_variant_dist_identities(small_index, small_queries):
+    # ||q - x||^2 = ||q||^2 + ||x||^2 - 2<q, x> links the L2 and IP branches;
+    # the residual and plain branches differ exactly by the centroid term
+    ix, Q = small_index, small_queries
+    rng = np.random.default_rng(5)
+    pos = rng.integers(0, ix.N, 300)
+    qi = rng.integers(0, len(Q), 300)
+    c, y, _ = _recon(ix, pos)
+    q = Q[qi].astype(np.float64)
+    d = {(mt, br): oracle.dist_ref(ix, Q, qi, ix.ids[pos], metric=mt, by_residual=br) for mt in (0, 1) for br in (0, 1)}
+    for br, X in ((1, c + y), (0, y)):
+        lhs = d[(0, br)] - (q * q).sum(1) - (X * X).sum(1)
+        assert np.allclose(lhs, 2.0 * d[(1, br)], rtol=1e-9, atol=1e-9)
+    assert np.allclose(d[(1, 1)] - d[(1, 0)], -(q * c).sum(1), rtol=1e-9, atol=1e-12)
+    # the GPU's LUT decomposition (second path): term1 + b + sum_j LUT
+    dsub = ix.d // ix.m
+    lut_ip = -(q * y).reshape(-1, ix.m, dsub).sum(2).sum(1)
+    assert np.allclose(d[(1, 1)], -(q * c).sum(1) + lut_ip, rtol=1e-12, atol=1e-12)
+    assert np.allclose(d[(0, 0)], (q * q).sum(1) + (y * y).sum(1) + 2 * lut_ip, rtol=1e-12, atol=1e-12)
+
+
+def test_lossless_plain_pq_is_exact_knn_both_metrics():
+    from sklearn.neighbors import NearestNeighbors
+    ix = datagen.make_index(3000, 16, 32, 4, seed=13, lossless=True, by_residual=0)
+    Q = datagen.make_queries(3000, 16, 32, 40, seed=13, stream=2)
+    X = ix.vectors.astype(np.float64)  # x_i := yhat_i
+    nn = NearestNeighbors(n_neighbors=11, algorithm="brute", metric="sqeuclidean").fit(X)
+    dist, ind = nn.kneighbors(Q.astype(np.float64))
+    r = oracle.search(ix, Q, ix.nlist, 10)
+    assert ix.by_residual == 0 and ix.metric == 0
+    for qi in range(len(Q)):
+        assert np.allclose(r["dist"][qi], dist[qi, :10], rtol=2e-6, atol=2e-7)
+        if dist[qi, 10] - dist[qi, 9] > 1e-5:
+            assert set(r["ids"][qi].tolist()) == set(ix.ids[ind[qi, :10]].tolist())
+    # maximum inner product: scikit-learn's cosine on rows of equal norm ranks as IP;
+    # here a direct argsort of X q (library matmul) is the reference
+    ri = oracle.search(ix, Q, ix.nlist, 10, metric=1)
+    S = Q.astype(np.float64) @ X.T
+    for qi in range(len(Q)):
+        o = np.argsort(-S[qi], kind="stable")[:11]
+        assert np.allclose(ri["dist"][qi], -S[qi, o[:10]], rtol=2e-6, atol=2e-7)
+        if S[qi, o[9]] - S[qi, o[10]] > 1e-5:
+            assert set(ri["ids"][qi].tolist()) == set(ix.ids[o[:10]].tolist())
