@@ -20,4 +20,5 @@ from .gen import (  # noqa: F401
     index_from_parts,
     list_sizes,
     deal_owners,
+    pack_nibbles,
 )

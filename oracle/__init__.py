@@ -41,15 +41,15 @@ def lib():
         P = ctypes.c_void_p
         I = ctypes.c_int32
         L.oracle_coarse.argtypes = [P, ctypes.c_int64, P, I, I, I, P, P, I, I]
-        L.oracle_search.argtypes = [P, ctypes.c_int64, I, P, I, P, I, P, P, P, P, I, I, P, P, P, P, P, P, I, I, I]
-        L.oracle_dist_many.argtypes = [P, I, P, P, I, P, P, P, P, ctypes.c_int64, P, I, I, I]
+        L.oracle_search.argtypes = [P, ctypes.c_int64, I, P, I, P, I, I, P, P, P, P, I, I, P, P, P, P, P, P, I, I, I]
+        L.oracle_dist_many.argtypes = [P, I, P, P, I, I, P, P, P, P, ctypes.c_int64, P, I, I, I]
         L.oracle_coarse_dist.argtypes = [P, P, ctypes.c_int32]
         L.oracle_coarse_dist.restype = ctypes.c_double
         L.oracle_adc_dist.argtypes = [P, P, P, P, ctypes.c_int32, ctypes.c_int32]
         L.oracle_adc_dist.restype = ctypes.c_double
         L.oracle_coarse_ip.argtypes = [P, P, ctypes.c_int32]
         L.oracle_coarse_ip.restype = ctypes.c_double
-        L.oracle_adc_dist_v.argtypes = [P, P, P, P, I, I, I, I]
+        L.oracle_adc_dist_v.argtypes = [P, P, P, P, I, I, I, I, I]
         L.oracle_adc_dist_v.restype = ctypes.c_double
         for f in (L.oracle_coarse, L.oracle_search, L.oracle_dist_many):
             f.restype = ctypes.c_int
@@ -78,6 +78,14 @@ def _variant(index, metric, by_residual):
     if by_residual is None:
         by_residual = int(getattr(index, "by_residual", 1)) if index is not None else 1
     return int(metric), int(by_residual)
+
+
+def _nbits(index) -> int:
+    """bits per sub-code (8, or 4 for the packed 4-bit PQ of NEXT-3)."""
+    nb = int(getattr(index, "nbits", 8))
+    if nb not in (4, 8):
+        raise ValueError("nbits must be 4 or 8")
+    return nb
 
 
 def coarse(Q, centroids, nprobe, nthreads=0, metric=0):
@@ -121,7 +129,8 @@ def search(index, Q, nprobe, k, hot=None, nthreads=0, metric=None, by_residual=N
     out = dict(ids=np.empty((nq, k), np.int64), dist=np.empty((nq, k), np.float64),
                miss=np.empty((nq, npr), np.uint8), probes=np.empty((nq, npr), np.int32),
                kth1=np.empty(nq, np.float64), ncand=np.empty(nq, np.int64))
-    rc = lib().oracle_search(_p(Q), nq, d, _p(C), L, _p(Y), index.m, _p(offs), _p(ids), _p(codes), _p(isht),
+    rc = lib().oracle_search(_p(Q), nq, d, _p(C), L, _p(Y), index.m, _nbits(index), _p(offs), _p(ids), _p(codes),
+                             _p(isht),
                              nprobe, k, _p(out["ids"]), _p(out["dist"]), _p(out["miss"]), _p(out["probes"]),
                              _p(out["kth1"]), _p(out["ncand"]), *_variant(index, metric, by_residual),
                              nthreads or default_threads())
@@ -158,7 +167,7 @@ def dist_ref(index, Q, qidx, ids, idmap: IdMap | None = None, nthreads=0, metric
         Q = _c(Q, np.float32)
         tmp = np.empty(len(sel), np.float64)
         lib().oracle_dist_many(_p(Q), index.d, _p(_c(index.centroids, np.float32)), _p(_c(index.codebooks, np.float32)),
-                               index.m, _p(_c(index.codes, np.uint8)), _p(_c(qidx[sel], np.int64)),
+                               index.m, _nbits(index), _p(_c(index.codes, np.uint8)), _p(_c(qidx[sel], np.int64)),
                                _p(_c(lst[sel], np.int32)), _p(_c(pos[sel], np.int64)), len(sel), _p(tmp),
                                *_variant(index, metric, by_residual), nthreads or default_threads())
         out[sel] = tmp

@@ -26,7 +26,11 @@
  *       the LUT of stage 2/3 accumulates.
  *   O7  result: k smallest candidates by (dist, id), padded with (-1, +inf);
  *       also the (k+1)-th distance (for the tie rule R3).
- * Variants (NEXT-3, readings A1'/A2' in DESIGN.md §2):
+ * Variants (NEXT-3, readings A1'/A2'/A4' in DESIGN.md §2):
+ *   nbits = 4 (the paper's 4-bit PQ): 16 codewords per
+ *       sub-space, Y is [m][16][dsub], a code row has ceil(m/2) bytes and
+ *       sub-code j is the low nibble of byte j/2 for even j, the high nibble
+ *       for odd j;
  *   by_residual = 0: xhat_i = concat_j Y[j][code_ij] (no centroid term);
  *   metric = 1 (inner product, "independent of the distance metric",
  *       PAPER.md:243): coarse key D[q,l] = -<q, c_l> and dist_i = -<q, xhat_i>,
@@ -122,17 +126,28 @@ double oracle_adc_dist(const float* q, const float* c_l, const float* Y, const u
     return s;
 }
 
+/* sub-code j of a code row: byte j (nbits 8), or nibble j (nbits 4: low
+ * nibble of byte j/2 for even j, high nibble for odd j) */
+static int32_t subcode(const uint8_t* code, int32_t j, int32_t nbits) {
+    if (nbits == 8) return code[j];
+    return (code[j >> 1] >> (4 * (j & 1))) & 15;
+}
+
+/* bytes of one code row */
+static int64_t row_bytes(int32_t m, int32_t nbits) { return ((int64_t)m * nbits + 7) / 8; }
+
 /* ---- O6 variants: xhat = [c_l +] concat_j Y[j][code_j] (by_residual), and
  * dist = sum_t (q_t - xhat_t)^2 (metric 0) or -sum_t q_t xhat_t (metric 1) ---- */
 double oracle_adc_dist_v(const float* q, const float* c_l, const float* Y, const uint8_t* code,
-                         int32_t d, int32_t m, int32_t metric, int32_t by_residual) {
-    if (metric == 0 && by_residual) return oracle_adc_dist(q, c_l, Y, code, d, m);
+                         int32_t d, int32_t m, int32_t nbits, int32_t metric, int32_t by_residual) {
+    if (metric == 0 && by_residual && nbits == 8) return oracle_adc_dist(q, c_l, Y, code, d, m);
     int32_t dsub = d / m;
+    int32_t ksub = 1 << nbits;
     double s = 0.0;
     for (int32_t t = 0; t < d; ++t) {
         int32_t j = t / dsub;
         int32_t u = t - j * dsub;
-        double xh = (double)Y[((int64_t)j * 256 + code[j]) * dsub + u];
+        double xh = (double)Y[((int64_t)j * ksub + subcode(code, j, nbits)) * dsub + u];
         if (by_residual) xh = (double)c_l[t] + xh;
         if (metric == 1) {
             double pr = (double)q[t] * xh;
@@ -163,11 +178,13 @@ static void insert_best(pair_t* best, int32_t kk, double dist, int64_t id) {
  * except out_ids/out_dist.
  */
 int oracle_search(const float* Q, int64_t nq, int32_t d, const float* C, int32_t nlist,
-                  const float* Y, int32_t m, const int64_t* offsets, const int64_t* ids,
+                  const float* Y, int32_t m, int32_t nbits, const int64_t* offsets, const int64_t* ids,
                   const uint8_t* codes, const uint8_t* is_hot, int32_t nprobe, int32_t k,
                   int64_t* out_ids, double* out_dist, uint8_t* miss, int32_t* probes,
                   double* kth1, int64_t* ncand, int32_t metric, int32_t by_residual, int32_t nthreads) {
     if (nprobe < 1 || k < 1 || m < 1 || d % m != 0 || metric < 0 || metric > 1) return 1;
+    if (nbits != 8 && nbits != 4) return 1;
+    const int64_t rb = row_bytes(m, nbits);
     int32_t np = nprobe < nlist ? nprobe : nlist;
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -194,7 +211,8 @@ int oracle_search(const float* Q, int64_t nq, int32_t d, const float* C, int32_t
             if (miss) miss[qi * np + p] = is_miss;
             if (is_miss) continue;
             for (int64_t i = offsets[l]; i < offsets[l + 1]; ++i) {
-                double dist = oracle_adc_dist_v(q, C + (int64_t)l * d, Y, codes + i * m, d, m, metric, by_residual);
+                double dist = oracle_adc_dist_v(q, C + (int64_t)l * d, Y, codes + i * rb, d, m, nbits, metric,
+                                                by_residual);
                 insert_best(best, kk, dist, ids[i]);
                 ++nc;
             }
@@ -215,7 +233,7 @@ int oracle_search(const float* Q, int64_t nq, int32_t d, const float* C, int32_t
  * dist_ref(q, vector): O6 for explicit (query row, list, position) triples,
  * used to check every distance the GPU returns (rule R2).
  */
-int oracle_dist_many(const float* Q, int32_t d, const float* C, const float* Y, int32_t m,
+int oracle_dist_many(const float* Q, int32_t d, const float* C, const float* Y, int32_t m, int32_t nbits,
                      const uint8_t* codes, const int64_t* qidx, const int32_t* list,
                      const int64_t* pos, int64_t n, double* out, int32_t metric, int32_t by_residual,
                      int32_t nthreads) {
@@ -224,8 +242,8 @@ int oracle_dist_many(const float* Q, int32_t d, const float* C, const float* Y, 
 #pragma omp parallel for schedule(static)
 #endif
     for (int64_t i = 0; i < n; ++i)
-        out[i] = oracle_adc_dist_v(Q + qidx[i] * d, C + (int64_t)list[i] * d, Y, codes + pos[i] * m, d, m,
-                                   metric, by_residual);
+        out[i] = oracle_adc_dist_v(Q + qidx[i] * d, C + (int64_t)list[i] * d, Y, codes + pos[i] * row_bytes(m, nbits),
+                                   d, m, nbits, metric, by_residual);
     return 0;
 }
 

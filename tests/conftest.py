@@ -61,3 +61,19 @@ def c1_queries():
     import datagen
     c = datagen.CONFIGS["C1"]
     return datagen.make_queries(c["N"], c["d"], c["nlist"], c["batch"], stream=2, alpha=c["alpha"])
+
+
+def golden_pq4_index():
+    """4-bit IndexArrays from tests/golden/tiny_pq4.json (hand-packed codes)."""
+    import datagen
+    g4 = load_golden("tiny_pq4.json")
+    g = load_golden(g4["index"])
+    cb = np.zeros((g["m"], g4["ksub"], g["dsub"]), np.float32)
+    for j, s, y in g["codewords_nonzero"]["entries"]:
+        cb[j, s] = y
+    codes = np.array([row for lst in g4["codes_packed_per_list"] for row in lst], np.uint8)
+    sizes = [len(lst) for lst in g4["codes_packed_per_list"]]
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    ids = np.array([i for l in g["lists"] for i in l["ids"]], np.int64)
+    return datagen.IndexArrays(d=g["d"], nlist=g["nlist"], m=g["m"], centroids=np.array(g["centroids"], np.float32),
+                               codebooks=cb, list_offsets=offs, ids=ids, codes=codes, nbits=4), g

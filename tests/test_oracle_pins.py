@@ -370,3 +370,59 @@ def test_lossless_plain_pq_is_exact_knn_both_metrics():
         assert np.allclose(ri["dist"][qi], -S[qi, o[:10]], rtol=2e-6, atol=2e-7)
         if S[qi, o[9]] - S[qi, o[10]] > 1e-5:
             assert set(ri["ids"][qi].tolist()) == set(ix.ids[o[:10]].tolist())
+
+
+# --- NEXT-3: 4-bit PQ (reading A4') -----------------------
+def _unpack4(codes, m):
+    j = np.arange(m)
+    return (codes[:, j // 2] >> (4 * (j % 2))) & 15
+
+
+def test_golden_tiny_pq4_hand_packed():
+    from conftest import golden_pq4_index
+    ix, g = golden_pq4_index()
+    Q = np.array(g["queries"], np.float32)
+    for case in g["cases"]:
+        r = oracle.search(ix, Q, case["nprobe"], case["k"], hot=case["hot"])
+        assert r["probes"].tolist() == case["probes"]
+        assert r["miss"].tolist() == case["miss"]
+        assert r["ids"].tolist() == case["ids"]
+        assert np.array_equal(r["dist"], np.array([[fval(x) for x in row] for row in case["dist"]]))
+
+
+def test_pack_nibbles_layout():
+    import torch
+    cc = torch.tensor([[1, 2, 3], [15, 0, 7]], dtype=torch.uint8)
+    assert datagen.pack_nibbles(cc).tolist() == [[0x21, 0x03], [0x0F, 0x07]]
+
+
+@pytest.mark.parametrize("metric,by_residual", [(0, 1), (1, 1), (0, 0)])
+def test_pq4_full_probe_equals_exhaustive(metric, by_residual):
+    ix = datagen.make_index(5000, 32, 48, 8, seed=17, nbits=4, metric=metric, by_residual=by_residual)
+    assert ix.codes.shape == (5000, 4) and ix.codebooks.shape == (8, 16, 4)
+    Q = datagen.make_queries(5000, 32, 48, 16, seed=17, stream=2)
+    codes = _unpack4(ix.codes, ix.m).astype(np.int64)
+    y = ix.codebooks[np.arange(ix.m)[None, :], codes].reshape(ix.N, ix.d).astype(np.float64)
+    lst = np.searchsorted(ix.list_offsets, np.arange(ix.N), side="right") - 1
+    X = ix.centroids[lst].astype(np.float64) + y if by_residual else y
+    Qd = Q.astype(np.float64)
+    D = -(Qd @ X.T) if metric else (Qd * Qd).sum(1)[:, None] + (X * X).sum(1)[None, :] - 2 * Qd @ X.T
+    r = oracle.search(ix, Q, ix.nlist, 10)
+    for qi in range(len(Q)):
+        o = np.lexsort((ix.ids, D[qi]))[:11]
+        assert np.allclose(r["dist"][qi], D[qi, o[:10]], rtol=1e-10, atol=1e-12)
+        if D[qi, o[10]] - D[qi, o[9]] > 1e-9:
+            assert set(r["ids"][qi].tolist()) == set(ix.ids[o[:10]].tolist())
+
+
+def test_pq4_lossless_is_exact_knn():
+    from sklearn.neighbors import NearestNeighbors
+    ix = datagen.make_index(3000, 16, 32, 4, seed=19, lossless=True, nbits=4)
+    Q = datagen.make_queries(3000, 16, 32, 40, seed=19, stream=2)
+    nn = NearestNeighbors(n_neighbors=11, algorithm="brute", metric="sqeuclidean").fit(ix.vectors.astype(np.float64))
+    dist, ind = nn.kneighbors(Q.astype(np.float64))
+    r = oracle.search(ix, Q, ix.nlist, 10)
+    for qi in range(len(Q)):
+        assert np.allclose(r["dist"][qi], dist[qi, :10], rtol=2e-6, atol=2e-7)
+        if dist[qi, 10] - dist[qi, 9] > 1e-5:
+            assert set(r["ids"][qi].tolist()) == set(ix.ids[ind[qi, :10]].tolist())
