@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--seed", type=int, default=2504_08930)
     p.add_argument("--metric", type=int, default=0, choices=[0, 1], help="0 squared L2, 1 inner product (NEXT-3)")
     p.add_argument("--by-residual", type=int, default=1, choices=[0, 1], help="1 residual PQ codes (NEXT-3: 0)")
+    p.add_argument("--nbits", type=int, default=8, choices=[4, 8], help="bits per PQ sub-code (NEXT-3: 4)")
+    p.add_argument("--m", type=int, default=None, help="override PQ sub-quantizer count")
     p.add_argument("--no-oracle", action="store_true")
     p.add_argument("--oracle-seconds", type=float, default=15.0)
     p.add_argument("--e2e-steps", type=int, default=None)
@@ -63,13 +65,14 @@ def parse():
 def cfg_of(a):
     import datagen
     c = dict(datagen.CONFIGS[a.config])
-    for key in ("N", "batch", "nprobe", "k", "alpha"):
+    for key in ("N", "batch", "nprobe", "k", "alpha", "m"):
         v = getattr(a, key)
         if v is not None:
             c[key] = v
     c["hot_mass"] = a.hot_mass
     c["metric"] = a.metric
     c["by_residual"] = a.by_residual
+    c["nbits"] = a.nbits
     return c
 
 
@@ -79,7 +82,7 @@ def workload_name(c, name):
     if c.get("metric", 0) == 1 or c.get("by_residual", 1) == 0:
         var = ", " + ("inner product" if c.get("metric", 0) == 1 else "L2") + \
               ("" if c.get("by_residual", 1) else ", non-residual PQ")
-    return (f"{name}: {c['N'] / 1e6:g}M x d{c['d']}, IVF{c['nlist']}, PQ{c['m']}x8, nprobe {c['nprobe']}, "
+    return (f"{name}: {c['N'] / 1e6:g}M x d{c['d']}, IVF{c['nlist']}, PQ{c['m']}x{c.get('nbits', 8)}, nprobe {c['nprobe']}, "
             f"k {c['k']}, batch {c['batch']}, Zipf alpha {c['alpha']}, {hot}{var}")
 
 
@@ -193,7 +196,7 @@ def gen_index(c, seed, rank, world, hot=None, gt_queries=None):
     t = time.time()
     cache = os.environ.get("VLR_GEN_CACHE")
     key = f"{c['N']}_{c['d']}_{c['nlist']}_{c['m']}_{seed}_{world}_{rank}_{'all' if hot is None else len(hot)}"
-    key += f"_mt{c['metric']}_br{c['by_residual']}"
+    key += f"_mt{c['metric']}_br{c['by_residual']}_nb{c['nbits']}"
     if gt_queries is not None:
         import hashlib
         key += f"_gt{len(gt_queries)}_{hashlib.md5(gt_queries.tobytes()).hexdigest()[:10]}"
@@ -204,12 +207,13 @@ def gen_index(c, seed, rank, world, hot=None, gt_queries=None):
             f = {n: np.ascontiguousarray(np.load(os.path.join(path, n + ".npy"), mmap_mode="r")) for n in names}
             gt = f.pop("gt_ids", None)
             ix = datagen.IndexArrays(d=c["d"], nlist=c["nlist"], m=c["m"], seed=seed, metric=c["metric"],
-                                     by_residual=c["by_residual"], **f)
+                                     by_residual=c["by_residual"], nbits=c["nbits"], **f)
             if gt is not None:
                 ix.gt_ids = gt
             return ix, time.time() - t
     ix = datagen.make_index(c["N"], c["d"], c["nlist"], c["m"], seed=seed, device="cuda", owned=owned,
-                            gt_queries=gt_queries, metric=c["metric"], by_residual=c["by_residual"])
+                            gt_queries=gt_queries, metric=c["metric"], by_residual=c["by_residual"],
+                            nbits=c["nbits"])
     if cache:
         os.makedirs(path, exist_ok=True)
         for n in names:
@@ -365,7 +369,7 @@ def main():
     stage_mean = {k2: float(np.mean([s[k2] for s in stages])) for k2 in stages[0]}
     # ---- algorithmic scan bytes: sum over owned hot probes of n_l * (m + 4)
     sizes = ix.list_sizes
-    per_vec = c["m"] + 4
+    per_vec = (c["m"] * c["nbits"] + 7) // 8 + 4
     step_bytes, hit = [], []
     for i in range(a.steps):
         prb = outs[i][3].cpu().numpy()
@@ -381,7 +385,9 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_scan_latest.json")) as f:
             tj = json.load(f)
-        if tj.get("config") == a.config and tj.get("batch") == B:
+        same = (tj.get("config") == a.config and tj.get("batch") == B and tj.get("nbits", 8) == c["nbits"]
+                and tj.get("m", datagen.CONFIGS[a.config]["m"]) == c["m"] and tj.get("metric", 0) == c["metric"])
+        if same:
             traffic = tj.get("dram_bytes_per_launch")
     except Exception:
         pass

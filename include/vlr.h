@@ -44,8 +44,8 @@ typedef enum {
   VLR_ERR_OOM = 6,             /* device allocation failed */
   VLR_ERR_CUDA = 7,            /* any other CUDA runtime error (no device, launch failure, ...) */
   VLR_ERR_NCCL = 8,            /* NCCL error; the communicator is aborted, the handle unusable */
-  VLR_ERR_UNSUPPORTED = 9      /* valid but outside this version: nbits != 8, metric not in {0, 1},
-                                  m > 128, k > 32, nprobe' > 2048 */
+  VLR_ERR_UNSUPPORTED = 9      /* valid but outside this version: nbits not in {4, 8}, metric not in
+                                  {0, 1}, m > 128 (8-bit) / 256 (4-bit), k > 32, nprobe' > 2048 */
 } vlr_status;
 
 /*
@@ -64,16 +64,19 @@ typedef enum {
 typedef struct {
   int32_t d;            /* vector dimension, >= 1 */
   int32_t nlist;        /* number of inverted lists / coarse centroids, >= 1 */
-  int32_t m;            /* PQ sub-quantizers, d % m == 0, 1 <= m <= 128 */
-  int32_t nbits;        /* bits per sub-code; must be 8 (256 codewords) */
+  int32_t m;            /* PQ sub-quantizers, d % m == 0, 1 <= m <= 128 (nbits 8) or 256 (nbits 4) */
+  int32_t nbits;        /* bits per sub-code: 8 (256 codewords) or 4 (16 codewords; the paper's 4-bit
+                           PQ, reading A4') */
   int32_t metric;       /* 0 = squared L2, 1 = inner product (distance reported as -<q, x>) */
   int32_t by_residual;  /* 1 = codes encode x - c_l, 0 = codes encode x */
   const float* centroids;      /* [nlist][d] row-major fp32 */
-  const float* codebooks;      /* [m][256][d/m] fp32 */
+  const float* codebooks;      /* [m][2^nbits][d/m] fp32 */
   const int64_t* list_offsets; /* [nlist+1]; list l = rows [offsets[l], offsets[l+1]); offsets[0] = 0,
                                   non-decreasing; N = offsets[nlist] (empty lists allowed) */
   const int64_t* ids;          /* [N] vector ids, >= 0, unique (-1 is the padding id) */
-  const uint8_t* codes;        /* [N][m]; byte j of row i = sub-code j of vector i */
+  const uint8_t* codes;        /* [N][ceil(m*nbits/8)]; nbits 8: byte j of row i = sub-code j of vector i;
+                                  nbits 4: sub-code j = low nibble of byte j/2 for even j, high nibble
+                                  for odd j */
   const int32_t* hot;          /* [n_hot] cluster ids resident on the GPUs; no duplicates.
                                   May be NULL iff n_hot == 0 (then every probe is a miss). */
   int32_t n_hot;

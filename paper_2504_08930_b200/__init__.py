@@ -151,6 +151,7 @@ class Index:
         attributes, when present, select the variant)."""
         kw.setdefault("metric", int(getattr(ix, "metric", 0)))
         kw.setdefault("by_residual", int(getattr(ix, "by_residual", 1)))
+        kw.setdefault("nbits", int(getattr(ix, "nbits", 8)))
         return cls.load(ix.centroids, ix.codebooks, ix.list_offsets, ix.ids, ix.codes, hot=hot, **kw)
 
     # ------------------------------------------------------------------ search

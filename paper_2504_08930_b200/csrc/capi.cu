@@ -94,7 +94,7 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   VLR_CUDA_TRY(dalloc(&w.item_off, nqs * cnp + 1));
   VLR_CUDA_TRY(dalloc(&w.item_local, nqs * cnp));
   VLR_CUDA_TRY(dalloc(&w.qtot, nqs));
-  VLR_CUDA_TRY(dalloc(&w.lut, nqs * ix.npairs * (kLutPairBytes / 4)));
+  VLR_CUDA_TRY(dalloc(&w.lut, nqs * ix.npairs * (ix.lut_pair_bytes / 4)));
   const size_t nslots = ((size_t)w.n_cta + nqs) * kScanWarps * ck;
   VLR_CUDA_TRY(dalloc(&w.pdist, nslots));
   VLR_CUDA_TRY(dalloc(&w.pid, nslots));
@@ -132,13 +132,16 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   if (cm.world < 1 || cm.rank < 0 || cm.rank >= cm.world) return fail(VLR_ERR_INVALID_ARG, "bad rank/world");
   if (D.d < 1 || D.nlist < 1 || D.m < 1) return fail(VLR_ERR_INVALID_ARG, "d, nlist, m must be >= 1");
   if (D.d % D.m != 0) return fail(VLR_ERR_DIM_MISMATCH, "d % m != 0");
-  if (D.nbits != 8) return fail(VLR_ERR_UNSUPPORTED, "nbits must be 8");
+  if (D.nbits != 8 && D.nbits != 4) return fail(VLR_ERR_UNSUPPORTED, "nbits must be 8 or 4");
   if (D.metric != 0 && D.metric != 1) return fail(VLR_ERR_UNSUPPORTED, "metric must be 0 (squared L2) or 1 (inner product)");
   if (D.by_residual != 0 && D.by_residual != 1) return fail(VLR_ERR_INVALID_ARG, "by_residual must be 0 or 1");
-  if (D.m > kMaxM) return fail(VLR_ERR_UNSUPPORTED, "m > 128");
+  if (D.nbits == 8 && D.m > kMaxM) return fail(VLR_ERR_UNSUPPORTED, "m > 128 (8-bit codes)");
+  if (D.nbits == 4 && D.m > kMaxM4) return fail(VLR_ERR_UNSUPPORTED, "m > 256 (4-bit codes)");
   if (!D.centroids || !D.codebooks || !D.list_offsets) return fail(VLR_ERR_INVALID_ARG, "null array");
   if (D.n_hot < 0 || (D.n_hot > 0 && !D.hot)) return fail(VLR_ERR_INVALID_ARG, "bad hot set");
   const int L = D.nlist, d = D.d, m = D.m, dsub = d / m;
+  const int ksub = 1 << D.nbits;
+  const int64_t cbytes = ((int64_t)m * D.nbits + 7) / 8;  // bytes of one input code row
   if (D.list_offsets[0] != 0) return fail(VLR_ERR_INVALID_ARG, "list_offsets[0] != 0");
   for (int l = 0; l < L; ++l)
     if (D.list_offsets[l + 1] < D.list_offsets[l]) return fail(VLR_ERR_INVALID_ARG, "list_offsets decreasing");
@@ -159,7 +162,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
     cn2[l] = D.metric == 1 ? 0.f : (float)s;  // IP: the filter holds -2<q,c>
     cmax2 = std::max(cmax2, s);
   }
-  const size_t ncb = (size_t)m * 256 * dsub;
+  const size_t ncb = (size_t)m * ksub * dsub;
   for (size_t i = 0; i < ncb; ++i)
     if (!std::isfinite(D.codebooks[i])) return fail(VLR_ERR_NONFINITE, "non-finite codebook");
   // hot set and owners (index splitter)
@@ -205,7 +208,16 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   ix.nlist = L;
   ix.m = m;
   ix.dsub = dsub;
-  ix.mpad = ((m + 31) / 32) * 32;
+  ix.nbits = D.nbits;
+  ix.ksub = ksub;
+  ix.lut_pair_bytes = ksub * 64 * 4;
+  if (D.nbits == 8) {
+    ix.mpad = ((m + 31) / 32) * 32;
+  } else {  // scan instantiations for 4-bit codes: 32, 64, 96, 128, 192, 256 sub-spaces
+    const int sizes[] = {32, 64, 96, 128, 192, 256};
+    for (int v : sizes)
+      if (m <= v) { ix.mpad = v; break; }
+  }
   ix.npairs = (ix.mpad + 63) / 64;
   ix.rank = cm.rank;
   ix.world = cm.world;
@@ -261,7 +273,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   LTRY(dalloc(&ix.owner, (size_t)L));
   LTRY(dalloc(&ix.local, (size_t)L));
   LTRY(dalloc(&ix.gbase, (size_t)ix.n_local + 1));
-  LTRY(dalloc(&ix.codes, (size_t)ix.n_groups * 32 * ix.mpad));
+  LTRY(dalloc(&ix.codes, (size_t)ix.n_groups * 32 * (ix.mpad * ix.nbits / 8)));
   LTRY(dalloc(&ix.bias, (size_t)ix.n_groups * 32));
   LTRY(dalloc(&ix.ids, (size_t)ix.n_groups * 32));
   LTRY(cudaMemcpyAsync(ix.centroids, D.centroids, sizeof(float) * L * d, cudaMemcpyHostToDevice, s));
@@ -285,7 +297,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   int32_t flag_h = 0;
   if (ix.n_vec > 0) {
     cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = dalloc(&scodes, (size_t)ix.n_vec * m);
+    if (e == cudaSuccess) e = dalloc(&scodes, (size_t)ix.n_vec * cbytes);
     if (e == cudaSuccess) e = dalloc(&sids, (size_t)ix.n_vec);
     if (e == cudaSuccess) e = dalloc(&svbase, vbase_h.size());
     if (e == cudaSuccess) e = dalloc(&slglob, lglob.size());
@@ -299,7 +311,8 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
       const int64_t a = D.list_offsets[l], b = D.list_offsets[r + 1];
       const int64_t dst = vbase_h[local[l]];
       if (b > a) {
-        e = cudaMemcpyAsync(scodes + dst * m, D.codes + a * m, (size_t)(b - a) * m, cudaMemcpyHostToDevice, s);
+        e = cudaMemcpyAsync(scodes + dst * cbytes, D.codes + a * cbytes, (size_t)(b - a) * cbytes,
+                            cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess)
           e = cudaMemcpyAsync(sids + dst, D.ids + a, (size_t)(b - a) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
       }
@@ -345,7 +358,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
     return bail(VLR_ERR_DUPLICATE_ID);
   }
   ix.bytes = (int64_t)L * d * 4 + (int64_t)L * ix.d8 * 2 + L * 4 + (int64_t)ncb * 4 + 2LL * L * 4 + (ix.n_local + 1) * 8 +
-             ix.n_groups * 32 * (ix.mpad + 4 + 8);
+             ix.n_groups * 32 * (ix.mpad * ix.nbits / 8 + 4 + 8);
   // NCCL communicator (collective)
   if (cm.world > 1 && cm.nccl_unique_id) {
     ncclUniqueId uid;

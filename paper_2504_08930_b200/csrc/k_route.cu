@@ -188,10 +188,32 @@ __global__ void __launch_bounds__(256) k_lut8(const float* __restrict__ Q, int n
   }
 }
 
+// 4-bit codes (16 codewords per sub-space): LUT_q[pair][c][jj], c < 16. One
+// CTA per (pair, query), thread (jj, c) = one fp32 dot of dsub terms; the 64
+// jj lanes of a code write 256 contiguous bytes.
+__global__ void __launch_bounds__(1024) k_lut16(const float* __restrict__ Q, int d, int m, int dsub,
+                                                const float* __restrict__ Y, int npairs, float scale,
+                                                float* __restrict__ lut) {
+  const int pair = blockIdx.x, q = blockIdx.y;
+  const int jj = threadIdx.x & 63, c = threadIdx.x >> 6;
+  const int j = pair * 64 + jj;
+  float t = 0.f;
+  if (j < m) {
+    const float* qv = Q + (size_t)q * d + (size_t)j * dsub;
+    const float* y = Y + ((size_t)j * 16 + c) * dsub;
+    for (int u = 0; u < dsub; ++u) t = fmaf(__ldg(qv + u), __ldg(y + u), t);
+  }
+  lut[(((size_t)q * npairs + pair) * 16 + c) * 64 + jj] = scale * t;
+}
+
 cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  dim3 grid(ix.npairs * 4, (nq + kLutQB - 1) / kLutQB);
   const float scale = ix.metric == 1 ? -1.f : -2.f;  // exact power-of-two scaling of the fp32 dot
+  if (ix.nbits == 4) {
+    k_lut16<<<dim3(ix.npairs, nq), 1024, 0, s>>>(Q, ix.d, ix.m, ix.dsub, ix.codebooks, ix.npairs, scale, ws.lut);
+    return cudaGetLastError();
+  }
+  dim3 grid(ix.npairs * 4, (nq + kLutQB - 1) / kLutQB);
   if (ix.dsub == 8 && (ix.d % 4) == 0) {
     k_lut8<<<grid, 256, 0, s>>>(Q, nq, ix.d, ix.m, ix.codebooks, ix.npairs, scale, ws.lut);
     return cudaGetLastError();

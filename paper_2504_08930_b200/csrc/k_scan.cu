@@ -22,6 +22,13 @@
 // gathers. One PRMT builds the byte address code*256 + (l^t)*4 (the code byte
 // goes to byte 1, the lane offset to byte 0); the slab/half offset is the LDS
 // immediate. Per lookup: PRMT + LDS + FADD (+1/R LOP3 for the lane offset).
+//
+// 4-bit codes (NEXT-3, the paper's IVF-FS code width): the same
+// kernel with NB = 4. A lane's 16-byte chunk holds 32 rotated NIBBLES (slot
+// s = 32r + t in nibble t of chunk r, low nibble first), the LUT is
+// [j/64][code 0..15][j%64] (4 KB per 64 sub-spaces), and each code word is
+// split once into its even and odd nibbles (w & 0x0F0F0F0F, (w >> 4) &
+// 0x0F0F0F0F) so the same one-PRMT address build applies.
 #include <cfloat>
 #include <cstdlib>
 
@@ -41,6 +48,7 @@ constexpr int kPfDist = VLR_PF_DIST;
 
 struct ScanArgs {
   int nq, np, k, npairs;
+  uint32_t lut_bytes;  // per query: npairs x ksub x 64 x 4
   const int32_t* plocal;
   const float* term1;
   const int64_t* item_off;
@@ -98,9 +106,11 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
   return v;
 }
 
-template <int MP>
+// MP padded sub-spaces of NB-bit codes: MP*NB/32 code words per lane, in
+// MP*NB/128 chunks of 16 bytes
+template <int MP, int NB>
 struct Grp {
-  uint32_t w[MP / 4];
+  uint32_t w[MP * NB / 32];
   float b, t1;
   long long gaddr;
 };
@@ -109,23 +119,24 @@ struct Grp {
 // (LSU prefetch, no data return; a 4 KB TMA bulk prefetch per group costs
 // ~0.3 us of TMA issue time, tools/tma_issue.cu): keeps DRAM requests in
 // flight beyond the register double buffer (K6).
-template <int MP>
+template <int MP, int NB>
 __device__ __forceinline__ void grp_prefetch(const ScanArgs& a, long long gg, long long& it, int lane) {
   while (a.item_off[it + 1] <= gg) ++it;
   const long long gaddr = a.gbase[a.plocal[it]] + (gg - a.item_off[it]);
-  if (lane < MP / 4)
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.codes + gaddr * 32 * MP + lane * 128) : "memory");
+  if (lane < MP * NB / 32)  // 128-byte lines of the group
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.codes + gaddr * (4 * MP * NB) + lane * 128) : "memory");
 }
 
-template <int MP, int EXP = 0>
-__device__ __forceinline__ void grp_load(Grp<MP>& G, const ScanArgs& a, long long gg, long long& it, int lane) {
+template <int MP, int NB, int EXP = 0>
+__device__ __forceinline__ void grp_load(Grp<MP, NB>& G, const ScanArgs& a, long long gg, long long& it, int lane) {
+  constexpr int kChunks = MP * NB / 128;
   while (a.item_off[it + 1] <= gg) ++it;
   const int loc = a.plocal[it];
   G.gaddr = a.gbase[loc] + (gg - a.item_off[it]);
   G.t1 = a.term1[it];
-  const uint4* src = reinterpret_cast<const uint4*>(a.codes) + G.gaddr * (2 * MP) + lane;
+  const uint4* src = reinterpret_cast<const uint4*>(a.codes) + G.gaddr * (32 * kChunks) + lane;
 #pragma unroll
-  for (int c = 0; c < MP / 16; ++c) {
+  for (int c = 0; c < kChunks; ++c) {
     uint4 v;
     if constexpr (EXP == 2) v = make_uint4(gg * 2654435761u + c, gg * 40503u + lane, c * 7919u, lane * 104729u);
     else v = ldg_stream(src + c * 32);
@@ -147,14 +158,25 @@ __device__ __forceinline__ float hi32(unsigned long long v) { return __uint_as_f
 
 // sum_j LUT[j][code_j] for this lane's vector, fixed order:
 // accumulator r collects sub-spaces 32r + (lane ^ t), t = 0..31 in order;
-// result ((acc0 + acc1) + (acc2 + acc3)).
-template <int MP>
-__device__ __forceinline__ float grp_adc(const Grp<MP>& G, const unsigned char* lutc, uint32_t lane4) {
+// accumulators are paired into FADD2s, result ((acc0 + acc1) + (acc2 + acc3))
+// (R = 4; a pairwise tree of the pair sums in general).
+template <int MP, int NB>
+__device__ __forceinline__ float grp_adc(const Grp<MP, NB>& G, const unsigned char* lutc, uint32_t lane4) {
   constexpr int R = MP / 32;
+  constexpr int kSlab = NB == 8 ? 65536 : 4096;  // LUT bytes per 64 sub-spaces
   auto look = [&](int t, int r, uint32_t off) -> float {
-    const int s = r * 32 + t;
-    const uint32_t addr = __byte_perm(G.w[s >> 2], off, 0x5504u | ((uint32_t)(s & 3) << 4));
-    return *reinterpret_cast<const float*>(lutc + addr + ((r >> 1) << 16) + ((r & 1) << 7));
+    uint32_t word, sel;
+    if constexpr (NB == 8) {
+      const int s = r * 32 + t;
+      word = G.w[s >> 2];
+      sel = (uint32_t)(s & 3);
+    } else {  // nibble t of chunk r: word r*4 + t/8, byte (t%8)/2, odd t = high nibble
+      const uint32_t w = G.w[r * 4 + (t >> 3)];
+      word = (t & 1) ? ((w >> 4) & 0x0F0F0F0Fu) : (w & 0x0F0F0F0Fu);
+      sel = (uint32_t)((t & 7) >> 1);
+    }
+    const uint32_t addr = __byte_perm(word, off, 0x5504u | (sel << 4));
+    return *reinterpret_cast<const float*>(lutc + addr + (r >> 1) * kSlab + ((r & 1) << 7));
   };
   if constexpr (R == 1) {
     float acc = 0.f;
@@ -162,18 +184,26 @@ __device__ __forceinline__ float grp_adc(const Grp<MP>& G, const unsigned char* 
     for (int t = 0; t < 32; ++t) acc += look(t, 0, lane4 ^ (uint32_t)(t << 2));
     return acc;
   } else {
-    unsigned long long a01 = 0ull, a23 = 0ull;
-    float a2 = 0.f;
+    constexpr int P = R / 2;
+    unsigned long long a2[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) a2[p] = 0ull;
+    float a1 = 0.f;
 #pragma unroll
     for (int t = 0; t < 32; ++t) {
       const uint32_t off = lane4 ^ (uint32_t)(t << 2);
-      fadd2(a01, look(t, 0, off), look(t, 1, off));
-      if constexpr (R == 3) a2 += look(t, 2, off);
-      if constexpr (R == 4) fadd2(a23, look(t, 2, off), look(t, 3, off));
+#pragma unroll
+      for (int p = 0; p < P; ++p) fadd2(a2[p], look(t, 2 * p, off), look(t, 2 * p + 1, off));
+      if constexpr (R & 1) a1 += look(t, R - 1, off);
     }
-    if constexpr (R == 2) return lo32(a01) + hi32(a01);
-    else if constexpr (R == 3) return (lo32(a01) + hi32(a01)) + a2;
-    else return (lo32(a01) + hi32(a01)) + (lo32(a23) + hi32(a23));
+    float ps[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) ps[p] = lo32(a2[p]) + hi32(a2[p]);
+#pragma unroll
+    for (int w = 1; w < P; w <<= 1)
+#pragma unroll
+      for (int p = 0; p + w < P; p += 2 * w) ps[p] = ps[p] + ps[p + w];
+    return (R & 1) ? ps[0] + a1 : ps[0];
   }
 }
 
@@ -195,17 +225,17 @@ __device__ __forceinline__ void list_offer(float& bd, long long& bid, float& thr
   offer32(bd, bid, thr, d, id, lane < k && d < CUDART_INF_F && d <= thr, k, lane);
 }
 
-template <int MP, int EXP>
-__device__ __forceinline__ void grp_finish(const Grp<MP>& G, const ScanArgs& a, const unsigned char* lutc,
+template <int MP, int NB, int EXP>
+__device__ __forceinline__ void grp_finish(const Grp<MP, NB>& G, const ScanArgs& a, const unsigned char* lutc,
                                            uint32_t lane4, int lane, float& bd, long long& bid, float& thr) {
   float s;
   if constexpr (EXP == 1) {  // timing experiment: no LUT gathers (ALU sum of code words)
     uint32_t x = 0;
 #pragma unroll
-    for (int i = 0; i < MP / 4; ++i) x ^= G.w[i];
+    for (int i = 0; i < MP * NB / 32; ++i) x ^= G.w[i];
     s = (float)(x & 0xffff) * 1e-9f;
   } else {
-    s = grp_adc<MP>(G, lutc, lane4);
+    s = grp_adc<MP, NB>(G, lutc, lane4);
   }
   const float dist = (G.t1 + G.b) + s;
   const bool cand = dist <= thr;
@@ -219,7 +249,7 @@ __device__ __forceinline__ void grp_finish(const Grp<MP>& G, const ScanArgs& a, 
   }
 }
 
-template <int MP, int EXP>
+template <int MP, int NB, int EXP>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
@@ -230,7 +260,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
   const long long W = a.item_off[nitems];
   const long long g0 = (long long)c * W / G, g1 = (long long)(c + 1) * W / G;
   if (g0 >= g1) return;
-  const uint32_t lut_bytes = (uint32_t)a.npairs * kLutPairBytes;
+  const uint32_t lut_bytes = a.lut_bytes;
   if (threadIdx.x == 0) {
     mbar_init(&mbar, 1);
     fence_mbar_init();
@@ -257,7 +287,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
       fence_proxy_async_smem();
       mbar_arrive_expect_tx(&mbar, lut_bytes);
       const unsigned char* src = reinterpret_cast<const unsigned char*>(a.lut) + (size_t)q * lut_bytes;
-      for (uint32_t off = 0; off < lut_bytes; off += 32768u) bulk_g2s(smem + off, src + off, 32768u, &mbar);
+      for (uint32_t off = 0; off < lut_bytes; off += 32768u)
+        bulk_g2s(smem + off, src + off, lut_bytes - off < 32768u ? lut_bytes - off : 32768u, &mbar);
     }
     mbar_wait(&mbar, phase);
     phase ^= 1u;
@@ -266,25 +297,25 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
     long long bid = -1;
     long long it = it0;
     long long gg = g + warp;
-    Grp<MP> A, B;
+    Grp<MP, NB> A, B;
     long long itp = it0;  // prefetch cursor: kPfDist groups (of this warp) ahead of the loads
     if (gg < seg_end) {
       for (int p = 1; p <= kPfDist; ++p)
-        if (gg + p * kScanWarps < seg_end) grp_prefetch<MP>(a, gg + p * kScanWarps, itp, lane);
-      grp_load<MP, EXP>(A, a, gg, it, lane);
+        if (gg + p * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gg + p * kScanWarps, itp, lane);
+      grp_load<MP, NB, EXP>(A, a, gg, it, lane);
     }
     while (gg < seg_end) {
       const long long gn = gg + kScanWarps;
       if constexpr (kPfDist > 0)
-        if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP>(a, gn + kPfDist * kScanWarps, itp, lane);
-      if (gn < seg_end) grp_load<MP, EXP>(B, a, gn, it, lane);
-      grp_finish<MP, EXP>(A, a, lutc, lane4, lane, bd, bid, thr);
+        if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gn + kPfDist * kScanWarps, itp, lane);
+      if (gn < seg_end) grp_load<MP, NB, EXP>(B, a, gn, it, lane);
+      grp_finish<MP, NB, EXP>(A, a, lutc, lane4, lane, bd, bid, thr);
       if (gn >= seg_end) break;
       const long long gm = gn + kScanWarps;
       if constexpr (kPfDist > 0)
-        if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP>(a, gm + kPfDist * kScanWarps, itp, lane);
-      if (gm < seg_end) grp_load<MP, EXP>(A, a, gm, it, lane);
-      grp_finish<MP, EXP>(B, a, lutc, lane4, lane, bd, bid, thr);
+        if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gm + kPfDist * kScanWarps, itp, lane);
+      if (gm < seg_end) grp_load<MP, NB, EXP>(A, a, gm, it, lane);
+      grp_finish<MP, NB, EXP>(B, a, lutc, lane4, lane, bd, bid, thr);
       gg = gm;
     }
     const long long slot = ((long long)(c + q) * kScanWarps + warp) * a.k;
@@ -309,16 +340,16 @@ int scan_ctas(const DeviceIndex& ix) {
   return sms;  // one persistent CTA per SM (128 KB LUT + 16 warps)
 }
 
-template <int MP, int EXP>
+template <int MP, int NB, int EXP>
 static cudaError_t launch_scan_e(const ScanArgs& a, int n_cta, cudaStream_t s) {
-  const size_t sm = (size_t)a.npairs * kLutPairBytes;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan<MP, EXP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kLutPairBytes));
+    cudaError_t e = cudaFuncSetAttribute(k_scan<MP, NB, EXP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(2 * kLutPairBytes));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_scan<MP, EXP><<<n_cta, kScanThreads, sm, s>>>(a);
+  k_scan<MP, NB, EXP><<<n_cta, kScanThreads, a.lut_bytes, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -333,25 +364,36 @@ static int scan_experiment() {
   return v;
 }
 
-template <int MP>
+template <int MP, int NB>
 static cudaError_t launch_scan_t(const ScanArgs& a, int n_cta, cudaStream_t s) {
-  if constexpr (MP == 128) {
+  if constexpr (MP == 128 && NB == 8) {
     const int x = scan_experiment();
-    if (x == 1) return launch_scan_e<MP, 1>(a, n_cta, s);
-    if (x == 2) return launch_scan_e<MP, 2>(a, n_cta, s);
+    if (x == 1) return launch_scan_e<MP, NB, 1>(a, n_cta, s);
+    if (x == 2) return launch_scan_e<MP, NB, 2>(a, n_cta, s);
   }
-  return launch_scan_e<MP, 0>(a, n_cta, s);
+  return launch_scan_e<MP, NB, 0>(a, n_cta, s);
 }
 
 cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  ScanArgs a{nq, np, k, ix.npairs, ws.plocal, ws.term1, ws.item_off, ix.gbase, ix.codes, ix.bias, ix.ids,
-             ws.lut, ws.pdist, ws.pid};
+  ScanArgs a{nq, np, k, ix.npairs, (uint32_t)(ix.npairs * ix.lut_pair_bytes), ws.plocal, ws.term1, ws.item_off,
+             ix.gbase, ix.codes, ix.bias, ix.ids, ws.lut, ws.pdist, ws.pid};
+  if (ix.nbits == 4) {
+    switch (ix.mpad) {
+      case 32: return launch_scan_t<32, 4>(a, ws.n_cta, s);
+      case 64: return launch_scan_t<64, 4>(a, ws.n_cta, s);
+      case 96: return launch_scan_t<96, 4>(a, ws.n_cta, s);
+      case 128: return launch_scan_t<128, 4>(a, ws.n_cta, s);
+      case 192: return launch_scan_t<192, 4>(a, ws.n_cta, s);
+      case 256: return launch_scan_t<256, 4>(a, ws.n_cta, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (ix.mpad) {
-    case 32: return launch_scan_t<32>(a, ws.n_cta, s);
-    case 64: return launch_scan_t<64>(a, ws.n_cta, s);
-    case 96: return launch_scan_t<96>(a, ws.n_cta, s);
-    case 128: return launch_scan_t<128>(a, ws.n_cta, s);
+    case 32: return launch_scan_t<32, 8>(a, ws.n_cta, s);
+    case 64: return launch_scan_t<64, 8>(a, ws.n_cta, s);
+    case 96: return launch_scan_t<96, 8>(a, ws.n_cta, s);
+    case 128: return launch_scan_t<128, 8>(a, ws.n_cta, s);
     default: return cudaErrorInvalidValue;
   }
 }

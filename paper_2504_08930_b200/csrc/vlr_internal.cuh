@@ -15,7 +15,8 @@ namespace vlr {
 // ---------------------------------------------------------------- constants
 constexpr int kWarp = 32;
 constexpr int kMaxK = 32;          // warp-register top-k (one entry per lane)
-constexpr int kMaxM = 128;         // padded sub-quantizer count of the scan kernel
+constexpr int kMaxM = 128;         // max sub-quantizers, 8-bit codes (padded count of the scan kernel)
+constexpr int kMaxM4 = 256;        // max sub-quantizers, 4-bit codes
 #ifndef VLR_SCAN_THREADS
 #define VLR_SCAN_THREADS 512
 #endif
@@ -24,7 +25,8 @@ constexpr int kScanWarps = kScanThreads / kWarp;
 constexpr int kCandCap = 8192;     // K2 candidate list capacity per query (overflow -> rescan)
 constexpr int kRefineChunk = 1024; // K3 candidates per exact-refine flush
 constexpr int kMaxNprobe = 2048;   // cap on nprobe' (K3 sort buffer; the paper's operating point)
-constexpr int kLutPairBytes = 256 * 64 * 4;  // one [256 codes][64 sub-spaces] fp32 slab
+constexpr int kLutPairBytes = 256 * 64 * 4;  // one [256 codes][64 sub-spaces] fp32 slab (8-bit codes)
+constexpr int kLutPairBytes4 = 16 * 64 * 4;  // one [16 codes][64 sub-spaces] fp32 slab (4-bit codes)
 
 // ---------------------------------------------------------------- errors
 struct Error {
@@ -45,6 +47,8 @@ void set_error(const std::string& msg);
 // ---------------------------------------------------------------- device data
 struct DeviceIndex {
   int d = 0, d8 = 0, nlist = 0, m = 0, mpad = 0, npairs = 0, dsub = 0;
+  int nbits = 8, ksub = 256;   // bits per sub-code (8, or 4: nibble-packed) and codewords per sub-space
+  int lut_pair_bytes = kLutPairBytes;  // LUT bytes per 64 sub-spaces (ksub * 64 * 4)
   int rank = 0, world = 1, device = 0;
   int metric = 0;              // 0 squared L2, 1 inner product (distance = -<q, x>)
   int by_residual = 1;         // 1: codes encode x - c_l
@@ -57,7 +61,7 @@ struct DeviceIndex {
   float c_inv = 1.f;           // 2^-c_exp
   alignas(64) unsigned char tmapA[128] = {};  // CUtensorMap of cf16 (box 64 x 128, SWIZZLE_128B)
   float cmax = 0.f;            // max ||c|| (host), for the filter band
-  float* codebooks = nullptr;  // [m][256][dsub]
+  float* codebooks = nullptr;  // [m][ksub][dsub]
   int32_t* owner = nullptr;    // [nlist] owner rank or -1 (mapping table)
   int32_t* local = nullptr;    // [nlist] local list index on this rank or -1
   std::vector<int32_t> owner_h;
@@ -65,7 +69,7 @@ struct DeviceIndex {
   int32_t n_local = 0;
   int64_t n_groups = 0, n_vec = 0;
   int64_t* gbase = nullptr;    // [n_local+1] first group of each local list
-  uint8_t* codes = nullptr;    // [n_groups][mpad/16][32 lanes][16 B], per-lane rotated
+  uint8_t* codes = nullptr;    // [n_groups][mpad*nbits/128 chunks][32 lanes][16 B], per-lane rotated
   float* bias = nullptr;       // [n_groups*32] b_i = ||yhat||^2 + 2<c_l, yhat> (+inf for padding)
   int64_t* ids = nullptr;      // [n_groups*32] (-1 for padding)
   int64_t bytes = 0;
@@ -91,7 +95,7 @@ struct Workspace {
   int64_t* item_off = nullptr; // [nq*np + 1] group prefix of owned work items
   int64_t* item_local = nullptr; // [nq*np] within-query group prefix
   int64_t* qtot = nullptr;     // [nq] groups owned per query
-  float* lut = nullptr;        // [nq][npairs][256][64]
+  float* lut = nullptr;        // [nq][npairs][ksub][64]
   float* pdist = nullptr;      // [(n_cta + nq) * warps * k] scan partials
   int64_t* pid = nullptr;
   void* send = nullptr;        // [nq][k] 16-byte entries (world > 1)

@@ -63,7 +63,7 @@ def test_load_validation_codes():
     # d % m != 0 (m = 3 for d = 4)
     Y3 = np.zeros((3, 256, 1), np.float32)
     assert status_of(lambda: load(C, Y3, offs, ids, np.zeros((5, 3), np.uint8), device=0)) == "DIM_MISMATCH"
-    assert status_of(lambda: load(C, Y, offs, ids, codes, nbits=4, device=0)) == "UNSUPPORTED"
+    assert status_of(lambda: load(C, Y, offs, ids, codes, nbits=6, device=0)) == "UNSUPPORTED"
     assert status_of(lambda: load(C, Y, offs, ids, codes, metric=2, device=0)) == "UNSUPPORTED"
     assert status_of(lambda: load(C, Y, offs, ids, codes, by_residual=2, device=0)) == "INVALID_ARG"
     Cn = C.copy(); Cn[1, 2] = np.nan

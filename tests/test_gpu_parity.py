@@ -407,3 +407,44 @@ def test_paper_operating_point_nprobe_2048_k25(metric):
         errs, g, o = run_parity(ix, Q, 2048, 25, hot=hh)
         assert not errs, errs
         assert g["probes"].shape == (40, 2048)
+
+
+# --------------------------------------------------------------- NEXT-3: 4-bit PQ
+def test_golden_tiny_pq4_on_gpu():
+    from conftest import golden_pq4_index
+    ix, g = golden_pq4_index()
+    Q = np.array(g["queries"], np.float32)
+    for case in g["cases"]:
+        h = vlr.Index.from_arrays(ix, hot=case["hot"])
+        r = gpu_search(h, Q, case["nprobe"], case["k"])
+        h.close()
+        assert r["probes"].tolist() == case["probes"]
+        assert r["miss"].tolist() == case["miss"]
+        assert r["ids"].tolist() == case["ids"]
+        exp = np.array([[fval(x) for x in row] for row in case["dist"]], np.float32)
+        assert np.array_equal(r["dist"], exp)
+
+
+@pytest.mark.parametrize("m,metric,by_residual", [(32, 0, 1), (64, 0, 1), (32, 1, 1), (32, 0, 0)])
+def test_c1_pq4_parity(c1_queries, m, metric, by_residual):
+    """4-bit codes (nibble-packed, 16 codewords; reading A4') on the C1 shape."""
+    c = datagen.CONFIGS["C1"]
+    ix = datagen.make_index(c["N"], c["d"], c["nlist"], m, nbits=4, metric=metric, by_residual=by_residual)
+    errs, g, o = run_parity(ix, c1_queries, c["nprobe"], c["k"])
+    assert not errs, errs
+    hot = np.arange(1, ix.nlist, 3)
+    for npb, k in ((1, 1), (64, 25), (1024, 10)):
+        errs, g, o = run_parity(ix, c1_queries[:24], npb, k, hot=hot)
+        assert not errs, (npb, k, errs)
+
+
+@pytest.mark.parametrize("d,m,L", [(32, 8, 50), (40, 20, 17), (64, 64, 40), (192, 96, 33), (128, 128, 64),
+                                   (144, 144, 30), (192, 192, 40), (256, 256, 70)])
+def test_pq4_m_variants(d, m, L):
+    """Every 4-bit scan instantiation (padded sub-spaces 32, 64, 96, 128, 192, 256)."""
+    ix = datagen.make_index(4000, d, L, m, seed=d + m, nbits=4)
+    Q = datagen.make_queries(4000, d, L, 20, seed=d + m, stream=2)
+    hot = np.arange(0, L, 2)
+    for npb, hh in ((8, None), (L, hot)):
+        errs, g, o = run_parity(ix, Q, npb, 10, hot=hh)
+        assert not errs, (d, m, L, errs)
