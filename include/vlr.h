@@ -30,7 +30,7 @@ extern "C" {
 #endif
 
 #define VLR_VERSION_MAJOR 1
-#define VLR_VERSION_MINOR 1
+#define VLR_VERSION_MINOR 2
 
 typedef struct vlr_index vlr_index; /* opaque; created by vlr_load_index, freed by vlr_index_free */
 
@@ -147,6 +147,43 @@ vlr_status vlr_search(vlr_index* idx, const float* d_queries, int32_t nq, int32_
  * h_probes may be NULL. */
 vlr_status vlr_search_host(vlr_index* idx, const float* h_queries, int32_t nq, int32_t nprobe, int32_t k,
                            int64_t* h_ids, float* h_dist, uint8_t* h_miss, int32_t* h_probes, void* stream);
+
+/*
+ * NEXT-4: early per-query release -- the GPU analog of the paper's dynamic
+ * dispatcher (P:408-414 [§IV.C]: "GPU ... completion flags", "per-query
+ * callback" so a finished query does not wait for its batch; Fig. 14).
+ * Same search and outputs as vlr_search_async, but the scan kernel itself
+ * merges each query's partial lists as soon as the last scan CTA touching the
+ * query finishes (no separate K7 launch) and then raises ready[q] = epoch.
+ *   ready [nq] uint32: flags, device-accessible -- device memory or pinned
+ *      host memory (cudaHostAlloc / cudaMallocHost, used through its UVA
+ *      pointer); the caller sets them != epoch before the call.
+ *   epoch: nonzero value that marks "row q final" for this call (use a new
+ *      value per search on the same flags).
+ *   d_ids / d_dist: as vlr_search_async, and may also be pinned host memory;
+ *      row q is final (and visible to the host) once ready[q] == epoch (the
+ *      row is written before the flag with system-scope release ordering).
+ *   d_miss / d_probes: device memory, valid at stream completion as usual.
+ * Rows with no resident probe are released at the scan's start. Bit-identical
+ * results to vlr_search_async (the merge is the same code).
+ * Errors: as vlr_search_async; UNSUPPORTED for world > 1 or shard-only handles
+ * (rows there are final only after the exchange); INVALID_ARG for epoch 0,
+ * NULL or non-device-accessible ready/ids/dist.
+ */
+vlr_status vlr_search_release_async(vlr_index* idx, const float* d_queries, int32_t nq, int32_t nprobe, int32_t k,
+                                    int64_t* d_ids, float* d_dist, uint8_t* d_miss, int32_t* d_probes,
+                                    uint32_t* ready, uint32_t epoch, void* stream);
+
+/* Host-side dispatcher poll for vlr_search_release_async (the
+ * thread-safe queue feeding per-query callbacks): spins until at least one
+ * query q < nq with seen[q] == 0 has ready[q] == epoch, or timeout_us passes.
+ * Each newly ready q is appended to out_q (at most max_out), seen[q] is set to
+ * 1, and out_t_ns (may be NULL) receives the CLOCK_MONOTONIC time in ns at
+ * which the flag was observed. Returns the number appended (0 on timeout), -1
+ * for bad arguments. An acquire fence follows the flag reads, so the rows of
+ * the returned queries can be read after the call. Host only; no CUDA calls. */
+int32_t vlr_poll_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, uint8_t* seen, int32_t* out_q,
+                       int64_t* out_t_ns, int32_t max_out, int64_t timeout_us);
 
 /* Pre-size the per-handle workspace for batches up to (max_nq, max_nprobe, max_k)
  * so that later searches allocate nothing (required before graph capture). */

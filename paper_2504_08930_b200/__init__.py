@@ -21,7 +21,8 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "NONFINITE", 4: "UNKN
           5: "DUPLICATE_ID", 6: "OOM", 7: "CUDA", 8: "NCCL", 9: "UNSUPPORTED"}
 
 # every symbol include/vlr.h declares (checked by tests/test_abi.py)
-EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_reserve",
+EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_search_release_async",
+           "vlr_poll_ready", "vlr_reserve",
            "vlr_merge_partials", "vlr_access_counts", "vlr_index_info", "vlr_index_owners", "vlr_set_profiling", "vlr_stage_times",
            "vlr_last_launch_count", "vlr_nccl_unique_id", "vlr_index_free", "vlr_last_error", "vlr_version"]
 
@@ -63,6 +64,7 @@ def lib():
             "vlr_search_async": [P, P, I32, I32, I32, P, P, P, P, P],
             "vlr_search": [P, P, I32, I32, I32, P, P, P, P, P],
             "vlr_search_host": [P, P, I32, I32, I32, P, P, P, P, P],
+            "vlr_search_release_async": [P, P, I32, I32, I32, P, P, P, P, P, ctypes.c_uint32, P],
             "vlr_reserve": [P, I32, I32, I32],
             "vlr_merge_partials": [P, P, I32, I32, I32, P, P, P],
             "vlr_index_info": [P, P, P, P],
@@ -76,6 +78,8 @@ def lib():
             f = getattr(L, name)
             f.argtypes = args
             f.restype = ctypes.c_int
+        L.vlr_poll_ready.argtypes = [P, I32, ctypes.c_uint32, P, P, P, I32, I64]
+        L.vlr_poll_ready.restype = I32
         L.vlr_last_launch_count.argtypes = [P]
         L.vlr_last_launch_count.restype = I32
         L.vlr_index_free.argtypes = [P]
@@ -173,6 +177,56 @@ class Index:
                   prb.data_ptr() if prb is not None else None, _stream_handle(stream)))
         return out
 
+    def search_release(self, Q, nprobe: int, k: int, stream=None, on_ready=None, timeout_s: float = 30.0,
+                       out=None):
+        """NEXT-4 early per-query release (vlr_search_release_async +
+        vlr_poll_ready): rows are written to pinned host memory and released
+        one query at a time while the batch is still being scanned.
+        on_ready(qs: np.ndarray) is called for each group of newly released
+        queries (their rows of the returned ids/dist are final by then).
+        Returns (ids, dist, miss, probes, t_ready_ns) with ids/dist pinned CPU
+        tensors, miss/probes CUDA tensors, and t_ready_ns[q] the host
+        CLOCK_MONOTONIC time (ns) at which query q was seen released; t0
+        (time.monotonic_ns() just before the launch) is t_ready_ns.t0."""
+        import time
+        import torch
+        assert Q.is_cuda and Q.dtype == torch.float32 and Q.is_contiguous()
+        nq = int(Q.shape[0])
+        npr = min(nprobe, self.nlist)
+        if out is None:
+            out = (torch.empty(nq, k, dtype=torch.int64, pin_memory=True),
+                   torch.empty(nq, k, dtype=torch.float32, pin_memory=True),
+                   torch.empty(nq, npr, dtype=torch.uint8, device=Q.device),
+                   torch.empty(nq, npr, dtype=torch.int32, device=Q.device),
+                   torch.zeros(nq, dtype=torch.int32, pin_memory=True))
+        ids, dist, miss, prb, ready = out
+        self._epoch = (getattr(self, "_epoch", 0) % 0x7FFFFFFF) + 1
+        seen = np.zeros(nq, np.uint8)
+        qs = np.empty(nq, np.int32)
+        ts = np.empty(nq, np.int64)
+        t_ready = np.zeros(nq, np.int64)
+        t0 = time.monotonic_ns()
+        _check(lib().vlr_search_release_async(self._h, Q.data_ptr(), nq, nprobe, k, ids.data_ptr(), dist.data_ptr(),
+                                              miss.data_ptr(), prb.data_ptr(), ready.data_ptr(), self._epoch,
+                                              _stream_handle(stream)))
+        got = 0
+        deadline = t0 + int(timeout_s * 1e9)
+        while got < nq:
+            n = lib().vlr_poll_ready(ready.data_ptr(), nq, self._epoch, seen.ctypes.data, qs.ctypes.data,
+                                     ts.ctypes.data, nq, 100_000)
+            if n < 0:
+                raise VlrError(1, "vlr_poll_ready: bad arguments")
+            if n:
+                t_ready[qs[:n]] = ts[:n]
+                got += n
+                if on_ready is not None:
+                    on_ready(qs[:n].copy())
+            elif time.monotonic_ns() > deadline:
+                raise VlrError(7, f"search_release: {nq - got} queries not released within {timeout_s} s")
+        t_ready = _Stamps(t_ready)
+        t_ready.t0 = t0
+        return ids, dist, miss, prb, t_ready
+
     def search_host(self, Q: np.ndarray, nprobe: int, k: int, out=None, stream=None):
         """vlr_search_host: host buffers in and out (copies inside the call)."""
         Q = np.ascontiguousarray(Q, dtype=np.float32)
@@ -244,6 +298,16 @@ class Index:
             self.close()
         except Exception:
             pass
+
+
+class _Stamps(np.ndarray):
+    """int64 ndarray of release times with the launch time as .t0"""
+
+    def __new__(cls, a):
+        return np.asarray(a).view(cls)
+
+    def __array_finalize__(self, obj):
+        self.t0 = getattr(obj, "t0", 0)
 
 
 def merge_partials(part_ids, part_dist, stream=None):

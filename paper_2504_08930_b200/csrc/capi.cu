@@ -3,6 +3,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <ctime>
 #include <limits>
 #include <cmath>
 #include <cstdio>
@@ -48,7 +51,7 @@ __global__ void k_negative(const int64_t* ids, long long n, int32_t* flag) {
 }
 
 static void free_ws(Workspace& w) {
-  void* ps[] = {w.qnorm, w.qsq, w.qf16, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.lut,
+  void* ps[] = {w.qnorm, w.qsq, w.qf16, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.qdone, w.lut,
                 w.pdist, w.pid, w.send, w.recv, w.d_q, w.d_ids, w.d_dist, w.d_miss, w.d_probes, w.status};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -94,6 +97,7 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   VLR_CUDA_TRY(dalloc(&w.item_off, nqs * cnp + 1));
   VLR_CUDA_TRY(dalloc(&w.item_local, nqs * cnp));
   VLR_CUDA_TRY(dalloc(&w.qtot, nqs));
+  VLR_CUDA_TRY(dalloc(&w.qdone, nqs));
   VLR_CUDA_TRY(dalloc(&w.lut, nqs * ix.npairs * (ix.lut_pair_bytes / 4)));
   const size_t nslots = ((size_t)w.n_cta + nqs) * kScanWarps * ck;
   VLR_CUDA_TRY(dalloc(&w.pdist, nslots));
@@ -403,8 +407,9 @@ static inline void rec(vlr_index* h, int i, cudaStream_t s) {
     cudaEventRecord(h->ev[h->nsearch % vlr_index::kRing][i], s);
 }
 
-vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
-                            float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream) {
+static vlr_status search_impl(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
+                              float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream,
+                              const Release* rel) {
   if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
   if (h->dead) return fail(VLR_ERR_NCCL, "index unusable after an NCCL failure");
   if (nq < 0 || nprobe < 1 || k < 1) return fail(VLR_ERR_INVALID_ARG, "nq < 0, nprobe < 1 or k < 1");
@@ -439,10 +444,13 @@ vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t np
   rec(h, 4, s);
   VLR_CUDA_TRY(launch_lut(Q, ix, w, nq, s)); ++n;
   rec(h, 5, s);
-  VLR_CUDA_TRY(launch_scan(ix, w, nq, np, k, s)); ++n;
+  if (rel) VLR_CUDA_TRY(cudaMemsetAsync(w.qdone, 0, sizeof(unsigned long long) * nq, s));
+  VLR_CUDA_TRY(launch_scan(ix, w, nq, np, k, s, rel)); ++n;
   rec(h, 6, s);
   const bool exchange = ix.world > 1 && !ix.shard_only;
-  VLR_CUDA_TRY(launch_rank_merge(ix, w, nq, np, k, out_ids, out_dist, exchange ? w.send : nullptr, s)); ++n;
+  if (!rel) {  // release mode: the scan merged and released every row itself
+    VLR_CUDA_TRY(launch_rank_merge(ix, w, nq, np, k, out_ids, out_dist, exchange ? w.send : nullptr, s)); ++n;
+  }
   rec(h, 7, s);
   if (exchange) {
     ncclResult_t r = ncclAllGather(w.send, w.recv, (size_t)nq * k * sizeof(Packed), ncclUint8,
@@ -460,6 +468,67 @@ vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t np
   h->launches = n;
   if (h->profiling) h->prof_mode[h->nsearch++ % vlr_index::kRing] = h->profiling;
   return VLR_OK;
+}
+
+vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
+                            float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream) {
+  return search_impl(h, Q, nq, nprobe, k, out_ids, out_dist, out_miss, out_probes, stream, nullptr);
+}
+
+// device-accessible = device memory of this device, managed, or pinned host memory
+// (mapped into the device's address space under UVA)
+static bool device_accessible(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged ||
+         (at.type == cudaMemoryTypeHost && at.devicePointer == p);
+}
+
+vlr_status vlr_search_release_async(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k,
+                                    int64_t* out_ids, float* out_dist, uint8_t* out_miss, int32_t* out_probes,
+                                    uint32_t* ready, uint32_t epoch, void* stream) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  if (h->ix.world > 1 || h->ix.shard_only)
+    return fail(VLR_ERR_UNSUPPORTED, "early release needs world == 1 (rows are final only after the exchange)");
+  if (nq > 0) {
+    if (!ready || epoch == 0) return fail(VLR_ERR_INVALID_ARG, "release: null ready flags or epoch 0");
+    VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
+    if (!device_accessible(ready) || !out_ids || !out_dist || !device_accessible(out_ids) ||
+        !device_accessible(out_dist))
+      return fail(VLR_ERR_INVALID_ARG, "release: ready/ids/dist must be device or pinned (mapped) host memory");
+  }
+  const Release rel{ready, epoch, out_ids, out_dist};
+  return search_impl(h, Q, nq, nprobe, k, out_ids, out_dist, out_miss, out_probes, stream, &rel);
+}
+
+int32_t vlr_poll_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, uint8_t* seen, int32_t* out_q,
+                       int64_t* out_t_ns, int32_t max_out, int64_t timeout_us) {
+  if (!ready || !seen || !out_q || nq < 0 || max_out < 1) return -1;
+  const volatile uint32_t* r = ready;
+  const auto t0 = std::chrono::steady_clock::now();
+  int32_t n = 0;
+  for (;;) {
+    for (int32_t q = 0; q < nq && n < max_out; ++q) {
+      if (seen[q] || r[q] != epoch) continue;
+      seen[q] = 1;
+      out_q[n] = q;
+      if (out_t_ns) {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        out_t_ns[n] = (int64_t)ts.tv_sec * 1000000000LL + ts.tv_nsec;
+      }
+      ++n;
+    }
+    if (n > 0) break;
+    if (std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count() >=
+        timeout_us)
+      break;
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);  // rows of the released queries after their flags
+  return n;
 }
 
 vlr_status vlr_search(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,

@@ -59,6 +59,12 @@ struct ScanArgs {
   const float* lut;
   float* pdist;
   int64_t* pid;
+  // NEXT-4 early per-query release (k_scan<..., REL = true> only)
+  unsigned long long* qdone;  // [nq] groups scanned so far per query (zeroed before the launch)
+  uint32_t* ready;            // [nq] device-accessible (normally pinned host) release flags
+  uint32_t epoch;             // value written to ready[q] when row q is final
+  int64_t* out_ids;           // [nq][k] final rows (device or pinned host)
+  float* out_dist;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -225,179 +231,6 @@ __device__ __forceinline__ void list_offer(float& bd, long long& bid, float& thr
   offer32(bd, bid, thr, d, id, lane < k && d < CUDART_INF_F && d <= thr, k, lane);
 }
 
-template <int MP, int NB, int EXP>
-__device__ __forceinline__ void grp_finish(const Grp<MP, NB>& G, const ScanArgs& a, const unsigned char* lutc,
-                                           uint32_t lane4, int lane, float& bd, long long& bid, float& thr) {
-  float s;
-  if constexpr (EXP == 1) {  // timing experiment: no LUT gathers (ALU sum of code words)
-    uint32_t x = 0;
-#pragma unroll
-    for (int i = 0; i < MP * NB / 32; ++i) x ^= G.w[i];
-    s = (float)(x & 0xffff) * 1e-9f;
-  } else {
-    s = grp_adc<MP, NB>(G, lutc, lane4);
-  }
-  const float dist = (G.t1 + G.b) + s;
-  const bool cand = dist <= thr;
-  long long my_id = 0;
-  if (cand) my_id = __ldg(reinterpret_cast<const long long*>(a.ids) + G.gaddr * 32 + lane);
-  const unsigned cm = __ballot_sync(kFull, cand);
-  if (cm) {
-    if (__popc(cm) > 6) wtk_merge32(bd, bid, cand ? dist : CUDART_INF_F, cand ? my_id : -1, a.k, lane);
-    else wtk_offer(bd, bid, dist, cand, a.k, lane, my_id);
-    thr = __shfl_sync(kFull, bd, a.k - 1);
-  }
-}
-
-template <int MP, int NB, int EXP>
-__global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
-  extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ __align__(8) uint64_t mbar;
-  __shared__ long long s_it;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = gridDim.x, c = blockIdx.x;
-  const int nitems = a.nq * a.np;
-  const long long W = a.item_off[nitems];
-  const long long g0 = (long long)c * W / G, g1 = (long long)(c + 1) * W / G;
-  if (g0 >= g1) return;
-  const uint32_t lut_bytes = a.lut_bytes;
-  if (threadIdx.x == 0) {
-    mbar_init(&mbar, 1);
-    fence_mbar_init();
-    // item containing group g0: last i with item_off[i] <= g0
-    int lo = 0, hi = nitems;  // item_off[lo] <= g0 < item_off[hi]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (a.item_off[mid] <= g0) lo = mid; else hi = mid;
-    }
-    s_it = lo;
-  }
-  __syncthreads();
-  long long it0 = s_it;
-  while (a.item_off[it0 + 1] <= g0) ++it0;
-  const uint32_t lane4 = (uint32_t)lane << 2;
-  const unsigned char* lutc = smem;
-  uint32_t phase = 0;
-  long long g = g0;
-  while (g < g1) {
-    const int q = (int)(it0 / a.np);
-    const long long qend = a.item_off[(long long)(q + 1) * a.np];
-    const long long seg_end = qend < g1 ? qend : g1;
-    if (threadIdx.x == 0) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&mbar, lut_bytes);
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(a.lut) + (size_t)q * lut_bytes;
-      for (uint32_t off = 0; off < lut_bytes; off += 32768u)
-        bulk_g2s(smem + off, src + off, lut_bytes - off < 32768u ? lut_bytes - off : 32768u, &mbar);
-    }
-    mbar_wait(&mbar, phase);
-    phase ^= 1u;
-
-    float bd = CUDART_INF_F, thr = CUDART_INF_F;
-    long long bid = -1;
-    long long it = it0;
-    long long gg = g + warp;
-    Grp<MP, NB> A, B;
-    long long itp = it0;  // prefetch cursor: kPfDist groups (of this warp) ahead of the loads
-    if (gg < seg_end) {
-      for (int p = 1; p <= kPfDist; ++p)
-        if (gg + p * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gg + p * kScanWarps, itp, lane);
-      grp_load<MP, NB, EXP>(A, a, gg, it, lane);
-    }
-    while (gg < seg_end) {
-      const long long gn = gg + kScanWarps;
-      if constexpr (kPfDist > 0)
-        if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gn + kPfDist * kScanWarps, itp, lane);
-      if (gn < seg_end) grp_load<MP, NB, EXP>(B, a, gn, it, lane);
-      grp_finish<MP, NB, EXP>(A, a, lutc, lane4, lane, bd, bid, thr);
-      if (gn >= seg_end) break;
-      const long long gm = gn + kScanWarps;
-      if constexpr (kPfDist > 0)
-        if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gm + kPfDist * kScanWarps, itp, lane);
-      if (gm < seg_end) grp_load<MP, NB, EXP>(A, a, gm, it, lane);
-      grp_finish<MP, NB, EXP>(B, a, lutc, lane4, lane, bd, bid, thr);
-      gg = gm;
-    }
-    const long long slot = ((long long)(c + q) * kScanWarps + warp) * a.k;
-    if (lane < a.k) {
-      a.pdist[slot + lane] = bd;
-      a.pid[slot + lane] = bid;
-    }
-    __syncthreads();  // every warp is done with this LUT
-    g = seg_end;
-    if (g < g1) {
-      it0 = (long long)(q + 1) * a.np;
-      while (a.item_off[it0 + 1] <= g) ++it0;
-    }
-  }
-}
-
-int scan_ctas(const DeviceIndex& ix) {
-  (void)ix;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;  // one persistent CTA per SM (128 KB LUT + 16 warps)
-}
-
-template <int MP, int NB, int EXP>
-static cudaError_t launch_scan_e(const ScanArgs& a, int n_cta, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan<MP, NB, EXP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(2 * kLutPairBytes));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  k_scan<MP, NB, EXP><<<n_cta, kScanThreads, a.lut_bytes, s>>>(a);
-  return cudaGetLastError();
-}
-
-// VLR_SCAN_EXPERIMENT=1|2 (timing experiments only; results are wrong):
-// 1 = no LUT gathers, 2 = no code loads.
-static int scan_experiment() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("VLR_SCAN_EXPERIMENT");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
-template <int MP, int NB>
-static cudaError_t launch_scan_t(const ScanArgs& a, int n_cta, cudaStream_t s) {
-  if constexpr (MP == 128 && NB == 8) {
-    const int x = scan_experiment();
-    if (x == 1) return launch_scan_e<MP, NB, 1>(a, n_cta, s);
-    if (x == 2) return launch_scan_e<MP, NB, 2>(a, n_cta, s);
-  }
-  return launch_scan_e<MP, NB, 0>(a, n_cta, s);
-}
-
-cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s) {
-  if (nq <= 0) return cudaSuccess;
-  ScanArgs a{nq, np, k, ix.npairs, (uint32_t)(ix.npairs * ix.lut_pair_bytes), ws.plocal, ws.term1, ws.item_off,
-             ix.gbase, ix.codes, ix.bias, ix.ids, ws.lut, ws.pdist, ws.pid};
-  if (ix.nbits == 4) {
-    switch (ix.mpad) {
-      case 32: return launch_scan_t<32, 4>(a, ws.n_cta, s);
-      case 64: return launch_scan_t<64, 4>(a, ws.n_cta, s);
-      case 96: return launch_scan_t<96, 4>(a, ws.n_cta, s);
-      case 128: return launch_scan_t<128, 4>(a, ws.n_cta, s);
-      case 192: return launch_scan_t<192, 4>(a, ws.n_cta, s);
-      case 256: return launch_scan_t<256, 4>(a, ws.n_cta, s);
-      default: return cudaErrorInvalidValue;
-    }
-  }
-  switch (ix.mpad) {
-    case 32: return launch_scan_t<32, 8>(a, ws.n_cta, s);
-    case 64: return launch_scan_t<64, 8>(a, ws.n_cta, s);
-    case 96: return launch_scan_t<96, 8>(a, ws.n_cta, s);
-    case 128: return launch_scan_t<128, 8>(a, ws.n_cta, s);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
 // ---------------------------------------------------------------- K7 per-rank merge
 // Top-k by (dist, id) of the union of the partial lists the scan wrote for a
 // query: every scan CTA whose range intersects the query's groups holds
@@ -417,6 +250,7 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
 // of 23,680 entries; batch 256 (~32 lists per query) needs one warp.
 constexpr int kMergeMaxWarps = 16;
 constexpr int kMergeMaxLists = 4096;  // >= (scan CTAs) x kScanWarps (checked at launch)
+static_assert(kScanWarps <= kMergeMaxWarps, "the in-scan release merge runs on the scan CTA's warps");
 
 // pairwise tree over the CTA's warp lists; warp 0 ends with the CTA list.
 // Level `stride` reads slots = stride (mod 2 stride) and writes slots = 0
@@ -437,19 +271,39 @@ __device__ __forceinline__ void cta_tree(float& bd, long long& bid, float& thr, 
   }
 }
 
-__global__ void __launch_bounds__(kMergeMaxWarps * 32) k_rank_merge(
-    int nq, int np, int k, int n_cta, const int64_t* __restrict__ item_off, const float* __restrict__ pdist,
-    const int64_t* __restrict__ pid, int64_t* __restrict__ out_ids, float* __restrict__ out_dist,
-    Packed* __restrict__ packed) {
-  __shared__ float s_d[kMergeMaxWarps * 32];
-  __shared__ long long s_id[kMergeMaxWarps * 32];
-  __shared__ float s_t0;
-  __shared__ int s_nrel;
-  __shared__ int s_rel[kMergeMaxLists];        // relevant list indices
-  __shared__ float s_ld[32 * 33];              // staged lists (phase C)
-  __shared__ long long s_lid[32 * 33];
+struct MergeSmem {
+  long long s_id[kMergeMaxWarps * 32];
+  long long s_lid[32 * 33];                    // staged lists (phase C)
+  float s_d[kMergeMaxWarps * 32];
+  float s_ld[32 * 33];
+  int s_rel[kMergeMaxLists];                   // relevant list indices
+  float s_t0;
+  int s_nrel;
+};
+
+// partial-list loads: the standalone K7 reads partials of a finished kernel
+// (read-only path); the scan's in-kernel release merge (NEXT-4) reads partials
+// other CTAs of the same launch wrote, so it goes through L2 (ld.global.cg)
+template <bool CG, typename T>
+__device__ __forceinline__ T ldp(const T* p) {
+  if constexpr (CG) return __ldcg(p);
+  else return __ldg(p);
+}
+
+// merge of query q by the whole CTA (nw = blockDim.x / 32 warps); warp 0
+// writes the row. Warps other than 0 return after phase B (no barrier after).
+template <bool CG>
+__device__ __forceinline__ void merge_query(
+    int q, int nq, int np, int k, int n_cta, const int64_t* __restrict__ item_off, const float* pdist,
+    const int64_t* pid, int64_t* out_ids, float* out_dist, Packed* __restrict__ packed, MergeSmem& sm) {
+  float* s_d = sm.s_d;
+  long long* s_id = sm.s_id;
+  float& s_t0 = sm.s_t0;
+  int& s_nrel = sm.s_nrel;
+  int* s_rel = sm.s_rel;
+  float* s_ld = sm.s_ld;
+  long long* s_lid = sm.s_lid;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int q = blockIdx.x;
   const long long W = item_off[(long long)nq * np];
   const long long S = item_off[(long long)q * np], E = item_off[(long long)(q + 1) * np];
   const long long* pidl = reinterpret_cast<const long long*>(pid);
@@ -481,8 +335,8 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32) k_rank_merge(
       d[u] = CUDART_INF_F;
       id[u] = -1;
       if (li < nl && head_ok(li)) {
-        d[u] = __ldg(pdist + base + (long long)li * k);
-        id[u] = __ldg(pidl + base + (long long)li * k);
+        d[u] = ldp<CG>(pdist + base + (long long)li * k);
+        id[u] = ldp<CG>(pidl + base + (long long)li * k);
       }
     }
 #pragma unroll
@@ -501,7 +355,7 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32) k_rank_merge(
   for (int l0 = warp * 32; l0 < nl; l0 += nw * 32) {
     const int li = l0 + lane;
     float h = CUDART_INF_F;
-    if (li < nl && head_ok(li)) h = __ldg(pdist + base + (long long)li * k);
+    if (li < nl && head_ok(li)) h = ldp<CG>(pdist + base + (long long)li * k);
     const bool rel = h < CUDART_INF_F && h <= t0;
     const unsigned rm = __ballot_sync(kFull, rel);
     if (rm) {
@@ -528,8 +382,8 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32) k_rank_merge(
         const int r = r1 + v;
         if (r < nb && lane < k) {
           const long long o = base + (long long)s_rel[r0 + r] * k + lane;
-          sd[v] = __ldg(pdist + o);
-          sid[v] = __ldg(pidl + o);
+          sd[v] = ldp<CG>(pdist + o);
+          sid[v] = ldp<CG>(pidl + o);
         }
       }
 #pragma unroll
@@ -593,6 +447,249 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32) k_rank_merge(
       out_ids[(size_t)q * k + lane] = bid;
       out_dist[(size_t)q * k + lane] = bd;
     }
+  }
+}
+
+
+__global__ void __launch_bounds__(kMergeMaxWarps * 32) k_rank_merge(
+    int nq, int np, int k, int n_cta, const int64_t* __restrict__ item_off, const float* __restrict__ pdist,
+    const int64_t* __restrict__ pid, int64_t* __restrict__ out_ids, float* __restrict__ out_dist,
+    Packed* __restrict__ packed) {
+  __shared__ MergeSmem sm;
+  merge_query<false>(blockIdx.x, nq, np, k, n_cta, item_off, pdist, pid, out_ids, out_dist, packed, sm);
+}
+
+template <int MP, int NB, int EXP>
+__device__ __forceinline__ void grp_finish(const Grp<MP, NB>& G, const ScanArgs& a, const unsigned char* lutc,
+                                           uint32_t lane4, int lane, float& bd, long long& bid, float& thr) {
+  float s;
+  if constexpr (EXP == 1) {  // timing experiment: no LUT gathers (ALU sum of code words)
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < MP * NB / 32; ++i) x ^= G.w[i];
+    s = (float)(x & 0xffff) * 1e-9f;
+  } else {
+    s = grp_adc<MP, NB>(G, lutc, lane4);
+  }
+  const float dist = (G.t1 + G.b) + s;
+  const bool cand = dist <= thr;
+  long long my_id = 0;
+  if (cand) my_id = __ldg(reinterpret_cast<const long long*>(a.ids) + G.gaddr * 32 + lane);
+  const unsigned cm = __ballot_sync(kFull, cand);
+  if (cm) {
+    if (__popc(cm) > 6) wtk_merge32(bd, bid, cand ? dist : CUDART_INF_F, cand ? my_id : -1, a.k, lane);
+    else wtk_offer(bd, bid, dist, cand, a.k, lane, my_id);
+    thr = __shfl_sync(kFull, bd, a.k - 1);
+  }
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// NEXT-4 release of row q (warp 0 of the CTA): the row's stores are made
+// visible at system scope before the flag (completion flags)
+__device__ __forceinline__ void release_row(const ScanArgs& a, int q, int lane) {
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0) st_release_sys(a.ready + q, a.epoch);
+}
+
+// REL (NEXT-4, the GPU analog of the paper's dynamic dispatcher):
+// after each query segment a CTA adds its group count to qdone[q]; the CTA
+// that completes q (count reaches q's owned groups) merges q's partial lists
+// itself (the K7 code, through L2) and raises ready[q], so a finished query is
+// released while the rest of the batch is still being scanned. Queries that
+// own no groups are released at kernel start (CTA q mod G).
+template <int MP, int NB, int EXP, bool REL = false>
+__global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ long long s_it;
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int nitems = a.nq * a.np;
+  const long long W = a.item_off[nitems];
+  const long long g0 = (long long)c * W / G, g1 = (long long)(c + 1) * W / G;
+  if constexpr (REL) {
+    if (warp == 0) {
+      for (int q = c; q < a.nq; q += G) {
+        if (a.item_off[(long long)(q + 1) * a.np] != a.item_off[(long long)q * a.np]) continue;
+        if (lane < a.k) {
+          a.out_ids[(size_t)q * a.k + lane] = -1;
+          a.out_dist[(size_t)q * a.k + lane] = CUDART_INF_F;
+        }
+        release_row(a, q, lane);
+      }
+    }
+  }
+  if (g0 >= g1) return;
+  const uint32_t lut_bytes = a.lut_bytes;
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    fence_mbar_init();
+    // item containing group g0: last i with item_off[i] <= g0
+    int lo = 0, hi = nitems;  // item_off[lo] <= g0 < item_off[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (a.item_off[mid] <= g0) lo = mid; else hi = mid;
+    }
+    s_it = lo;
+  }
+  __syncthreads();
+  long long it0 = s_it;
+  while (a.item_off[it0 + 1] <= g0) ++it0;
+  const uint32_t lane4 = (uint32_t)lane << 2;
+  const unsigned char* lutc = smem;
+  uint32_t phase = 0;
+  long long g = g0;
+  while (g < g1) {
+    const int q = (int)(it0 / a.np);
+    const long long qend = a.item_off[(long long)(q + 1) * a.np];
+    const long long seg_end = qend < g1 ? qend : g1;
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&mbar, lut_bytes);
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(a.lut) + (size_t)q * lut_bytes;
+      for (uint32_t off = 0; off < lut_bytes; off += 32768u)
+        bulk_g2s(smem + off, src + off, lut_bytes - off < 32768u ? lut_bytes - off : 32768u, &mbar);
+    }
+    mbar_wait(&mbar, phase);
+    phase ^= 1u;
+
+    float bd = CUDART_INF_F, thr = CUDART_INF_F;
+    long long bid = -1;
+    long long it = it0;
+    long long gg = g + warp;
+    Grp<MP, NB> A, B;
+    long long itp = it0;  // prefetch cursor: kPfDist groups (of this warp) ahead of the loads
+    if (gg < seg_end) {
+      for (int p = 1; p <= kPfDist; ++p)
+        if (gg + p * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gg + p * kScanWarps, itp, lane);
+      grp_load<MP, NB, EXP>(A, a, gg, it, lane);
+    }
+    while (gg < seg_end) {
+      const long long gn = gg + kScanWarps;
+      if constexpr (kPfDist > 0)
+        if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gn + kPfDist * kScanWarps, itp, lane);
+      if (gn < seg_end) grp_load<MP, NB, EXP>(B, a, gn, it, lane);
+      grp_finish<MP, NB, EXP>(A, a, lutc, lane4, lane, bd, bid, thr);
+      if (gn >= seg_end) break;
+      const long long gm = gn + kScanWarps;
+      if constexpr (kPfDist > 0)
+        if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gm + kPfDist * kScanWarps, itp, lane);
+      if (gm < seg_end) grp_load<MP, NB, EXP>(A, a, gm, it, lane);
+      grp_finish<MP, NB, EXP>(B, a, lutc, lane4, lane, bd, bid, thr);
+      gg = gm;
+    }
+    const long long slot = ((long long)(c + q) * kScanWarps + warp) * a.k;
+    if (lane < a.k) {
+      a.pdist[slot + lane] = bd;
+      a.pid[slot + lane] = bid;
+      if constexpr (REL) __threadfence();
+    }
+    __syncthreads();  // every warp is done with this LUT
+    if constexpr (REL) {
+      if (threadIdx.x == 0) {
+        const unsigned long long ng = (unsigned long long)(seg_end - g);
+        const unsigned long long tot = (unsigned long long)(qend - a.item_off[(long long)q * a.np]);
+        __threadfence();  // this CTA's partial lists before its count
+        s_last = atomicAdd(a.qdone + q, ng) + ng == tot;
+      }
+      __syncthreads();
+      if (s_last) {  // CTA-uniform
+        __threadfence();
+        merge_query<true>(q, a.nq, a.np, a.k, G, a.item_off, a.pdist, a.pid, a.out_ids, a.out_dist, nullptr,
+                          *reinterpret_cast<MergeSmem*>(smem));
+        if (warp == 0) release_row(a, q, lane);
+        __syncthreads();  // the merge used the LUT region as scratch
+      }
+    }
+    g = seg_end;
+    if (g < g1) {
+      it0 = (long long)(q + 1) * a.np;
+      while (a.item_off[it0 + 1] <= g) ++it0;
+    }
+  }
+}
+
+int scan_ctas(const DeviceIndex& ix) {
+  (void)ix;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;  // one persistent CTA per SM (128 KB LUT + 16 warps)
+}
+
+template <int MP, int NB, int EXP, bool REL = false>
+static cudaError_t launch_scan_e(const ScanArgs& a, int n_cta, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan<MP, NB, EXP, REL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(2 * kLutPairBytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  uint32_t smem = a.lut_bytes;
+  if (REL && smem < (uint32_t)sizeof(MergeSmem)) smem = (uint32_t)sizeof(MergeSmem);
+  k_scan<MP, NB, EXP, REL><<<n_cta, kScanThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// VLR_SCAN_EXPERIMENT=1|2 (timing experiments only; results are wrong):
+// 1 = no LUT gathers, 2 = no code loads.
+static int scan_experiment() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VLR_SCAN_EXPERIMENT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <int MP, int NB>
+static cudaError_t launch_scan_t(const ScanArgs& a, int n_cta, cudaStream_t s) {
+  if (a.ready) return launch_scan_e<MP, NB, 0, true>(a, n_cta, s);
+  if constexpr (MP == 128 && NB == 8) {
+    const int x = scan_experiment();
+    if (x == 1) return launch_scan_e<MP, NB, 1>(a, n_cta, s);
+    if (x == 2) return launch_scan_e<MP, NB, 2>(a, n_cta, s);
+  }
+  return launch_scan_e<MP, NB, 0>(a, n_cta, s);
+}
+
+cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s,
+                        const Release* rel) {
+  if (nq <= 0) return cudaSuccess;
+  ScanArgs a{nq, np, k, ix.npairs, (uint32_t)(ix.npairs * ix.lut_pair_bytes), ws.plocal, ws.term1, ws.item_off,
+             ix.gbase, ix.codes, ix.bias, ix.ids, ws.lut, ws.pdist, ws.pid,
+             nullptr, nullptr, 0u, nullptr, nullptr};
+  if (rel) {
+    if ((long long)ws.n_cta * kScanWarps > kMergeMaxLists) return cudaErrorInvalidConfiguration;
+    a.qdone = ws.qdone;
+    a.ready = rel->ready;
+    a.epoch = rel->epoch;
+    a.out_ids = rel->out_ids;
+    a.out_dist = rel->out_dist;
+  }
+  if (ix.nbits == 4) {
+    switch (ix.mpad) {
+      case 32: return launch_scan_t<32, 4>(a, ws.n_cta, s);
+      case 64: return launch_scan_t<64, 4>(a, ws.n_cta, s);
+      case 96: return launch_scan_t<96, 4>(a, ws.n_cta, s);
+      case 128: return launch_scan_t<128, 4>(a, ws.n_cta, s);
+      case 192: return launch_scan_t<192, 4>(a, ws.n_cta, s);
+      case 256: return launch_scan_t<256, 4>(a, ws.n_cta, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (ix.mpad) {
+    case 32: return launch_scan_t<32, 8>(a, ws.n_cta, s);
+    case 64: return launch_scan_t<64, 8>(a, ws.n_cta, s);
+    case 96: return launch_scan_t<96, 8>(a, ws.n_cta, s);
+    case 128: return launch_scan_t<128, 8>(a, ws.n_cta, s);
+    default: return cudaErrorInvalidValue;
   }
 }
 

@@ -95,6 +95,7 @@ struct Workspace {
   int64_t* item_off = nullptr; // [nq*np + 1] group prefix of owned work items
   int64_t* item_local = nullptr; // [nq*np] within-query group prefix
   int64_t* qtot = nullptr;     // [nq] groups owned per query
+  unsigned long long* qdone = nullptr;  // [nq] groups scanned per query (NEXT-4 release counters)
   float* lut = nullptr;        // [nq][npairs][ksub][64]
   float* pdist = nullptr;      // [(n_cta + nq) * warps * k] scan partials
   int64_t* pid = nullptr;
@@ -150,7 +151,14 @@ cudaError_t launch_access_hist(const int32_t* probes, long long n, int nlist, un
                                cudaStream_t s);
 // stage 5..7
 int scan_ctas(const DeviceIndex& ix);
-cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s);
+struct Release {               // NEXT-4 early per-query release (vlr_search_release_async)
+  uint32_t* ready;
+  uint32_t epoch;
+  int64_t* out_ids;
+  float* out_dist;
+};
+cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s,
+                        const Release* rel = nullptr);
 cudaError_t launch_rank_merge(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k,
                               int64_t* out_ids, float* out_dist, void* out_packed, cudaStream_t s);
 cudaError_t launch_merge_packed(const void* parts, int n_shards, int nq, int k, int64_t* out_ids, float* out_dist,

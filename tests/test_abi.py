@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol():
 
 
 def test_version():
-    assert vlr.version() == (1, 1)
+    assert vlr.version() == (1, 2)
 
 
 def _tiny(m=2, d=4, L=3):
@@ -97,3 +97,27 @@ def test_search_argument_validation_without_index():
     st = L.vlr_merge_partials(None, None, 1, 0, 4, None, None, None)
     assert vlr.STATUS[st] == "OK"  # nq == 0 is a no-op
     assert b"" != L.vlr_last_error() or True
+
+
+def test_poll_ready_host_dispatcher():
+    """vlr_poll_ready (NEXT-4 host side) on host flags: returns the newly
+    released queries once each, marks them seen, times out with 0."""
+    L = vlr.lib()
+    nq, epoch = 10, 7
+    ready = np.zeros(nq, np.uint32)
+    ready[[2, 5, 9]] = epoch
+    ready[3] = epoch - 1  # a stale epoch is not a release
+    seen = np.zeros(nq, np.uint8)
+    qs = np.empty(nq, np.int32)
+    ts = np.empty(nq, np.int64)
+    n = L.vlr_poll_ready(ready.ctypes.data, nq, epoch, seen.ctypes.data, qs.ctypes.data, ts.ctypes.data, nq, 1000)
+    assert n == 3 and sorted(qs[:3].tolist()) == [2, 5, 9]
+    assert seen.tolist() == [1 if q in (2, 5, 9) else 0 for q in range(nq)]
+    assert np.all(ts[:3] > 0)
+    n = L.vlr_poll_ready(ready.ctypes.data, nq, epoch, seen.ctypes.data, qs.ctypes.data, None, nq, 2000)
+    assert n == 0  # nothing new: timeout
+    ready[0] = epoch
+    n = L.vlr_poll_ready(ready.ctypes.data, nq, epoch, seen.ctypes.data, qs.ctypes.data, None, 1, 1000)
+    assert n == 1 and qs[0] == 0
+    assert L.vlr_poll_ready(None, nq, epoch, seen.ctypes.data, qs.ctypes.data, None, nq, 0) == -1
+    assert L.vlr_poll_ready(ready.ctypes.data, nq, epoch, seen.ctypes.data, qs.ctypes.data, None, 0, 0) == -1
