@@ -492,19 +492,24 @@ def release_leg(a, c, h, Qdev, outs, K):
     import torch
     R = min(a.steps, 20)
     batch_ms, q_ms, last_ms, equal = [], [], [], True
+    scan_plain, scan_rel = [], []
+    h.set_profiling(2)
     for i in range(R):
         Q = Qdev[a.warmup + i]
         torch.cuda.synchronize()
         t0 = time.monotonic_ns()
         h.search(Q, c["nprobe"], K, out=outs[i], sync=True)
         batch_ms.append((time.monotonic_ns() - t0) / 1e6)
+        scan_plain.append(h.stage_times(0)["scan"])
         torch.cuda.synchronize()
         ids, dist, _, _, t = h.search_release(Q, c["nprobe"], K)
         torch.cuda.synchronize()
+        scan_rel.append(h.stage_times(0)["scan"])
         lat = (np.asarray(t, np.int64) - t.t0) / 1e6
         q_ms.append(lat)
         last_ms.append(float(lat.max()))
         equal &= bool(torch.equal(ids, outs[i][0].cpu()) and torch.equal(dist, outs[i][1].cpu()))
+    h.set_profiling(False)
     ql = np.concatenate(q_ms)
     bm = np.array(batch_ms)
     return {"per_query_ms": {"mean": float(ql.mean()), "p50": float(np.percentile(ql, 50)),
@@ -512,6 +517,7 @@ def release_leg(a, c, h, Qdev, outs, K):
             "batch_ms": {"mean": float(bm.mean()), "p50": float(np.percentile(bm, 50)),
                          "p99": float(np.percentile(bm, 99))},
             "last_release_ms_mean": float(np.mean(last_ms)),
+            "scan_ms_device": {"batch": float(np.mean(scan_plain)), "release": float(np.mean(scan_rel))},
             "mean_latency_reduction": float(1.0 - ql.mean() / bm.mean()),
             "bitwise_equal_to_batch_search": equal, "batches": R,
             "how": "host CLOCK_MONOTONIC from launch to the query's release flag (vlr_poll_ready) vs launch to "

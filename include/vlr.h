@@ -152,9 +152,11 @@ vlr_status vlr_search_host(vlr_index* idx, const float* h_queries, int32_t nq, i
  * NEXT-4: early per-query release -- the GPU analog of the paper's dynamic
  * dispatcher (P:408-414 [§IV.C]: "GPU ... completion flags", "per-query
  * callback" so a finished query does not wait for its batch; Fig. 14).
- * Same search and outputs as vlr_search_async, but the scan kernel itself
- * merges each query's partial lists as soon as the last scan CTA touching the
- * query finishes (no separate K7 launch) and then raises ready[q] = epoch.
+ * Same search and outputs as vlr_search_async, but the batch is scanned in
+ * query waves on all SMs but one, and a resident merger CTA (on the remaining
+ * SM, forked onto a second stream and joined back to `stream`) merges each
+ * query's partial lists as soon as the scan has finished the query, then
+ * raises ready[q] = epoch (no separate K7 launch after the scan).
  *   ready [nq] uint32: flags, device-accessible -- device memory or pinned
  *      host memory (cudaHostAlloc / cudaMallocHost, used through its UVA
  *      pointer); the caller sets them != epoch before the call.
@@ -164,8 +166,9 @@ vlr_status vlr_search_host(vlr_index* idx, const float* h_queries, int32_t nq, i
  *      row q is final (and visible to the host) once ready[q] == epoch (the
  *      row is written before the flag with system-scope release ordering).
  *   d_miss / d_probes: device memory, valid at stream completion as usual.
- * Rows with no resident probe are released at the scan's start. Bit-identical
- * results to vlr_search_async (the merge is the same code).
+ * Rows with no resident probe are released first, as padding. Results are
+ * bit-identical to vlr_search_async (same distances, same merge code). Not
+ * graph-capturable (the epoch is a launch argument).
  * Errors: as vlr_search_async; UNSUPPORTED for world > 1 or shard-only handles
  * (rows there are final only after the exchange); INVALID_ARG for epoch 0,
  * NULL or non-device-accessible ready/ids/dist.
@@ -184,6 +187,14 @@ vlr_status vlr_search_release_async(vlr_index* idx, const float* d_queries, int3
  * the returned queries can be read after the call. Host only; no CUDA calls. */
 int32_t vlr_poll_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, uint8_t* seen, int32_t* out_q,
                        int64_t* out_t_ns, int32_t max_out, int64_t timeout_us);
+
+/* Native dispatcher loop for vlr_search_release_async without per-query
+ * callbacks: spins until every q < nq has ready[q] == epoch or timeout_us
+ * passes; out_t_ns (may be NULL) [nq] receives, per query, the
+ * CLOCK_MONOTONIC time in ns at which its flag was first observed. Returns
+ * the number of released queries (nq on success), -1 for bad arguments. An
+ * acquire fence follows the flag reads. Host only; no CUDA calls. */
+int32_t vlr_wait_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, int64_t* out_t_ns, int64_t timeout_us);
 
 /* Pre-size the per-handle workspace for batches up to (max_nq, max_nprobe, max_k)
  * so that later searches allocate nothing (required before graph capture). */

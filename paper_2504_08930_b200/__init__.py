@@ -22,7 +22,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "NONFINITE", 4: "UNKN
 
 # every symbol include/vlr.h declares (checked by tests/test_abi.py)
 EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_search_release_async",
-           "vlr_poll_ready", "vlr_reserve",
+           "vlr_poll_ready", "vlr_wait_ready", "vlr_reserve",
            "vlr_merge_partials", "vlr_access_counts", "vlr_index_info", "vlr_index_owners", "vlr_set_profiling", "vlr_stage_times",
            "vlr_last_launch_count", "vlr_nccl_unique_id", "vlr_index_free", "vlr_last_error", "vlr_version"]
 
@@ -80,6 +80,8 @@ def lib():
             f.restype = ctypes.c_int
         L.vlr_poll_ready.argtypes = [P, I32, ctypes.c_uint32, P, P, P, I32, I64]
         L.vlr_poll_ready.restype = I32
+        L.vlr_wait_ready.argtypes = [P, I32, ctypes.c_uint32, P, I64]
+        L.vlr_wait_ready.restype = I32
         L.vlr_last_launch_count.argtypes = [P]
         L.vlr_last_launch_count.restype = I32
         L.vlr_index_free.argtypes = [P]
@@ -211,6 +213,10 @@ class Index:
                                               _stream_handle(stream)))
         got = 0
         deadline = t0 + int(timeout_s * 1e9)
+        if on_ready is None:  # native dispatcher loop (no per-query Python work while the batch runs)
+            got = lib().vlr_wait_ready(ready.data_ptr(), nq, self._epoch, t_ready.ctypes.data, int(timeout_s * 1e6))
+            if got < nq:
+                raise VlrError(7, f"search_release: {nq - max(got, 0)} queries not released within {timeout_s} s")
         while got < nq:
             n = lib().vlr_poll_ready(ready.data_ptr(), nq, self._epoch, seen.ctypes.data, qs.ctypes.data,
                                      ts.ctypes.data, nq, 100_000)

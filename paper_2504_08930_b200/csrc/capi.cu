@@ -99,7 +99,7 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   VLR_CUDA_TRY(dalloc(&w.qtot, nqs));
   VLR_CUDA_TRY(dalloc(&w.qdone, nqs));
   VLR_CUDA_TRY(dalloc(&w.lut, nqs * ix.npairs * (ix.lut_pair_bytes / 4)));
-  const size_t nslots = ((size_t)w.n_cta + nqs) * kScanWarps * ck;
+  const size_t nslots = ((size_t)w.n_cta * kReleaseWaves + nqs) * kScanWarps * ck;  // slot (c + q + wave * n_cta)
   VLR_CUDA_TRY(dalloc(&w.pdist, nslots));
   VLR_CUDA_TRY(dalloc(&w.pid, nslots));
   if (ix.world > 1 && !ix.shard_only) {
@@ -387,6 +387,9 @@ void vlr_index_free(vlr_index* h) {
   for (auto& row : h->ev)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
+  if (h->rel_fork) cudaEventDestroy(h->rel_fork);
+  if (h->rel_join) cudaEventDestroy(h->rel_join);
+  if (h->rel_stream) cudaStreamDestroy(h->rel_stream);
   free_ws(h->ws);
   free_index(h->ix);
   delete h;
@@ -500,7 +503,13 @@ vlr_status vlr_search_release_async(vlr_index* h, const float* Q, int32_t nq, in
         !device_accessible(out_dist))
       return fail(VLR_ERR_INVALID_ARG, "release: ready/ids/dist must be device or pinned (mapped) host memory");
   }
-  const Release rel{ready, epoch, out_ids, out_dist};
+  if (!h->rel_stream) {
+    VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
+    VLR_CUDA_TRY(cudaStreamCreateWithFlags(&h->rel_stream, cudaStreamNonBlocking));
+    VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->rel_fork, cudaEventDisableTiming));
+    VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->rel_join, cudaEventDisableTiming));
+  }
+  const Release rel{ready, epoch, out_ids, out_dist, h->rel_stream, h->rel_fork, h->rel_join};
   return search_impl(h, Q, nq, nprobe, k, out_ids, out_dist, out_miss, out_probes, stream, &rel);
 }
 
@@ -528,6 +537,34 @@ int32_t vlr_poll_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, uint8_
       break;
   }
   std::atomic_thread_fence(std::memory_order_acquire);  // rows of the released queries after their flags
+  return n;
+}
+
+int32_t vlr_wait_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, int64_t* out_t_ns, int64_t timeout_us) {
+  if (!ready || nq < 0) return -1;
+  const volatile uint32_t* r = ready;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<uint8_t> seen((size_t)nq, 0);
+  int32_t n = 0, lo = 0;  // queries below lo are all seen
+  while (n < nq) {
+    bool any = false;
+    for (int32_t q = lo; q < nq; ++q) {
+      if (seen[q] || r[q] != epoch) continue;
+      seen[q] = 1;
+      any = true;
+      ++n;
+      if (out_t_ns) {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        out_t_ns[q] = (int64_t)ts.tv_sec * 1000000000LL + ts.tv_nsec;
+      }
+    }
+    while (lo < nq && seen[lo]) ++lo;
+    if (!any && std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count() >=
+                    timeout_us)
+      break;
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   return n;
 }
 

@@ -65,6 +65,7 @@ struct ScanArgs {
   uint32_t epoch;             // value written to ready[q] when row q is final
   int64_t* out_ids;           // [nq][k] final rows (device or pinned host)
   float* out_dist;
+  int waves;                  // REL: the batch is scanned in this many query waves
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -292,10 +293,15 @@ __device__ __forceinline__ T ldp(const T* p) {
 
 // merge of query q by the whole CTA (nw = blockDim.x / 32 warps); warp 0
 // writes the row. Warps other than 0 return after phase B (no barrier after).
+// The scan split the group range [WL, WH) of q's wave statically over n_cta
+// CTAs; q's groups are [S, E); CTA c's lists for q sit at
+// slot (c + q + zoff) (zoff = wave * n_cta keeps the slots of different waves
+// apart; 0 without waves).
 template <bool CG>
 __device__ __forceinline__ void merge_query(
-    int q, int nq, int np, int k, int n_cta, const int64_t* __restrict__ item_off, const float* pdist,
-    const int64_t* pid, int64_t* out_ids, float* out_dist, Packed* __restrict__ packed, MergeSmem& sm) {
+    int q, int k, int n_cta, long long WL, long long WH, long long zoff, long long S, long long E,
+    const float* pdist, const int64_t* pid, int64_t* out_ids, float* out_dist, Packed* __restrict__ packed,
+    MergeSmem& sm) {
   float* s_d = sm.s_d;
   long long* s_id = sm.s_id;
   float& s_t0 = sm.s_t0;
@@ -304,8 +310,7 @@ __device__ __forceinline__ void merge_query(
   float* s_ld = sm.s_ld;
   long long* s_lid = sm.s_lid;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const long long W = item_off[(long long)nq * np];
-  const long long S = item_off[(long long)q * np], E = item_off[(long long)(q + 1) * np];
+  const long long W = WH - WL;
   const long long* pidl = reinterpret_cast<const long long*>(pid);
   float bd = CUDART_INF_F, thr = CUDART_INF_F;
   long long bid = -1;
@@ -315,14 +320,14 @@ __device__ __forceinline__ void merge_query(
   if (E > S) {
     // largest c with start(c) = floor(c W / G) <= g  <=>  c W < (g + 1) G
     auto cta_of = [&](long long g) {
-      const long long c = ((g + 1) * n_cta - 1) / W;
+      const long long c = ((g - WL + 1) * n_cta - 1) / W;
       return (int)(c < n_cta - 1 ? c : n_cta - 1);
     };
     cf = cta_of(S);
     nl = (cta_of(E - 1) - cf + 1) * kScanWarps;
     maybe_empty = W < n_cta;  // otherwise every CTA owns >= 1 group
   }
-  const long long base = (long long)(cf + q) * kScanWarps * k;  // list li starts at base + li * k
+  const long long base = (long long)(cf + q + zoff) * kScanWarps * k;  // list li starts at base + li * k
   auto head_ok = [&](int li) { return !maybe_empty || start(cf + li / kScanWarps) != start(cf + li / kScanWarps + 1); };
   // ---- phase A: k smallest heads
   constexpr int U = 4;
@@ -456,7 +461,9 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32) k_rank_merge(
     const int64_t* __restrict__ pid, int64_t* __restrict__ out_ids, float* __restrict__ out_dist,
     Packed* __restrict__ packed) {
   __shared__ MergeSmem sm;
-  merge_query<false>(blockIdx.x, nq, np, k, n_cta, item_off, pdist, pid, out_ids, out_dist, packed, sm);
+  const int q = blockIdx.x;
+  merge_query<false>(q, k, n_cta, 0, item_off[(long long)nq * np], 0, item_off[(long long)q * np],
+                     item_off[(long long)(q + 1) * np], pdist, pid, out_ids, out_dist, packed, sm);
 }
 
 template <int MP, int NB, int EXP>
@@ -483,133 +490,208 @@ __device__ __forceinline__ void grp_finish(const Grp<MP, NB>& G, const ScanArgs&
   }
 }
 
+// ---------------------------------------------------------------- NEXT-4 release
+// REL scan (NEXT-4, the GPU analog of the paper's dynamic dispatcher,
+// P:408-414): the scan runs on all SMs but one and, after each query segment,
+// adds the segment's group count to qdone[q] (release-ordered after the
+// segment's partial lists). One resident merger CTA (k_release_merge, on the
+// remaining SM, launched on a forked stream) picks up every query whose count
+// is complete, merges its partial lists with the K7 code (through L2) and
+// raises ready[q]. The merge is not inlined into the scan: its registers make
+// the MP = 128 scan loop spill. So that queries complete
+// progressively rather than all at the end, the REL batch is cut at query
+// boundaries into a.waves waves (wave z = queries [z nq / Z, (z+1) nq / Z));
+// every CTA scans its static share of wave 0, then of wave 1, ... (no grid
+// barrier: each CTA's share of a wave is proportional, so waves finish in
+// order). Without REL there is one wave: the plain static split of the stream.
+__device__ __forceinline__ void rel_segment_done(const ScanArgs& a, int q, long long ng) {
+  if (threadIdx.x == 0) {
+    __threadfence();  // this CTA's partial lists (stored before the caller's barrier) before its count
+    atomicAdd(a.qdone + q, (unsigned long long)ng);
+  }
+}
+
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-
-// NEXT-4 release of row q (warp 0 of the CTA): the row's stores are made
-// visible at system scope before the flag (completion flags)
-__device__ __forceinline__ void release_row(const ScanArgs& a, int q, int lane) {
-  __threadfence_system();
-  __syncwarp();
-  if (lane == 0) st_release_sys(a.ready + q, a.epoch);
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
-// REL (NEXT-4, the GPU analog of the paper's dynamic dispatcher):
-// after each query segment a CTA adds its group count to qdone[q]; the CTA
-// that completes q (count reaches q's owned groups) merges q's partial lists
-// itself (the K7 code, through L2) and raises ready[q], so a finished query is
-// released while the rest of the batch is still being scanned. Queries that
-// own no groups are released at kernel start (CTA q mod G).
+constexpr unsigned long long kMerged = 1ull << 63;  // qdone[q] mark: q merged and released
+
+// the resident merger CTA (kMergeMaxWarps warps): G = the scan's grid size
+__global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanArgs a, int G, int32_t* status) {
+  __shared__ MergeSmem sm;
+  __shared__ int s_q;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nq = a.nq, np = a.np, Z = a.waves;
+  int lo = 0;  // queries < lo are merged (warp 0's view)
+#ifdef VLR_REL_DEBUG
+  if (threadIdx.x == 0) printf("merger start nq %d np %d Z %d G %d qdone0 %llu tot0 %lld\n", nq, np, Z, G,
+                               ld_acquire_gpu(a.qdone), (long long)(a.item_off[np] - a.item_off[0]));
+#endif
+  for (int done = 0; done < nq; ++done) {
+    if (warp == 0) {
+      int found = -1;
+      const unsigned long long t0 = globaltimer_ns();
+      for (uint32_t spin = 0;; ++spin) {
+        while (lo < nq && (ld_acquire_gpu(a.qdone + lo) & kMerged)) ++lo;
+        for (int base = lo; base < nq && found < 0; base += 32) {
+          const int q = base + lane;
+          bool ok = false;
+          if (q < nq) {
+            const unsigned long long v = ld_acquire_gpu(a.qdone + q);
+            ok = !(v & kMerged) && v == (unsigned long long)(a.item_off[(long long)(q + 1) * np] -
+                                                             a.item_off[(long long)q * np]);
+          }
+          const unsigned m = __ballot_sync(kFull, ok);
+          if (m) found = base + __ffs(m) - 1;
+        }
+        if (found >= 0) break;
+        __nanosleep(128);
+        if ((spin & 255u) == 255u && globaltimer_ns() - t0 > 4000000000ull) break;  // bounded: never hang
+      }
+      if (lane == 0) {
+        s_q = found;
+        if (found < 0) atomicOr(status, 2);  // the host poll then times out with an error
+      }
+    }
+    __syncthreads();
+    const int q = s_q;
+#ifdef VLR_REL_DEBUG
+    if (threadIdx.x == 0 && (done < 2 || q < 0))
+      printf("merger done %d q %d qdone0 %llu\n", done, q, ld_acquire_gpu(a.qdone));
+#endif
+    if (q < 0) return;
+    __threadfence();
+    // the wave of q and its group range (the scan's static split, k_scan)
+    int z = (int)(((long long)(q + 1) * Z - 1) / nq);
+    z = z < Z - 1 ? z : Z - 1;
+    const long long WL = a.item_off[(long long)((long long)z * nq / Z) * np];
+    const long long WH = a.item_off[(long long)((long long)(z + 1) * nq / Z) * np];
+    merge_query<true>(q, a.k, G, WL, WH, (long long)z * G, a.item_off[(long long)q * np],
+                      a.item_off[(long long)(q + 1) * np], a.pdist, a.pid, a.out_ids, a.out_dist, nullptr, sm);
+    if (warp == 0) {
+      __threadfence_system();  // row q (possibly in pinned host memory) before its flag
+      __syncwarp();
+      if (lane == 0) {
+        st_release_sys(a.ready + q, a.epoch);
+        atomicOr(a.qdone + q, kMerged);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <int MP, int NB, int EXP, bool REL = false>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ long long s_it;
-  __shared__ int s_last;
+  __shared__ long long s_ng;
+  __shared__ int s_z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = gridDim.x, c = blockIdx.x;
-  const int nitems = a.nq * a.np;
-  const long long W = a.item_off[nitems];
-  const long long g0 = (long long)c * W / G, g1 = (long long)(c + 1) * W / G;
-  if constexpr (REL) {
-    if (warp == 0) {
-      for (int q = c; q < a.nq; q += G) {
-        if (a.item_off[(long long)(q + 1) * a.np] != a.item_off[(long long)q * a.np]) continue;
-        if (lane < a.k) {
-          a.out_ids[(size_t)q * a.k + lane] = -1;
-          a.out_dist[(size_t)q * a.k + lane] = CUDART_INF_F;
-        }
-        release_row(a, q, lane);
-      }
-    }
-  }
-  if (g0 >= g1) return;
+  const int Z = REL ? a.waves : 1;
   const uint32_t lut_bytes = a.lut_bytes;
   if (threadIdx.x == 0) {
     mbar_init(&mbar, 1);
     fence_mbar_init();
-    // item containing group g0: last i with item_off[i] <= g0
-    int lo = 0, hi = nitems;  // item_off[lo] <= g0 < item_off[hi]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (a.item_off[mid] <= g0) lo = mid; else hi = mid;
-    }
-    s_it = lo;
   }
-  __syncthreads();
-  long long it0 = s_it;
-  while (a.item_off[it0 + 1] <= g0) ++it0;
   const uint32_t lane4 = (uint32_t)lane << 2;
   const unsigned char* lutc = smem;
   uint32_t phase = 0;
-  long long g = g0;
-  while (g < g1) {
-    const int q = (int)(it0 / a.np);
-    const long long qend = a.item_off[(long long)(q + 1) * a.np];
-    const long long seg_end = qend < g1 ? qend : g1;
-    if (threadIdx.x == 0) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&mbar, lut_bytes);
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(a.lut) + (size_t)q * lut_bytes;
-      for (uint32_t off = 0; off < lut_bytes; off += 32768u)
-        bulk_g2s(smem + off, src + off, lut_bytes - off < 32768u ? lut_bytes - off : 32768u, &mbar);
-    }
-    mbar_wait(&mbar, phase);
-    phase ^= 1u;
-
-    float bd = CUDART_INF_F, thr = CUDART_INF_F;
-    long long bid = -1;
-    long long it = it0;
-    long long gg = g + warp;
-    Grp<MP, NB> A, B;
-    long long itp = it0;  // prefetch cursor: kPfDist groups (of this warp) ahead of the loads
-    if (gg < seg_end) {
-      for (int p = 1; p <= kPfDist; ++p)
-        if (gg + p * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gg + p * kScanWarps, itp, lane);
-      grp_load<MP, NB, EXP>(A, a, gg, it, lane);
-    }
-    while (gg < seg_end) {
-      const long long gn = gg + kScanWarps;
-      if constexpr (kPfDist > 0)
-        if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gn + kPfDist * kScanWarps, itp, lane);
-      if (gn < seg_end) grp_load<MP, NB, EXP>(B, a, gn, it, lane);
-      grp_finish<MP, NB, EXP>(A, a, lutc, lane4, lane, bd, bid, thr);
-      if (gn >= seg_end) break;
-      const long long gm = gn + kScanWarps;
-      if constexpr (kPfDist > 0)
-        if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gm + kPfDist * kScanWarps, itp, lane);
-      if (gm < seg_end) grp_load<MP, NB, EXP>(A, a, gm, it, lane);
-      grp_finish<MP, NB, EXP>(B, a, lutc, lane4, lane, bd, bid, thr);
-      gg = gm;
-    }
-    const long long slot = ((long long)(c + q) * kScanWarps + warp) * a.k;
-    if (lane < a.k) {
-      a.pdist[slot + lane] = bd;
-      a.pid[slot + lane] = bid;
-      if constexpr (REL) __threadfence();
-    }
-    __syncthreads();  // every warp is done with this LUT
+  // REL: the wave index lives in shared memory and is re-read where needed, so
+  // no register is held across the scan loop for it (the MP = 128 loop needs
+  // all 128 registers)
+  if constexpr (REL) {
+    if (threadIdx.x == 0) s_z = 0;
+    __syncthreads();
+  }
+  auto zcur = [&]() -> int { return *reinterpret_cast<volatile int*>(&s_z); };
+  for (int z1 = 0; z1 < Z; ++z1) {
+    if constexpr (REL) __syncthreads();  // s_z of the previous wave written
+    const int z = REL ? zcur() : z1;
+    const int i_lo = (int)((long long)z * a.nq / Z) * a.np, i_hi = (int)((long long)(z + 1) * a.nq / Z) * a.np;
+    const long long WL = a.item_off[i_lo], WH = a.item_off[i_hi];
+    const long long g0 = WL + (long long)c * (WH - WL) / G, g1 = WL + (long long)(c + 1) * (WH - WL) / G;
     if constexpr (REL) {
-      if (threadIdx.x == 0) {
-        const unsigned long long ng = (unsigned long long)(seg_end - g);
-        const unsigned long long tot = (unsigned long long)(qend - a.item_off[(long long)q * a.np]);
-        __threadfence();  // this CTA's partial lists before its count
-        s_last = atomicAdd(a.qdone + q, ng) + ng == tot;
-      }
-      __syncthreads();
-      if (s_last) {  // CTA-uniform
-        __threadfence();
-        merge_query<true>(q, a.nq, a.np, a.k, G, a.item_off, a.pdist, a.pid, a.out_ids, a.out_dist, nullptr,
-                          *reinterpret_cast<MergeSmem*>(smem));
-        if (warp == 0) release_row(a, q, lane);
-        __syncthreads();  // the merge used the LUT region as scratch
-      }
+      __syncthreads();  // every thread has read s_z
+      if (threadIdx.x == 0) s_z = z + 1;
     }
-    g = seg_end;
-    if (g < g1) {
-      it0 = (long long)(q + 1) * a.np;
-      while (a.item_off[it0 + 1] <= g) ++it0;
+    if (g0 >= g1) continue;  // CTA-uniform
+    __syncthreads();  // s_it of the previous wave consumed
+    if (threadIdx.x == 0) {
+      // item containing group g0: last i with item_off[i] <= g0
+      int lo = i_lo, hi = i_hi;  // item_off[lo] <= g0 < item_off[hi]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (a.item_off[mid] <= g0) lo = mid; else hi = mid;
+      }
+      s_it = lo;
+    }
+    __syncthreads();
+    long long it0 = s_it;
+    while (a.item_off[it0 + 1] <= g0) ++it0;
+    long long g = g0;
+    while (g < g1) {
+      const int q = (int)(it0 / a.np);
+      const long long qend = a.item_off[(long long)(q + 1) * a.np];
+      const long long seg_end = qend < g1 ? qend : g1;
+      if (threadIdx.x == 0) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&mbar, lut_bytes);
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(a.lut) + (size_t)q * lut_bytes;
+        for (uint32_t off = 0; off < lut_bytes; off += 32768u)
+          bulk_g2s(smem + off, src + off, lut_bytes - off < 32768u ? lut_bytes - off : 32768u, &mbar);
+      }
+      if constexpr (REL) {  // segment length through shared memory: nothing extra stays live across the scan loop
+        if (threadIdx.x == 0) s_ng = seg_end - g;
+      }
+      mbar_wait(&mbar, phase);
+      phase ^= 1u;
+
+      float bd = CUDART_INF_F, thr = CUDART_INF_F;
+      long long bid = -1;
+      long long it = it0;
+      long long gg = g + warp;
+      Grp<MP, NB> A, B;
+      long long itp = it0;  // prefetch cursor: kPfDist groups (of this warp) ahead of the loads
+      if (gg < seg_end) {
+        for (int p = 1; p <= kPfDist; ++p)
+          if (gg + p * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gg + p * kScanWarps, itp, lane);
+        grp_load<MP, NB, EXP>(A, a, gg, it, lane);
+      }
+      while (gg < seg_end) {
+        const long long gn = gg + kScanWarps;
+        if constexpr (kPfDist > 0)
+          if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gn + kPfDist * kScanWarps, itp, lane);
+        if (gn < seg_end) grp_load<MP, NB, EXP>(B, a, gn, it, lane);
+        grp_finish<MP, NB, EXP>(A, a, lutc, lane4, lane, bd, bid, thr);
+        if (gn >= seg_end) break;
+        const long long gm = gn + kScanWarps;
+        if constexpr (kPfDist > 0)
+          if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gm + kPfDist * kScanWarps, itp, lane);
+        if (gm < seg_end) grp_load<MP, NB, EXP>(A, a, gm, it, lane);
+        grp_finish<MP, NB, EXP>(B, a, lutc, lane4, lane, bd, bid, thr);
+        gg = gm;
+      }
+      const long long slot = ((long long)(c + q) + (long long)(REL ? zcur() - 1 : 0) * G) * kScanWarps * a.k + warp * a.k;
+      if (lane < a.k) {
+        a.pdist[slot + lane] = bd;
+        a.pid[slot + lane] = bid;
+        if constexpr (REL) __threadfence();
+      }
+      __syncthreads();  // every warp is done with this LUT
+      if constexpr (REL) rel_segment_done(a, q, s_ng);
+      g = seg_end;
+      if (g < g1) {
+        it0 = (long long)(q + 1) * a.np;
+        while (a.item_off[it0 + 1] <= g) ++it0;
+      }
     }
   }
 }
@@ -629,11 +711,12 @@ static cudaError_t launch_scan_e(const ScanArgs& a, int n_cta, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(k_scan<MP, NB, EXP, REL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(2 * kLutPairBytes));
     if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa;  // forces the (lazy) module load now
+    if ((e = cudaFuncGetAttributes(&fa, k_scan<MP, NB, EXP, REL>)) != cudaSuccess) return e;
     configured = true;
   }
-  uint32_t smem = a.lut_bytes;
-  if (REL && smem < (uint32_t)sizeof(MergeSmem)) smem = (uint32_t)sizeof(MergeSmem);
-  k_scan<MP, NB, EXP, REL><<<n_cta, kScanThreads, smem, s>>>(a);
+  if (n_cta == 0) return cudaSuccess;  // configure (and so load) only
+  k_scan<MP, NB, EXP, REL><<<n_cta, kScanThreads, a.lut_bytes, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -659,36 +742,71 @@ static cudaError_t launch_scan_t(const ScanArgs& a, int n_cta, cudaStream_t s) {
   return launch_scan_e<MP, NB, 0>(a, n_cta, s);
 }
 
+static cudaError_t launch_scan_k(const DeviceIndex& ix, const ScanArgs& a, int n_cta, cudaStream_t s);
+
 cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s,
                         const Release* rel) {
   if (nq <= 0) return cudaSuccess;
   ScanArgs a{nq, np, k, ix.npairs, (uint32_t)(ix.npairs * ix.lut_pair_bytes), ws.plocal, ws.term1, ws.item_off,
              ix.gbase, ix.codes, ix.bias, ix.ids, ws.lut, ws.pdist, ws.pid,
-             nullptr, nullptr, 0u, nullptr, nullptr};
+             nullptr, nullptr, 0u, nullptr, nullptr, 1};
+  int G = ws.n_cta;
   if (rel) {
-    if ((long long)ws.n_cta * kScanWarps > kMergeMaxLists) return cudaErrorInvalidConfiguration;
+    if ((long long)ws.n_cta * kScanWarps > kMergeMaxLists || ws.n_cta < 2) return cudaErrorInvalidConfiguration;
+    G = ws.n_cta - 1;  // one SM for the resident merger CTA
     a.qdone = ws.qdone;
     a.ready = rel->ready;
     a.epoch = rel->epoch;
     a.out_ids = rel->out_ids;
     a.out_dist = rel->out_dist;
+    static int env_waves = -1;  // VLR_RELEASE_WAVES: experiment override of the wave count
+    if (env_waves < 0) {
+      const char* e = getenv("VLR_RELEASE_WAVES");
+      env_waves = e ? atoi(e) : 0;
+    }
+    const int zw = env_waves > 0 ? env_waves : kReleaseWaves;
+    a.waves = nq < zw ? nq : zw;
+    // Both kernels must be loaded before the fork: with lazy module loading, loading a kernel while the
+    // spinning merger runs waits for the merger (and the merger waits for the scan).
+    static bool merger_loaded = false;
+    cudaError_t e = launch_scan_k(ix, a, 0, s);
+    if (e != cudaSuccess) return e;
+    if (!merger_loaded) {
+      cudaFuncAttributes fa;
+      if ((e = cudaFuncGetAttributes(&fa, k_release_merge)) != cudaSuccess) return e;
+      merger_loaded = true;
+    }
+    // fork: the merger CTA runs concurrently with the scan on a second stream, joined back before return
+    e = cudaEventRecord(rel->fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(rel->stream, rel->fork, 0);
+    if (e != cudaSuccess) return e;
+    k_release_merge<<<1, kMergeMaxWarps * 32, 0, rel->stream>>>(a, G, ws.status);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    e = launch_scan_k(ix, a, G, s);
+    if (e == cudaSuccess) e = cudaEventRecord(rel->join, rel->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, rel->join, 0);
+    return e;
   }
+  return launch_scan_k(ix, a, G, s);
+}
+
+static cudaError_t launch_scan_k(const DeviceIndex& ix, const ScanArgs& a, int n_cta, cudaStream_t s) {
   if (ix.nbits == 4) {
     switch (ix.mpad) {
-      case 32: return launch_scan_t<32, 4>(a, ws.n_cta, s);
-      case 64: return launch_scan_t<64, 4>(a, ws.n_cta, s);
-      case 96: return launch_scan_t<96, 4>(a, ws.n_cta, s);
-      case 128: return launch_scan_t<128, 4>(a, ws.n_cta, s);
-      case 192: return launch_scan_t<192, 4>(a, ws.n_cta, s);
-      case 256: return launch_scan_t<256, 4>(a, ws.n_cta, s);
+      case 32: return launch_scan_t<32, 4>(a, n_cta, s);
+      case 64: return launch_scan_t<64, 4>(a, n_cta, s);
+      case 96: return launch_scan_t<96, 4>(a, n_cta, s);
+      case 128: return launch_scan_t<128, 4>(a, n_cta, s);
+      case 192: return launch_scan_t<192, 4>(a, n_cta, s);
+      case 256: return launch_scan_t<256, 4>(a, n_cta, s);
       default: return cudaErrorInvalidValue;
     }
   }
   switch (ix.mpad) {
-    case 32: return launch_scan_t<32, 8>(a, ws.n_cta, s);
-    case 64: return launch_scan_t<64, 8>(a, ws.n_cta, s);
-    case 96: return launch_scan_t<96, 8>(a, ws.n_cta, s);
-    case 128: return launch_scan_t<128, 8>(a, ws.n_cta, s);
+    case 32: return launch_scan_t<32, 8>(a, n_cta, s);
+    case 64: return launch_scan_t<64, 8>(a, n_cta, s);
+    case 96: return launch_scan_t<96, 8>(a, n_cta, s);
+    case 128: return launch_scan_t<128, 8>(a, n_cta, s);
     default: return cudaErrorInvalidValue;
   }
 }

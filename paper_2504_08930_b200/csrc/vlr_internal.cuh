@@ -24,6 +24,7 @@ constexpr int kScanThreads = VLR_SCAN_THREADS;  // 16 warps per scan CTA (tuning
 constexpr int kScanWarps = kScanThreads / kWarp;
 constexpr int kCandCap = 8192;     // K2 candidate list capacity per query (overflow -> rescan)
 constexpr int kRefineChunk = 1024; // K3 candidates per exact-refine flush
+constexpr int kReleaseWaves = 16; // NEXT-4: query waves of the release-mode scan
 constexpr int kMaxNprobe = 2048;   // cap on nprobe' (K3 sort buffer; the paper's operating point)
 constexpr int kLutPairBytes = 256 * 64 * 4;  // one [256 codes][64 sub-spaces] fp32 slab (8-bit codes)
 constexpr int kLutPairBytes4 = 16 * 64 * 4;  // one [16 codes][64 sub-spaces] fp32 slab (4-bit codes)
@@ -123,6 +124,8 @@ struct vlr_index {
   int64_t nsearch = 0;       // searches recorded while profiling
   int launches = 0;
   bool dead = false;  // NCCL failure
+  cudaStream_t rel_stream = nullptr;  // NEXT-4 merger stream + fork/join events (created on first use)
+  cudaEvent_t rel_fork = nullptr, rel_join = nullptr;
   std::string last_err;
 };
 
@@ -156,6 +159,8 @@ struct Release {               // NEXT-4 early per-query release (vlr_search_rel
   uint32_t epoch;
   int64_t* out_ids;
   float* out_dist;
+  cudaStream_t stream;         // the merger CTA's stream (forked from / joined to the search stream)
+  cudaEvent_t fork, join;
 };
 cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s,
                         const Release* rel = nullptr);

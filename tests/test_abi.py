@@ -121,3 +121,15 @@ def test_poll_ready_host_dispatcher():
     assert n == 1 and qs[0] == 0
     assert L.vlr_poll_ready(None, nq, epoch, seen.ctypes.data, qs.ctypes.data, None, nq, 0) == -1
     assert L.vlr_poll_ready(ready.ctypes.data, nq, epoch, seen.ctypes.data, qs.ctypes.data, None, 0, 0) == -1
+
+
+def test_wait_ready_host_dispatcher():
+    L = vlr.lib()
+    nq, epoch = 6, 3
+    ready = np.full(nq, epoch, np.uint32)
+    ts = np.zeros(nq, np.int64)
+    assert L.vlr_wait_ready(ready.ctypes.data, nq, epoch, ts.ctypes.data, 1000) == nq
+    assert np.all(ts > 0)
+    ready[4] = 0
+    assert L.vlr_wait_ready(ready.ctypes.data, nq, epoch, None, 2000) == nq - 1  # timeout: one missing
+    assert L.vlr_wait_ready(None, nq, epoch, None, 0) == -1
