@@ -520,69 +520,99 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
   return v;
 }
 
-constexpr unsigned long long kMerged = 1ull << 63;  // qdone[q] mark: q merged and released
-
-// the resident merger CTA (kMergeMaxWarps warps): G = the scan's grid size
-__global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanArgs a, int G, int32_t* status) {
-  __shared__ MergeSmem sm;
-  __shared__ int s_q;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nq = a.nq, np = a.np, Z = a.waves;
-  int lo = 0;  // queries < lo are merged (warp 0's view)
-#ifdef VLR_REL_DEBUG
-  if (threadIdx.x == 0) printf("merger start nq %d np %d Z %d G %d qdone0 %llu tot0 %lld\n", nq, np, Z, G,
-                               ld_acquire_gpu(a.qdone), (long long)(a.item_off[np] - a.item_off[0]));
-#endif
-  for (int done = 0; done < nq; ++done) {
-    if (warp == 0) {
-      int found = -1;
-      const unsigned long long t0 = globaltimer_ns();
-      for (uint32_t spin = 0;; ++spin) {
-        while (lo < nq && (ld_acquire_gpu(a.qdone + lo) & kMerged)) ++lo;
-        for (int base = lo; base < nq && found < 0; base += 32) {
-          const int q = base + lane;
-          bool ok = false;
-          if (q < nq) {
-            const unsigned long long v = ld_acquire_gpu(a.qdone + q);
-            ok = !(v & kMerged) && v == (unsigned long long)(a.item_off[(long long)(q + 1) * np] -
-                                                             a.item_off[(long long)q * np]);
-          }
-          const unsigned m = __ballot_sync(kFull, ok);
-          if (m) found = base + __ffs(m) - 1;
-        }
-        if (found >= 0) break;
-        __nanosleep(128);
-        if ((spin & 255u) == 255u && globaltimer_ns() - t0 > 4000000000ull) break;  // bounded: never hang
+// Warp merge of query q's partial lists (same result as K7: the k smallest
+// (dist, id) of the union, ids unique). The lists of CTAs cf.. of q's wave
+// (slot c + q + zoff, kScanWarps lists of k sorted entries each):
+//  A. the k smallest list heads give T0 (k distinct entries are <= T0);
+//  B. every list whose head is <= T0 (at most k plus ties) is offered whole.
+__device__ __forceinline__ void warp_merge_query(const ScanArgs& a, int q, int G, long long WL, long long WH,
+                                                 long long zoff, long long S, long long E, int lane, float& bd,
+                                                 long long& bid) {
+  const int k = a.k;
+  const long long W = WH - WL;
+  const long long* pidl = reinterpret_cast<const long long*>(a.pid);
+  float thr = CUDART_INF_F;
+  bd = CUDART_INF_F;
+  bid = -1;
+  if (E <= S) return;
+  auto cta_of = [&](long long g) {
+    const long long c = ((g - WL + 1) * G - 1) / W;
+    return (int)(c < G - 1 ? c : G - 1);
+  };
+  auto start = [&](int c) { return (long long)c * W / G; };
+  const int cf = cta_of(S);
+  const int nl = (cta_of(E - 1) - cf + 1) * kScanWarps;
+  const bool maybe_empty = W < G;
+  const long long base = (long long)(cf + q + zoff) * kScanWarps * k;
+  auto head_ok = [&](int li) { return !maybe_empty || start(cf + li / kScanWarps) != start(cf + li / kScanWarps + 1); };
+  for (int l0 = 0; l0 < nl; l0 += 32) {  // A
+    const int li = l0 + lane;
+    float d = CUDART_INF_F;
+    long long id = -1;
+    if (li < nl && head_ok(li)) {
+      d = __ldcg(a.pdist + base + (long long)li * k);
+      id = __ldcg(pidl + base + (long long)li * k);
+    }
+    offer32(bd, bid, thr, d, id, d < CUDART_INF_F && d <= thr, k, lane);
+  }
+  const float t0 = __shfl_sync(kFull, bd, k - 1);
+  bd = CUDART_INF_F;
+  bid = -1;
+  thr = CUDART_INF_F;
+  for (int l0 = 0; l0 < nl; l0 += 32) {  // B
+    const int li = l0 + lane;
+    float h = CUDART_INF_F;
+    if (li < nl && head_ok(li)) h = __ldcg(a.pdist + base + (long long)li * k);
+    unsigned rm = __ballot_sync(kFull, h < CUDART_INF_F && h <= t0);
+    while (rm) {
+      const int r = __ffs(rm) - 1;
+      rm &= rm - 1;
+      const long long o = base + (long long)(l0 + r) * k + lane;
+      float d = CUDART_INF_F;
+      long long id = -1;
+      if (lane < k) {
+        d = __ldcg(a.pdist + o);
+        id = __ldcg(pidl + o);
       }
-      if (lane == 0) {
-        s_q = found;
-        if (found < 0) atomicOr(status, 2);  // the host poll then times out with an error
+      list_offer(bd, bid, thr, d, id, k, lane);
+    }
+  }
+}
+
+// the resident merger CTA: warp w merges and releases queries w, w + nw, ...
+// in order, each as soon as the scan has finished it (qdone[q] == its groups);
+// G = the scan's grid size
+__global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanArgs a, int G, int32_t* status) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nq = a.nq, np = a.np, Z = a.waves;
+  for (int q = warp; q < nq; q += nw) {
+    const long long S = a.item_off[(long long)q * np], E = a.item_off[(long long)(q + 1) * np];
+    if (lane == 0) {
+      const unsigned long long t0 = globaltimer_ns();
+      for (uint32_t spin = 0; ld_acquire_gpu(a.qdone + q) != (unsigned long long)(E - S); ++spin) {
+        __nanosleep(64);
+        if ((spin & 1023u) == 1023u && globaltimer_ns() - t0 > 4000000000ull) {  // bounded: never hang
+          atomicOr(status, 2);  // the host wait then times out with an error
+          break;
+        }
       }
     }
-    __syncthreads();
-    const int q = s_q;
-#ifdef VLR_REL_DEBUG
-    if (threadIdx.x == 0 && (done < 2 || q < 0))
-      printf("merger done %d q %d qdone0 %llu\n", done, q, ld_acquire_gpu(a.qdone));
-#endif
-    if (q < 0) return;
+    __syncwarp();
     __threadfence();
-    // the wave of q and its group range (the scan's static split, k_scan)
-    int z = (int)(((long long)(q + 1) * Z - 1) / nq);
+    int z = (int)(((long long)(q + 1) * Z - 1) / nq);  // q's wave and its group range (k_scan's split)
     z = z < Z - 1 ? z : Z - 1;
     const long long WL = a.item_off[(long long)((long long)z * nq / Z) * np];
     const long long WH = a.item_off[(long long)((long long)(z + 1) * nq / Z) * np];
-    merge_query<true>(q, a.k, G, WL, WH, (long long)z * G, a.item_off[(long long)q * np],
-                      a.item_off[(long long)(q + 1) * np], a.pdist, a.pid, a.out_ids, a.out_dist, nullptr, sm);
-    if (warp == 0) {
-      __threadfence_system();  // row q (possibly in pinned host memory) before its flag
-      __syncwarp();
-      if (lane == 0) {
-        st_release_sys(a.ready + q, a.epoch);
-        atomicOr(a.qdone + q, kMerged);
-      }
+    float bd;
+    long long bid;
+    warp_merge_query(a, q, G, WL, WH, (long long)z * G, S, E, lane, bd, bid);
+    if (lane < a.k) {
+      a.out_ids[(size_t)q * a.k + lane] = bid;
+      a.out_dist[(size_t)q * a.k + lane] = bd;
     }
-    __syncthreads();
+    __threadfence_system();  // row q (possibly in pinned host memory) before its flag
+    __syncwarp();
+    if (lane == 0) st_release_sys(a.ready + q, a.epoch);
   }
 }
 

@@ -24,7 +24,7 @@ constexpr int kScanThreads = VLR_SCAN_THREADS;  // 16 warps per scan CTA (tuning
 constexpr int kScanWarps = kScanThreads / kWarp;
 constexpr int kCandCap = 8192;     // K2 candidate list capacity per query (overflow -> rescan)
 constexpr int kRefineChunk = 1024; // K3 candidates per exact-refine flush
-constexpr int kReleaseWaves = 16; // NEXT-4: query waves of the release-mode scan
+constexpr int kReleaseWaves = 8;  // NEXT-4: query waves of the release-mode scan
 constexpr int kMaxNprobe = 2048;   // cap on nprobe' (K3 sort buffer; the paper's operating point)
 constexpr int kLutPairBytes = 256 * 64 * 4;  // one [256 codes][64 sub-spaces] fp32 slab (8-bit codes)
 constexpr int kLutPairBytes4 = 16 * 64 * 4;  // one [16 codes][64 sub-spaces] fp32 slab (4-bit codes)
