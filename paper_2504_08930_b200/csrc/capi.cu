@@ -214,10 +214,15 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   ix.dsub = dsub;
   ix.nbits = D.nbits;
   ix.ksub = ksub;
-  ix.lut_pair_bytes = ksub * 64 * 4;
-  if (D.nbits == 8) {
-    ix.mpad = ((m + 31) / 32) * 32;
-  } else {  // scan instantiations for 4-bit codes: 32, 64, 96, 128, 192, 256 sub-spaces
+  {
+    const char* nib = getenv("VLR_PQ4_NIBBLE");  // 4-bit nibble-slot scan instead of pair tables (experiments)
+    ix.code_bits = (D.nbits == 4 && nib && atoi(nib) == 1) ? 4 : 8;
+  }
+  ix.code_m = (D.nbits == 4 && ix.code_bits == 8) ? (m + 1) / 2 : m;  // pair mode: one slot per packed byte
+  ix.lut_pair_bytes = (1 << ix.code_bits) * 64 * 4;
+  if (ix.code_bits == 8) {
+    ix.mpad = ((ix.code_m + 31) / 32) * 32;
+  } else {  // scan instantiations for 4-bit slots: 32, 64, 96, 128, 192, 256 sub-spaces
     const int sizes[] = {32, 64, 96, 128, 192, 256};
     for (int v : sizes)
       if (m <= v) { ix.mpad = v; break; }
@@ -277,7 +282,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   LTRY(dalloc(&ix.owner, (size_t)L));
   LTRY(dalloc(&ix.local, (size_t)L));
   LTRY(dalloc(&ix.gbase, (size_t)ix.n_local + 1));
-  LTRY(dalloc(&ix.codes, (size_t)ix.n_groups * 32 * (ix.mpad * ix.nbits / 8)));
+  LTRY(dalloc(&ix.codes, (size_t)ix.n_groups * 32 * (ix.mpad * ix.code_bits / 8)));
   LTRY(dalloc(&ix.bias, (size_t)ix.n_groups * 32));
   LTRY(dalloc(&ix.ids, (size_t)ix.n_groups * 32));
   LTRY(cudaMemcpyAsync(ix.centroids, D.centroids, sizeof(float) * L * d, cudaMemcpyHostToDevice, s));
@@ -362,7 +367,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
     return bail(VLR_ERR_DUPLICATE_ID);
   }
   ix.bytes = (int64_t)L * d * 4 + (int64_t)L * ix.d8 * 2 + L * 4 + (int64_t)ncb * 4 + 2LL * L * 4 + (ix.n_local + 1) * 8 +
-             ix.n_groups * 32 * (ix.mpad * ix.nbits / 8 + 4 + 8);
+             ix.n_groups * 32 * (ix.mpad * ix.code_bits / 8 + 4 + 8);
   // NCCL communicator (collective)
   if (cm.world > 1 && cm.nccl_unique_id) {
     ncclUniqueId uid;

@@ -8,8 +8,9 @@
 //          512-byte LDG.128 per chunk per warp; lane v's sub-codes are
 //          ROTATED: slot s = 32r + t holds sub-code j = 32r + (v ^ t) (0 for
 //          j >= m), the order the scan's conflict-free LUT gathers consume
-//          them in. A slot is a byte (8-bit codes) or a nibble (4-bit codes:
-//          slot s is the low nibble of byte s/2 for even s).
+//          them in. A slot is a byte (8-bit codes; 4-bit codes in pair
+//          mode: slot j' = packed byte j' = sub-codes 2j', 2j'+1) or a nibble
+//          (4-bit nibble mode: slot s is the low nibble of byte s/2 for even s).
 //   bias:  b_v = ||yhat_v||^2 + 2 <c_l, yhat_v> computed in fp64, rounded to
 //          fp32 (+inf for padding slots, so they never enter a top-k);
 //          ||yhat_v||^2 without residual codes, 0 for the inner-product
@@ -27,7 +28,8 @@ __device__ __forceinline__ uint32_t in_code(const uint8_t* row, int j, int nbits
   return nbits == 8 ? row[j] : (row[j >> 1] >> (4 * (j & 1))) & 15u;
 }
 
-__global__ void k_layout(int d, int m, int mpad, int dsub, int nbits, int metric, int by_residual, int n_local,
+__global__ void k_layout(int d, int m, int mpad, int dsub, int nbits, int code_m, int code_bits, int metric,
+                         int by_residual, int n_local,
                          long long n_slots,
                          const int64_t* __restrict__ gbase, const int64_t* __restrict__ vbase,
                          const int32_t* __restrict__ lglob, const uint8_t* __restrict__ scodes,
@@ -46,9 +48,9 @@ __global__ void k_layout(int d, int m, int mpad, int dsub, int nbits, int metric
     const long long pos = (grp - gbase[list]) * 32 + lane;
     const long long len = vbase[list + 1] - vbase[list];
     const int ksub = 1 << nbits;
-    const int nchunk = mpad * nbits / 128;  // 16-byte chunks per lane
+    const int nchunk = mpad * code_bits / 128;  // 16-byte chunks per lane
     const long long rowb = ((long long)m * nbits + 7) / 8;
-    uint4* gdst = reinterpret_cast<uint4*>(codes + grp * 32LL * (mpad * nbits / 8));
+    uint4* gdst = reinterpret_cast<uint4*>(codes + grp * 32LL * (mpad * code_bits / 8));
     if (pos < len) {
       const long long v = vbase[list] + pos;
       const uint8_t* src = scodes + v * rowb;
@@ -65,7 +67,8 @@ __global__ void k_layout(int d, int m, int mpad, int dsub, int nbits, int metric
       }
       bias[slot] = (float)b;
       ids[slot] = sids[v];
-      const int per_byte = 8 / nbits;  // slots per byte
+      // slots: sub-codes (8-bit codes, 4-bit nibble mode) or packed bytes (4-bit pair mode, code_m = ceil(m/2))
+      const int per_byte = 8 / code_bits;  // slots per byte
       for (int ch = 0; ch < nchunk; ++ch) {
         uint32_t w[4];
         for (int q = 0; q < 4; ++q) {
@@ -75,7 +78,7 @@ __global__ void k_layout(int d, int m, int mpad, int dsub, int nbits, int metric
             for (int h = 0; h < per_byte; ++h) {
               const int s = (ch * 16 + q * 4 + bb) * per_byte + h;  // slot
               const int j = 32 * (s >> 5) + (lane ^ (s & 31));
-              byte |= (j < m ? in_code(src, j, nbits) : 0u) << (nbits * h);
+              byte |= (j < code_m ? in_code(src, j, code_bits) : 0u) << (code_bits * h);
             }
             word |= byte << (8 * bb);
           }
@@ -98,7 +101,8 @@ cudaError_t launch_layout(const DeviceIndex& ix, const uint8_t* stage_codes, con
   const int threads = 256;
   long long blocks = (n_slots + threads - 1) / threads;
   if (blocks > 148 * 64) blocks = 148 * 64;
-  k_layout<<<(int)blocks, threads, 0, s>>>(ix.d, ix.m, ix.mpad, ix.dsub, ix.nbits, ix.metric, ix.by_residual,
+  k_layout<<<(int)blocks, threads, 0, s>>>(ix.d, ix.m, ix.mpad, ix.dsub, ix.nbits, ix.code_m, ix.code_bits,
+                                           ix.metric, ix.by_residual,
                                            ix.n_local, n_slots, ix.gbase, vbase, lglob, stage_codes, stage_ids,
                                            ix.centroids, ix.codebooks, ix.codes, ix.bias, ix.ids);
   return cudaGetLastError();

@@ -206,9 +206,44 @@ __global__ void __launch_bounds__(1024) k_lut16(const float* __restrict__ Q, int
   lut[(((size_t)q * npairs + pair) * 16 + c) * 64 + jj] = scale * t;
 }
 
+// 4-bit codes, PAIR mode (default; DESIGN.md §K6 4-bit): slot j' = packed byte
+// b of sub-codes 2j' (low nibble) and 2j'+1 (high nibble), looked up in a
+// 256-entry pair table LUT2_q[j'][b] = LUT_q[2j'][b & 15] + LUT_q[2j'+1][b >> 4]
+// (fp32; a missing sub-space 2j'+1 = m contributes 0). Same layout as the
+// 8-bit LUT ([pair of 64 slots][256][64]), so the 8-bit scan consumes it with
+// half the lookups of the nibble scan. One CTA per (64 slots, query): the 2 x
+// 16 x 64 sub-dots go to shared memory, then 256 x 64 sums are written.
+__global__ void __launch_bounds__(256) k_lut_pair(const float* __restrict__ Q, int d, int m, int dsub,
+                                                  const float* __restrict__ Y, int npairs, float scale,
+                                                  float* __restrict__ lut) {
+  __shared__ float s_t[2][16][64];
+  const int pair = blockIdx.x, q = blockIdx.y;
+  for (int i = threadIdx.x; i < 2 * 16 * 64; i += blockDim.x) {
+    const int jj = i & 63, c = (i >> 6) & 15, hf = i >> 10;
+    const int j = 2 * (pair * 64 + jj) + hf;
+    float t = 0.f;
+    if (j < m) {
+      const float* qv = Q + (size_t)q * d + (size_t)j * dsub;
+      const float* y = Y + ((size_t)j * 16 + c) * dsub;
+      for (int u = 0; u < dsub; ++u) t = fmaf(__ldg(qv + u), __ldg(y + u), t);
+    }
+    s_t[hf][c][jj] = scale * t;
+  }
+  __syncthreads();
+  float* out = lut + ((size_t)q * npairs + pair) * 256 * 64;
+  for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) {
+    const int jj = i & 63, c = i >> 6;
+    out[i] = s_t[0][c & 15][jj] + s_t[1][c >> 4][jj];
+  }
+}
+
 cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
   const float scale = ix.metric == 1 ? -1.f : -2.f;  // exact power-of-two scaling of the fp32 dot
+  if (ix.nbits == 4 && ix.code_bits == 8) {
+    k_lut_pair<<<dim3(ix.npairs, nq), 256, 0, s>>>(Q, ix.d, ix.m, ix.dsub, ix.codebooks, ix.npairs, scale, ws.lut);
+    return cudaGetLastError();
+  }
   if (ix.nbits == 4) {
     k_lut16<<<dim3(ix.npairs, nq), 1024, 0, s>>>(Q, ix.d, ix.m, ix.dsub, ix.codebooks, ix.npairs, scale, ws.lut);
     return cudaGetLastError();

@@ -821,7 +821,7 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
 }
 
 static cudaError_t launch_scan_k(const DeviceIndex& ix, const ScanArgs& a, int n_cta, cudaStream_t s) {
-  if (ix.nbits == 4) {
+  if (ix.code_bits == 4) {
     switch (ix.mpad) {
       case 32: return launch_scan_t<32, 4>(a, n_cta, s);
       case 64: return launch_scan_t<64, 4>(a, n_cta, s);

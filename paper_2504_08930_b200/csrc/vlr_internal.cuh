@@ -49,7 +49,11 @@ void set_error(const std::string& msg);
 struct DeviceIndex {
   int d = 0, d8 = 0, nlist = 0, m = 0, mpad = 0, npairs = 0, dsub = 0;
   int nbits = 8, ksub = 256;   // bits per sub-code (8, or 4: nibble-packed) and codewords per sub-space
-  int lut_pair_bytes = kLutPairBytes;  // LUT bytes per 64 sub-spaces (ksub * 64 * 4)
+  int lut_pair_bytes = kLutPairBytes;  // LUT bytes per 64 code slots (256 or 16 codes x 64 x 4)
+  // scan code slots: 8-bit codes and 4-bit PAIR mode (default for nbits 4: one slot = one packed byte =
+  // two sub-codes, looked up in a 256-entry pair table, DESIGN.md §K6 4-bit) have code_bits 8; the
+  // nibble mode (VLR_PQ4_NIBBLE=1 at load) has code_bits 4, one slot per sub-code
+  int code_bits = 8, code_m = 0;
   int rank = 0, world = 1, device = 0;
   int metric = 0;              // 0 squared L2, 1 inner product (distance = -<q, x>)
   int by_residual = 1;         // 1: codes encode x - c_l
@@ -70,7 +74,7 @@ struct DeviceIndex {
   int32_t n_local = 0;
   int64_t n_groups = 0, n_vec = 0;
   int64_t* gbase = nullptr;    // [n_local+1] first group of each local list
-  uint8_t* codes = nullptr;    // [n_groups][mpad*nbits/128 chunks][32 lanes][16 B], per-lane rotated
+  uint8_t* codes = nullptr;    // [n_groups][mpad*code_bits/128 chunks][32 lanes][16 B], per-lane rotated
   float* bias = nullptr;       // [n_groups*32] b_i = ||yhat||^2 + 2<c_l, yhat> (+inf for padding)
   int64_t* ids = nullptr;      // [n_groups*32] (-1 for padding)
   int64_t bytes = 0;

@@ -448,3 +448,36 @@ def test_pq4_m_variants(d, m, L):
     for npb, hh in ((8, None), (L, hot)):
         errs, g, o = run_parity(ix, Q, npb, 10, hot=hh)
         assert not errs, (d, m, L, errs)
+
+
+@pytest.fixture
+def pq4_nibble_mode(monkeypatch):
+    """4-bit nibble-slot scan (VLR_PQ4_NIBBLE=1, read at vlr_load_index) instead of the default pair tables."""
+    monkeypatch.setenv("VLR_PQ4_NIBBLE", "1")
+
+
+@pytest.mark.parametrize("d,m,L", [(32, 8, 50), (40, 20, 17), (64, 64, 40), (192, 96, 33), (128, 128, 64),
+                                   (144, 144, 30), (192, 192, 40), (256, 256, 70)])
+def test_pq4_nibble_mode_m_variants(pq4_nibble_mode, d, m, L):
+    """The nibble-slot 4-bit scan (every instantiation) stays parity-green next to the default pair mode."""
+    ix = datagen.make_index(4000, d, L, m, seed=d + m, nbits=4)
+    Q = datagen.make_queries(4000, d, L, 20, seed=d + m, stream=2)
+    for npb, hh in ((8, None), (L, np.arange(0, L, 2))):
+        errs, g, o = run_parity(ix, Q, npb, 10, hot=hh)
+        assert not errs, (d, m, L, errs)
+
+
+def test_pq4_pair_and_nibble_modes_agree(c1_queries, monkeypatch):
+    """Pair tables (LUT2[j'][b] = LUT[2j'][b&15] + LUT[2j'+1][b>>4]) and nibble
+    slots sum the same terms in different fp32 orders: identical probes and
+    masks, distances within the parity tolerance of each other, both green."""
+    c = datagen.CONFIGS["C1"]
+    ix = datagen.make_index(c["N"], c["d"], c["nlist"], 64, nbits=4)
+    errs, gp, _ = run_parity(ix, c1_queries, c["nprobe"], c["k"])
+    assert not errs, errs
+    monkeypatch.setenv("VLR_PQ4_NIBBLE", "1")
+    errs, gn, _ = run_parity(ix, c1_queries, c["nprobe"], c["k"])
+    assert not errs, errs
+    assert np.array_equal(gp["probes"], gn["probes"]) and np.array_equal(gp["miss"], gn["miss"])
+    tol = 1e-5 * np.maximum(np.abs(gn["dist"]), 0.25)
+    assert np.all(np.abs(gp["dist"] - gn["dist"]) <= 2 * tol)
