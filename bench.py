@@ -414,6 +414,11 @@ def main():
     release = None
     if world == 1 and not a.ncu:
         release = release_leg(a, c, h, Qdev, outs, K)
+    # ---- NEXT-2: GPU access profile of a calibration stream -> per-rank work share of the paper's deal vs
+    # the traffic-aware deal at G = 2/4/8 (over the timed batches' probes), and a full-shard refresh time
+    shards = None
+    if world == 1 and not a.ncu:
+        shards = shard_leg(a, c, h, ix, hot, outs, K)
     # ---- oracle: cpu_baseline + sampled full-size parity (rank 0, N = 1)
     cpu = None
     par = None
@@ -475,6 +480,7 @@ def main():
             "residency": residency,
             "e2e": e2e, "clocks": clk, "cpu_baseline": cpu, "parity_sample": par, "recall": recall,
             "release": release,
+            "shards": shards,
             "gen_s": round(gen_s, 1), "load_s": round(load_s, 1),
         }
         if counts is not None:
@@ -486,6 +492,44 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def shard_leg(a, c, h, ix, hot, outs, K):
+    import torch
+    import datagen
+    import paper_2504_08930_b200 as vlr
+    B = outs[0][0].shape[0]
+    ncal = 4
+    Qc = torch.from_numpy(datagen.make_queries(c["N"], c["d"], c["nlist"], ncal * B, seed=a.seed, stream=1,
+                                               alpha=c["alpha"], device="cuda")).cuda().reshape(ncal, B, c["d"])
+    counts = torch.zeros(c["nlist"], dtype=torch.int64, device="cuda")
+    for i in range(ncal):
+        _, _, _, prb = h.search(Qc[i].contiguous(), c["nprobe"], K, sync=True)
+        h.access_counts(prb, counts)
+    counts = counts.cpu().numpy()
+    hot_ids = np.arange(c["nlist"], dtype=np.int32) if hot is None else np.asarray(hot, np.int32)
+    sizes = ix.list_sizes.astype(np.float64)
+    probes = np.concatenate([o[3].cpu().numpy().reshape(-1) for o in outs])
+    per_list = np.bincount(probes, minlength=c["nlist"]).astype(np.float64) * sizes  # vectors scanned per list
+    bal = {}
+    for G in (2, 4, 8):
+        row = {}
+        for name, cnt in (("paper_round_robin", None), ("traffic_aware", counts)):
+            own = np.full(c["nlist"], -1, np.int64)
+            own[hot_ids] = vlr.deal_owners(ix.list_offsets, hot_ids, G, counts=cnt)
+            load = np.bincount(own[own >= 0], weights=per_list[own >= 0], minlength=G)
+            row[name] = float(load.max() / load.mean())
+        bal[str(G)] = row
+    t = time.perf_counter()
+    h.update_hot_arrays(ix, hot=hot)
+    reload_s = time.perf_counter() - t
+    return {"work_share_max_over_mean": bal,
+            "how": "vectors each rank would scan for the timed batches' probes; owners from vlr_deal_owners "
+                   "(paper: size-descending round-robin, P:339; traffic-aware: LPT on size x access count of a "
+                   "%d-query calibration stream profiled on the GPU with vlr_access_counts)" % (ncal * B),
+            "refresh_s": reload_s,
+            "refresh_how": "vlr_update_hot of this rank's whole shard (host arrays -> new device residency, swap; "
+                           "the paper reports <10 s per shard, P:421)"}
 
 
 def release_leg(a, c, h, Qdev, outs, K):

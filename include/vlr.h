@@ -217,6 +217,33 @@ vlr_status vlr_merge_partials(const int64_t* d_part_ids, const float* d_part_dis
 vlr_status vlr_access_counts(const vlr_index* idx, const int32_t* d_probes, int64_t n, int64_t* d_counts,
                              void* stream);
 
+/* NEXT-2 index splitter: owner rank of each hot list, written to
+ * out_owner[i] for hot[i] (host arrays; list_offsets [nlist+1] as in
+ * vlr_index_desc). counts == NULL: the paper's deal -- size descending, ties
+ * by ascending cluster id, round-robin over `world` ranks (the default
+ * of vlr_load_index). counts [nlist] (access counts of a calibration stream,
+ * e.g. vlr_access_counts): traffic-aware deal -- load = size x count,
+ * descending, each list to the least-loaded rank (greedy LPT). Pass the
+ * result as vlr_index_desc.hot_owner. Host only. INVALID_ARG /
+ * UNKNOWN_CLUSTER as vlr_load_index. */
+vlr_status vlr_deal_owners(const int64_t* list_offsets, int32_t nlist, const int64_t* counts, const int32_t* hot,
+                           int32_t n_hot, int32_t world, int32_t* out_owner);
+
+/* NEXT-2 shard refresh (P:416-425 [§IV.D]: re-profile, re-partition, reload
+ * the shard; "<10 s per shard"): rebuild this handle's resident lists
+ * for a new hot set / owner assignment in `desc` (same d, nlist, m, nbits,
+ * metric, by_residual as the handle, else INVALID_ARG; all arrays host,
+ * copied). The new residency is built in fresh device memory while the
+ * current one keeps serving: searches issued from other host threads
+ * meanwhile run on the old residency. Then, after the device has finished
+ * the work already enqueued, the handle switches atomically (w.r.t. this
+ * library's calls) and the old residency is freed. Peak device memory = old
+ * + new shard. Synchronous; not collective (with world > 1, each rank
+ * refreshes its own shard and the caller keeps the owner tables consistent,
+ * e.g. by passing the same desc on every rank). Errors as vlr_load_index; on
+ * error the handle is unchanged. */
+vlr_status vlr_update_hot(vlr_index* idx, const vlr_index_desc* desc);
+
 /* Device bytes held by the handle, number of resident lists and vectors on this rank. */
 vlr_status vlr_index_info(const vlr_index* idx, int64_t* bytes_on_device, int32_t* n_owned_lists,
                           int64_t* n_owned_vectors);

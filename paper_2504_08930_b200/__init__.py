@@ -22,7 +22,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "NONFINITE", 4: "UNKN
 
 # every symbol include/vlr.h declares (checked by tests/test_abi.py)
 EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_search_release_async",
-           "vlr_poll_ready", "vlr_wait_ready", "vlr_reserve",
+           "vlr_poll_ready", "vlr_wait_ready", "vlr_reserve", "vlr_deal_owners", "vlr_update_hot",
            "vlr_merge_partials", "vlr_access_counts", "vlr_index_info", "vlr_index_owners", "vlr_set_profiling", "vlr_stage_times",
            "vlr_last_launch_count", "vlr_nccl_unique_id", "vlr_index_free", "vlr_last_error", "vlr_version"]
 
@@ -66,6 +66,8 @@ def lib():
             "vlr_search_host": [P, P, I32, I32, I32, P, P, P, P, P],
             "vlr_search_release_async": [P, P, I32, I32, I32, P, P, P, P, P, ctypes.c_uint32, P],
             "vlr_reserve": [P, I32, I32, I32],
+            "vlr_deal_owners": [P, I32, P, P, I32, I32, P],
+            "vlr_update_hot": [P, P],
             "vlr_merge_partials": [P, P, I32, I32, I32, P, P, P],
             "vlr_index_info": [P, P, P, P],
             "vlr_access_counts": [P, P, I64, P, P],
@@ -150,6 +152,28 @@ class Index:
         h = ctypes.c_void_p()
         _check(lib().vlr_load_index(ctypes.byref(desc), ctypes.byref(comm), ctypes.byref(h)))
         return cls(h, d, nlist, rank, world, device)
+
+    def update_hot(self, centroids, codebooks, list_offsets, ids, codes, hot=None, hot_owner=None, *, nbits=8,
+                   metric=0, by_residual=1):
+        """vlr_update_hot (NEXT-2 shard refresh): rebuild the resident lists for
+        a new hot set while the current residency keeps serving."""
+        C = _host(centroids, np.float32)
+        Y = _host(codebooks, np.float32)
+        offs = _host(list_offsets, np.int64)
+        idv = _host(ids, np.int64)
+        cd = _host(codes, np.uint8)
+        nlist, d = C.shape
+        m = Y.shape[0] if Y.ndim == 3 else int(cd.shape[1])
+        hotv = np.arange(nlist, dtype=np.int32) if hot is None else _host(hot, np.int32).reshape(-1)
+        own = None if hot_owner is None else _host(hot_owner, np.int32).reshape(-1)
+        desc = _Desc(d, nlist, m, nbits, metric, by_residual, _ptr(C), _ptr(Y), _ptr(offs), _ptr(idv), _ptr(cd),
+                     _ptr(hotv), int(hotv.size), _ptr(own))
+        _check(lib().vlr_update_hot(self._h, ctypes.byref(desc)))
+
+    def update_hot_arrays(self, ix, hot=None, hot_owner=None):
+        self.update_hot(ix.centroids, ix.codebooks, ix.list_offsets, ix.ids, ix.codes, hot=hot, hot_owner=hot_owner,
+                        nbits=int(getattr(ix, "nbits", 8)), metric=int(getattr(ix, "metric", 0)),
+                        by_residual=int(getattr(ix, "by_residual", 1)))
 
     @classmethod
     def from_arrays(cls, ix, hot=None, **kw):
@@ -314,6 +338,19 @@ class _Stamps(np.ndarray):
 
     def __array_finalize__(self, obj):
         self.t0 = getattr(obj, "t0", 0)
+
+
+def deal_owners(list_offsets, hot, world: int, counts=None) -> np.ndarray:
+    """vlr_deal_owners: owner rank per hot list -- the paper's size-descending
+    round-robin (counts=None) or the traffic-aware LPT deal (counts =
+    per-cluster access counts, NEXT-2)."""
+    offs = _host(list_offsets, np.int64)
+    hotv = _host(hot, np.int32).reshape(-1)
+    cnt = None if counts is None else _host(counts, np.int64).reshape(-1)
+    out = np.empty(hotv.size, np.int32)
+    _check(lib().vlr_deal_owners(offs.ctypes.data, int(offs.size - 1), cnt.ctypes.data if cnt is not None else None,
+                                 _ptr(hotv), int(hotv.size), int(world), _ptr(out)))
+    return out
 
 
 def merge_partials(part_ids, part_dist, stream=None):

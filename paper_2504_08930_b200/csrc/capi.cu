@@ -118,11 +118,92 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   return VLR_OK;
 }
 
+// Index splitter. Without counts: the paper's deal -- hot lists
+// sorted by size descending (ties: ascending cluster id), dealt round-robin
+// over ranks. With counts (NEXT-2 traffic-aware deal):
+// load_l = size_l * count_l (the bytes a rank scans for list l per profiled
+// stream), lists sorted by load descending (ties: size descending, then id),
+// each given to the rank with the least load so far (ties: lowest rank) --
+// greedy LPT, which bounds the max rank load by 4/3 of the optimum.
+static void deal(const int64_t* offs, const int64_t* counts, const int32_t* hot, int32_t n_hot, int32_t world,
+                 int32_t* out_owner) {
+  std::vector<int32_t> ord((size_t)n_hot);
+  std::iota(ord.begin(), ord.end(), 0);
+  auto size = [&](int32_t i) { return offs[hot[i] + 1] - offs[hot[i]]; };
+  if (!counts) {
+    std::sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
+      return size(a) != size(b) ? size(a) > size(b) : hot[a] < hot[b];
+    });
+    for (size_t r = 0; r < ord.size(); ++r) out_owner[ord[r]] = (int32_t)(r % world);
+    return;
+  }
+  auto load = [&](int32_t i) { return (double)size(i) * (double)counts[hot[i]]; };
+  std::sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
+    if (load(a) != load(b)) return load(a) > load(b);
+    return size(a) != size(b) ? size(a) > size(b) : hot[a] < hot[b];
+  });
+  std::vector<double> acc((size_t)world, 0.0);
+  for (int32_t i : ord) {
+    int32_t best = 0;
+    for (int32_t r = 1; r < world; ++r)
+      if (acc[r] < acc[best]) best = r;
+    out_owner[i] = best;
+    acc[best] += load(i);
+  }
+}
+
 }  // namespace vlr
 
 using namespace vlr;
 
 extern "C" {
+
+vlr_status vlr_deal_owners(const int64_t* list_offsets, int32_t nlist, const int64_t* counts, const int32_t* hot,
+                           int32_t n_hot, int32_t world, int32_t* out_owner) {
+  if (!list_offsets || nlist < 1 || n_hot < 0 || world < 1 || (n_hot > 0 && (!hot || !out_owner)))
+    return fail(VLR_ERR_INVALID_ARG, "vlr_deal_owners: bad args");
+  std::vector<uint8_t> seen((size_t)nlist, 0);
+  for (int32_t i = 0; i < n_hot; ++i) {
+    if (hot[i] < 0 || hot[i] >= nlist) return fail(VLR_ERR_UNKNOWN_CLUSTER, "hot cluster id out of range");
+    if (seen[hot[i]]++) return fail(VLR_ERR_UNKNOWN_CLUSTER, "hot cluster listed twice");
+  }
+  if (counts)
+    for (int32_t l = 0; l < nlist; ++l)
+      if (counts[l] < 0) return fail(VLR_ERR_INVALID_ARG, "negative access count");
+  deal(list_offsets, counts, hot, n_hot, world, out_owner);
+  return VLR_OK;
+}
+
+vlr_status vlr_update_hot(vlr_index* h, const vlr_index_desc* desc) {
+  if (!h || !desc) return fail(VLR_ERR_INVALID_ARG, "vlr_update_hot: null handle/desc");
+  const DeviceIndex& cur = h->ix;
+  if (desc->d != cur.d || desc->nlist != cur.nlist || desc->m != cur.m || desc->nbits != cur.nbits ||
+      desc->metric != cur.metric || desc->by_residual != cur.by_residual)
+    return fail(VLR_ERR_INVALID_ARG, "vlr_update_hot: index shape/variant differs from the handle's");
+  // build the new residency as a separate shard-only handle (no communicator), while the
+  // current one keeps serving (searches on other host threads take h->mu only to enqueue)
+  vlr_comm_desc cm{cur.rank, cur.world, cur.device, nullptr};
+  vlr_index* n = nullptr;
+  vlr_status st = vlr_load_index(desc, &cm, &n);
+  if (st != VLR_OK) return st;
+  {
+    std::lock_guard<std::mutex> lock(h->mu);
+    VLR_CUDA_TRY(cudaSetDevice(cur.device));
+    VLR_CUDA_TRY(cudaDeviceSynchronize());  // searches already enqueued on the old residency finish first
+    DeviceIndex old = h->ix;
+    n->ix.nccl = old.nccl;  // the communicator and the handle's mode stay
+    n->ix.shard_only = old.shard_only;
+    old.nccl = nullptr;
+    if (n->ix.mpad != old.mpad || n->ix.npairs != old.npairs || n->ix.lut_pair_bytes != old.lut_pair_bytes) {
+      free_ws(h->ws);  // scan/LUT shapes changed (e.g. a different 4-bit mode): size the workspace again
+    }
+    h->ix = n->ix;
+    n->ix = old;  // freed with the temporary handle
+  }
+  vlr_index_free(n);
+  return VLR_OK;
+}
+
 
 const char* vlr_last_error(void) { return g_err.c_str(); }
 int32_t vlr_version(void) { return (VLR_VERSION_MAJOR << 16) | VLR_VERSION_MINOR; }
@@ -185,13 +266,9 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
         owner[hot[i]] = D.hot_owner[i];
       }
     } else {
-      // size descending, ties by ascending cluster id, round-robin over ranks
-      std::vector<int32_t> ord(hot);
-      std::sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
-        const int64_t sa = D.list_offsets[a + 1] - D.list_offsets[a], sb = D.list_offsets[b + 1] - D.list_offsets[b];
-        return sa != sb ? sa > sb : a < b;
-      });
-      for (size_t i = 0; i < ord.size(); ++i) owner[ord[i]] = (int32_t)(i % cm.world);
+      std::vector<int32_t> own((size_t)D.n_hot);
+      deal(D.list_offsets, nullptr, hot.data(), D.n_hot, cm.world, own.data());
+      for (int i = 0; i < D.n_hot; ++i) owner[hot[i]] = own[i];
     }
   }
   // device
@@ -419,6 +496,7 @@ static vlr_status search_impl(vlr_index* h, const float* Q, int32_t nq, int32_t 
                               float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream,
                               const Release* rel) {
   if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  std::lock_guard<std::mutex> lock(h->mu);
   if (h->dead) return fail(VLR_ERR_NCCL, "index unusable after an NCCL failure");
   if (nq < 0 || nprobe < 1 || k < 1) return fail(VLR_ERR_INVALID_ARG, "nq < 0, nprobe < 1 or k < 1");
   if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32 (v1)");

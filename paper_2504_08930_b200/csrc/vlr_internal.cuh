@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -128,6 +129,7 @@ struct vlr_index {
   int64_t nsearch = 0;       // searches recorded while profiling
   int launches = 0;
   bool dead = false;  // NCCL failure
+  std::mutex mu;  // held while a search is enqueued and while vlr_update_hot swaps the residency
   cudaStream_t rel_stream = nullptr;  // NEXT-4 merger stream + fork/join events (created on first use)
   cudaEvent_t rel_fork = nullptr, rel_join = nullptr;
   std::string last_err;

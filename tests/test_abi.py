@@ -133,3 +133,49 @@ def test_wait_ready_host_dispatcher():
     ready[4] = 0
     assert L.vlr_wait_ready(ready.ctypes.data, nq, epoch, None, 2000) == nq - 1  # timeout: one missing
     assert L.vlr_wait_ready(None, nq, epoch, None, 0) == -1
+
+
+def _rr_reference(offs, hot, world):
+    sizes = np.diff(offs)
+    order = sorted(range(len(hot)), key=lambda i: (-int(sizes[hot[i]]), int(hot[i])))
+    own = np.empty(len(hot), np.int32)
+    for r, i in enumerate(order):
+        own[i] = r % world
+    return own
+
+
+def test_deal_owners_round_robin_and_traffic_lpt():
+    """vlr_deal_owners (NEXT-2 splitter): counts=NULL is the paper's
+    size-descending round-robin; with counts, the greedy LPT deal by
+    size x count replays step by step and balances Zipf traffic better."""
+    rng = np.random.default_rng(4)
+    nlist = 400
+    sizes = rng.integers(0, 300, nlist)
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    hot = rng.permutation(nlist)[:250].astype(np.int32)
+    counts = (1e5 / np.arange(1, nlist + 1) ** 1.1)[rng.permutation(nlist)].astype(np.int64)
+    for world in (1, 2, 3, 8):
+        own = vlr.deal_owners(offs, hot, world)
+        assert np.array_equal(own, _rr_reference(offs, hot, world))
+        lpt = vlr.deal_owners(offs, hot, world, counts=counts)
+        load = sizes[hot].astype(np.float64) * counts[hot]
+        # replay the greedy: descending load (ties: size desc, id), each to the least-loaded rank
+        order = sorted(range(len(hot)), key=lambda i: (-load[i], -int(sizes[hot[i]]), int(hot[i])))
+        acc = np.zeros(world)
+        for i in order:
+            r = int(np.argmin(acc))
+            assert lpt[i] == r
+            acc[r] += load[i]
+        rr = np.bincount(own, weights=load, minlength=world)
+        assert acc.max() <= rr.max() + 1e-9
+        assert acc.max() <= load.sum() / world + load.max() + 1e-9  # list-scheduling bound
+    assert vlr.deal_owners(offs, np.zeros(0, np.int32), 4).size == 0
+    with pytest.raises(vlr.VlrError) as e:
+        vlr.deal_owners(offs, np.array([1, 1], np.int32), 2)
+    assert e.value.name == "UNKNOWN_CLUSTER"
+    with pytest.raises(vlr.VlrError) as e:
+        vlr.deal_owners(offs, np.array([nlist], np.int32), 2)
+    assert e.value.name == "UNKNOWN_CLUSTER"
+    with pytest.raises(vlr.VlrError) as e:
+        vlr.deal_owners(offs, hot, 0)
+    assert e.value.name == "INVALID_ARG"

@@ -481,3 +481,79 @@ def test_pq4_pair_and_nibble_modes_agree(c1_queries, monkeypatch):
     assert np.array_equal(gp["probes"], gn["probes"]) and np.array_equal(gp["miss"], gn["miss"])
     tol = 1e-5 * np.maximum(np.abs(gn["dist"]), 0.25)
     assert np.all(np.abs(gp["dist"] - gn["dist"]) <= 2 * tol)
+
+
+def test_update_hot_refresh_equals_fresh_load(c1_index, c1_queries):
+    """NEXT-2 shard refresh: after vlr_update_hot to a new hot set
+    the handle answers exactly like a handle freshly loaded with that set
+    (bitwise), and the oracle agrees; a mismatched index is refused and leaves
+    the handle unchanged."""
+    import threading
+    c = datagen.CONFIGS["C1"]
+    ix, Q = c1_index, c1_queries
+    rng = np.random.default_rng(5)
+    hot_a = np.sort(rng.choice(ix.nlist, ix.nlist // 3, replace=False))
+    hot_b = np.sort(rng.choice(ix.nlist, ix.nlist // 2, replace=False))
+    h = vlr.Index.from_arrays(ix, hot=hot_a)
+    ga = gpu_search(h, Q, c["nprobe"], c["k"])
+    # serve from another thread while the refresh builds
+    stop, errs_bg = threading.Event(), []
+    Qd = torch.from_numpy(Q).cuda()
+
+    def serve():
+        s = torch.cuda.Stream()
+        try:
+            while not stop.is_set():
+                with torch.cuda.stream(s):
+                    h.search(Qd, c["nprobe"], c["k"], stream=s, sync=True)
+        except Exception as e:  # pragma: no cover
+            errs_bg.append(e)
+    t = threading.Thread(target=serve)
+    t.start()
+    h.update_hot_arrays(ix, hot=hot_b)
+    stop.set()
+    t.join()
+    assert not errs_bg, errs_bg
+    gb = gpu_search(h, Q, c["nprobe"], c["k"])
+    f = vlr.Index.from_arrays(ix, hot=hot_b)
+    gf = gpu_search(f, Q, c["nprobe"], c["k"])
+    f.close()
+    for key in gf:
+        assert np.array_equal(gb[key], gf[key]), key
+    o = oracle.search(ix, Q, c["nprobe"], c["k"], hot=hot_b)
+    assert not check(ix, Q, gb, o, hot=hot_b, idmap=oracle.IdMap(ix))
+    assert not np.array_equal(ga["miss"], gb["miss"])
+    other = datagen.make_index(20_000, 64, 128, 16, seed=3)
+    with pytest.raises(vlr.VlrError) as e:
+        h.update_hot_arrays(other)
+    assert e.value.name == "INVALID_ARG"
+    gb2 = gpu_search(h, Q, c["nprobe"], c["k"])
+    assert np.array_equal(gb2["ids"], gb["ids"])
+    h.close()
+
+
+def test_traffic_aware_deal_shards_equal_monolithic(c1_index, c1_queries):
+    """A traffic-aware owner assignment (vlr_deal_owners with access counts)
+    shards the hot lists differently but the merged shard results are bitwise
+    the single-GPU result (R5)."""
+    c = datagen.CONFIGS["C1"]
+    Qc = datagen.make_queries(c["N"], c["d"], c["nlist"], 1000, stream=1, alpha=1.2)
+    counts = datagen.access_counts(c1_index.centroids, Qc, c["nprobe"])
+    hot = np.arange(c1_index.nlist, dtype=np.int32)
+    G = 4
+    own = vlr.deal_owners(c1_index.list_offsets, hot, G, counts=counts)
+    assert not np.array_equal(own, vlr.deal_owners(c1_index.list_offsets, hot, G))
+    h = vlr.Index.from_arrays(c1_index)
+    a = gpu_search(h, c1_queries, c["nprobe"], c["k"])
+    h.close()
+    Qd = torch.from_numpy(c1_queries).cuda()
+    pi, pd = [], []
+    for r in range(G):
+        hs = vlr.Index.from_arrays(c1_index, hot=hot, hot_owner=own, rank=r, world=G)
+        assert np.array_equal(hs.owners(), own)
+        ids, dist, _, _ = hs.search(Qd, c["nprobe"], c["k"], sync=True)
+        pi.append(ids)
+        pd.append(dist)
+        hs.close()
+    mi, md = vlr.merge_partials(torch.stack(pi), torch.stack(pd))
+    assert np.array_equal(mi.cpu().numpy(), a["ids"]) and np.array_equal(md.cpu().numpy(), a["dist"])
