@@ -499,7 +499,7 @@ def shard_leg(a, c, h, ix, hot, outs, K):
     import datagen
     import paper_2504_08930_b200 as vlr
     B = outs[0][0].shape[0]
-    ncal = 4
+    ncal = 16
     Qc = torch.from_numpy(datagen.make_queries(c["N"], c["d"], c["nlist"], ncal * B, seed=a.seed, stream=1,
                                                alpha=c["alpha"], device="cuda")).cuda().reshape(ncal, B, c["d"])
     counts = torch.zeros(c["nlist"], dtype=torch.int64, device="cuda")

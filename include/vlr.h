@@ -222,7 +222,7 @@ vlr_status vlr_access_counts(const vlr_index* idx, const int32_t* d_probes, int6
  * vlr_index_desc). counts == NULL: the paper's deal -- size descending, ties
  * by ascending cluster id, round-robin over `world` ranks (the default
  * of vlr_load_index). counts [nlist] (access counts of a calibration stream,
- * e.g. vlr_access_counts): traffic-aware deal -- load = size x count,
+ * e.g. vlr_access_counts): traffic-aware deal -- load = size x (count + 1),
  * descending, each list to the least-loaded rank (greedy LPT). Pass the
  * result as vlr_index_desc.hot_owner. Host only. INVALID_ARG /
  * UNKNOWN_CLUSTER as vlr_load_index. */

@@ -121,8 +121,8 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
 // Index splitter. Without counts: the paper's deal -- hot lists
 // sorted by size descending (ties: ascending cluster id), dealt round-robin
 // over ranks. With counts (NEXT-2 traffic-aware deal):
-// load_l = size_l * count_l (the bytes a rank scans for list l per profiled
-// stream), lists sorted by load descending (ties: size descending, then id),
+// load_l = size_l * (count_l + 1) (the vectors a rank scans for list l per
+// profiled stream, Laplace-smoothed), lists sorted by load descending (ties: size descending, then id),
 // each given to the rank with the least load so far (ties: lowest rank) --
 // greedy LPT, which bounds the max rank load by 4/3 of the optimum.
 static void deal(const int64_t* offs, const int64_t* counts, const int32_t* hot, int32_t n_hot, int32_t world,
@@ -137,7 +137,9 @@ static void deal(const int64_t* offs, const int64_t* counts, const int32_t* hot,
     for (size_t r = 0; r < ord.size(); ++r) out_owner[ord[r]] = (int32_t)(r % world);
     return;
   }
-  auto load = [&](int32_t i) { return (double)size(i) * (double)counts[hot[i]]; };
+  // +1: Laplace smoothing, so lists the calibration stream never probed still carry their size
+  // (with a raw count of 0 they would all pile onto one rank: adding 0 never changes the least-loaded rank)
+  auto load = [&](int32_t i) { return (double)size(i) * ((double)counts[hot[i]] + 1.0); };
   std::sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
     if (load(a) != load(b)) return load(a) > load(b);
     return size(a) != size(b) ? size(a) > size(b) : hot[a] < hot[b];

@@ -147,7 +147,8 @@ def _rr_reference(offs, hot, world):
 def test_deal_owners_round_robin_and_traffic_lpt():
     """vlr_deal_owners (NEXT-2 splitter): counts=NULL is the paper's
     size-descending round-robin; with counts, the greedy LPT deal by
-    size x count replays step by step and balances Zipf traffic better."""
+    size x (count + 1) replays step by step and balances the profiled traffic
+    no worse than round-robin."""
     rng = np.random.default_rng(4)
     nlist = 400
     sizes = rng.integers(0, 300, nlist)
@@ -158,7 +159,7 @@ def test_deal_owners_round_robin_and_traffic_lpt():
         own = vlr.deal_owners(offs, hot, world)
         assert np.array_equal(own, _rr_reference(offs, hot, world))
         lpt = vlr.deal_owners(offs, hot, world, counts=counts)
-        load = sizes[hot].astype(np.float64) * counts[hot]
+        load = sizes[hot].astype(np.float64) * (counts[hot] + 1.0)
         # replay the greedy: descending load (ties: size desc, id), each to the least-loaded rank
         order = sorted(range(len(hot)), key=lambda i: (-load[i], -int(sizes[hot[i]]), int(hot[i])))
         acc = np.zeros(world)
