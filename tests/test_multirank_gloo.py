@@ -69,6 +69,34 @@ def _worker(rank, world, port, out_q):
         cnt = torch.tensor([len(mine)])
         tot = [torch.zeros_like(cnt) for _ in range(world)]
         dist.all_gather(tot, cnt)
+        # the library's deal (vlr_deal_owners, host only) is the same round-robin deal
+        import paper_2504_08930_b200 as vlr
+        ok = ok and np.array_equal(vlr.deal_owners(full.list_offsets, hot, world), own[hot])
+        # NEXT-2 distributed profiling: each rank counts the probes of its half of a calibration
+        # stream, the counts are summed across ranks, and every rank derives the same
+        # traffic-aware deal; the merged partials over that deal still equal the monolithic search
+        Qc = datagen.make_queries(N, d, L, 200, seed=21, stream=1)
+        half = Qc[rank::world]
+        pr, _ = oracle.coarse(half, full.centroids, npb)
+        cnt_l = torch.from_numpy(np.bincount(pr.reshape(-1), minlength=L).astype(np.int64))
+        dist.all_reduce(cnt_l, op=dist.ReduceOp.SUM)
+        own_t = torch.from_numpy(vlr.deal_owners(full.list_offsets, hot, world, counts=cnt_l.numpy()).astype(np.int64))
+        go = [torch.empty_like(own_t) for _ in range(world)]
+        dist.all_gather(go, own_t)
+        ok = ok and all(torch.equal(g, own_t) for g in go)
+        mine_t = hot[own_t.numpy() == rank]
+        part = oracle.search(full, Q, npb, k, hot=mine_t, nthreads=2)
+        ids = torch.from_numpy(part["ids"].copy())
+        dd = torch.from_numpy(part["dist"].copy())
+        dist.all_gather(gi, ids)
+        dist.all_gather(gd, dd)
+        ai = torch.stack(gi).numpy()
+        ad = torch.stack(gd).numpy()
+        for q in range(len(Q)):
+            i = ai[:, q].reshape(-1)
+            dv = ad[:, q].reshape(-1)
+            o = np.lexsort((np.where(i < 0, np.iinfo(np.int64).max, i), dv))[:k]
+            ok = ok and np.array_equal(i[o], ref["ids"][q]) and np.array_equal(dv[o], ref["dist"][q])
         # max-over-ranks timing reduction used by bench.py
         t = torch.tensor([float(rank + 1)], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
