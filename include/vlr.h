@@ -196,6 +196,17 @@ int32_t vlr_poll_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, uint8_
  * acquire fence follows the flag reads. Host only; no CUDA calls. */
 int32_t vlr_wait_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, int64_t* out_t_ns, int64_t timeout_us);
 
+/* vlr_search_host without the final synchronisation (serving pipelines):
+ * the H2D copy, the search and the D2H copies are enqueued on `stream` and
+ * the call returns; h_* outputs are valid once `stream` has completed this
+ * work (cudaStreamSynchronize / an event). Back-to-back calls on one stream
+ * are safe (stream order protects the handle's staging buffers) and keep the
+ * GPU busy across batches. h_queries and the outputs must be pinned host
+ * memory (pageable memory makes the copies synchronous) and stay valid until
+ * completion. A non-finite query is reported by the next call on the handle. */
+vlr_status vlr_search_host_async(vlr_index* idx, const float* h_queries, int32_t nq, int32_t nprobe, int32_t k,
+                                 int64_t* h_ids, float* h_dist, uint8_t* h_miss, int32_t* h_probes, void* stream);
+
 /* Pre-size the per-handle workspace for batches up to (max_nq, max_nprobe, max_k)
  * so that later searches allocate nothing (required before graph capture). */
 vlr_status vlr_reserve(vlr_index* idx, int32_t max_nq, int32_t max_nprobe, int32_t max_k);

@@ -21,7 +21,8 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "NONFINITE", 4: "UNKN
           5: "DUPLICATE_ID", 6: "OOM", 7: "CUDA", 8: "NCCL", 9: "UNSUPPORTED"}
 
 # every symbol include/vlr.h declares (checked by tests/test_abi.py)
-EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_search_release_async",
+EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_search_host_async",
+           "vlr_search_release_async",
            "vlr_poll_ready", "vlr_wait_ready", "vlr_reserve", "vlr_deal_owners", "vlr_update_hot",
            "vlr_merge_partials", "vlr_access_counts", "vlr_index_info", "vlr_index_owners", "vlr_set_profiling", "vlr_stage_times",
            "vlr_last_launch_count", "vlr_nccl_unique_id", "vlr_index_free", "vlr_last_error", "vlr_version"]
@@ -64,6 +65,7 @@ def lib():
             "vlr_search_async": [P, P, I32, I32, I32, P, P, P, P, P],
             "vlr_search": [P, P, I32, I32, I32, P, P, P, P, P],
             "vlr_search_host": [P, P, I32, I32, I32, P, P, P, P, P],
+            "vlr_search_host_async": [P, P, I32, I32, I32, P, P, P, P, P],
             "vlr_search_release_async": [P, P, I32, I32, I32, P, P, P, P, P, ctypes.c_uint32, P],
             "vlr_reserve": [P, I32, I32, I32],
             "vlr_deal_owners": [P, I32, P, P, I32, I32, P],
@@ -276,6 +278,12 @@ class Index:
         """vlr_search_host on raw (e.g. pinned torch) host pointers."""
         _check(lib().vlr_search_host(self._h, q_ptr, nq, nprobe, k, ids_ptr, dist_ptr, miss_ptr, probes_ptr,
                                      _stream_handle(stream)))
+
+    def search_host_ptr_async(self, q_ptr: int, nq: int, nprobe: int, k: int, ids_ptr: int, dist_ptr: int,
+                              miss_ptr: int, probes_ptr: int | None, stream=None):
+        """vlr_search_host_async on raw pinned host pointers (no synchronisation)."""
+        _check(lib().vlr_search_host_async(self._h, q_ptr, nq, nprobe, k, ids_ptr, dist_ptr, miss_ptr, probes_ptr,
+                                           _stream_handle(stream)))
 
     def reserve(self, max_nq: int, max_nprobe: int, max_k: int):
         _check(lib().vlr_reserve(self._h, max_nq, max_nprobe, max_k))

@@ -665,8 +665,9 @@ vlr_status vlr_search(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, 
   return VLR_OK;
 }
 
-vlr_status vlr_search_host(vlr_index* h, const float* hQ, int32_t nq, int32_t nprobe, int32_t k, int64_t* h_ids,
-                           float* h_dist, uint8_t* h_miss, int32_t* h_probes, void* stream) {
+static vlr_status search_host_impl(vlr_index* h, const float* hQ, int32_t nq, int32_t nprobe, int32_t k,
+                                   int64_t* h_ids, float* h_dist, uint8_t* h_miss, int32_t* h_probes, void* stream,
+                                   bool sync) {
   if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
   if (nq < 0 || nprobe < 1 || k < 1) return fail(VLR_ERR_INVALID_ARG, "nq < 0, nprobe < 1 or k < 1");
   if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32 (v1)");
@@ -687,12 +688,23 @@ vlr_status vlr_search_host(vlr_index* h, const float* hQ, int32_t nq, int32_t np
   VLR_CUDA_TRY(cudaMemcpyAsync(h_miss, w.d_miss, (size_t)nq * np, cudaMemcpyDeviceToHost, s));
   if (h_probes)
     VLR_CUDA_TRY(cudaMemcpyAsync(h_probes, w.d_probes, sizeof(int32_t) * nq * np, cudaMemcpyDeviceToHost, s));
+  if (!sync) return VLR_OK;  // results land when `stream` reaches this point; status: next call
   VLR_CUDA_TRY(cudaStreamSynchronize(s));
   if (*w.h_status & 1) {
     *w.h_status = 0;
     return fail(VLR_ERR_NONFINITE, "non-finite query");
   }
   return VLR_OK;
+}
+
+vlr_status vlr_search_host(vlr_index* h, const float* hQ, int32_t nq, int32_t nprobe, int32_t k, int64_t* h_ids,
+                           float* h_dist, uint8_t* h_miss, int32_t* h_probes, void* stream) {
+  return search_host_impl(h, hQ, nq, nprobe, k, h_ids, h_dist, h_miss, h_probes, stream, true);
+}
+
+vlr_status vlr_search_host_async(vlr_index* h, const float* hQ, int32_t nq, int32_t nprobe, int32_t k,
+                                 int64_t* h_ids, float* h_dist, uint8_t* h_miss, int32_t* h_probes, void* stream) {
+  return search_host_impl(h, hQ, nq, nprobe, k, h_ids, h_dist, h_miss, h_probes, stream, false);
 }
 
 vlr_status vlr_merge_partials(const int64_t* part_ids, const float* part_dist, int32_t n_shards, int32_t nq, int32_t k,
