@@ -557,3 +557,24 @@ def test_traffic_aware_deal_shards_equal_monolithic(c1_index, c1_queries):
         hs.close()
     mi, md = vlr.merge_partials(torch.stack(pi), torch.stack(pd))
     assert np.array_equal(mi.cpu().numpy(), a["ids"]) and np.array_equal(md.cpu().numpy(), a["dist"])
+
+
+def test_search_host_async_pipeline_matches_blocking(c1_index):
+    """vlr_search_host_async back to back on one stream (pinned buffers, one
+    final sync) returns, per batch, exactly what the blocking call returns."""
+    h = vlr.Index.from_arrays(c1_index)
+    Qs = datagen.make_queries(100_000, 128, 1024, 4 * 48, stream=4).reshape(4, 48, 128)
+    ref = [h.search_host(Q, 16, 10) for Q in Qs]
+    hq = torch.from_numpy(Qs.copy()).pin_memory()
+    ids = torch.empty(4, 48, 10, dtype=torch.int64).pin_memory()
+    dist = torch.empty(4, 48, 10, dtype=torch.float32).pin_memory()
+    miss = torch.empty(4, 48, 16, dtype=torch.uint8).pin_memory()
+    prb = torch.empty(4, 48, 16, dtype=torch.int32).pin_memory()
+    for i in range(4):
+        h.search_host_ptr_async(hq[i].data_ptr(), 48, 16, 10, ids[i].data_ptr(), dist[i].data_ptr(),
+                                miss[i].data_ptr(), prb[i].data_ptr())
+    torch.cuda.current_stream().synchronize()
+    for i in range(4):
+        assert np.array_equal(ids[i].numpy(), ref[i][0]) and np.array_equal(dist[i].numpy(), ref[i][1])
+        assert np.array_equal(miss[i].numpy(), ref[i][2]) and np.array_equal(prb[i].numpy(), ref[i][3])
+    h.close()
