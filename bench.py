@@ -28,7 +28,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-METRIC = "IVF-PQ search queries/s (batch 256, nprobe 128, k 10)"
+
+
+def metric_name(B, nprobe, k):
+    return f"IVF-PQ search queries/s (batch {B}, nprobe {nprobe}, k {k})"
 UNIT = "queries/s"
 
 
@@ -270,7 +273,7 @@ def run_reference(a):
             times.append(time.time() - t)
     tot = sum(times)
     val = a.steps * S / tot
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": 1, "steps": a.steps,
+    line = {"impl": "reference", "metric": metric_name(B, c["nprobe"], c["k"]), "value": val, "unit": UNIT, "n_gpus": 1, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded clustered embeddings, Zipf queries)",
             "config": {"workload": workload_name(c, a.config), "seed": a.seed, "sample_queries_per_step": S},
@@ -477,7 +480,7 @@ def main():
     value = a.steps * B / (ms_total * 1e-3)
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "metric": metric_name(B, c["nprobe"], K), "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_total / a.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded clustered embeddings, Zipf-skewed queries; generated on the GPU)",
             "config": {"workload": workload_name(c, a.config), "N": c["N"], "d": c["d"], "nlist": c["nlist"], "m": c["m"],

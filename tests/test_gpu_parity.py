@@ -578,3 +578,33 @@ def test_search_host_async_pipeline_matches_blocking(c1_index):
         assert np.array_equal(ids[i].numpy(), ref[i][0]) and np.array_equal(dist[i].numpy(), ref[i][1])
         assert np.array_equal(miss[i].numpy(), ref[i][2]) and np.array_equal(prb[i].numpy(), ref[i][3])
     h.close()
+
+
+def test_cuda_graph_capture_and_replay(c1_index):
+    """include/vlr.h: vlr_search_async is CUDA-graph capturable once
+    vlr_reserve has sized the workspace; replays give the eager results for
+    new query contents in the same buffers."""
+    h = vlr.Index.from_arrays(c1_index)
+    B, npb, k = 48, 16, 10
+    h.reserve(B, npb, k)
+    Qs = datagen.make_queries(100_000, 128, 1024, 3 * B, stream=5).reshape(3, B, 128)
+    ref = [gpu_search(h, Q, npb, k) for Q in Qs]
+    Qd = torch.from_numpy(Qs[0].copy()).cuda()
+    out = (torch.empty(B, k, dtype=torch.int64, device="cuda"), torch.empty(B, k, dtype=torch.float32, device="cuda"),
+           torch.empty(B, npb, dtype=torch.uint8, device="cuda"), torch.empty(B, npb, dtype=torch.int32, device="cuda"))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        h.search(Qd, npb, k, out=out, stream=s)  # warm-up on the capture stream
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        h.search(Qd, npb, k, out=out, stream=s)
+    for i in (1, 2, 0):
+        Qd.copy_(torch.from_numpy(Qs[i]))
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(out[0].cpu().numpy(), ref[i]["ids"])
+        assert np.array_equal(out[1].cpu().numpy(), ref[i]["dist"])
+        assert np.array_equal(out[3].cpu().numpy(), ref[i]["probes"])
+    del g
+    h.close()
