@@ -28,11 +28,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
+UNIT = "queries/s"
 
 
 def metric_name(B, nprobe, k):
     return f"IVF-PQ search queries/s (batch {B}, nprobe {nprobe}, k {k})"
-UNIT = "queries/s"
 
 
 def parse():
