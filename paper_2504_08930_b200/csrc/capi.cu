@@ -102,7 +102,7 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   const size_t nslots = ((size_t)w.n_cta * kReleaseWaves + nqs) * kScanWarps * ck;  // slot (c + q + wave * n_cta)
   VLR_CUDA_TRY(dalloc(&w.pdist, nslots));
   VLR_CUDA_TRY(dalloc(&w.pid, nslots));
-  if (ix.world > 1 && !ix.shard_only) {
+  if (ix.nccl) {  // exchange buffers (world > 1 with a communicator, or the forced 1-rank exchange)
     VLR_CUDA_TRY(dalloc(reinterpret_cast<Packed**>(&w.send), nqs * ck));
     VLR_CUDA_TRY(dalloc(reinterpret_cast<Packed**>(&w.recv), nqs * ck * ix.world));
   }
@@ -448,7 +448,11 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   ix.bytes = (int64_t)L * d * 4 + (int64_t)L * ix.d8 * 2 + L * 4 + (int64_t)ncb * 4 + 2LL * L * 4 + (ix.n_local + 1) * 8 +
              ix.n_groups * 32 * (ix.mpad * ix.code_bits / 8 + 4 + 8);
   // NCCL communicator (collective)
-  if (cm.world > 1 && cm.nccl_unique_id) {
+  // VLR_FORCE_EXCHANGE=1 with world == 1 and an NCCL id: a 1-rank communicator, so the exchange path
+  // (rank merge into packed entries -> ncclAllGather -> K8 merge) runs on a single GPU (tests)
+  const char* fx = getenv("VLR_FORCE_EXCHANGE");
+  const bool force_x = cm.world == 1 && fx && atoi(fx) == 1;
+  if ((cm.world > 1 || force_x) && cm.nccl_unique_id) {
     ncclUniqueId uid;
     std::memcpy(&uid, cm.nccl_unique_id, sizeof(uid));
     ncclComm_t comm_h;
@@ -535,7 +539,7 @@ static vlr_status search_impl(vlr_index* h, const float* Q, int32_t nq, int32_t 
   if (rel) VLR_CUDA_TRY(cudaMemsetAsync(w.qdone, 0, sizeof(unsigned long long) * nq, s));
   VLR_CUDA_TRY(launch_scan(ix, w, nq, np, k, s, rel)); ++n;
   rec(h, 6, s);
-  const bool exchange = ix.world > 1 && !ix.shard_only;
+  const bool exchange = ix.nccl != nullptr;
   if (!rel) {  // release mode: the scan merged and released every row itself
     VLR_CUDA_TRY(launch_rank_merge(ix, w, nq, np, k, out_ids, out_dist, exchange ? w.send : nullptr, s)); ++n;
   }
@@ -579,7 +583,7 @@ vlr_status vlr_search_release_async(vlr_index* h, const float* Q, int32_t nq, in
                                     int64_t* out_ids, float* out_dist, uint8_t* out_miss, int32_t* out_probes,
                                     uint32_t* ready, uint32_t epoch, void* stream) {
   if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
-  if (h->ix.world > 1 || h->ix.shard_only)
+  if (h->ix.world > 1 || h->ix.shard_only || h->ix.nccl)
     return fail(VLR_ERR_UNSUPPORTED, "early release needs world == 1 (rows are final only after the exchange)");
   if (nq > 0) {
     if (!ready || epoch == 0) return fail(VLR_ERR_INVALID_ARG, "release: null ready flags or epoch 0");

@@ -608,3 +608,21 @@ def test_cuda_graph_capture_and_replay(c1_index):
         assert np.array_equal(out[3].cpu().numpy(), ref[i]["probes"])
     del g
     h.close()
+
+
+def test_nccl_exchange_path_single_rank(c1_index, c1_queries, monkeypatch):
+    """The G > 1 exchange path (K7 into packed 16-B entries -> ncclAllGather on
+    the search stream -> K8 merge-select) run on one GPU through a 1-rank NCCL
+    communicator (VLR_FORCE_EXCHANGE=1): bitwise the plain search."""
+    c = datagen.CONFIGS["C1"]
+    h = vlr.Index.from_arrays(c1_index)
+    a = gpu_search(h, c1_queries, c["nprobe"], c["k"])
+    n_plain = h.last_launch_count
+    h.close()
+    monkeypatch.setenv("VLR_FORCE_EXCHANGE", "1")
+    hx = vlr.Index.from_arrays(c1_index, nccl_id=vlr.nccl_unique_id())
+    b = gpu_search(hx, c1_queries, c["nprobe"], c["k"])
+    assert hx.last_launch_count == n_plain + 1  # + K8
+    for key in a:
+        assert np.array_equal(a[key], b[key]), key
+    hx.close()
