@@ -222,6 +222,159 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 }
 
+// Persistent variant for nq <= 256 (one accumulator of nN <= 256 columns per
+// tile): one CTA per SM loops over the 128-centroid tiles t = blockIdx.x,
+// t += gridDim.x, with a DOUBLE-BUFFERED TMEM accumulator (2 x nN <= 512
+// columns) so the epilogue of tile i (warps 2-5) overlaps the TMA/MMA
+// mainloop of tile i+1, and the smem ring (up to 4 stages of 48 KB at nN =
+// 256) stays full across tile boundaries. The per-element arithmetic is that
+// of k_filter_tc (same operands, same fp32 MMA accumulation over K, same
+// epilogue), so the band proof is unchanged.
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s32(b)) : "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_filter_tc_p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int L, int nq,
+                  int kblocks, int nN, int stages, const float* __restrict__ cn2, const float* __restrict__ qinv,
+                  float c_inv, float* __restrict__ dt, float* __restrict__ gmin, int ngroups) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ float s_inv[256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = (L + kTcM - 1) / kTcM;
+  const uint32_t bytesA = kTcM * 128, bytesB = (uint32_t)(nN * 128);
+  const uint32_t stage_bytes = bytesA + bytesB;
+  uint32_t ncols = 32;
+  while ((int)ncols < 2 * nN) ncols <<= 1;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mb_init(&tfull[b], 1);
+      mb_init(&tempty[b], 4);  // one arrival per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tmem_base)), "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tbase = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          const uint32_t s = g % (uint32_t)stages, ph = (g / (uint32_t)stages) & 1u;
+          mb_wait(&empty[s], ph ^ 1u);
+          uint8_t* sA = smem + (size_t)s * stage_bytes;
+          mb_expect_tx(&full[s], stage_bytes);
+          tma_2d(sA, &tmA, kb * kTcBK, t * kTcM, &full[s]);
+          tma_2d(sA + bytesA, &tmB, kb * kTcBK, 0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(nN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+      uint32_t g = 0;
+      int i = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const int ab = i & 1, u = i >> 1;
+        if (u >= 1) mb_wait(&tempty[ab], (uint32_t)(u - 1) & 1u);  // the epilogue has drained this buffer
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t dacc = tbase + (uint32_t)(ab * nN);
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          const uint32_t s = g % (uint32_t)stages, ph = (g / (uint32_t)stages) & 1u;
+          mb_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t aaddr = s32(smem + (size_t)s * stage_bytes);
+          const uint32_t baddr = aaddr + bytesA;
+#pragma unroll
+          for (int kk = 0; kk < kTcBK / 16; ++kk)
+            mma_f16(dacc, sw128_desc(aaddr + kk * 32), sw128_desc(baddr + kk * 32), idesc, (kb | kk) != 0 ? 1u : 0u);
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&tfull[ab]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int lg = warp & 3;
+    for (int j = threadIdx.x - 64; j < nN; j += 128) s_inv[j] = j < nq ? qinv[j] * c_inv : 0.f;
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    int i = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const int ab = i & 1, u = i >> 1;
+      mb_wait(&tfull[ab], (uint32_t)u & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int row = t * kTcM + lg * 32 + lane;
+      const float cn = row < L ? cn2[row] : 0.f;
+      const int grp = t * 4 + lg;
+      for (int c = 0; c < nN; c += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)(ab * nN + c);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        if (c + 16 < nN) {
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+                "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                "=r"(v[30]), "=r"(v[31])
+              : "r"(taddr + 16u));
+        } else {
+#pragma unroll
+          for (int j = 16; j < 32; ++j) v[j] = __float_as_uint(CUDART_INF_F);
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float f[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          f[j] = row < L ? cn - 2.f * (__uint_as_float(v[j]) * s_inv[c + j < nN ? c + j : 0]) : CUDART_INF_F;
+          const int q = c + j;
+          if (row < L && q < nq && q < nN) dt[(size_t)q * L + row] = f[j];
+        }
+#pragma unroll
+        for (int w = 16; w >= 1; w >>= 1) {
+          const bool upper = (lane & w) != 0;
+#pragma unroll
+          for (int j = 0; j < w; ++j) {
+            const float send = upper ? f[j] : f[j + w];
+            const float keep = upper ? f[j + w] : f[j];
+            f[j] = fminf(keep, __shfl_xor_sync(kFull, send, w));
+          }
+        }
+        const int q = c + lane;
+        if (q < nq && q < nN && grp < ngroups) gmin[(size_t)q * ngroups + grp] = f[0];
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mb_arrive(&tempty[ab]);  // this warp's TMEM lanes of buffer ab are read
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols));
+  }
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -269,6 +422,33 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   CUtensorMap tmB;
   cudaError_t e = make_tmap_2d(&tmB, Qh, nq, ix.d8, box_rows_b);
   if (e != cudaSuccess) return e;
+  const int kblocks = (ix.d8 + kTcBK - 1) / kTcBK;
+  static int persistent = -1;  // VLR_FILTER_PERSISTENT=0: the one-tile-per-CTA kernel for every batch (experiments)
+  if (persistent < 0) {
+    const char* e = getenv("VLR_FILTER_PERSISTENT");
+    persistent = e ? atoi(e) : 1;
+  }
+  if (nacc == 1 && persistent) {
+    const uint32_t sb = kTcM * 128 + (uint32_t)(nN * 128);
+    int stages = (int)((200 * 1024) / sb);
+    if (stages > kTcMaxStages) stages = kTcMaxStages;
+    if (stages < 2) stages = 2;
+    const size_t smem = (size_t)stages * sb + 1024;
+    static size_t configured_p = 0;
+    if (smem > configured_p) {
+      e = cudaFuncSetAttribute(k_filter_tc_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      configured_p = smem;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ntiles = (ix.nlist + kTcM - 1) / kTcM;
+    k_filter_tc_p<<<ntiles < sms ? ntiles : sms, kTcThreads, smem, s>>>(
+        *reinterpret_cast<const CUtensorMap*>(ix.tmapA), tmB, ix.nlist, nq, kblocks, nN, stages, ix.cnorm2, qinv,
+        ix.c_inv, dt, gmin, (ix.nlist + 31) / 32);
+    return cudaGetLastError();
+  }
   const uint32_t stage_bytes = kTcM * 128 + (uint32_t)(nacc * nN * 128);
   // ~100 KB of stages so that two CTAs share an SM: one CTA's epilogue
   // overlaps the other's TMA/MMA pipeline
@@ -282,7 +462,6 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  const int kblocks = (ix.d8 + kTcBK - 1) / kTcBK;
   dim3 grid((ix.nlist + kTcM - 1) / kTcM, (nq + nN * nacc - 1) / (nN * nacc));
   k_filter_tc<<<grid, kTcThreads, smem, s>>>(*reinterpret_cast<const CUtensorMap*>(ix.tmapA), tmB, ix.nlist, nq,
                                               kblocks, nN, nacc, stages, ix.cnorm2, qinv, ix.c_inv, dt, gmin,
