@@ -423,10 +423,13 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   cudaError_t e = make_tmap_2d(&tmB, Qh, nq, ix.d8, box_rows_b);
   if (e != cudaSuccess) return e;
   const int kblocks = (ix.d8 + kTcBK - 1) / kTcBK;
-  static int persistent = -1;  // VLR_FILTER_PERSISTENT=0: the one-tile-per-CTA kernel for every batch (experiments)
+  // VLR_FILTER_PERSISTENT=1: the persistent double-buffered kernel for batches <= 256 (experiment; measured
+  // 0.102 ms vs 0.060 ms for the one-tile-per-CTA kernel at C4, batch 256: latency-bound at 1 CTA per SM,
+  // DRAM 20% / L2 16% of peak, profiles/k1_persistent_r01.md). Off by default.
+  static int persistent = -1;
   if (persistent < 0) {
     const char* e = getenv("VLR_FILTER_PERSISTENT");
-    persistent = e ? atoi(e) : 1;
+    persistent = e ? atoi(e) : 0;
   }
   if (nacc == 1 && persistent) {
     const uint32_t sb = kTcM * 128 + (uint32_t)(nN * 128);
