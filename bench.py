@@ -509,7 +509,7 @@ def main():
             line["top20_share"] = datagen.topk_share(counts)
         print(json.dumps(line), flush=True)
     if a.sweep_out:
-        sweep(a, c, h, pool, world, rank)
+        sweep(a, c, h, pool, world, rank, gt=getattr(ix, "gt_ids", None))
     h.close()
     if world > 1:
         import torch.distributed as dist
@@ -590,11 +590,22 @@ def release_leg(a, c, h, Qdev, outs, K):
                    "stream completion of vlr_search on the same batch; rows in pinned host memory"}
 
 
-def sweep(a, c, h, pool, world, rank):
+def sweep(a, c, h, pool, world, rank, gt=None):
     """C5: batch x nprobe sweep on the loaded index (device-timed, CUDA events,
-    max over ranks); one JSON line per point in --sweep-out."""
+    max over ranks); one JSON line per point in --sweep-out. With ground truth
+    (N = 1), each nprobe also gets recall@10 of the ground-truth batch against
+    exact flat search (recall monotone in nprobe)."""
     import torch
     K = c["k"]
+    recall_at = {}
+    if gt is not None and rank == 0:
+        Bg = c["batch"]
+        qg = torch.from_numpy(pool[a.warmup * Bg:(a.warmup + 1) * Bg].copy()).cuda()
+        for npb in [16, 32, 64, 128, 256, 512]:
+            ids, _, _, _ = h.search(qg, npb, 10, sync=True)
+            got = ids.cpu().numpy()
+            recall_at[npb] = float(np.mean([len(set(g.tolist()) & set(t[:10].tolist())) / 10
+                                            for g, t in zip(got, gt)]))
     batches = [1, 2, 4, 8, 16, 32, 64, 128, 256, 512]
     nprobes = [16, 32, 64, 128, 256, 512]
     qd = torch.from_numpy(pool).cuda()
@@ -626,6 +637,8 @@ def sweep(a, c, h, pool, world, rank):
                               "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
             "lat_ms_top5": [round(float(x), 4) for x in np.sort(lat)[::-1][:5]],
                               "steps": steps})
+                if B == c["batch"] and npb in recall_at:
+                    lines[-1]["recall_at_10"] = recall_at[npb]
     if rank == 0:
         with open(a.sweep_out, "w") as f:
             for ln in lines:
