@@ -29,9 +29,11 @@ static vlr_status fail(vlr_status st, const std::string& msg) {
 }
 
 // relative bound on the filter's dot-product error (DESIGN.md §5 band proof):
-// operands pre-rounded to TF32 with cvt.rna (relative error <= 2^-11 each,
-// products exact in fp32), fp32 accumulation over d terms in the tensor core
-// bounded conservatively by d * 2^-23 (order and rounding mode unspecified).
+// operands scaled by powers of two and rounded to fp16 (RN, 11-bit significand:
+// relative error <= 2^-11 each for normal results; the subnormal-flush term is
+// added by the caller's band), products exact in fp32, fp32
+// accumulation over d terms in the tensor core bounded conservatively by
+// d * 2^-23 (order and rounding mode unspecified).
 static float filter_edot(int d) { return 2.0f * 4.8828125e-4f + 2.3841858e-7f + 1.01f * (float)d * 1.1920929e-7f; }
 
 template <class T>
