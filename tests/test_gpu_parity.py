@@ -626,3 +626,28 @@ def test_nccl_exchange_path_single_rank(c1_index, c1_queries, monkeypatch):
     for key in a:
         assert np.array_equal(a[key], b[key]), key
     hx.close()
+
+
+def test_persistent_filter_variant_parity():
+    """K1 experiment kernel (k_filter_tc_p, VLR_FILTER_PERSISTENT=1, read once
+    per process): probes stay bit-exact and results pass the parity rules.
+    Runs in a subprocess so the flag does not leak into this process."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, 'tests');"
+        "import datagen, oracle, paper_2504_08930_b200 as vlr; from parity import check;"
+        "ix = datagen.make_index(100_000, 128, 1024, 16);"
+        "Q = datagen.make_queries(100_000, 128, 1024, 200, stream=2);"
+        "h = vlr.Index.from_arrays(ix);"
+        "bad = 0\n"
+        "for nq, npb in ((1, 16), (64, 16), (200, 300)):\n"
+        "    ids, dist, miss, prb = h.search(torch.from_numpy(Q[:nq]).cuda(), npb, 10, sync=True)\n"
+        "    g = dict(ids=ids.cpu().numpy(), dist=dist.cpu().numpy(), miss=miss.cpu().numpy(), probes=prb.cpu().numpy())\n"
+        "    bad += len(check(ix, Q[:nq], g, oracle.search(ix, Q[:nq], npb, 10), idmap=oracle.IdMap(ix)))\n"
+        "sys.exit(1 if bad else 0)\n")
+    import os
+    env = dict(os.environ, VLR_FILTER_PERSISTENT="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
