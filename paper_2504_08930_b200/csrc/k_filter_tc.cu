@@ -30,6 +30,7 @@ constexpr int kTcM = 128;        // centroids per tile (MMA M)
 constexpr int kTcBK = 64;        // fp16 elements per K block (128 B = one SW128 row)
 constexpr int kTcThreads = 192;  // 6 warps
 constexpr int kTcMaxStages = 6;
+constexpr int kTcCluster = 4;    // default B-multicast cluster size (launch_filter_tc)
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -63,6 +64,35 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0
       "l"(map), "r"(c0), "r"(c1), "r"(s32(bar))
       : "memory");
 }
+// B-operand multicast across a cluster of CL CTAs (adjacent centroid tiles):
+// CTA r loads rows [r nN/CL, (r+1) nN/CL) of the query tile and the TMA
+// writes them into the same smem offset of every CTA in ctaMask, completing
+// bytes on each destination's mbarrier at the same offset.
+__device__ __forceinline__ void tma_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                          uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(s32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(s32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          s32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  __syncwarp();  // .aligned: the whole warp executes the cluster barrier together
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   // UMMA shared-memory descriptor, K-major SWIZZLE_128B: start>>4, LBO = 1 (unused),
   // SBO = 1024 B (8 rows x 128 B), version 1 (bits 46-47), layout type 2 (bits 61-63)
@@ -81,6 +111,7 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+template <int CL>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_filter_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int L, int nq,
                 int kblocks, int nN, int nacc, int stages, const float* __restrict__ cn2,
@@ -102,7 +133,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < stages; ++s) {
       mb_init(&full[s], 1);
-      mb_init(&empty[s], 1);
+      mb_init(&empty[s], CL);  // CL > 1: every cluster CTA's MMAs must have read the stage (B is multicast)
     }
     mb_init(&tfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -115,8 +146,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();  // peers' barriers initialised before any multicast lands
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tbase = tmem_base;
+  const uint32_t crank = CL > 1 ? cluster_rank() : 0u;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -128,8 +162,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         uint8_t* sB = sA + bytesA;
         mb_expect_tx(&full[s], stage_bytes);
         tma_2d(sA, &tmA, kb * kTcBK, m0, &full[s]);
-        for (int r = 0; r < nacc * nN; r += 256) {
-          tma_2d(sB + (size_t)r * 128, &tmB, kb * kTcBK, q0 + r, &full[s]);
+        if constexpr (CL > 1) {  // nacc == 1: this CTA's 1/CL of the query rows, to every cluster CTA
+          const int rq = nN / CL;
+          tma_2d_mc(sB + (size_t)crank * rq * 128, &tmB, kb * kTcBK, q0 + (int)crank * rq, &full[s], kMask);
+        } else {
+          for (int r = 0; r < nacc * nN; r += 256) {
+            tma_2d(sB + (size_t)r * 128, &tmB, kb * kTcBK, q0 + r, &full[s]);
+          }
         }
       }
     }
@@ -152,7 +191,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mma_f16(tbase + (uint32_t)(acc * nN), ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
         }
-        mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+        if constexpr (CL > 1) mma_commit_mc(&empty[s], kMask);  // frees stage s in every cluster CTA's count
+        else mma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
       }
       mma_commit(&tfull);  // accumulator complete
     }
@@ -216,6 +256,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while peers may still multicast into it
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols));
@@ -418,7 +459,19 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
     nacc = 2;
     nN = 256;
   }
-  const int box_rows_b = nN < 256 ? nN : 256;
+  // B multicast cluster size (VLR_FILTER_CLUSTER, default kTcCluster): CL CTAs on adjacent centroid tiles
+  // each load 1/CL of the query tile and multicast it to the others (rows per slice a multiple of 8 = one
+  // SW128 atom). One accumulator (nq <= 256) only.
+  static int cl_env = -1;
+  if (cl_env < 0) {
+    const char* ce = getenv("VLR_FILTER_CLUSTER");
+    cl_env = ce ? atoi(ce) : kTcCluster;
+  }
+  int CL = 1;
+  if (nacc == 1)
+    for (int c : {4, 2})
+      if (c <= cl_env && nN % (8 * c) == 0) { CL = c; break; }
+  const int box_rows_b = (nN < 256 ? nN : 256) / CL;
   CUtensorMap tmB;
   cudaError_t e = make_tmap_2d(&tmB, Qh, nq, ix.d8, box_rows_b);
   if (e != cudaSuccess) return e;
@@ -459,17 +512,41 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   if (stages > kTcMaxStages) stages = kTcMaxStages;
   if (stages < 2) stages = 2;
   const size_t smem = (size_t)stages * stage_bytes + 1024;
-  static size_t configured = 0;
-  if (smem > configured) {
-    e = cudaFuncSetAttribute(k_filter_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static size_t configured[3] = {0, 0, 0};
+  const int ci = CL == 4 ? 2 : CL == 2 ? 1 : 0;
+  if (smem > configured[ci]) {
+    e = CL == 4   ? cudaFuncSetAttribute(k_filter_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+        : CL == 2 ? cudaFuncSetAttribute(k_filter_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                  : cudaFuncSetAttribute(k_filter_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
+    configured[ci] = smem;
   }
-  dim3 grid((ix.nlist + kTcM - 1) / kTcM, (nq + nN * nacc - 1) / (nN * nacc));
-  k_filter_tc<<<grid, kTcThreads, smem, s>>>(*reinterpret_cast<const CUtensorMap*>(ix.tmapA), tmB, ix.nlist, nq,
-                                              kblocks, nN, nacc, stages, ix.cnorm2, qinv, ix.c_inv, dt, gmin,
-                                              (ix.nlist + 31) / 32);
-  return cudaGetLastError();
+  const int tiles = (ix.nlist + kTcM - 1) / kTcM;
+  dim3 grid((tiles + CL - 1) / CL * CL, (nq + nN * nacc - 1) / (nN * nacc));  // whole clusters (extra tiles: OOB)
+  const CUtensorMap& tmA = *reinterpret_cast<const CUtensorMap*>(ix.tmapA);
+  const int ngroups = (ix.nlist + 31) / 32;
+  if (CL == 1) {
+    k_filter_tc<1><<<grid, kTcThreads, smem, s>>>(tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages, ix.cnorm2, qinv,
+                                                  ix.c_inv, dt, gmin, ngroups);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (CL == 4)
+    return cudaLaunchKernelEx(&cfg, k_filter_tc<4>, tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages,
+                              (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups);
+  return cudaLaunchKernelEx(&cfg, k_filter_tc<2>, tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages,
+                            (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups);
 }
 
 // fp16(c * scale) (round to nearest even) into a d8-padded copy; scale is a power of two
