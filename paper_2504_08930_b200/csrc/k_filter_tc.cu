@@ -30,7 +30,9 @@ constexpr int kTcM = 128;        // centroids per tile (MMA M)
 constexpr int kTcBK = 64;        // fp16 elements per K block (128 B = one SW128 row)
 constexpr int kTcThreads = 192;  // 6 warps
 constexpr int kTcMaxStages = 6;
-constexpr int kTcCluster = 4;    // default B-multicast cluster size (launch_filter_tc)
+constexpr int kTcCluster = 1;    // default B-multicast cluster size (launch_filter_tc): 1 = off. Measured at
+                                 // C4, batch 256: 0.060 ms (1), 0.066 (2), 0.067 (4) -- the filter is not
+                                 // bound by the re-read query tile (profiles/k1_persistent_r01.md)
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -459,6 +461,14 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
     nacc = 2;
     nN = 256;
   }
+  // VLR_FILTER_PERSISTENT=1: the persistent double-buffered kernel for batches <= 256 (experiment; measured
+  // 0.102 ms vs 0.060 ms for the one-tile-per-CTA kernel at C4, batch 256: latency-bound at 1 CTA per SM,
+  // DRAM 20% / L2 16% of peak, profiles/k1_persistent_r01.md). Off by default.
+  static int persistent = -1;
+  if (persistent < 0) {
+    const char* e = getenv("VLR_FILTER_PERSISTENT");
+    persistent = e ? atoi(e) : 0;
+  }
   // B multicast cluster size (VLR_FILTER_CLUSTER, default kTcCluster): CL CTAs on adjacent centroid tiles
   // each load 1/CL of the query tile and multicast it to the others (rows per slice a multiple of 8 = one
   // SW128 atom). One accumulator (nq <= 256) only.
@@ -468,7 +478,7 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
     cl_env = ce ? atoi(ce) : kTcCluster;
   }
   int CL = 1;
-  if (nacc == 1)
+  if (nacc == 1 && !persistent)
     for (int c : {4, 2})
       if (c <= cl_env && nN % (8 * c) == 0) { CL = c; break; }
   const int box_rows_b = (nN < 256 ? nN : 256) / CL;
@@ -476,14 +486,6 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   cudaError_t e = make_tmap_2d(&tmB, Qh, nq, ix.d8, box_rows_b);
   if (e != cudaSuccess) return e;
   const int kblocks = (ix.d8 + kTcBK - 1) / kTcBK;
-  // VLR_FILTER_PERSISTENT=1: the persistent double-buffered kernel for batches <= 256 (experiment; measured
-  // 0.102 ms vs 0.060 ms for the one-tile-per-CTA kernel at C4, batch 256: latency-bound at 1 CTA per SM,
-  // DRAM 20% / L2 16% of peak, profiles/k1_persistent_r01.md). Off by default.
-  static int persistent = -1;
-  if (persistent < 0) {
-    const char* e = getenv("VLR_FILTER_PERSISTENT");
-    persistent = e ? atoi(e) : 0;
-  }
   if (nacc == 1 && persistent) {
     const uint32_t sb = kTcM * 128 + (uint32_t)(nN * 128);
     int stages = (int)((200 * 1024) / sb);
