@@ -628,10 +628,13 @@ def test_nccl_exchange_path_single_rank(c1_index, c1_queries, monkeypatch):
     hx.close()
 
 
-def test_persistent_filter_variant_parity():
-    """K1 experiment kernel (k_filter_tc_p, VLR_FILTER_PERSISTENT=1, read once
-    per process): probes stay bit-exact and results pass the parity rules.
-    Runs in a subprocess so the flag does not leak into this process."""
+@pytest.mark.parametrize("flag,val", [("VLR_FILTER_PERSISTENT", "1"), ("VLR_FILTER_CLUSTER", "2"),
+                                      ("VLR_FILTER_CLUSTER", "4")])
+def test_filter_variant_parity(flag, val):
+    """K1 experiment kernels (persistent k_filter_tc_p; query-tile multicast
+    over 2- or 4-CTA clusters), flags read once per process: probes stay
+    bit-exact and results pass the parity rules, for batches 1, 64 and 200
+    (nN 16, 64, 208). Runs in a subprocess so the flag does not leak."""
     import subprocess
     import sys
     code = (
@@ -647,7 +650,7 @@ def test_persistent_filter_variant_parity():
         "    bad += len(check(ix, Q[:nq], g, oracle.search(ix, Q[:nq], npb, 10), idmap=oracle.IdMap(ix)))\n"
         "sys.exit(1 if bad else 0)\n")
     import os
-    env = dict(os.environ, VLR_FILTER_PERSISTENT="1")
+    env = dict(os.environ, **{flag: val})
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
