@@ -30,6 +30,9 @@ constexpr int kTcM = 128;        // centroids per tile (MMA M)
 constexpr int kTcBK = 64;        // fp16 elements per K block (128 B = one SW128 row)
 constexpr int kTcThreads = 192;  // 6 warps
 constexpr int kTcMaxStages = 6;
+#ifndef VLR_K1_EXPERIMENT
+#define VLR_K1_EXPERIMENT 0  // timing-only builds (tools/variants.py): 1 no dt stores, 2 no MMAs, 3 no epilogue
+#endif
 constexpr int kTcCluster = 1;    // default B-multicast cluster size (launch_filter_tc): 1 = off. Measured at
                                  // C4, batch 256: 0.060 ms (1), 0.066 (2), 0.067 (4) -- the filter is not
                                  // bound by the re-read query tile (profiles/k1_persistent_r01.md)
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const uint64_t ad = sw128_desc(aaddr + kk * 32);
           for (int acc = 0; acc < nacc; ++acc) {
             const uint64_t bd = sw128_desc(baddr + (uint32_t)(acc * nN * 128) + kk * 32);
-            mma_f16(tbase + (uint32_t)(acc * nN), ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+            if (VLR_K1_EXPERIMENT != 2) mma_f16(tbase + (uint32_t)(acc * nN), ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
         }
         if constexpr (CL > 1) mma_commit_mc(&empty[s], kMask);  // frees stage s in every cluster CTA's count
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // coalesced) and the min over this warp's 32 centroids of each column
     // (transpose-reduce: 31 shuffles leave column j's min in lane j).
     const int grp = blockIdx.x * 4 + lg;
-    for (int c = 0; c < ncols_used; c += 32) {
+    for (int c = 0; c < (VLR_K1_EXPERIMENT == 3 ? 0 : ncols_used); c += 32) {
       uint32_t v[32];
       const uint32_t taddr = tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)c;
       asm volatile(
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int j = 0; j < 32; ++j) {
         f[j] = row < L ? cn - 2.f * (__uint_as_float(v[j]) * s_inv[c + j]) : CUDART_INF_F;
         const int q = q0 + c + j;
-        if (row < L && q < nq && c + j < ncols_used) dt[(size_t)q * L + row] = f[j];
+        if (VLR_K1_EXPERIMENT != 1 && row < L && q < nq && c + j < ncols_used) dt[(size_t)q * L + row] = f[j];
       }
 #pragma unroll
       for (int w = 16; w >= 1; w >>= 1) {
