@@ -62,7 +62,7 @@ static void free_ws(Workspace& w) {
 }
 
 static void free_index(DeviceIndex& ix) {
-  void* ps[] = {ix.centroids, ix.cf16, ix.cnorm2, ix.codebooks, ix.owner, ix.local, ix.gbase, ix.codes, ix.bias, ix.ids};
+  void* ps[] = {ix.centroids, ix.cf16, ix.cf16t, ix.cnorm2, ix.codebooks, ix.owner, ix.local, ix.gbase, ix.codes, ix.bias, ix.ids};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (ix.nccl) ncclCommDestroy(reinterpret_cast<ncclComm_t>(ix.nccl));
@@ -370,6 +370,8 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   LTRY(cudaMemcpyAsync(ix.cnorm2, cn2.data(), sizeof(float) * L, cudaMemcpyHostToDevice, s));
   LTRY(launch_round_f16(ix.centroids, L, d, ix.d8, std::ldexp(1.0f, ix.c_exp), ix.cf16, s));
   LTRY(make_tmap_2d(ix.tmapA, ix.cf16, L, ix.d8, 128));
+  LTRY(dalloc(&ix.cf16t, (size_t)((L + 127) / 128) * 128 * (size_t)((ix.d8 + 63) / 64) * 64));
+  LTRY(launch_tile_f16(ix, s));
   LTRY(cudaMemcpyAsync(ix.codebooks, D.codebooks, sizeof(float) * ncb, cudaMemcpyHostToDevice, s));
   LTRY(cudaMemcpyAsync(ix.owner, owner.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, s));
   LTRY(cudaMemcpyAsync(ix.local, local.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, s));
@@ -447,7 +449,7 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
     set_error("duplicate vector id among resident vectors");
     return bail(VLR_ERR_DUPLICATE_ID);
   }
-  ix.bytes = (int64_t)L * d * 4 + (int64_t)L * ix.d8 * 2 + L * 4 + (int64_t)ncb * 4 + 2LL * L * 4 + (ix.n_local + 1) * 8 +
+  ix.bytes = (int64_t)L * d * 4 + (int64_t)L * ix.d8 * 2 + (int64_t)((L + 127) / 128) * 128 * ((ix.d8 + 63) / 64) * 64 * 2 + L * 4 + (int64_t)ncb * 4 + 2LL * L * 4 + (ix.n_local + 1) * 8 +
              ix.n_groups * 32 * (ix.mpad * ix.code_bits / 8 + 4 + 8);
   // NCCL communicator (collective)
   // VLR_FORCE_EXCHANGE=1 with world == 1 and an NCCL id: a 1-rank communicator, so the exchange path

@@ -81,6 +81,12 @@ __device__ __forceinline__ void tma_2d_mc(void* dst, const CUtensorMap* map, int
       "l"(map), "r"(c0), "r"(c1), "r"(s32(bar)), "h"(mask)
       : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_16k(void* dst, const void* src, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16384, [%2];" ::"r"(
+                   s32(dst)),
+               "l"(src), "r"(s32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -121,7 +127,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     k_filter_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int L, int nq,
                 int kblocks, int nN, int nacc, int stages, const float* __restrict__ cn2,
                 const float* __restrict__ qinv, float c_inv, float* __restrict__ dt, float* __restrict__ gmin,
-                int ngroups) {
+                int ngroups, const uint16_t* __restrict__ At) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull;
@@ -166,7 +172,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         uint8_t* sA = smem + (size_t)s * stage_bytes;
         uint8_t* sB = sA + bytesA;
         mb_expect_tx(&full[s], stage_bytes);
-        tma_2d(sA, &tmA, kb * kTcBK, m0, &full[s]);
+        if (At) bulk_g2s_16k(sA, At + ((size_t)blockIdx.x * kblocks + kb) * (kTcM * kTcBK), &full[s]);
+        else tma_2d(sA, &tmA, kb * kTcBK, m0, &full[s]);
         if constexpr (CL > 1) {  // nacc == 1: this CTA's 1/CL of the query rows, to every cluster CTA
           const int rq = nN / CL;
           tma_2d_mc(sB + (size_t)crank * rq * 128, &tmB, kb * kTcBK, q0 + (int)crank * rq, &full[s], kMask);
@@ -530,9 +537,16 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   dim3 grid((tiles + CL - 1) / CL * CL, (nq + nN * nacc - 1) / (nN * nacc));  // whole clusters (extra tiles: OOB)
   const CUtensorMap& tmA = *reinterpret_cast<const CUtensorMap*>(ix.tmapA);
   const int ngroups = (ix.nlist + 31) / 32;
+  static int tiled = -1;  // VLR_FILTER_TILED=0: 2-D tensor TMA of A from the row-major fp16 copy (experiments)
+  if (tiled < 0) {
+    const char* te = getenv("VLR_FILTER_TILED");
+    tiled = te ? atoi(te) : 1;
+  }
+  const uint16_t* At = (tiled && ix.cf16t && (int)grid.x * kTcM <= ((ix.nlist + kTcM - 1) / kTcM) * kTcM)
+                           ? ix.cf16t : nullptr;
   if (CL == 1) {
     k_filter_tc<1><<<grid, kTcThreads, smem, s>>>(tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages, ix.cnorm2, qinv,
-                                                  ix.c_inv, dt, gmin, ngroups);
+                                                  ix.c_inv, dt, gmin, ngroups, At);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -549,9 +563,9 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   cfg.numAttrs = 1;
   if (CL == 4)
     return cudaLaunchKernelEx(&cfg, k_filter_tc<4>, tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages,
-                              (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups);
+                              (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups, At);
   return cudaLaunchKernelEx(&cfg, k_filter_tc<2>, tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages,
-                            (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups);
+                            (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups, At);
 }
 
 // fp16(c * scale) (round to nearest even) into a d8-padded copy; scale is a power of two
@@ -572,6 +586,38 @@ cudaError_t launch_round_f16(const float* src, int rows, int d, int d8, float sc
   long long blocks = (n + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   k_round_f16<<<(int)blocks, 256, 0, s>>>(src, rows, d, d8, scale, dst);
+  return cudaGetLastError();
+}
+
+// A operand pre-tiled and pre-swizzled (load time): At[tile][kb] = the 16 KB
+// SWIZZLE_128B image of rows [128 tile, 128 tile + 128) x cols [64 kb, 64 kb + 64)
+// of cf16 (row r at byte 128 r, its 16-byte chunk j at chunk position j ^ (r & 7);
+// rows >= L and cols >= d8 zero). One plain 1-D bulk copy of 16 KB into a
+// 1024-aligned smem stage then lands exactly what the 2-D SW128 tensor TMA
+// would, but each CTA streams a contiguous 256 KB region of HBM (the tensor
+// TMA's 128-byte row pieces at a 2 KB stride measured DRAM-locality-bound).
+__global__ void k_tile_f16(const uint16_t* __restrict__ cf16, int L, int d8, int kblocks, int ntiles,
+                           uint4* __restrict__ At) {
+  const long long n = (long long)ntiles * kblocks * 128 * 8;  // 16-byte chunks
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int pos = (int)(i & 7);                 // chunk position in the smem row
+    const int r = (int)((i >> 3) & 127);
+    const long long tk = i >> 10;                 // tile * kblocks + kb
+    const int kb = (int)(tk % kblocks), tile = (int)(tk / kblocks);
+    const int j = pos ^ (r & 7);                  // source chunk
+    const int row = tile * 128 + r, col = kb * 64 + j * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (row < L && col < d8) v = *reinterpret_cast<const uint4*>(cf16 + (size_t)row * d8 + col);
+    At[i] = v;
+  }
+}
+
+cudaError_t launch_tile_f16(const DeviceIndex& ix, cudaStream_t s) {
+  const int kblocks = (ix.d8 + kTcBK - 1) / kTcBK, ntiles = (ix.nlist + kTcM - 1) / kTcM;
+  const long long n = (long long)ntiles * kblocks * 1024;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_tile_f16<<<(int)blocks, 256, 0, s>>>(ix.cf16, ix.nlist, ix.d8, kblocks, ntiles, reinterpret_cast<uint4*>(ix.cf16t));
   return cudaGetLastError();
 }
 

@@ -63,6 +63,7 @@ struct DeviceIndex {
   float* centroids = nullptr;  // [nlist][d]
   float* cnorm2 = nullptr;     // [nlist] ||c||^2 (fp64 -> fp32); zeros for metric 1 (filter = -2<q,c>)
   uint16_t* cf16 = nullptr;    // [nlist][d8] fp16(c * 2^c_exp) (RN), zero-padded to d8 (filter operand A)
+  uint16_t* cf16t = nullptr;   // [ceil(nlist/128)][ceil(d8/64)][128][64] the same, tiled + SW128-swizzled (K1 A loads)
   int c_exp = 0;               // power-of-two centroid scale: max |c * 2^c_exp| < 2^14
   float c_inv = 1.f;           // 2^-c_exp
   alignas(64) unsigned char tmapA[128] = {};  // CUtensorMap of cf16 (box 64 x 128, SWIZZLE_128B)
@@ -148,6 +149,7 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
                              cudaStream_t s);
 cudaError_t launch_round_f16(const float* src, int rows, int d, int d8, float scale, uint16_t* dst, cudaStream_t s);
 cudaError_t make_tmap_2d(void* map, const uint16_t* base, int rows, int cols, int box_rows);
+cudaError_t launch_tile_f16(const DeviceIndex& ix, cudaStream_t s);
 cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float band_rel,
                           cudaStream_t s);
 cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s);
