@@ -122,6 +122,9 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+#ifdef VLR_K1_TRACE
+__device__ unsigned long long g_k1_trace[4096][6];  // per CTA: start, setup done, first stage full, tfull, end, smid
+#endif
 template <int CL>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_filter_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int L, int nq,
@@ -133,6 +136,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __shared__ __align__(8) uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull;
   __shared__ uint32_t tmem_base;
   __shared__ float s_inv[512];  // per query column: 2^-(e_q + e_c)
+#ifdef VLR_K1_TRACE
+  const unsigned long long tr0 = globaltimer_ns();
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * kTcM;
   const int q0 = blockIdx.y * (nN * nacc);
@@ -161,6 +167,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tbase = tmem_base;
   const uint32_t crank = CL > 1 ? cluster_rank() : 0u;
+#ifdef VLR_K1_TRACE
+  const int trc = blockIdx.x + blockIdx.y * gridDim.x;
+  if (threadIdx.x == 0 && trc < 4096) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_k1_trace[trc][0] = tr0;
+    g_k1_trace[trc][1] = globaltimer_ns();
+    g_k1_trace[trc][5] = smid;
+  }
+#endif
   constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
 
   if (warp == 0) {
@@ -192,6 +208,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int s = kb % stages;
         const uint32_t ph = (uint32_t)(kb / stages) & 1u;
         mb_wait(&full[s], ph);
+#ifdef VLR_K1_TRACE
+        if (kb == 0 && trc < 4096) g_k1_trace[trc][2] = globaltimer_ns();
+#endif
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t aaddr = s32(smem + (size_t)s * stage_bytes);
         const uint32_t baddr = aaddr + bytesA;
@@ -220,6 +239,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
     mb_wait(&tfull, 0);
+#ifdef VLR_K1_TRACE
+    if (threadIdx.x == 64 && trc < 4096) g_k1_trace[trc][3] = globaltimer_ns();
+#endif
     asm volatile("tcgen05.fence::after_thread_sync;");
     // 32 query columns at a time: dt stores (lanes = 32 consecutive centroids,
     // coalesced) and the min over this warp's 32 centroids of each column
@@ -266,6 +288,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (q < nq && c + lane < ncols_used && grp < ngroups) gmin[(size_t)q * ngroups + grp] = f[0];
     }
   }
+#ifdef VLR_K1_TRACE
+  if (threadIdx.x == 64 && trc < 4096) g_k1_trace[trc][4] = globaltimer_ns();
+#endif
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while peers may still multicast into it
@@ -611,6 +636,13 @@ __global__ void k_tile_f16(const uint16_t* __restrict__ cf16, int L, int d8, int
     At[i] = v;
   }
 }
+
+#ifdef VLR_K1_TRACE
+extern "C" int vlr_debug_k1_trace(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_k1_trace, sizeof(unsigned long long) * 6 * (n < 4096 ? n : 4096)) == cudaSuccess
+             ? 0 : -1;
+}
+#endif
 
 cudaError_t launch_tile_f16(const DeviceIndex& ix, cudaStream_t s) {
   const int kblocks = (ix.d8 + kTcBK - 1) / kTcBK, ntiles = (ix.nlist + kTcM - 1) / kTcM;
