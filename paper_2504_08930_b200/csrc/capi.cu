@@ -482,6 +482,9 @@ void vlr_index_free(vlr_index* h) {
   if (h->rel_fork) cudaEventDestroy(h->rel_fork);
   if (h->rel_join) cudaEventDestroy(h->rel_join);
   if (h->rel_stream) cudaStreamDestroy(h->rel_stream);
+  if (h->lut_fork) cudaEventDestroy(h->lut_fork);
+  if (h->lut_join) cudaEventDestroy(h->lut_join);
+  if (h->lut_stream) cudaStreamDestroy(h->lut_stream);
   free_ws(h->ws);
   free_index(h->ix);
   delete h;
@@ -530,6 +533,25 @@ static vlr_status search_impl(vlr_index* h, const float* Q, int32_t nq, int32_t 
   rec(h, 0, s);
   VLR_CUDA_TRY(launch_qprep(Q, nq, ix.d, ix.d8, w.qnorm, w.qsq, w.qf16, w.qinv, w.status, s)); ++n;
   VLR_CUDA_TRY(launch_filter_tc(w.qf16, w.qinv, nq, ix, w.dt, w.gmin, s)); ++n;
+  if (h->lut_side < 0) {
+    const char* e = getenv("VLR_LUT_SERIAL");
+    h->lut_side = (e && e[0] == '1') ? 0 : 1;
+  }
+  const bool lut_side = h->lut_side == 1 && h->profiling != 1;  // per-stage profiling keeps stages serial
+  if (lut_side) {
+    if (!h->lut_stream) {
+      VLR_CUDA_TRY(cudaStreamCreateWithFlags(&h->lut_stream, cudaStreamNonBlocking));
+      VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->lut_fork, cudaEventDisableTiming));
+      VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->lut_join, cudaEventDisableTiming));
+    }
+    // forked after K1 so K5's CTAs do not take SM slots from the filter's two waves;
+    // everything before the fork on s (incl. the previous search's scan, which
+    // read w.lut) is ordered before K5
+    VLR_CUDA_TRY(cudaEventRecord(h->lut_fork, s));
+    VLR_CUDA_TRY(cudaStreamWaitEvent(h->lut_stream, h->lut_fork, 0));
+    VLR_CUDA_TRY(launch_lut(Q, ix, w, nq, h->lut_stream)); ++n;
+    VLR_CUDA_TRY(cudaEventRecord(h->lut_join, h->lut_stream));
+  }
   rec(h, 1, s);
   VLR_CUDA_TRY(launch_select(ix, w, nq, np, filter_edot(ix.d), s)); ++n;
   rec(h, 2, s);
@@ -538,7 +560,11 @@ static vlr_status search_impl(vlr_index* h, const float* Q, int32_t nq, int32_t 
   rec(h, 3, s);
   VLR_CUDA_TRY(launch_offsets(w, nq, np, s)); ++n;
   rec(h, 4, s);
-  VLR_CUDA_TRY(launch_lut(Q, ix, w, nq, s)); ++n;
+  if (lut_side) {
+    VLR_CUDA_TRY(cudaStreamWaitEvent(s, h->lut_join, 0));
+  } else {
+    VLR_CUDA_TRY(launch_lut(Q, ix, w, nq, s)); ++n;
+  }
   rec(h, 5, s);
   if (rel) VLR_CUDA_TRY(cudaMemsetAsync(w.qdone, 0, sizeof(unsigned long long) * nq, s));
   VLR_CUDA_TRY(launch_scan(ix, w, nq, np, k, s, rel)); ++n;

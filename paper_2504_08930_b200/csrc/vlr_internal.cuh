@@ -133,6 +133,11 @@ struct vlr_index {
   std::mutex mu;  // held while a search is enqueued and while vlr_update_hot swaps the residency
   cudaStream_t rel_stream = nullptr;  // NEXT-4 merger stream + fork/join events (created on first use)
   cudaEvent_t rel_fork = nullptr, rel_join = nullptr;
+  // K5 side stream: the LUT depends only on Q (residual decomposition),
+  // so it runs beside K2-K4 (latency-bound, few CTAs) and joins before the scan
+  cudaStream_t lut_stream = nullptr;
+  cudaEvent_t lut_fork = nullptr, lut_join = nullptr;
+  int lut_side = -1;  // -1 unset; 0 serial (VLR_LUT_SERIAL=1, A/B timing), 1 forked
   std::string last_err;
 };
 
