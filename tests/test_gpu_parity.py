@@ -654,3 +654,33 @@ def test_filter_variant_parity(flag, val):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_lut_side_stream_equals_serial(c1_index, c1_queries, monkeypatch):
+    """K5 on its forked side stream (default) vs the serial order
+    (VLR_LUT_SERIAL=1): bitwise-identical results, also for back-to-back
+    searches with different query batches on one stream without a sync in
+    between (the fork must order K5 after the previous search's scan, which
+    read the same LUT buffer)."""
+    c = datagen.CONFIGS["C1"]
+    Qa = torch.from_numpy(np.ascontiguousarray(c1_queries)).cuda()
+    Qb = torch.from_numpy(np.ascontiguousarray(c1_queries[::-1])).cuda()
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("VLR_LUT_SERIAL", mode)  # read once per handle at its first search
+        h = vlr.Index.from_arrays(c1_index)
+        outs = []
+        for Q in (Qa, Qb, Qa, Qb):
+            outs.append(h.search(Q, c["nprobe"], c["k"], sync=False))
+        torch.cuda.synchronize()
+        res[mode] = [[t.cpu().numpy() for t in o] for o in outs]
+        h.close()
+    for a, b in zip(res["0"], res["1"]):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    for i in (0, 1):  # the repeated batches agree with their first run
+        for x, y in zip(res["0"][i], res["0"][i + 2]):
+            assert np.array_equal(x, y)
+    errs = check(c1_index, c1_queries, dict(zip(("ids", "dist", "miss", "probes"), res["0"][0])),
+                 oracle.search(c1_index, c1_queries, c["nprobe"], c["k"]), idmap=oracle.IdMap(c1_index))
+    assert not errs, errs
