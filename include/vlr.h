@@ -111,6 +111,9 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
 /*
  * Batched search (stream-ordered, no host synchronisation; CUDA-graph
  * capturable once vlr_reserve has sized the workspace for (nq, nprobe, k)).
+ * Internally the LUT build runs on a handle-owned side stream forked from and
+ * joined back to `stream` with events (VLR_LUT_SERIAL=1 keeps it on `stream`);
+ * all work is complete when `stream`'s work up to this call is complete.
  *
  *  d_queries [nq][d] device fp32.   nq >= 0 (nq == 0 is a no-op).
  *  nprobe >= 1; clamped to nprobe' = min(nprobe, nlist); nprobe' <= 2048
