@@ -373,18 +373,22 @@ __device__ __forceinline__ double scalar_exact(const double* __restrict__ qs, co
 // K3a: exact fp64 D of every listed candidate, 4 warps per CTA, warp <-> 32
 // candidates of one query; grid (nq, kCandCap / 128). CTAs past the query's
 // candidate count (or queries whose list overflowed) exit at once.
+// product configuration (S, W) = (3, 4): 56 KB of shared memory per CTA -> 4 CTAs/SM, so the ~512
+// non-empty CTAs of a 256-query C4 batch run in one round (S = 4: 72 KB, 3 CTAs/SM, two rounds).
+// Measured K3a+K3b at C4 (tools/k3a_sweep.sh, profiles/k3a_sweep_r01.txt): (4,4) 0.087-0.088 ms,
+// (3,4) 0.070, (2,4) 0.071, (2,8) 0.075, (2,2) 0.073, (4,2) 0.093. VLR_EXACT_CFG=S,W selects another.
 constexpr int kExactWarps = 4;
-constexpr int kExactStages = 4;
+constexpr int kExactStages = 3;
 
-template <int MET>
-__global__ void __launch_bounds__(kExactWarps * 32) k_exact(const float* __restrict__ Q, const float* __restrict__ C,
-                                                            int d, const int32_t* __restrict__ cand,
-                                                            const int32_t* __restrict__ ncand,
-                                                            double* __restrict__ exact) {
+template <int MET, int S, int W>
+__global__ void __launch_bounds__(W * 32) k_exact(const float* __restrict__ Q, const float* __restrict__ C,
+                                                  int d, const int32_t* __restrict__ cand,
+                                                  const int32_t* __restrict__ ncand,
+                                                  double* __restrict__ exact) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int q = blockIdx.x;
   const int nc = ncand[q];
-  const int g0 = blockIdx.y * kExactWarps * 32;
+  const int g0 = blockIdx.y * W * 32;
   if (nc > kCandCap || g0 >= nc) return;
   double* qs = reinterpret_cast<double*>(sm);
   float* tiles = reinterpret_cast<float*>(qs + ((d + 1) & ~1));
@@ -393,36 +397,50 @@ __global__ void __launch_bounds__(kExactWarps * 32) k_exact(const float* __restr
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t* lst = cand + (size_t)q * kCandCap;
   // groups of 32 candidates: this warp takes g = g0 + 32*warp + stride*i
-  const int stride = gridDim.y * kExactWarps * 32;
+  const int stride = gridDim.y * W * 32;
   for (int g = g0 + warp * 32; g < nc; g += stride) {
     const int j = g + lane;
     const int rid = lst[j < nc ? j : g];
     double D;
     if ((d & 3) == 0)
-      D = warp_exact<kExactStages, MET>(qs, C, d, rid, tiles + warp * (kExactStages * 1024), lane);
+      D = warp_exact<S, MET>(qs, C, d, rid, tiles + warp * (S * 1024), lane);
     else
       D = scalar_exact<MET>(qs, C, d, rid);
     if (j < nc) exact[(size_t)q * kCandCap + j] = D;
   }
 }
 
-size_t exact_smem(int d) {
-  return (size_t)((d + 1) & ~1) * sizeof(double) + (size_t)kExactWarps * kExactStages * 1024 * sizeof(float);
-}
-
-cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
-  if (nq <= 0) return cudaSuccess;
-  const size_t sm = exact_smem(ix.d);
+template <int S, int W>
+static cudaError_t launch_exact_t(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
+  const size_t sm = (size_t)((ix.d + 1) & ~1) * sizeof(double) + (size_t)W * S * 1024 * sizeof(float);
   static size_t configured[2] = {0, 0};
-  auto fn = ix.metric == 1 ? k_exact<1> : k_exact<0>;
+  auto fn = ix.metric == 1 ? k_exact<1, S, W> : k_exact<0, S, W>;
   if (sm > 48 * 1024 && sm > configured[ix.metric]) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     configured[ix.metric] = sm;
   }
-  dim3 grid(nq, 8);  // 8 x 4 warps; queries with > 1024 candidates loop
-  fn<<<grid, kExactWarps * 32, sm, s>>>(Q, ix.centroids, ix.d, ws.cand, ws.ncand, ws.exact);
+  dim3 grid(nq, 1024 / (W * 32));  // 1024 candidates per pass; queries with more loop
+  fn<<<grid, W * 32, sm, s>>>(Q, ix.centroids, ix.d, ws.cand, ws.ncand, ws.exact);
   return cudaGetLastError();
+}
+
+cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
+  if (nq <= 0) return cudaSuccess;
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* e = getenv("VLR_EXACT_CFG");
+    cfg = 34;
+    if (e && e[0] && e[1] == ',' && e[2]) cfg = (e[0] - '0') * 10 + (e[2] - '0');
+  }
+  switch (cfg) {
+    case 24: return launch_exact_t<2, 4>(Q, ix, ws, nq, s);
+    case 44: return launch_exact_t<4, 4>(Q, ix, ws, nq, s);
+    case 28: return launch_exact_t<2, 8>(Q, ix, ws, nq, s);
+    case 22: return launch_exact_t<2, 2>(Q, ix, ws, nq, s);
+    case 42: return launch_exact_t<4, 2>(Q, ix, ws, nq, s);
+    default: return launch_exact_t<kExactStages, kExactWarps>(Q, ix, ws, nq, s);
+  }
 }
 
 template <int MET>
