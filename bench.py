@@ -59,6 +59,10 @@ def parse():
     p.add_argument("--ncu", action="store_true", help="short run for ncu: no e2e/oracle/clocks")
     p.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampling")
     p.add_argument("--dump-lat", default=None, help="diagnostics: write per-step latencies (ms) and scan times here")
+    p.add_argument("--dry-run-1gpu", action="store_true",
+                   help="N > 1 plumbing on ONE shared GPU: gloo process group, shard-only handles, the staged "
+                        "sharded search with the exchanges over gloo (host), vlr_merge_partials; timing is not a "
+                        "multi-GPU number")
     p.add_argument("--sweep-out", default=None,
                    help="also run the C5 batch x nprobe sweep on the same index and write JSON lines here")
     return p.parse_args()
@@ -157,17 +161,26 @@ class Clocks:
                 "power_w_max": max(pw) if pw else None}
 
 
-def dist_setup():
+def dist_setup(dry=False):
+    """One process per GPU (torchrun env). dry: every rank on cuda:0 with a gloo group."""
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if dry else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dry:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
+
+
+def _coll_dev():
+    import torch.distributed as dist
+    return "cpu" if dist.get_backend() == "gloo" else "cuda"
 
 
 def allmax(x, world):
@@ -175,9 +188,29 @@ def allmax(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+    t = torch.tensor([float(x)], device=_coll_dev(), dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gather_stack(t, world):
+    """rank-ordered stack [world, *t.shape] of every rank's CUDA tensor t (the
+    dry run's transport: host memory over gloo)."""
+    import torch
+    import torch.distributed as dist
+    c = t.cpu() if _coll_dev() == "cpu" else t.contiguous()
+    parts = [torch.empty_like(c) for _ in range(world)]
+    dist.all_gather(parts, c)
+    return torch.stack(parts).cuda()
+
+
+def all_objects(obj, world):
+    if world == 1:
+        return [obj]
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, obj)
+    return out
 
 
 def barrier(world):
@@ -295,7 +328,9 @@ def main():
     import paper_2504_08930_b200 as vlr
     from paper_2504_08930_b200 import build as vbuild
 
-    rank, world, local = dist_setup()
+    dry = bool(a.dry_run_1gpu)
+    rank, world, local = dist_setup(dry)
+    dry = dry and world > 1
     if world != a.gpus and rank == 0:
         print(f"warning: --gpus {a.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     if rank == 0:
@@ -310,10 +345,12 @@ def main():
     # accumulated while the index vectors are generated (N = 1 only)
     pool = datagen.make_queries(c["N"], c["d"], c["nlist"], (a.warmup + a.steps) * B, seed=a.seed, stream=2,
                                 alpha=c["alpha"], device="cuda")
-    gtq = pool[a.warmup * B:(a.warmup + 1) * B] if (world == 1 and not a.ncu) else None
+    # ground truth of the first timed batch, accumulated while the vectors are generated (N > 1: each rank
+    # over its own lists, merged below)
+    gtq = pool[a.warmup * B:(a.warmup + 1) * B] if not a.ncu else None
     ix, gen_s = gen_index(c, a.seed, rank, world, hot=hot, gt_queries=gtq)
     nccl_id = None
-    if world > 1:
+    if world > 1 and not dry:
         import torch.distributed as dist
         obj = [vlr.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -332,8 +369,22 @@ def main():
              torch.empty(B, NP, dtype=torch.uint8, device="cuda"), torch.empty(B, NP, dtype=torch.int32, device="cuda"))
             for _ in range(a.steps)]
     stream = torch.cuda.current_stream()
+
+    def step(Q, out):
+        """one batch search: the collective NCCL search, or (dry run) the staged sharded search with the
+        exchanges over gloo and the partial top-k merged by vlr_merge_partials"""
+        if not dry:
+            h.search(Q, c["nprobe"], K, out=out, stream=stream)
+            return
+        ids, dd, miss, prb = h.search_staged(Q, c["nprobe"], K, lambda t: gather_stack(t, world), stream=stream)
+        mi, md = vlr.merge_partials(gather_stack(ids, world), gather_stack(dd, world), stream=stream)
+        out[0].copy_(mi)
+        out[1].copy_(md)
+        out[2].copy_(miss)
+        out[3].copy_(prb)
+
     for i in range(a.warmup):
-        h.search(Qdev[i], c["nprobe"], K, out=outs[0], stream=stream)
+        step(Qdev[i], outs[0])
     torch.cuda.synchronize()
     h.set_profiling(2)  # timed region: only the two events around the scan (roofline), nothing else
     launches = h.last_launch_count
@@ -348,7 +399,7 @@ def main():
     e0.record(stream)
     for i in range(a.steps):
         ev[i][0].record(stream)
-        h.search(Qdev[a.warmup + i], c["nprobe"], K, out=outs[i], stream=stream)
+        step(Qdev[a.warmup + i], outs[i])
         ev[i][1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -365,7 +416,7 @@ def main():
     h.set_profiling(1)
     nprof = min(a.steps, 16)
     for i in range(nprof):
-        h.search(Qdev[a.warmup + i], c["nprobe"], K, out=outs[i], stream=stream)
+        step(Qdev[a.warmup + i], outs[i])
     torch.cuda.synchronize()
     h.set_profiling(False)
     stages = [h.stage_times(back=j) for j in range(nprof)]
@@ -396,7 +447,7 @@ def main():
         pass
     # ---- e2e through the C-ABI with host buffers (pinned), copies inside the timed region
     e2e = None
-    if not a.ncu:
+    if not a.ncu and not dry:
         ne = a.e2e_steps or a.steps
         hq = torch.from_numpy(pool[: B * ne].reshape(ne, B, c["d"]).copy()).pin_memory()
         hid = torch.empty(B, K, dtype=torch.int64).pin_memory()
@@ -446,14 +497,25 @@ def main():
     par = None
     if rank == 0 and world == 1 and not a.no_oracle and not a.ncu:
         cpu, par = oracle_leg(a, c, ix, hot, pool, outs)
+    if world > 1 and not a.no_oracle and not a.ncu:
+        par = dist_parity_leg(a, c, ix, hot, pool, outs, owners, rank, world)
     recall = None
     if getattr(ix, "gt_ids", None) is not None:
+        gt_ids = ix.gt_ids
+        if world > 1:  # each rank's GT covers its own lists: merge the partial top-10s by (dist, id)
+            parts = all_objects((ix.gt_ids, ix.gt_dist), world)
+            ci = np.concatenate([p[0] for p in parts], 1)
+            cd = np.concatenate([p[1] for p in parts], 1)
+            o = np.lexsort((ci, cd), axis=1)[:, :ix.gt_ids.shape[1]]
+            gt_ids = np.take_along_axis(ci, o, 1)
         got = outs[0][0].cpu().numpy()
         kk = min(10, K)
-        r = [len(set(g[:kk].tolist()) & set(t[:kk].tolist())) / kk for g, t in zip(got, ix.gt_ids)]
+        r = [len(set(g[:kk].tolist()) & set(t[:kk].tolist())) / kk for g, t in zip(got, gt_ids)]
+        cover = "all N float vectors" if hot is None else "the vectors generated on this node"
         recall = {"recall_at_10": float(np.mean(r)), "queries": len(r),
-                  "ground_truth": "exact fp32 flat search over all N float vectors (regenerated during index "
-                                  "generation), first timed batch; results are bitwise identical at any G (R5)"}
+                  "ground_truth": f"exact fp32 flat search over {cover} (regenerated during index generation"
+                                  + (", each rank over its own lists, merged" if world > 1 else "")
+                                  + "), first timed batch"}
     # ---- coarse contraction (K1, tcgen05 kind::f16): 2*B*L*d flops per launch; the stage
     # also holds the tiny q-prep kernel, so this understates K1's own rate slightly
     cf_ms = float(stage_mean["coarse_filter"]) if stage_mean else None
@@ -478,14 +540,21 @@ def main():
                            "all_hit_share": float((hq == 1.0).mean()), "all_miss_share": float((hq == 0.0).mean())},
                  "calibration_mass": c["hot_mass"]}
     value = a.steps * B / (ms_total * 1e-3)
+    # per-rank work share (the size-based deal balances bytes, not traffic)
+    shares = np.array(all_objects(float(step_bytes.sum()), world))
+    work_share = float(shares.max() / max(shares.mean(), 1.0))
     if rank == 0:
         line = {
             "metric": metric_name(B, c["nprobe"], K), "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": ms_total / a.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic (seeded clustered embeddings, Zipf-skewed queries; generated on the GPU)",
+            "dtype": "f32", "dry_run": dry, "data": "synthetic (seeded clustered embeddings, Zipf-skewed queries; generated on the GPU)",
             "config": {"workload": workload_name(c, a.config), "N": c["N"], "d": c["d"], "nlist": c["nlist"], "m": c["m"],
                        "nprobe": c["nprobe"], "k": K, "batch": B, "alpha": c["alpha"], "hot_mass": c["hot_mass"],
-                       "seed": a.seed, "parallelism": f"hot-list shards x{world}, NCCL partial top-k merge",
+                       "seed": a.seed,
+                       "parallelism": (f"hot-list shards x{world}, centroid-sharded coarse stage, "
+                                       + ("exchanges over gloo through host memory, all ranks on ONE GPU (dry run)"
+                                          if dry else "NCCL all-gathers + GPU merge-select")) if world > 1
+                                      else "one GPU",
                        "l2": "inputs larger than L2 (index %.1f GB/GPU, %.2f GB scanned per batch)" % (
                            info["bytes_on_device"] / 1e9, float(step_bytes.mean()) / 1e9)},
             "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
@@ -499,6 +568,7 @@ def main():
             "stage_ms_source": "separate untimed pass (16 searches) with CUDA events at every stage boundary; "
                                "the timed region records only the two events around the scan",
             "hit_rate_mean": float(np.mean(np.concatenate(hit))),
+            "work_share_max_over_mean": work_share,
             "residency": residency,
             "e2e": e2e, "clocks": clk, "cpu_baseline": cpu, "parity_sample": par, "recall": recall,
             "release": release,
@@ -652,6 +722,46 @@ def sweep(a, c, h, pool, world, rank, gt=None):
         with open(a.sweep_out, "w") as f:
             for ln in lines:
                 f.write(json.dumps(ln) + "\n")
+
+
+def dist_parity_leg(a, c, ix, hot, pool, outs, owners, rank, world, S=32):
+    """N > 1 sampled parity (the hybrid = monolithic rule S:473): every rank runs the
+    oracle over the lists it owns (its codes are the only ones generated on it), computes dist_ref of the
+    returned ids it owns, and rank 0 merges the rank partials into the oracle over all resident lists and
+    checks the GPU's final rows (identical on every rank) with rules R1-R4."""
+    import oracle
+    from parity import check, merge_partials_np
+    oracle.build()
+    B = c["batch"]
+    S = min(S, B)
+    Qs = pool[a.warmup * B:a.warmup * B + S]
+    mine = np.nonzero(owners == rank)[0].astype(np.int32)
+    t = time.time()
+    part = oracle.search(ix, Qs, c["nprobe"], c["k"], hot=mine, nthreads=max(1, oracle.default_threads() // 2))
+    el = time.time() - t
+    g = outs[0]
+    gpu = dict(ids=g[0].cpu().numpy()[:S], dist=g[1].cpu().numpy()[:S], miss=g[2].cpu().numpy()[:S],
+               probes=g[3].cpu().numpy()[:S])
+    valid = gpu["ids"] >= 0
+    rows = np.repeat(np.arange(S)[:, None], gpu["ids"].shape[1], 1)[valid]
+    idmap = oracle.IdMap(ix)
+    ok, lst, _ = idmap.locate(gpu["ids"][valid])
+    here = ok & (owners[lst] == rank)
+    ref = np.full(len(rows), np.nan)
+    if here.any():
+        ref[here] = oracle.dist_ref(ix, Qs, rows[here], gpu["ids"][valid][here], idmap=idmap)
+    parts = all_objects(dict(part=part, ref=ref, here=here, el=el), world)
+    if rank != 0:
+        return None
+    orc = merge_partials_np([p["part"] for p in parts], c["k"])
+    ref_all = np.full(len(rows), np.nan)
+    for p in parts:
+        ref_all[p["here"]] = p["ref"][p["here"]]
+    errs = check(ix, Qs, gpu, orc, hot=hot, idmap=idmap, ref=ref_all)
+    return {"queries": S, "ranks": world,
+            "rules": "R1 probes+mask bit-exact, R2 dist 1e-5 rel, R3 id sets, R4 order/padding; oracle run per "
+                     "rank over its own lists and merged on rank 0 (hybrid = monolithic)",
+            "pass": not errs, "errors": errs[:3], "oracle_s_max_rank": max(p["el"] for p in parts)}
 
 
 def oracle_leg(a, c, ix, hot, pool, outs):

@@ -15,8 +15,10 @@
  *  - "host" pointers are ordinary CPU memory (pinned or pageable);
  *    "device" pointers are CUDA global memory on the index's device.
  *  - Streams are passed as void* (a cudaStream_t); NULL = legacy default.
- *  - One in-flight search per index handle (the workspace is per handle);
- *    distinct handles are independent.
+ *  - One in-flight search per index handle (the workspace is per handle):
+ *    calls on one handle from several host threads are serialised while they
+ *    enqueue, and must pass the SAME stream so that the device work is
+ *    ordered too; distinct handles are independent.
  *  - There is no CPU fallback: every step of search runs in this library's
  *    sm_100a kernels. Without a usable GPU, load_index fails with VLR_ERR_CUDA.
  */
@@ -30,7 +32,7 @@ extern "C" {
 #endif
 
 #define VLR_VERSION_MAJOR 1
-#define VLR_VERSION_MINOR 2
+#define VLR_VERSION_MINOR 3
 
 typedef struct vlr_index vlr_index; /* opaque; created by vlr_load_index, freed by vlr_index_free */
 
@@ -92,10 +94,30 @@ typedef struct {
  *   (the 128-byte ncclUniqueId, created by rank 0 and broadcast by the caller,
  *   e.g. through torch.distributed); vlr_load_index and vlr_search* are then
  *   COLLECTIVE: every rank calls them with identical arguments (SPMD).
+ *   Partitioning: the hot lists are dealt over
+ *   the ranks (below), and the COARSE QUANTIZER is sharded too: rank r filters
+ *   only its contiguous range of 128-centroid tiles, the ranks exchange their
+ *   nprobe' smallest group minima (all-gather 1), each rank refines its own
+ *   candidates exactly and the ranks exchange their sorted top-nprobe' exact
+ *   (distance, cluster) lists (all-gather 2); every rank then holds the exact
+ *   global probes (bitwise those of world == 1). The partial top-k of the
+ *   owned probes are all-gathered and merged on every rank (all-gather 3).
+ *   The communicator is non-blocking: every NCCL step, and vlr_search's wait,
+ *   is bounded by the environment variable VLR_NCCL_TIMEOUT_MS (default
+ *   300000); an NCCL error or that timeout aborts the communicator and
+ *   returns VLR_ERR_NCCL (the handle is then unusable; free it).
+ *   VLR_COARSE_REPLICATED=1 at load: every rank runs the full coarse stage
+ *   instead (no coarse exchanges; for comparison).
  * world > 1 with nccl_unique_id == NULL: "shard-only" mode: this handle holds
- *   rank `rank`'s share of the hot lists and search returns this shard's
- *   PARTIAL top-k; combine shards with vlr_merge_partials (used to test
- *   sharding on one GPU).
+ *   rank `rank`'s share of the hot lists. vlr_search runs the replicated
+ *   coarse stage and returns this shard's PARTIAL top-k; the staged calls
+ *   (vlr_coarse_stage1/2, vlr_search_stage3) run the sharded coarse stage
+ *   with the exchanges done by the caller. Combine shards with
+ *   vlr_merge_partials. (Used to test sharding on one GPU, and for callers
+ *   that bring their own transport.)
+ * Fault injection (tests): VLR_FAULT_STALL_US=n delays every search of a
+ *   handle with a communicator by a bounded n-microsecond device stall before
+ *   its first collective.
  */
 typedef struct {
   int32_t rank;
@@ -140,7 +162,9 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
 vlr_status vlr_search_async(vlr_index* idx, const float* d_queries, int32_t nq, int32_t nprobe, int32_t k,
                             int64_t* d_ids, float* d_dist, uint8_t* d_miss, int32_t* d_probes, void* stream);
 
-/* vlr_search_async + stream synchronisation + device status check. */
+/* vlr_search_async + wait for completion + device status check. With a
+ * communicator the wait polls the stream and the communicator's asynchronous
+ * error state, bounded by VLR_NCCL_TIMEOUT_MS (-> VLR_ERR_NCCL, see above). */
 vlr_status vlr_search(vlr_index* idx, const float* d_queries, int32_t nq, int32_t nprobe, int32_t k,
                       int64_t* d_ids, float* d_dist, uint8_t* d_miss, int32_t* d_probes, void* stream);
 
@@ -209,6 +233,35 @@ int32_t vlr_wait_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, int64_
  * completion. A non-finite query is reported by the next call on the handle. */
 vlr_status vlr_search_host_async(vlr_index* idx, const float* h_queries, int32_t nq, int32_t nprobe, int32_t k,
                                  int64_t* h_ids, float* h_dist, uint8_t* h_miss, int32_t* h_probes, void* stream);
+
+/*
+ * Staged search (shard-only handles: world > 1, nccl_unique_id == NULL): the
+ * collective search of one batch cut at its exchange points, so that the
+ * caller moves the data between ranks (any transport). Every rank calls, in
+ * order, on the same stream, with the same queries and arguments:
+ *  1. vlr_coarse_stage1 -> d_x1 [nq][nprobe'] fp32 (device): this rank's
+ *     nprobe' smallest filter group minima (K1 on its centroid tiles, K2).
+ *     The caller all-gathers x1 in rank order -> x1_all [world][nq][nprobe'].
+ *  2. vlr_coarse_stage2(x1_all) -> d_x2 [nq][nprobe'] 16-byte entries
+ *     {double D; int32 l; int32 pad} (device): this rank's candidates refined
+ *     exactly (fp64), its top nprobe' sorted by (D, l),
+ *     padding (+inf, -1). The caller all-gathers x2 -> x2_all
+ *     [world][nq][nprobe'] entries.
+ *  3. vlr_search_stage3(x2_all) -> the exact global probes and miss mask (as
+ *     vlr_search_async, identical on every rank) and THIS SHARD's partial
+ *     top-k in d_ids / d_dist; the caller gathers the partials and merges them
+ *     with vlr_merge_partials.
+ * Constraints: world x nprobe' <= 16384; 1 <= k <= 32; nq >= 1; the calls of
+ * one batch must not be interleaved with other searches on the handle
+ * (INVALID_ARG otherwise). Status and errors as vlr_search_async.
+ */
+vlr_status vlr_coarse_stage1(vlr_index* idx, const float* d_queries, int32_t nq, int32_t nprobe, float* d_x1,
+                             void* stream);
+vlr_status vlr_coarse_stage2(vlr_index* idx, const float* d_queries, int32_t nq, int32_t nprobe,
+                             const float* d_x1_all, void* d_x2, void* stream);
+vlr_status vlr_search_stage3(vlr_index* idx, const float* d_queries, int32_t nq, int32_t nprobe, int32_t k,
+                             const void* d_x2_all, int64_t* d_ids, float* d_dist, uint8_t* d_miss,
+                             int32_t* d_probes, void* stream);
 
 /* Pre-size the per-handle workspace for batches up to (max_nq, max_nprobe, max_k)
  * so that later searches allocate nothing (required before graph capture). */

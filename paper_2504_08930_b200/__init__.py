@@ -22,7 +22,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "NONFINITE", 4: "UNKN
 
 # every symbol include/vlr.h declares (checked by tests/test_abi.py)
 EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_search_host_async",
-           "vlr_search_release_async",
+           "vlr_search_release_async", "vlr_coarse_stage1", "vlr_coarse_stage2", "vlr_search_stage3",
            "vlr_poll_ready", "vlr_wait_ready", "vlr_reserve", "vlr_deal_owners", "vlr_update_hot",
            "vlr_merge_partials", "vlr_access_counts", "vlr_index_info", "vlr_index_owners", "vlr_set_profiling", "vlr_stage_times",
            "vlr_last_launch_count", "vlr_nccl_unique_id", "vlr_index_free", "vlr_last_error", "vlr_version"]
@@ -67,6 +67,9 @@ def lib():
             "vlr_search_host": [P, P, I32, I32, I32, P, P, P, P, P],
             "vlr_search_host_async": [P, P, I32, I32, I32, P, P, P, P, P],
             "vlr_search_release_async": [P, P, I32, I32, I32, P, P, P, P, P, ctypes.c_uint32, P],
+            "vlr_coarse_stage1": [P, P, I32, I32, P, P],
+            "vlr_coarse_stage2": [P, P, I32, I32, P, P, P],
+            "vlr_search_stage3": [P, P, I32, I32, I32, P, P, P, P, P, P],
             "vlr_reserve": [P, I32, I32, I32],
             "vlr_deal_owners": [P, I32, P, P, I32, I32, P],
             "vlr_update_hot": [P, P],
@@ -204,6 +207,55 @@ class Index:
         _check(fn(self._h, Q.data_ptr(), nq, nprobe, k, ids.data_ptr(), dist.data_ptr(), miss.data_ptr(),
                   prb.data_ptr() if prb is not None else None, _stream_handle(stream)))
         return out
+
+    # ------------------------------------------------------------------ staged (caller-exchanged) search
+    def coarse_stage1(self, Q, nprobe: int, stream=None):
+        """vlr_coarse_stage1 -> x1: float32 CUDA [nq, nprobe'] (this rank's
+        nprobe' smallest filter group minima)."""
+        import torch
+        assert Q.is_cuda and Q.dtype == torch.float32 and Q.is_contiguous()
+        nq, npr = int(Q.shape[0]), min(nprobe, self.nlist)
+        x1 = torch.empty(nq, npr, dtype=torch.float32, device=Q.device)
+        _check(lib().vlr_coarse_stage1(self._h, Q.data_ptr(), nq, nprobe, x1.data_ptr(), _stream_handle(stream)))
+        return x1
+
+    def coarse_stage2(self, Q, nprobe: int, x1_all, stream=None):
+        """vlr_coarse_stage2(x1_all [world, nq, nprobe'] float32 CUDA) -> x2:
+        int64 CUDA [nq, nprobe', 2] (16-byte {double D; int32 l; int32 pad}
+        entries: this rank's sorted exact top-nprobe')."""
+        import torch
+        nq, npr = int(Q.shape[0]), min(nprobe, self.nlist)
+        x1_all = x1_all.contiguous()
+        x2 = torch.empty(nq, npr, 2, dtype=torch.int64, device=Q.device)
+        _check(lib().vlr_coarse_stage2(self._h, Q.data_ptr(), nq, nprobe, x1_all.data_ptr(), x2.data_ptr(),
+                                       _stream_handle(stream)))
+        return x2
+
+    def search_stage3(self, Q, nprobe: int, k: int, x2_all, out=None, stream=None):
+        """vlr_search_stage3(x2_all [world, nq, nprobe', 2] int64 CUDA) ->
+        (ids, dist, miss, probes): global probes / mask, THIS shard's partial top-k."""
+        import torch
+        nq, npr = int(Q.shape[0]), min(nprobe, self.nlist)
+        if out is None:
+            dev = Q.device
+            out = (torch.empty(nq, k, dtype=torch.int64, device=dev), torch.empty(nq, k, dtype=torch.float32, device=dev),
+                   torch.empty(nq, npr, dtype=torch.uint8, device=dev), torch.empty(nq, npr, dtype=torch.int32, device=dev))
+        ids, dist, miss, prb = out
+        x2_all = x2_all.contiguous()
+        _check(lib().vlr_search_stage3(self._h, Q.data_ptr(), nq, nprobe, k, x2_all.data_ptr(), ids.data_ptr(),
+                                       dist.data_ptr(), miss.data_ptr(), prb.data_ptr() if prb is not None else None,
+                                       _stream_handle(stream)))
+        return out
+
+    def search_staged(self, Q, nprobe: int, k: int, allgather, stream=None, out=None):
+        """The sharded collective search with a caller-supplied transport:
+        allgather(t) must return the rank-ordered stack [world, *t.shape] of
+        every rank's t (a CUDA tensor), e.g. over torch.distributed. Returns
+        (ids, dist, miss, probes) with this shard's PARTIAL top-k (merge the
+        gathered partials with merge_partials)."""
+        x1 = self.coarse_stage1(Q, nprobe, stream=stream)
+        x2 = self.coarse_stage2(Q, nprobe, allgather(x1), stream=stream)
+        return self.search_stage3(Q, nprobe, k, allgather(x2), out=out, stream=stream)
 
     def search_release(self, Q, nprobe: int, k: int, stream=None, on_ready=None, timeout_s: float = 30.0,
                        out=None):

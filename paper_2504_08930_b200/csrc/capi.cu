@@ -7,11 +7,14 @@
 #include <chrono>
 #include <ctime>
 #include <limits>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <cub/device/device_radix_sort.cuh>
 #include <numeric>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -22,6 +25,25 @@ namespace vlr {
 
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+
+cudaError_t ensure_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;  // (device, kernel) -> configured bytes
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({dev, fn});
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  if (bytes > 48 * 1024) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+  }
+  cudaFuncAttributes fa;  // forces the (lazy) module load now, not inside a later fork/spin
+  if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return e;
+  done[{dev, fn}] = std::max(bytes, it != done.end() ? it->second : (size_t)0);
+  return cudaSuccess;
+}
 
 static vlr_status fail(vlr_status st, const std::string& msg) {
   g_err = msg;
@@ -53,7 +75,7 @@ __global__ void k_negative(const int64_t* ids, long long n, int32_t* flag) {
 }
 
 static void free_ws(Workspace& w) {
-  void* ps[] = {w.qnorm, w.qsq, w.qf16, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.qdone, w.lut,
+  void* ps[] = {w.qnorm, w.qsq, w.qf16, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.x1, w.x1_all, w.x2, w.x2_all, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.qdone, w.lut,
                 w.pdist, w.pid, w.send, w.recv, w.d_q, w.d_ids, w.d_dist, w.d_miss, w.d_probes, w.status};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -92,6 +114,12 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   VLR_CUDA_TRY(dalloc(&w.cand, nqs * kCandCap));
   VLR_CUDA_TRY(dalloc(&w.ncand, nqs));
   VLR_CUDA_TRY(dalloc(&w.exact, nqs * kCandCap));
+  VLR_CUDA_TRY(dalloc(&w.x1, nqs * cnp));
+  VLR_CUDA_TRY(dalloc(&w.x2, nqs * cnp));
+  if (ix.world > 1 || ix.nccl) {  // gathered coarse-stage buffers (NCCL or the caller's transport, vlr_coarse_stage*)
+    VLR_CUDA_TRY(dalloc(&w.x1_all, nqs * cnp * ix.world));
+    VLR_CUDA_TRY(dalloc(&w.x2_all, nqs * cnp * ix.world));
+  }
   VLR_CUDA_TRY(dalloc(&w.bound, nqs));
   VLR_CUDA_TRY(dalloc(&w.probes, nqs * cnp));
   VLR_CUDA_TRY(dalloc(&w.term1, nqs * cnp));
@@ -101,7 +129,7 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   VLR_CUDA_TRY(dalloc(&w.qtot, nqs));
   VLR_CUDA_TRY(dalloc(&w.qdone, nqs));
   VLR_CUDA_TRY(dalloc(&w.lut, nqs * ix.npairs * (ix.lut_pair_bytes / 4)));
-  const size_t nslots = ((size_t)w.n_cta * kReleaseWaves + nqs) * kScanWarps * ck;  // slot (c + q + wave * n_cta)
+  const size_t nslots = ((size_t)w.n_cta * kMaxReleaseWaves + nqs) * kScanWarps * ck;  // slot (c + q + wave * n_cta)
   VLR_CUDA_TRY(dalloc(&w.pdist, nslots));
   VLR_CUDA_TRY(dalloc(&w.pid, nslots));
   if (ix.nccl) {  // exchange buffers (world > 1 with a communicator, or the forced 1-rank exchange)
@@ -156,6 +184,102 @@ static void deal(const int64_t* offs, const int64_t* counts, const int32_t* hot,
   }
 }
 
+// ---------------------------------------------------------------- NCCL (non-blocking communicator)
+// The communicator is created non-blocking (ncclConfig_t.blocking = 0), so no
+// NCCL call can hang the caller: every call that returns ncclInProgress is
+// polled with ncclCommGetAsyncError up to VLR_NCCL_TIMEOUT_MS (default 300000 ms);
+// an error or a timeout aborts the communicator (ncclCommAbort makes the
+// enqueued NCCL kernels exit) and marks the handle dead -> VLR_ERR_NCCL.
+static int64_t nccl_timeout_ms() {
+  const char* e = getenv("VLR_NCCL_TIMEOUT_MS");
+  const long long v = e ? atoll(e) : 0;
+  return v > 0 ? (int64_t)v : (int64_t)300000;
+}
+
+static vlr_status nccl_dead(vlr_index* h, const std::string& what) {
+  if (h->ix.nccl) ncclCommAbort(reinterpret_cast<ncclComm_t>(h->ix.nccl));
+  h->ix.nccl = nullptr;
+  h->dead = true;
+  return fail(VLR_ERR_NCCL, what + " (communicator aborted; the index handle is unusable)");
+}
+
+// wait until a non-blocking NCCL call has completed its host-side part
+static ncclResult_t nccl_settle(ncclComm_t comm, ncclResult_t r, int64_t timeout_ms, bool* timed_out) {
+  *timed_out = false;
+  if (r != ncclInProgress) return r;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    ncclResult_t st = ncclSuccess;
+    ncclResult_t q = ncclCommGetAsyncError(comm, &st);
+    if (q != ncclSuccess) return q;
+    if (st != ncclInProgress) return st;
+    if (std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count() >
+        timeout_ms) {
+      *timed_out = true;
+      return ncclInProgress;
+    }
+    std::this_thread::yield();
+  }
+}
+
+static ncclResult_t nccl_settle_init(ncclComm_t* comm, int world, ncclUniqueId uid, int rank, ncclConfig_t* cfg,
+                                     bool* timed_out) {
+  *timed_out = false;
+  ncclResult_t r = ncclCommInitRankConfig(comm, world, uid, rank, cfg);
+  if (r != ncclInProgress) return r;
+  return nccl_settle(*comm, r, nccl_timeout_ms(), timed_out);
+}
+
+static vlr_status nccl_allgather(vlr_index* h, const void* send, void* recv, size_t bytes, cudaStream_t s,
+                                 const char* what) {
+  ncclComm_t comm = reinterpret_cast<ncclComm_t>(h->ix.nccl);
+  bool to = false;
+  ncclResult_t r = nccl_settle(comm, ncclAllGather(send, recv, bytes, ncclUint8, comm, s), nccl_timeout_ms(), &to);
+  if (to) return nccl_dead(h, std::string("ncclAllGather (") + what + ") not enqueued within VLR_NCCL_TIMEOUT_MS");
+  if (r != ncclSuccess) return nccl_dead(h, std::string("ncclAllGather (") + what + "): " + ncclGetErrorString(r));
+  return VLR_OK;
+}
+
+// a bounded device stall before the first collective of a search (VLR_FAULT_STALL_US, fault injection for
+// the timeout tests: a peer that never arrives looks like this to the waiting rank)
+__global__ void k_stall(unsigned long long ns) {
+  const unsigned long long t0 = globaltimer_ns();
+  while (globaltimer_ns() - t0 < ns) __nanosleep(1000);
+}
+static cudaError_t fault_stall(cudaStream_t s) {
+  static long long us = -1;
+  if (us < 0) {
+    const char* e = getenv("VLR_FAULT_STALL_US");
+    us = e ? atoll(e) : 0;
+  }
+  if (us <= 0) return cudaSuccess;
+  k_stall<<<1, 32, 0, s>>>((unsigned long long)us * 1000ull);
+  return cudaGetLastError();
+}
+
+// synchronise `s`; with a communicator, poll the stream and the communicator's
+// asynchronous error state instead of blocking, up to VLR_NCCL_TIMEOUT_MS
+static vlr_status wait_stream(vlr_index* h, cudaStream_t s) {
+  if (!h->ix.nccl) {
+    VLR_CUDA_TRY(cudaStreamSynchronize(s));
+    return VLR_OK;
+  }
+  ncclComm_t comm = reinterpret_cast<ncclComm_t>(h->ix.nccl);
+  const int64_t tmo = nccl_timeout_ms();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return VLR_OK;
+    if (q != cudaErrorNotReady) VLR_CUDA_TRY(q);
+    ncclResult_t st = ncclSuccess;
+    if (ncclCommGetAsyncError(comm, &st) != ncclSuccess || (st != ncclSuccess && st != ncclInProgress))
+      return nccl_dead(h, std::string("NCCL asynchronous error: ") + ncclGetErrorString(st));
+    if (std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count() > tmo)
+      return nccl_dead(h, "search did not complete within VLR_NCCL_TIMEOUT_MS (a peer rank stopped?)");
+    std::this_thread::yield();
+  }
+}
+
 }  // namespace vlr
 
 using namespace vlr;
@@ -197,6 +321,7 @@ vlr_status vlr_update_hot(vlr_index* h, const vlr_index_desc* desc) {
     DeviceIndex old = h->ix;
     n->ix.nccl = old.nccl;  // the communicator and the handle's mode stay
     n->ix.shard_only = old.shard_only;
+    n->ix.coarse_sharded = old.coarse_sharded;
     old.nccl = nullptr;
     if (n->ix.mpad != old.mpad || n->ix.npairs != old.npairs || n->ix.lut_pair_bytes != old.lut_pair_bytes) {
       free_ws(h->ws);  // scan/LUT shapes changed (e.g. a different 4-bit mode): size the workspace again
@@ -315,6 +440,12 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   ix.by_residual = D.by_residual;
   ix.device = dev;
   ix.shard_only = cm.world > 1 && cm.nccl_unique_id == nullptr;
+  {  // this rank's centroid range for the sharded coarse stage: whole 128-centroid tiles, dealt contiguously
+    const int T = (L + 127) / 128;
+    const int t_lo = (int)((int64_t)cm.rank * T / cm.world), t_hi = (int)((int64_t)(cm.rank + 1) * T / cm.world);
+    ix.c_lo = std::min(L, t_lo * 128);
+    ix.c_hi = std::min(L, t_hi * 128);
+  }
   ix.cmax = (float)std::sqrt(cmax2) * 1.0000002f;
   {  // power-of-two filter scale: max |c| 2^c_exp in [2^13, 2^14) (fp16 range), exponent clamped
     int e = 0;
@@ -459,13 +590,24 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   if ((cm.world > 1 || force_x) && cm.nccl_unique_id) {
     ncclUniqueId uid;
     std::memcpy(&uid, cm.nccl_unique_id, sizeof(uid));
-    ncclComm_t comm_h;
-    ncclResult_t r = ncclCommInitRank(&comm_h, cm.world, uid, cm.rank);
-    if (r != ncclSuccess) {
-      set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    ncclComm_t comm_h = nullptr;
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 0;  // no NCCL call may hang the caller: poll with a timeout (nccl_settle)
+    bool to = false;
+    ncclResult_t r = nccl_settle_init(&comm_h, cm.world, uid, cm.rank, &cfg, &to);
+    if (to || r != ncclSuccess) {
+      if (comm_h) ncclCommAbort(comm_h);
+      set_error(to ? std::string("ncclCommInitRankConfig: not all ranks joined within VLR_NCCL_TIMEOUT_MS")
+                   : std::string("ncclCommInitRankConfig: ") + ncclGetErrorString(r));
       return bail(VLR_ERR_NCCL);
     }
     ix.nccl = comm_h;
+  }
+  {
+    // the collective search shards the coarse stage (also on a forced 1-rank communicator, where the
+    // exchanges are self-copies: tests); VLR_COARSE_REPLICATED=1: every rank runs the full coarse stage
+    const char* rep_env = getenv("VLR_COARSE_REPLICATED");
+    ix.coarse_sharded = ix.nccl != nullptr && !(rep_env && atoi(rep_env) == 1);
   }
   *out = h;
   return VLR_OK;
@@ -496,7 +638,21 @@ vlr_status vlr_reserve(vlr_index* h, int32_t max_nq, int32_t max_nprobe, int32_t
   cudaSetDevice(h->ix.device);
   const int np = std::min(max_nprobe, h->ix.nlist);
   if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 2048");
+  std::lock_guard<std::mutex> lock(h->mu);
   return ensure_ws(h, std::max(max_nq, 1), np, max_k);
+}
+
+// device status word (mirrored to pinned host memory at the end of every search):
+// bit 0 = a non-finite query (qprep), bit 1 = the NEXT-4 merger's bounded wait
+// expired (those queries were neither merged nor released). Reported and cleared
+// by the first call that sees it.
+static vlr_status take_status(Workspace& w, const char* when) {
+  const int32_t st = *w.h_status;
+  if (!st) return VLR_OK;
+  *w.h_status = 0;
+  if (st & 1) return fail(VLR_ERR_NONFINITE, std::string("non-finite query") + when);
+  return fail(VLR_ERR_CUDA, std::string("release merger timed out waiting for the scan; the affected queries "
+                                        "were not released") + when);
 }
 
 static inline void rec(vlr_index* h, int i, cudaStream_t s) {
@@ -505,91 +661,164 @@ static inline void rec(vlr_index* h, int i, cudaStream_t s) {
     cudaEventRecord(h->ev[h->nsearch % vlr_index::kRing][i], s);
 }
 
-static vlr_status search_impl(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
-                              float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream,
-                              const Release* rel) {
-  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
-  std::lock_guard<std::mutex> lock(h->mu);
+// ---------------------------------------------------------------- the search pipeline
+// Phases (the staged API exposes the two exchange points between them; the
+// collective search runs them back to back with NCCL all-gathers):
+//  A  qprep, K1 filter (this rank's centroid tiles when sharded), LUT fork,
+//     K2 (single GPU / replicated: + K3a + K3b route; sharded: stage 1 -> x1)
+//  B  (sharded) K2 stage 2 from x1_all, K3a exact, K3b local -> x2
+//  C  (sharded: K3b merge of x2_all + route), K4b offsets, LUT join, K6 scan,
+//     K7 rank merge (-> packed entries when a communicator exchanges results)
+struct Pipe {
+  const float* Q;
+  int nq, np, k;
+  cudaStream_t s;
+  int n = 0;  // launches
+};
+
+static vlr_status lut_fork(vlr_index* h, Pipe& p) {
+  if (h->lut_side < 0) {
+    const char* e = getenv("VLR_LUT_SERIAL");
+    h->lut_side = (e && e[0] == '1') ? 0 : 1;
+  }
+  h->lut_forked = h->lut_side == 1 && h->profiling != 1;  // per-stage profiling keeps stages serial
+  if (!h->lut_forked) return VLR_OK;
+  if (!h->lut_stream) {
+    VLR_CUDA_TRY(cudaStreamCreateWithFlags(&h->lut_stream, cudaStreamNonBlocking));
+    VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->lut_fork, cudaEventDisableTiming));
+    VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->lut_join, cudaEventDisableTiming));
+  }
+  // forked after K1 so K5's CTAs do not take SM slots from the filter's waves;
+  // everything before the fork on s (incl. the previous search's scan, which
+  // read w.lut) is ordered before K5
+  VLR_CUDA_TRY(cudaEventRecord(h->lut_fork, p.s));
+  VLR_CUDA_TRY(cudaStreamWaitEvent(h->lut_stream, h->lut_fork, 0));
+  VLR_CUDA_TRY(launch_lut(p.Q, h->ix, h->ws, p.nq, h->lut_stream)); ++p.n;
+  VLR_CUDA_TRY(cudaEventRecord(h->lut_join, h->lut_stream));
+  return VLR_OK;
+}
+
+static vlr_status phase_a(vlr_index* h, Pipe& p, bool sharded, uint8_t* out_miss, int32_t* out_probes) {
+  DeviceIndex& ix = h->ix;
+  Workspace& w = h->ws;
+  VLR_CUDA_TRY(cudaMemsetAsync(w.status, 0, sizeof(int32_t), p.s));
+  rec(h, 0, p.s);
+  VLR_CUDA_TRY(launch_qprep(p.Q, p.nq, ix.d, ix.d8, w.qnorm, w.qsq, w.qf16, w.qinv, w.status, p.s)); ++p.n;
+  const int t_lo = sharded ? ix.c_lo / 128 : 0;
+  const int t_hi = sharded ? (ix.c_hi + 127) / 128 : (ix.nlist + 127) / 128;
+  VLR_CUDA_TRY(launch_filter_tc(w.qf16, w.qinv, p.nq, ix, t_lo, t_hi, w.dt, w.gmin, p.s)); ++p.n;
+  vlr_status st = lut_fork(h, p);
+  if (st != VLR_OK) return st;
+  rec(h, 1, p.s);
+  VLR_CUDA_TRY(launch_select(ix, w, p.nq, p.np, filter_edot(ix.d), sharded ? kSelStage1 : kSelFull, p.s)); ++p.n;
+  if (sharded) return VLR_OK;
+  rec(h, 2, p.s);
+  VLR_CUDA_TRY(launch_exact(p.Q, ix, w, p.nq, p.s)); ++p.n;
+  VLR_CUDA_TRY(launch_refine(p.Q, ix, w, p.nq, p.np, out_miss, out_probes, kRefRoute, p.s)); ++p.n;
+  rec(h, 3, p.s);
+  return VLR_OK;
+}
+
+static vlr_status phase_b(vlr_index* h, Pipe& p) {
+  DeviceIndex& ix = h->ix;
+  Workspace& w = h->ws;
+  VLR_CUDA_TRY(launch_select(ix, w, p.nq, p.np, filter_edot(ix.d), kSelStage2, p.s)); ++p.n;
+  rec(h, 2, p.s);
+  VLR_CUDA_TRY(launch_exact(p.Q, ix, w, p.nq, p.s)); ++p.n;
+  VLR_CUDA_TRY(launch_refine(p.Q, ix, w, p.nq, p.np, nullptr, nullptr, kRefLocal, p.s)); ++p.n;
+  return VLR_OK;
+}
+
+static vlr_status phase_c(vlr_index* h, Pipe& p, bool sharded, int64_t* out_ids, float* out_dist, uint8_t* out_miss,
+                          int32_t* out_probes, const Release* rel, bool packed) {
+  DeviceIndex& ix = h->ix;
+  Workspace& w = h->ws;
+  if (sharded) {
+    VLR_CUDA_TRY(launch_refine(p.Q, ix, w, p.nq, p.np, out_miss, out_probes, kRefMerge, p.s)); ++p.n;
+    rec(h, 3, p.s);
+  }
+  VLR_CUDA_TRY(launch_offsets(w, p.nq, p.np, p.s)); ++p.n;
+  rec(h, 4, p.s);
+  if (h->lut_forked) {
+    VLR_CUDA_TRY(cudaStreamWaitEvent(p.s, h->lut_join, 0));
+  } else {
+    VLR_CUDA_TRY(launch_lut(p.Q, ix, w, p.nq, p.s)); ++p.n;
+  }
+  rec(h, 5, p.s);
+  if (rel) VLR_CUDA_TRY(cudaMemsetAsync(w.qdone, 0, sizeof(unsigned long long) * p.nq, p.s));
+  VLR_CUDA_TRY(launch_scan(ix, w, p.nq, p.np, p.k, p.s, rel)); ++p.n;
+  rec(h, 6, p.s);
+  if (!rel) {  // release mode: the scan merged and released every row itself
+    VLR_CUDA_TRY(launch_rank_merge(ix, w, p.nq, p.np, p.k, out_ids, out_dist, packed ? w.send : nullptr, p.s)); ++p.n;
+  }
+  rec(h, 7, p.s);
+  return VLR_OK;
+}
+
+static vlr_status check_search_args(vlr_index* h, int32_t nq, int32_t nprobe, int32_t k, int* np) {
   if (h->dead) return fail(VLR_ERR_NCCL, "index unusable after an NCCL failure");
   if (nq < 0 || nprobe < 1 || k < 1) return fail(VLR_ERR_INVALID_ARG, "nq < 0, nprobe < 1 or k < 1");
   if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32 (v1)");
+  *np = std::min(nprobe, h->ix.nlist);
+  if (*np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 2048");
+  if (h->ix.world * *np > kMaxWorldProbes && h->ix.world > 1)
+    return fail(VLR_ERR_UNSUPPORTED, "world x nprobe' > 16384 (sharded coarse stage)");
+  return VLR_OK;
+}
+
+// enqueue one search; the caller holds h->mu (the workspace and the residency are per handle)
+static vlr_status search_locked(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
+                                float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream,
+                                const Release* rel) {
+  int np = 0;
+  vlr_status st = check_search_args(h, nq, nprobe, k, &np);
+  if (st != VLR_OK) return st;
   DeviceIndex& ix = h->ix;
-  const int np = std::min(nprobe, ix.nlist);
-  if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 2048");
   h->launches = 0;
   if (nq == 0) return VLR_OK;
   if (!Q || !out_ids || !out_dist || !out_miss) return fail(VLR_ERR_INVALID_ARG, "null buffer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   VLR_CUDA_TRY(cudaSetDevice(ix.device));
-  vlr_status st = ensure_ws(h, nq, np, k);
+  st = ensure_ws(h, nq, np, k);
   if (st != VLR_OK) return st;
   Workspace& w = h->ws;
-  if (*w.h_status & 1) {  // reported by a previous async search
-    *w.h_status = 0;
-    return fail(VLR_ERR_NONFINITE, "non-finite query (detected in a previous search on this handle)");
-  }
-  VLR_CUDA_TRY(cudaMemsetAsync(w.status, 0, sizeof(int32_t), s));
-  int n = 0;
-  rec(h, 0, s);
-  VLR_CUDA_TRY(launch_qprep(Q, nq, ix.d, ix.d8, w.qnorm, w.qsq, w.qf16, w.qinv, w.status, s)); ++n;
-  VLR_CUDA_TRY(launch_filter_tc(w.qf16, w.qinv, nq, ix, w.dt, w.gmin, s)); ++n;
-  if (h->lut_side < 0) {
-    const char* e = getenv("VLR_LUT_SERIAL");
-    h->lut_side = (e && e[0] == '1') ? 0 : 1;
-  }
-  const bool lut_side = h->lut_side == 1 && h->profiling != 1;  // per-stage profiling keeps stages serial
-  if (lut_side) {
-    if (!h->lut_stream) {
-      VLR_CUDA_TRY(cudaStreamCreateWithFlags(&h->lut_stream, cudaStreamNonBlocking));
-      VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->lut_fork, cudaEventDisableTiming));
-      VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->lut_join, cudaEventDisableTiming));
-    }
-    // forked after K1 so K5's CTAs do not take SM slots from the filter's two waves;
-    // everything before the fork on s (incl. the previous search's scan, which
-    // read w.lut) is ordered before K5
-    VLR_CUDA_TRY(cudaEventRecord(h->lut_fork, s));
-    VLR_CUDA_TRY(cudaStreamWaitEvent(h->lut_stream, h->lut_fork, 0));
-    VLR_CUDA_TRY(launch_lut(Q, ix, w, nq, h->lut_stream)); ++n;
-    VLR_CUDA_TRY(cudaEventRecord(h->lut_join, h->lut_stream));
-  }
-  rec(h, 1, s);
-  VLR_CUDA_TRY(launch_select(ix, w, nq, np, filter_edot(ix.d), s)); ++n;
-  rec(h, 2, s);
-  VLR_CUDA_TRY(launch_exact(Q, ix, w, nq, s)); ++n;
-  VLR_CUDA_TRY(launch_refine(Q, ix, w, nq, np, out_miss, out_probes, s)); ++n;
-  rec(h, 3, s);
-  VLR_CUDA_TRY(launch_offsets(w, nq, np, s)); ++n;
-  rec(h, 4, s);
-  if (lut_side) {
-    VLR_CUDA_TRY(cudaStreamWaitEvent(s, h->lut_join, 0));
-  } else {
-    VLR_CUDA_TRY(launch_lut(Q, ix, w, nq, s)); ++n;
-  }
-  rec(h, 5, s);
-  if (rel) VLR_CUDA_TRY(cudaMemsetAsync(w.qdone, 0, sizeof(unsigned long long) * nq, s));
-  VLR_CUDA_TRY(launch_scan(ix, w, nq, np, k, s, rel)); ++n;
-  rec(h, 6, s);
+  st = take_status(w, " (detected in a previous search on this handle)");
+  if (st != VLR_OK) return st;
   const bool exchange = ix.nccl != nullptr;
-  if (!rel) {  // release mode: the scan merged and released every row itself
-    VLR_CUDA_TRY(launch_rank_merge(ix, w, nq, np, k, out_ids, out_dist, exchange ? w.send : nullptr, s)); ++n;
+  if (exchange) {  // an error of an earlier asynchronous search on this communicator
+    ncclResult_t as = ncclSuccess;
+    if (ncclCommGetAsyncError(reinterpret_cast<ncclComm_t>(ix.nccl), &as) != ncclSuccess ||
+        (as != ncclSuccess && as != ncclInProgress))
+      return nccl_dead(h, std::string("NCCL asynchronous error of an earlier search: ") + ncclGetErrorString(as));
   }
-  rec(h, 7, s);
+  const bool sharded = exchange && ix.coarse_sharded;
+  Pipe p{Q, nq, np, k, s};
+  if ((st = phase_a(h, p, sharded, out_miss, out_probes)) != VLR_OK) return st;
+  if (exchange) VLR_CUDA_TRY(fault_stall(s));
+  if (sharded) {
+    if ((st = nccl_allgather(h, w.x1, w.x1_all, sizeof(float) * nq * np, s, "coarse stage 1")) != VLR_OK) return st;
+    if ((st = phase_b(h, p)) != VLR_OK) return st;
+    if ((st = nccl_allgather(h, w.x2, w.x2_all, sizeof(CoarseEntry) * nq * np, s, "coarse stage 2")) != VLR_OK)
+      return st;
+  }
+  if ((st = phase_c(h, p, sharded, out_ids, out_dist, out_miss, out_probes, rel, exchange)) != VLR_OK) return st;
   if (exchange) {
-    ncclResult_t r = ncclAllGather(w.send, w.recv, (size_t)nq * k * sizeof(Packed), ncclUint8,
-                                   reinterpret_cast<ncclComm_t>(ix.nccl), s);
-    if (r != ncclSuccess) {
-      ncclCommAbort(reinterpret_cast<ncclComm_t>(ix.nccl));
-      ix.nccl = nullptr;
-      h->dead = true;
-      return fail(VLR_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
-    }
-    VLR_CUDA_TRY(launch_merge_packed(w.recv, ix.world, nq, k, out_ids, out_dist, s)); ++n;
+    if ((st = nccl_allgather(h, w.send, w.recv, (size_t)nq * k * sizeof(Packed), s, "results")) != VLR_OK) return st;
+    VLR_CUDA_TRY(launch_merge_packed(w.recv, ix.world, nq, k, out_ids, out_dist, s)); ++p.n;
   }
   rec(h, 8, s);
   VLR_CUDA_TRY(cudaMemcpyAsync(w.h_status, w.status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  h->launches = n;
+  h->launches = p.n;
   if (h->profiling) h->prof_mode[h->nsearch++ % vlr_index::kRing] = h->profiling;
   return VLR_OK;
+}
+
+static vlr_status search_impl(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
+                              float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream,
+                              const Release* rel) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  std::lock_guard<std::mutex> lock(h->mu);
+  return search_locked(h, Q, nq, nprobe, k, out_ids, out_dist, out_miss, out_probes, stream, rel);
 }
 
 vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
@@ -691,12 +920,8 @@ vlr_status vlr_search(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, 
                       float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream) {
   vlr_status st = vlr_search_async(h, Q, nq, nprobe, k, out_ids, out_dist, out_miss, out_probes, stream);
   if (st != VLR_OK || nq == 0) return st;
-  VLR_CUDA_TRY(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)));
-  if (*h->ws.h_status & 1) {
-    *h->ws.h_status = 0;
-    return fail(VLR_ERR_NONFINITE, "non-finite query");
-  }
-  return VLR_OK;
+  if ((st = wait_stream(h, reinterpret_cast<cudaStream_t>(stream))) != VLR_OK) return st;
+  return take_status(h->ws, "");
 }
 
 static vlr_status search_host_impl(vlr_index* h, const float* hQ, int32_t nq, int32_t nprobe, int32_t k,
@@ -710,25 +935,29 @@ static vlr_status search_host_impl(vlr_index* h, const float* hQ, int32_t nq, in
   const int np = std::min(nprobe, h->ix.nlist);
   if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 2048");
   VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
-  vlr_status st = ensure_ws(h, nq, np, k);
-  if (st != VLR_OK) return st;
-  Workspace& w = h->ws;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  VLR_CUDA_TRY(cudaMemcpyAsync(w.d_q, hQ, sizeof(float) * nq * h->ix.d, cudaMemcpyHostToDevice, s));
-  st = vlr_search_async(h, w.d_q, nq, nprobe, k, w.d_ids, w.d_dist, w.d_miss, h_probes ? w.d_probes : nullptr, stream);
-  if (st != VLR_OK) return st;
-  VLR_CUDA_TRY(cudaMemcpyAsync(h_ids, w.d_ids, sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, s));
-  VLR_CUDA_TRY(cudaMemcpyAsync(h_dist, w.d_dist, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, s));
-  VLR_CUDA_TRY(cudaMemcpyAsync(h_miss, w.d_miss, (size_t)nq * np, cudaMemcpyDeviceToHost, s));
-  if (h_probes)
-    VLR_CUDA_TRY(cudaMemcpyAsync(h_probes, w.d_probes, sizeof(int32_t) * nq * np, cudaMemcpyDeviceToHost, s));
-  if (!sync) return VLR_OK;  // results land when `stream` reaches this point; status: next call
-  VLR_CUDA_TRY(cudaStreamSynchronize(s));
-  if (*w.h_status & 1) {
-    *w.h_status = 0;
-    return fail(VLR_ERR_NONFINITE, "non-finite query");
+  {
+    // the staging buffers belong to the handle's workspace, which ensure_ws may reallocate and
+    // vlr_update_hot may free: size, stage and enqueue under the handle's mutex
+    std::lock_guard<std::mutex> lock(h->mu);
+    vlr_status st = ensure_ws(h, nq, np, k);
+    if (st != VLR_OK) return st;
+    Workspace& w = h->ws;
+    VLR_CUDA_TRY(cudaMemcpyAsync(w.d_q, hQ, sizeof(float) * nq * h->ix.d, cudaMemcpyHostToDevice, s));
+    st = search_locked(h, w.d_q, nq, nprobe, k, w.d_ids, w.d_dist, w.d_miss, h_probes ? w.d_probes : nullptr, stream,
+                       nullptr);
+    if (st != VLR_OK) return st;
+    VLR_CUDA_TRY(cudaMemcpyAsync(h_ids, w.d_ids, sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, s));
+    VLR_CUDA_TRY(cudaMemcpyAsync(h_dist, w.d_dist, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, s));
+    VLR_CUDA_TRY(cudaMemcpyAsync(h_miss, w.d_miss, (size_t)nq * np, cudaMemcpyDeviceToHost, s));
+    if (h_probes)
+      VLR_CUDA_TRY(cudaMemcpyAsync(h_probes, w.d_probes, sizeof(int32_t) * nq * np, cudaMemcpyDeviceToHost, s));
   }
-  return VLR_OK;
+  Workspace& w = h->ws;
+  if (!sync) return VLR_OK;  // results land when `stream` reaches this point; status: next call
+  vlr_status st = wait_stream(h, s);
+  if (st != VLR_OK) return st;
+  return take_status(w, "");
 }
 
 vlr_status vlr_search_host(vlr_index* h, const float* hQ, int32_t nq, int32_t nprobe, int32_t k, int64_t* h_ids,
@@ -739,6 +968,85 @@ vlr_status vlr_search_host(vlr_index* h, const float* hQ, int32_t nq, int32_t np
 vlr_status vlr_search_host_async(vlr_index* h, const float* hQ, int32_t nq, int32_t nprobe, int32_t k,
                                  int64_t* h_ids, float* h_dist, uint8_t* h_miss, int32_t* h_probes, void* stream) {
   return search_host_impl(h, hQ, nq, nprobe, k, h_ids, h_dist, h_miss, h_probes, stream, false);
+}
+
+// ---------------------------------------------------------------- staged (caller-exchanged) search
+// The collective search split at its two coarse-stage exchange points and its
+// result exchange, for shard-only handles (world > 1, no communicator): the
+// caller moves x1 / x2 between the ranks with any transport and merges the
+// partial results with vlr_merge_partials. Same kernels as the NCCL path.
+static vlr_status staged_begin(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int* np) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  if (!h->ix.shard_only) return fail(VLR_ERR_INVALID_ARG, "staged search needs a shard-only handle (world > 1, no communicator)");
+  vlr_status st = check_search_args(h, nq, nprobe, k, np);
+  if (st != VLR_OK) return st;
+  if (nq < 1 || !Q) return fail(VLR_ERR_INVALID_ARG, "staged search: nq >= 1 and queries required");
+  VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
+  return ensure_ws(h, nq, *np, k);
+}
+
+vlr_status vlr_coarse_stage1(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, float* d_x1, void* stream) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  std::lock_guard<std::mutex> lock(h->mu);
+  int np = 0;
+  vlr_status st = staged_begin(h, Q, nq, nprobe, 1, &np);
+  if (st != VLR_OK) return st;
+  if (!d_x1) return fail(VLR_ERR_INVALID_ARG, "null x1");
+  if ((st = take_status(h->ws, " (detected in a previous search on this handle)")) != VLR_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Pipe p{Q, nq, np, 1, s};
+  if ((st = phase_a(h, p, true, nullptr, nullptr)) != VLR_OK) return st;
+  VLR_CUDA_TRY(cudaMemcpyAsync(d_x1, h->ws.x1, sizeof(float) * nq * np, cudaMemcpyDeviceToDevice, s));
+  h->stage = 1;
+  h->stage_nq = nq;
+  h->stage_np = np;
+  h->launches = p.n;
+  return VLR_OK;
+}
+
+vlr_status vlr_coarse_stage2(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, const float* d_x1_all, void* d_x2,
+                             void* stream) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  std::lock_guard<std::mutex> lock(h->mu);
+  int np = 0;
+  vlr_status st = staged_begin(h, Q, nq, nprobe, 1, &np);
+  if (st != VLR_OK) return st;
+  if (!d_x1_all || !d_x2) return fail(VLR_ERR_INVALID_ARG, "null x1_all / x2");
+  if (h->stage != 1 || h->stage_nq != nq || h->stage_np != np)
+    return fail(VLR_ERR_INVALID_ARG, "vlr_coarse_stage2 must follow vlr_coarse_stage1 of the same batch");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Workspace& w = h->ws;
+  VLR_CUDA_TRY(cudaMemcpyAsync(w.x1_all, d_x1_all, sizeof(float) * nq * np * h->ix.world, cudaMemcpyDeviceToDevice, s));
+  Pipe p{Q, nq, np, 1, s};
+  if ((st = phase_b(h, p)) != VLR_OK) return st;
+  VLR_CUDA_TRY(cudaMemcpyAsync(d_x2, w.x2, sizeof(CoarseEntry) * nq * np, cudaMemcpyDeviceToDevice, s));
+  h->stage = 2;
+  h->launches += p.n;
+  return VLR_OK;
+}
+
+vlr_status vlr_search_stage3(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, const void* d_x2_all,
+                             int64_t* d_ids, float* d_dist, uint8_t* d_miss, int32_t* d_probes, void* stream) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  std::lock_guard<std::mutex> lock(h->mu);
+  int np = 0;
+  vlr_status st = staged_begin(h, Q, nq, nprobe, k, &np);
+  if (st != VLR_OK) return st;
+  if (!d_x2_all || !d_ids || !d_dist || !d_miss) return fail(VLR_ERR_INVALID_ARG, "null buffer");
+  if (h->stage != 2 || h->stage_nq != nq || h->stage_np != np)
+    return fail(VLR_ERR_INVALID_ARG, "vlr_search_stage3 must follow vlr_coarse_stage2 of the same batch");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Workspace& w = h->ws;
+  VLR_CUDA_TRY(cudaMemcpyAsync(w.x2_all, d_x2_all, sizeof(CoarseEntry) * nq * np * h->ix.world,
+                               cudaMemcpyDeviceToDevice, s));
+  Pipe p{Q, nq, np, k, s};
+  if ((st = phase_c(h, p, true, d_ids, d_dist, d_miss, d_probes, nullptr, false)) != VLR_OK) return st;
+  rec(h, 8, s);
+  VLR_CUDA_TRY(cudaMemcpyAsync(w.h_status, w.status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  h->stage = 0;
+  h->launches += p.n;
+  if (h->profiling) h->prof_mode[h->nsearch++ % vlr_index::kRing] = h->profiling;
+  return VLR_OK;
 }
 
 vlr_status vlr_merge_partials(const int64_t* part_ids, const float* part_dist, int32_t n_shards, int32_t nq, int32_t k,

@@ -93,148 +93,221 @@ cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, fl
 // ----------------------------------------------------------------- K2 select
 // One CTA per query. theta' = the np-th smallest of the 32-centroid group
 // minima written by K1 (a subset order statistic, so theta' >= theta~, the
-// np-th smallest filter value), found by a bitonic sort in
+// np-th smallest filter value), found by a radix select in
 // shared memory; if there are fewer groups than np, theta' = +inf (every
 // centroid is a candidate). Then one coalesced pass over the filter row
 // compacts {l : dt[l] <= theta' + 2 Delta*}.
+//
+// Centroid-sharded coarse stage (world > 1):
+// rank r filters only its centroid range [lo, hi) (K1 writes those columns),
+// and the global theta' is assembled from every rank's share in two modes:
+//  kSelStage1: theta_r = the np-th smallest of the rank's OWN group minima;
+//     x1[q][0..np) = the multiset of its np smallest group minima (values
+//     < theta_r, then theta_r repeated; +inf padding if the range has fewer
+//     than np groups). No compaction.
+//  kSelStage2: theta' = the np-th smallest of the G*np values gathered from
+//     every rank (x1_all [G][nq][np]): the np smallest group minima of all L
+//     centroids are among them, so theta' is exactly the single-GPU theta'
+//     (+inf when fewer than np groups exist in total); then the compaction
+//     over [lo, hi) as in kSelFull. The band bound is the same expression of
+//     replicated scalars on every rank, so the union of the ranks' candidate
+//     sets is the single-GPU candidate set.
 constexpr int kSelThreads = 1024;
-constexpr int kSelMaxGroups = 16384;  // nlist <= 512K for the sorted-minima path
+constexpr int kSelMaxGroups = 16384;  // groups per rank <= 16384 (nlist <= 512K) for the sorted-minima path
 
+// radix select (4 x 8-bit digits) of the want-th smallest (1-based) of n order-preserving keys in shared
+// memory; the whole CTA calls it, the result is CTA-uniform
+__device__ unsigned radix_select_kth(const unsigned* skeys, int n, unsigned want) {
+  __shared__ unsigned hist[256];
+  __shared__ unsigned s_prefix, s_want;
+  const int lane = threadIdx.x & 31;
+  unsigned prefix = 0u, mask = 0u;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      const unsigned key = i < n ? skeys[i] : 0u;
+      const bool act = i < n && (key & mask) == prefix;
+      const unsigned bin = (key >> shift) & 255u;
+      const unsigned am = __ballot_sync(kFull, act);
+      if (act) {
+        const unsigned peers = __match_any_sync(am, bin);
+        if (lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned)__popc(peers));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      unsigned loc[8], tot = 0u;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) { loc[b] = hist[lane * 8 + b]; tot += loc[b]; }
+      unsigned incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const unsigned excl = incl - tot;
+      if (excl < want && want <= incl) {
+        unsigned c = excl;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          if (c < want && want <= c + loc[b]) {
+            s_prefix = prefix | ((unsigned)(lane * 8 + b) << shift);
+            s_want = want - c;
+          }
+          c += loc[b];
+        }
+      }
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    want = s_want;
+    mask |= 255u << shift;
+    __syncthreads();  // s_prefix / s_want / hist reused by the next digit
+  }
+  return prefix;
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restrict__ dt, const float* __restrict__ gmin,
-                                                        int L, int np, const float* __restrict__ qnorm, float cmax,
+                                                        int L, int lo, int hi, int np, int world,
+                                                        const float* __restrict__ qnorm, float cmax,
                                                         float e_dot, float e_abs, const float* __restrict__ qinv,
-                                                        float c_inv, int32_t* __restrict__ cand,
+                                                        float c_inv, const float* __restrict__ x1_all,
+                                                        float* __restrict__ x1, int32_t* __restrict__ cand,
                                                         int32_t* __restrict__ ncand, float* __restrict__ bound_out) {
   extern __shared__ unsigned skeys[];
   __shared__ unsigned s_cnt;
   const int q = blockIdx.x;
+  const int nq = gridDim.x;
   const int lane = threadIdx.x & 31;
-  const int ng = (L + 31) / 32;
+  const int ngL = (L + 31) / 32;               // groups of all L centroids (gmin row stride)
+  const int g0 = lo / 32, ng = (hi + 31) / 32 - g0;  // this rank's groups
   float theta = CUDART_INF_F;
-  if (ng >= np && ng <= kSelMaxGroups) {
-    // radix select (4 x 8-bit digits) of the np-th smallest group minimum
-    __shared__ unsigned hist[256];
-    __shared__ unsigned s_prefix, s_want;
-    for (int i = threadIdx.x; i < ng; i += blockDim.x) skeys[i] = fkey(gmin[(size_t)q * ng + i]);
-    unsigned prefix = 0u, mask = 0u, want = (unsigned)np;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
-      __syncthreads();
-      for (int i0 = 0; i0 < ng; i0 += blockDim.x) {
-        const int i = i0 + threadIdx.x;
-        const unsigned key = i < ng ? skeys[i] : 0u;
-        const bool act = i < ng && (key & mask) == prefix;
-        const unsigned bin = (key >> shift) & 255u;
-        const unsigned am = __ballot_sync(kFull, act);
-        if (act) {
-          const unsigned peers = __match_any_sync(am, bin);
-          if (lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned)__popc(peers));
-        }
-      }
-      __syncthreads();
-      if (threadIdx.x < 32) {
-        unsigned loc[8], tot = 0u;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) { loc[b] = hist[lane * 8 + b]; tot += loc[b]; }
-        unsigned incl = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned v = __shfl_up_sync(kFull, incl, o);
-          if (lane >= o) incl += v;
-        }
-        const unsigned excl = incl - tot;
-        if (excl < want && want <= incl) {
-          unsigned c = excl;
-#pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            if (c < want && want <= c + loc[b]) {
-              s_prefix = prefix | ((unsigned)(lane * 8 + b) << shift);
-              s_want = want - c;
-            }
-            c += loc[b];
-          }
-        }
-      }
-      __syncthreads();
-      prefix = s_prefix;
-      want = s_want;
-      mask |= 255u << shift;
+  if constexpr (MODE == kSelStage2) {
+    const int n = world * np;  // <= kSelMaxGroups (checked at launch)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int r = i / np, j = i - r * np;
+      skeys[i] = fkey(x1_all[((size_t)r * nq + q) * np + j]);
     }
-    theta = fkey_inv(prefix);
-  }
-  const float qn = qnorm[q];
-  const float u = 5.9604645e-8f;  // 2^-24
-  // fp16 subnormal flush of the scaled operands (absolute):
-  // A = sqrt(d) 2^-25 (||q|| c_inv + c_max q_inv)(1 + 2^-11) + d 2^-50 c_inv q_inv,
-  // e_abs = sqrt(d) 2^-25 (1 + 2^-11), d 2^-50 = e_abs^2 / (1 + 2^-11)^2 <= e_abs^2
-  const float qi = qinv[q];
-  const float abs_dot = e_abs * (qn * c_inv + cmax * qi) + e_abs * e_abs * (c_inv * qi) + 1.2e-38f;
-  const float delta = 2.0f * (2.0f * (e_dot + 2.0f * u) * qn * cmax + 4.0f * u * (cmax * cmax + qn * qn) +
-                              2.0f * abs_dot);
-  const float bnd = theta + 2.0f * delta;
-  if (threadIdx.x == 0) {
-    s_cnt = 0u;
-    bound_out[q] = bnd;
-  }
-  __syncthreads();
-  const float* row = dt + (size_t)q * L;
-  int32_t* out = cand + (size_t)q * kCandCap;
-  auto emit = [&](bool keep, int i) {
-    const unsigned km = __ballot_sync(kFull, keep);
-    if (km == 0u) return;
-    unsigned base = 0u;
-    if (lane == 0) base = atomicAdd(&s_cnt, (unsigned)__popc(km));
-    base = __shfl_sync(kFull, base, 0);
-    if (keep) {
-      const unsigned pos = base + __popc(km & ((1u << lane) - 1u));
-      if (pos < (unsigned)kCandCap) out[pos] = i;
-    }
-  };
-  if ((L & 3) == 0) {
-    const float4* r4 = reinterpret_cast<const float4*>(row);
-    constexpr int U = 2;  // loads in flight per thread before any emit (32 regs: 2 CTAs per SM)
-    for (int i0 = 0; i0 < L / 4; i0 += U * blockDim.x) {
-      float4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * blockDim.x + threadIdx.x;
-        v[u] = i < L / 4 ? __ldg(r4 + i) : make_float4(CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * blockDim.x + threadIdx.x;
-        const bool in = i < L / 4;
-        emit(in && v[u].x <= bnd, 4 * i);
-        emit(in && v[u].y <= bnd, 4 * i + 1);
-        emit(in && v[u].z <= bnd, 4 * i + 2);
-        emit(in && v[u].w <= bnd, 4 * i + 3);
-      }
-    }
+    __syncthreads();
+    theta = fkey_inv(radix_select_kth(skeys, n, (unsigned)np));
   } else {
-    for (int i0 = 0; i0 < L; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      emit(i < L && row[i] <= bnd, i);
+    if (ng >= np && ng <= kSelMaxGroups) {
+      for (int i = threadIdx.x; i < ng; i += blockDim.x) skeys[i] = fkey(gmin[(size_t)q * ngL + g0 + i]);
+      __syncthreads();
+      theta = fkey_inv(radix_select_kth(skeys, ng, (unsigned)np));
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) ncand[q] = (int32_t)s_cnt;
+  if constexpr (MODE == kSelStage1) {
+    // x1 row: the np smallest group minima of this range as a multiset
+    float* out = x1 + (size_t)q * np;
+    if (threadIdx.x == 0) s_cnt = 0u;
+    __syncthreads();
+    // fewer than np groups: all of them, +inf padding (theta' stays exact). More than kSelMaxGroups: the
+    // first np (any np genuine group minima give an np-th smallest >= theta~, a valid but looser bound)
+    if (ng < np || ng > kSelMaxGroups) {
+      for (int i = threadIdx.x; i < np; i += blockDim.x) out[i] = i < ng ? gmin[(size_t)q * ngL + g0 + i] : CUDART_INF_F;
+      return;
+    }
+    for (int i0 = 0; i0 < ng; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      const bool keep = i < ng && skeys[i] < fkey(theta);
+      const unsigned km = __ballot_sync(kFull, keep);
+      if (km == 0u) continue;
+      unsigned base = 0u;
+      if (lane == 0) base = atomicAdd(&s_cnt, (unsigned)__popc(km));
+      base = __shfl_sync(kFull, base, 0);
+      if (keep) out[base + __popc(km & ((1u << lane) - 1u))] = fkey_inv(skeys[i]);
+    }
+    __syncthreads();
+    for (int i = (int)s_cnt + threadIdx.x; i < np; i += blockDim.x) out[i] = theta;  // fewer than np are < theta
+    return;
+  } else {
+    const float qn = qnorm[q];
+    const float u = 5.9604645e-8f;  // 2^-24
+    // fp16 subnormal flush of the scaled operands (absolute):
+    // A = sqrt(d) 2^-25 (||q|| c_inv + c_max q_inv)(1 + 2^-11) + d 2^-50 c_inv q_inv,
+    // e_abs = sqrt(d) 2^-25 (1 + 2^-11), d 2^-50 = e_abs^2 / (1 + 2^-11)^2 <= e_abs^2
+    const float qi = qinv[q];
+    const float abs_dot = e_abs * (qn * c_inv + cmax * qi) + e_abs * e_abs * (c_inv * qi) + 1.2e-38f;
+    const float delta = 2.0f * (2.0f * (e_dot + 2.0f * u) * qn * cmax + 4.0f * u * (cmax * cmax + qn * qn) +
+                                2.0f * abs_dot);
+    const float bnd = theta + 2.0f * delta;
+    if (threadIdx.x == 0) {
+      s_cnt = 0u;
+      bound_out[q] = bnd;
+    }
+    __syncthreads();
+    const float* row = dt + (size_t)q * L;
+    int32_t* out = cand + (size_t)q * kCandCap;
+    auto emit = [&](bool keep, int i) {
+      const unsigned km = __ballot_sync(kFull, keep);
+      if (km == 0u) return;
+      unsigned base = 0u;
+      if (lane == 0) base = atomicAdd(&s_cnt, (unsigned)__popc(km));
+      base = __shfl_sync(kFull, base, 0);
+      if (keep) {
+        const unsigned pos = base + __popc(km & ((1u << lane) - 1u));
+        if (pos < (unsigned)kCandCap) out[pos] = i;
+      }
+    };
+    const int n = hi - lo;
+    if ((L & 3) == 0 && (lo & 3) == 0 && (n & 3) == 0) {
+      const float4* r4 = reinterpret_cast<const float4*>(row + lo);
+      constexpr int U = 2;  // loads in flight per thread before any emit (32 regs: 2 CTAs per SM)
+      for (int i0 = 0; i0 < n / 4; i0 += U * blockDim.x) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * blockDim.x + threadIdx.x;
+          v[u] = i < n / 4 ? __ldg(r4 + i) : make_float4(CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * blockDim.x + threadIdx.x;
+          const bool in = i < n / 4;
+          emit(in && v[u].x <= bnd, lo + 4 * i);
+          emit(in && v[u].y <= bnd, lo + 4 * i + 1);
+          emit(in && v[u].z <= bnd, lo + 4 * i + 2);
+          emit(in && v[u].w <= bnd, lo + 4 * i + 3);
+        }
+      }
+    } else {
+      for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        emit(i < n && row[lo + i] <= bnd, lo + i);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) ncand[q] = (int32_t)s_cnt;
+  }
 }
 
-cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float e_dot, cudaStream_t s) {
+// mode: kSelFull (single GPU / replicated coarse), kSelStage1 (-> ws.x1), kSelStage2 (ws.x1_all -> candidates)
+cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float e_dot, int mode,
+                          cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  const int ng = (ix.nlist + 31) / 32;
-  int n2 = 1;
-  while (n2 < ng) n2 <<= 1;
-  const size_t sm = ng <= kSelMaxGroups ? (size_t)ng * sizeof(unsigned) : 0;
-  static size_t configured = 0;
-  if (sm > 48 * 1024 && sm > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    configured = sm;
+  const int lo = mode == kSelFull ? 0 : ix.c_lo, hi = mode == kSelFull ? ix.nlist : ix.c_hi;
+  const int ng = (hi + 31) / 32 - lo / 32;
+  size_t n_keys = ng <= kSelMaxGroups ? (size_t)ng : 0;
+  if (mode == kSelStage2) {
+    n_keys = (size_t)ix.world * np;
+    if (n_keys > (size_t)kSelMaxGroups) return cudaErrorInvalidValue;  // world * nprobe' <= 16384
   }
+  const size_t sm = n_keys * sizeof(unsigned);
+  const void* fn = mode == kSelStage1 ? (const void*)k_select<kSelStage1>
+                   : mode == kSelStage2 ? (const void*)k_select<kSelStage2> : (const void*)k_select<kSelFull>;
+  cudaError_t e = ensure_smem(fn, sm);
+  if (e != cudaSuccess) return e;
   const float e_abs = sqrtf((float)ix.d) * 2.9802322e-8f * 1.00049f * 1.0001f;  // sqrt(d) 2^-25 (1 + 2^-11), rounded up
-  k_select<<<nq, kSelThreads, sm, s>>>(ws.dt, ws.gmin, ix.nlist, np, ws.qnorm, ix.cmax, e_dot, e_abs, ws.qinv,
-                                       ix.c_inv, ws.cand, ws.ncand, ws.bound);
+#define VLR_SEL_ARGS ws.dt, ws.gmin, ix.nlist, lo, hi, np, ix.world, ws.qnorm, ix.cmax, e_dot, e_abs, ws.qinv, \
+                     ix.c_inv, ws.x1_all, ws.x1, ws.cand, ws.ncand, ws.bound
+  if (mode == kSelStage1) k_select<kSelStage1><<<nq, kSelThreads, sm, s>>>(VLR_SEL_ARGS);
+  else if (mode == kSelStage2) k_select<kSelStage2><<<nq, kSelThreads, sm, s>>>(VLR_SEL_ARGS);
+  else k_select<kSelFull><<<nq, kSelThreads, sm, s>>>(VLR_SEL_ARGS);
+#undef VLR_SEL_ARGS
   return cudaGetLastError();
 }
 
@@ -413,13 +486,9 @@ __global__ void __launch_bounds__(W * 32) k_exact(const float* __restrict__ Q, c
 template <int S, int W>
 static cudaError_t launch_exact_t(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
   const size_t sm = (size_t)((ix.d + 1) & ~1) * sizeof(double) + (size_t)W * S * 1024 * sizeof(float);
-  static size_t configured[2] = {0, 0};
   auto fn = ix.metric == 1 ? k_exact<1, S, W> : k_exact<0, S, W>;
-  if (sm > 48 * 1024 && sm > configured[ix.metric]) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    configured[ix.metric] = sm;
-  }
+  cudaError_t e = ensure_smem((const void*)fn, sm);
+  if (e != cudaSuccess) return e;
   dim3 grid(nq, 1024 / (W * 32));  // 1024 candidates per pass; queries with more loop
   fn<<<grid, W * 32, sm, s>>>(Q, ix.centroids, ix.d, ws.cand, ws.ncand, ws.exact);
   return cudaGetLastError();
@@ -443,14 +512,26 @@ cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace&
   }
 }
 
-template <int MET>
+// K3b modes: kRefRoute (single GPU: sort the candidates, keep nprobe', route),
+// kRefLocal (sharded coarse stage 2: this rank's candidates -> its sorted top
+// nprobe' exact (D, l) list x2[q], no routing), kRefMerge (sharded stage 3:
+// the G sorted lists gathered from every rank, x2_all [G][nq][np] -> the
+// global top nprobe', then the router). kRefMerge sorts exactly the multiset
+// kRefRoute would (the global top nprobe' of the union of the ranks'
+// candidate sets is contained in the union of their local top nprobe'), so the
+// probes are bitwise those of the single-GPU path.
+
+template <int MET, int MODE>
 __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restrict__ Q, const float* __restrict__ C,
-                                                           int d, int L, int np, int scap, int by_residual,
+                                                           int d, int L, int lo, int hi, int np, int scap,
+                                                           int by_residual, int world,
                                                            const float* __restrict__ qsq, const float* __restrict__ dt,
                                                            const int32_t* __restrict__ cand,
                                                            const int32_t* __restrict__ ncand,
                                                            const float* __restrict__ bound,
                                                            const double* __restrict__ exact,
+                                                           CoarseEntry* __restrict__ x2,
+                                                           const CoarseEntry* __restrict__ x2_all,
                                                            int32_t* __restrict__ probes, float* __restrict__ term1,
                                                            int rank, const int32_t* __restrict__ owner,
                                                            const int32_t* __restrict__ local,
@@ -467,120 +548,167 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
   double* qs = reinterpret_cast<double*>(lbuf + kRefineChunk);        // [d]
   __shared__ int s_cnt;
   const int q = blockIdx.x;
+  const int nq = gridDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = (double)Q[(size_t)q * d + t];
-  const int nc = ncand[q];
-  const bool listed = nc <= kCandCap;
-  const int src_len = listed ? nc : L;
-  const float bnd = bound[q];
-  const int32_t* lst = cand + (size_t)q * kCandCap;
-  const float* row = dt + (size_t)q * L;
-  const bool vec_ok = (d & 3) == 0;
   int nbest = 0;
-  int pos = 0;
-  __syncthreads();
-  while (pos < src_len) {
-    // gather up to kRefineChunk candidate ids
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
-    if (listed) {
+  if constexpr (MODE == kRefMerge) {
+    // G sorted lists of np entries; padding (+inf, -1) is skipped
+    const int src_len = world * np;
+    for (int pos = 0; pos < src_len; pos += kRefineChunk) {
+      if (threadIdx.x == 0) s_cnt = 0;
+      __syncthreads();
       const int take = min(kRefineChunk, src_len - pos);
-      for (int i = threadIdx.x; i < take; i += blockDim.x) lbuf[i] = lst[pos + i];
-      pos += take;
-      if (threadIdx.x == 0) s_cnt = take;
-    } else {
-      while (pos < src_len) {
-        __syncthreads();
-        if (s_cnt + (int)blockDim.x > kRefineChunk) break;
-        const int i = pos + threadIdx.x;
-        if (i < src_len && row[i] <= bnd) lbuf[atomicAdd(&s_cnt, 1)] = i;
-        pos += blockDim.x;
-      }
-    }
-    __syncthreads();
-    const int cnt = s_cnt;
-    // exact distances: precomputed by K3a for listed candidates; the overflow
-    // (rescan) path computes them here, 32 candidates per warp pass
-    if (listed) {
-      const double* ex = exact + (size_t)q * kCandCap + (pos - cnt);
-      for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
-        key[nbest + j] = ex[j];
-        id[nbest + j] = lbuf[j];
-      }
-    } else {
-      for (int g = warp * 32; warp < kRescanWarps && g < cnt; g += kRescanWarps * 32) {
-        const int j = g + lane;
-        const int rid = j < cnt ? lbuf[j] : lbuf[g];
-        const double dsum = vec_ok ? warp_exact<2, MET>(qs, C, d, rid, tiles + warp * 2048, lane)
-                                   : scalar_exact<MET>(qs, C, d, rid);
-        if (j < cnt) {
-          key[nbest + j] = dsum;
-          id[nbest + j] = rid;
+      for (int i = threadIdx.x; i < take; i += blockDim.x) {
+        const int r = (pos + i) / np, j = (pos + i) - r * np;
+        const CoarseEntry e = x2_all[((size_t)r * nq + q) * np + j];
+        if (e.l >= 0) {
+          const int at = nbest + atomicAdd(&s_cnt, 1);
+          key[at] = e.D;
+          id[at] = e.l;
         }
       }
+      __syncthreads();
+      const int tot = nbest + s_cnt;
+      int n2 = 1;
+      while (n2 < tot) n2 <<= 1;
+      for (int j = tot + threadIdx.x; j < n2; j += blockDim.x) {
+        key[j] = DBL_MAX;
+        id[j] = 0x7fffffff;
+      }
+      bitonic_sort(key, id, n2);
+      nbest = min(np, tot);
     }
-    const int tot = nbest + cnt;
-    int n2 = 1;
-    while (n2 < tot) n2 <<= 1;
-    for (int j = tot + threadIdx.x; j < n2; j += blockDim.x) {
-      key[j] = DBL_MAX;
-      id[j] = 0x7fffffff;
+  } else {
+    for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = (double)Q[(size_t)q * d + t];
+    const int nc = ncand[q];
+    const bool listed = nc <= kCandCap;
+    const int src_len = listed ? nc : hi - lo;
+    const float bnd = bound[q];
+    const int32_t* lst = cand + (size_t)q * kCandCap;
+    const float* row = dt + (size_t)q * L + lo;  // rescan of this rank's filter columns [lo, hi)
+    const bool vec_ok = (d & 3) == 0;
+    int pos = 0;
+    __syncthreads();
+    while (pos < src_len) {
+      // gather up to kRefineChunk candidate ids
+      if (threadIdx.x == 0) s_cnt = 0;
+      __syncthreads();
+      if (listed) {
+        const int take = min(kRefineChunk, src_len - pos);
+        for (int i = threadIdx.x; i < take; i += blockDim.x) lbuf[i] = lst[pos + i];
+        pos += take;
+        if (threadIdx.x == 0) s_cnt = take;
+      } else {
+        while (pos < src_len) {
+          // uniform snapshot of the count: every thread reads it between two barriers, before any thread
+          // of this iteration adds to it (a read racing with other warps' atomicAdd could make some
+          // threads break and others loop on: barrier divergence)
+          __syncthreads();
+          const int cnt_now = s_cnt;
+          __syncthreads();
+          if (cnt_now + (int)blockDim.x > kRefineChunk) break;
+          const int i = pos + threadIdx.x;
+          if (i < src_len && row[i] <= bnd) lbuf[atomicAdd(&s_cnt, 1)] = lo + i;
+          pos += blockDim.x;
+        }
+      }
+      __syncthreads();
+      const int cnt = s_cnt;
+      // exact distances: precomputed by K3a for listed candidates; the overflow
+      // (rescan) path computes them here, 32 candidates per warp pass
+      if (listed) {
+        const double* ex = exact + (size_t)q * kCandCap + (pos - cnt);
+        for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+          key[nbest + j] = ex[j];
+          id[nbest + j] = lbuf[j];
+        }
+      } else {
+        for (int g = warp * 32; warp < kRescanWarps && g < cnt; g += kRescanWarps * 32) {
+          const int j = g + lane;
+          const int rid = j < cnt ? lbuf[j] : lbuf[g];
+          const double dsum = vec_ok ? warp_exact<2, MET>(qs, C, d, rid, tiles + warp * 2048, lane)
+                                     : scalar_exact<MET>(qs, C, d, rid);
+          if (j < cnt) {
+            key[nbest + j] = dsum;
+            id[nbest + j] = rid;
+          }
+        }
+      }
+      const int tot = nbest + cnt;
+      int n2 = 1;
+      while (n2 < tot) n2 <<= 1;
+      for (int j = tot + threadIdx.x; j < n2; j += blockDim.x) {
+        key[j] = DBL_MAX;
+        id[j] = 0x7fffffff;
+      }
+      bitonic_sort(key, id, n2);
+      nbest = min(np, tot);
     }
-    bitonic_sort(key, id, n2);
-    nbest = min(np, tot);
   }
-  // ---- router epilogue (K4 fused): mask, owned work items
-  // and their within-query prefix (groups of 32 vectors); K4b adds the
-  // query bases. Items p of this query are handled kRefinePer per thread in order.
-  __shared__ long long s_wsum[kRefineWarps];
-  long long g2[kRefinePer];
-  const int p0 = kRefinePer * threadIdx.x;
-  // term1: the key itself with residual codes (||q-c||^2
-  // or -<q,c>); without, ||q||^2 (L2) or 0 (IP)
-  const float t1c = by_residual ? 0.f : (MET == 1 ? 0.f : qsq[q]);
-#pragma unroll
-  for (int h = 0; h < kRefinePer; ++h) {
-    const int p = p0 + h;
-    g2[h] = 0;
-    if (p < np) {
-      // nbest == np whenever the candidate set holds >= np clusters (always: the
-      // band contains the np smallest)
-      const int l = p < nbest ? id[p] : -1;
-      const size_t o = (size_t)q * np + p;
-      probes[o] = l;
-      term1[o] = p < nbest ? (by_residual ? __double2float_rn(key[p]) : t1c) : CUDART_INF_F;
-      const int own = l >= 0 ? owner[l] : -1;
-      miss[o] = own < 0 ? 1 : 0;
-      if (probes_out) probes_out[o] = l;
-      const int loc = (own == rank) ? local[l] : -1;
-      plocal[o] = loc;
-      if (loc >= 0) g2[h] = gbase[loc + 1] - gbase[loc];
+  if constexpr (MODE == kRefLocal) {
+    // this rank's sorted top-np exact list, padded with (+inf, -1)
+    for (int p = threadIdx.x; p < np; p += blockDim.x) {
+      CoarseEntry e;
+      e.D = p < nbest ? key[p] : CUDART_INF;
+      e.l = p < nbest ? id[p] : -1;
+      e.pad = 0;
+      x2[(size_t)q * np + p] = e;
     }
-  }
-  long long mine = 0;
+    return;
+  } else {
+    // ---- router epilogue (K4 fused): mask, owned work items
+    // and their within-query prefix (groups of 32 vectors); K4b adds the
+    // query bases. Items p of this query are handled kRefinePer per thread in order.
+    __shared__ long long s_wsum[kRefineWarps];
+    long long g2[kRefinePer];
+    const int p0 = kRefinePer * threadIdx.x;
+    // term1: the key itself with residual codes (||q-c||^2
+    // or -<q,c>); without, ||q||^2 (L2) or 0 (IP)
+    const float t1c = by_residual ? 0.f : (MET == 1 ? 0.f : qsq[q]);
 #pragma unroll
-  for (int h = 0; h < kRefinePer; ++h) mine += g2[h];
-  long long incl = mine;
+    for (int h = 0; h < kRefinePer; ++h) {
+      const int p = p0 + h;
+      g2[h] = 0;
+      if (p < np) {
+        // nbest == np whenever the candidate set holds >= np clusters (always: the
+        // band contains the np smallest)
+        const int l = p < nbest ? id[p] : -1;
+        const size_t o = (size_t)q * np + p;
+        probes[o] = l;
+        term1[o] = p < nbest ? (by_residual ? __double2float_rn(key[p]) : t1c) : CUDART_INF_F;
+        const int own = l >= 0 ? owner[l] : -1;
+        miss[o] = own < 0 ? 1 : 0;
+        if (probes_out) probes_out[o] = l;
+        const int loc = (own == rank) ? local[l] : -1;
+        plocal[o] = loc;
+        if (loc >= 0) g2[h] = gbase[loc + 1] - gbase[loc];
+      }
+    }
+    long long mine = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const long long v = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) s_wsum[warp] = incl;
-  __syncthreads();
-  long long wbase = 0, total = 0;
-  for (int w = 0; w < kRefineWarps; ++w) {
-    const long long v = s_wsum[w];
-    if (w < warp) wbase += v;
-    total += v;
-  }
-  long long ex = wbase + incl - mine;
+    for (int h = 0; h < kRefinePer; ++h) mine += g2[h];
+    long long incl = mine;
 #pragma unroll
-  for (int h = 0; h < kRefinePer; ++h) {
-    if (p0 + h < np) item_local[(size_t)q * np + p0 + h] = ex;
-    ex += g2[h];
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    long long wbase = 0, total = 0;
+    for (int w = 0; w < kRefineWarps; ++w) {
+      const long long v = s_wsum[w];
+      if (w < warp) wbase += v;
+      total += v;
+    }
+    long long ex = wbase + incl - mine;
+#pragma unroll
+    for (int h = 0; h < kRefinePer; ++h) {
+      if (p0 + h < np) item_local[(size_t)q * np + p0 + h] = ex;
+      ex += g2[h];
+    }
+    if (threadIdx.x == 0) qtot[q] = total;
   }
-  if (threadIdx.x == 0) qtot[q] = total;
 }
 
 size_t refine_smem(int d, int scap) {
@@ -588,22 +716,30 @@ size_t refine_smem(int d, int scap) {
          kRefineChunk * sizeof(int) + (size_t)d * sizeof(double);
 }
 
+template <int MET>
+static const void* refine_fn(int mode) {
+  return mode == kRefLocal ? (const void*)k_refine<MET, kRefLocal>
+         : mode == kRefMerge ? (const void*)k_refine<MET, kRefMerge> : (const void*)k_refine<MET, kRefRoute>;
+}
+
+// mode kRefRoute / kRefLocal (-> ws.x2) / kRefMerge (ws.x2_all -> probes, route)
 cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, int np, uint8_t* miss,
-                          int32_t* probes_out, cudaStream_t s) {
+                          int32_t* probes_out, int mode, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
+  // kRefMerge sorts chunks of up to kRefineChunk entries with the running np best, as the other modes
   const int scap = sort_cap(np);
   const size_t sm = refine_smem(ix.d, scap);
-  static size_t configured[2] = {0, 0};
-  auto fn = ix.metric == 1 ? k_refine<1> : k_refine<0>;
-  if (sm > 48 * 1024 && sm > configured[ix.metric]) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    configured[ix.metric] = sm;
-  }
-  fn<<<nq, kRefineThreads, sm, s>>>(Q, ix.centroids, ix.d, ix.nlist, np, scap, ix.by_residual, ws.qsq, ws.dt, ws.cand,
-                                    ws.ncand, ws.bound, ws.exact, ws.probes, ws.term1, ix.rank, ix.owner, ix.local,
-                                    ix.gbase, miss, probes_out, ws.plocal, ws.item_local, ws.qtot);
-  return cudaGetLastError();
+  const void* fn = ix.metric == 1 ? refine_fn<1>(mode) : refine_fn<0>(mode);
+  cudaError_t e = ensure_smem(fn, sm);
+  if (e != cudaSuccess) return e;
+  const int lo = mode == kRefRoute ? 0 : ix.c_lo, hi = mode == kRefRoute ? ix.nlist : ix.c_hi;
+  void* args[] = {(void*)&Q, (void*)&ix.centroids, (void*)&ix.d, (void*)&ix.nlist, (void*)&lo, (void*)&hi,
+                  (void*)&np, (void*)&scap, (void*)&ix.by_residual, (void*)&ix.world, (void*)&ws.qsq,
+                  (void*)&ws.dt, (void*)&ws.cand, (void*)&ws.ncand, (void*)&ws.bound, (void*)&ws.exact,
+                  (void*)&ws.x2, (void*)&ws.x2_all, (void*)&ws.probes, (void*)&ws.term1, (void*)&ix.rank,
+                  (void*)&ix.owner, (void*)&ix.local, (void*)&ix.gbase, (void*)&miss, (void*)&probes_out,
+                  (void*)&ws.plocal, (void*)&ws.item_local, (void*)&ws.qtot};
+  return cudaLaunchKernel(fn, dim3(nq), dim3(kRefineThreads), args, sm, s);
 }
 
 }  // namespace vlr

@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     k_filter_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int L, int nq,
                 int kblocks, int nN, int nacc, int stages, const float* __restrict__ cn2,
                 const float* __restrict__ qinv, float c_inv, float* __restrict__ dt, float* __restrict__ gmin,
-                int ngroups, const uint16_t* __restrict__ At) {
+                int ngroups, const uint16_t* __restrict__ At, int t0) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull;
@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const unsigned long long tr0 = globaltimer_ns();
 #endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kTcM;
+  const int tile = t0 + (int)blockIdx.x;  // centroid tile (this rank's range starts at tile t0)
+  const int m0 = tile * kTcM;
   const int q0 = blockIdx.y * (nN * nacc);
   const uint32_t bytesA = kTcM * 128, bytesB = (uint32_t)(nacc * nN * 128);
   const uint32_t stage_bytes = bytesA + bytesB;
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         uint8_t* sA = smem + (size_t)s * stage_bytes;
         uint8_t* sB = sA + bytesA;
         mb_expect_tx(&full[s], stage_bytes);
-        if (At) bulk_g2s_16k(sA, At + ((size_t)blockIdx.x * kblocks + kb) * (kTcM * kTcBK), &full[s]);
+        if (At) bulk_g2s_16k(sA, At + ((size_t)tile * kblocks + kb) * (kTcM * kTcBK), &full[s]);
         else tma_2d(sA, &tmA, kb * kTcBK, m0, &full[s]);
         if constexpr (CL > 1) {  // nacc == 1: this CTA's 1/CL of the query rows, to every cluster CTA
           const int rq = nN / CL;
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // 32 query columns at a time: dt stores (lanes = 32 consecutive centroids,
     // coalesced) and the min over this warp's 32 centroids of each column
     // (transpose-reduce: 31 shuffles leave column j's min in lane j).
-    const int grp = blockIdx.x * 4 + lg;
+    const int grp = tile * 4 + lg;
     for (int c = 0; c < (VLR_K1_EXPERIMENT == 3 ? 0 : ncols_used); c += 32) {
       uint32_t v[32];
       const uint32_t taddr = tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)c;
@@ -485,9 +486,11 @@ cudaError_t make_tmap_2d(void* map_, const uint16_t* base, int rows, int cols, i
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, float* dt, float* gmin,
-                             cudaStream_t s) {
-  if (nq <= 0) return cudaSuccess;
+cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, int t_lo, int t_hi,
+                             float* dt, float* gmin, cudaStream_t s) {
+  if (nq <= 0 || t_hi <= t_lo) return cudaSuccess;
+  const int ntiles_all = (ix.nlist + kTcM - 1) / kTcM;
+  const bool full_range = t_lo == 0 && t_hi == ntiles_all;
   int nacc, nN;
   if (nq <= 256) {
     nacc = 1;
@@ -513,26 +516,23 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
     cl_env = ce ? atoi(ce) : kTcCluster;
   }
   int CL = 1;
-  if (nacc == 1 && !persistent)
+  const bool use_persistent = persistent && full_range;
+  if (nacc == 1 && !use_persistent)
     for (int c : {4, 2})
-      if (c <= cl_env && nN % (8 * c) == 0) { CL = c; break; }
+      if (c <= cl_env && nN % (8 * c) == 0 && (t_hi - t_lo) % c == 0) { CL = c; break; }
   const int box_rows_b = (nN < 256 ? nN : 256) / CL;
   CUtensorMap tmB;
   cudaError_t e = make_tmap_2d(&tmB, Qh, nq, ix.d8, box_rows_b);
   if (e != cudaSuccess) return e;
   const int kblocks = (ix.d8 + kTcBK - 1) / kTcBK;
-  if (nacc == 1 && persistent) {
+  if (nacc == 1 && use_persistent) {
     const uint32_t sb = kTcM * 128 + (uint32_t)(nN * 128);
     int stages = (int)((200 * 1024) / sb);
     if (stages > kTcMaxStages) stages = kTcMaxStages;
     if (stages < 2) stages = 2;
     const size_t smem = (size_t)stages * sb + 1024;
-    static size_t configured_p = 0;
-    if (smem > configured_p) {
-      e = cudaFuncSetAttribute(k_filter_tc_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      configured_p = smem;
-    }
+    e = ensure_smem((const void*)k_filter_tc_p, smem);
+    if (e != cudaSuccess) return e;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -549,17 +549,11 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   if (stages > kTcMaxStages) stages = kTcMaxStages;
   if (stages < 2) stages = 2;
   const size_t smem = (size_t)stages * stage_bytes + 1024;
-  static size_t configured[3] = {0, 0, 0};
-  const int ci = CL == 4 ? 2 : CL == 2 ? 1 : 0;
-  if (smem > configured[ci]) {
-    e = CL == 4   ? cudaFuncSetAttribute(k_filter_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-        : CL == 2 ? cudaFuncSetAttribute(k_filter_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                  : cudaFuncSetAttribute(k_filter_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured[ci] = smem;
-  }
-  const int tiles = (ix.nlist + kTcM - 1) / kTcM;
-  dim3 grid((tiles + CL - 1) / CL * CL, (nq + nN * nacc - 1) / (nN * nacc));  // whole clusters (extra tiles: OOB)
+  e = ensure_smem(CL == 4 ? (const void*)k_filter_tc<4> : CL == 2 ? (const void*)k_filter_tc<2> : (const void*)k_filter_tc<1>,
+                  smem);
+  if (e != cudaSuccess) return e;
+  const int tiles = t_hi - t_lo;
+  dim3 grid(tiles, (nq + nN * nacc - 1) / (nN * nacc));  // CL divides tiles
   const CUtensorMap& tmA = *reinterpret_cast<const CUtensorMap*>(ix.tmapA);
   const int ngroups = (ix.nlist + 31) / 32;
   static int tiled = -1;  // VLR_FILTER_TILED=0: 2-D tensor TMA of A from the row-major fp16 copy (experiments)
@@ -567,11 +561,10 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
     const char* te = getenv("VLR_FILTER_TILED");
     tiled = te ? atoi(te) : 1;
   }
-  const uint16_t* At = (tiled && ix.cf16t && (int)grid.x * kTcM <= ((ix.nlist + kTcM - 1) / kTcM) * kTcM)
-                           ? ix.cf16t : nullptr;
+  const uint16_t* At = (tiled && ix.cf16t) ? ix.cf16t : nullptr;
   if (CL == 1) {
     k_filter_tc<1><<<grid, kTcThreads, smem, s>>>(tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages, ix.cnorm2, qinv,
-                                                  ix.c_inv, dt, gmin, ngroups, At);
+                                                  ix.c_inv, dt, gmin, ngroups, At, t_lo);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -588,9 +581,9 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   cfg.numAttrs = 1;
   if (CL == 4)
     return cudaLaunchKernelEx(&cfg, k_filter_tc<4>, tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages,
-                              (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups, At);
+                              (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups, At, t_lo);
   return cudaLaunchKernelEx(&cfg, k_filter_tc<2>, tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages,
-                            (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups, At);
+                            (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups, At, t_lo);
 }
 
 // fp16(c * scale) (round to nearest even) into a d8-padded copy; scale is a power of two

@@ -69,12 +69,8 @@ cudaError_t launch_offsets(const Workspace& ws, int nq, int np, cudaStream_t s) 
   if (blocks > 148 * 4) blocks = 148 * 4;
   if (blocks < 1) blocks = 1;
   const size_t sm = (size_t)(nq + 1) * sizeof(long long);
-  static size_t configured = 0;
-  if (sm > 48 * 1024 && sm > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_offsets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    configured = sm;
-  }
+  cudaError_t e = ensure_smem((const void*)k_offsets, sm);
+  if (e != cudaSuccess) return e;
   k_offsets<<<(int)blocks, kOffThreads, sm, s>>>(nq, np, ws.qtot, ws.item_local, ws.item_off);
   return cudaGetLastError();
 }
@@ -254,12 +250,8 @@ cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& w
     return cudaGetLastError();
   }
   const size_t sm = (size_t)kLutQB * (ix.m < 64 ? ix.m : 64) * (ix.dsub + 1) * sizeof(float);
-  static size_t configured = 0;
-  if (sm > 48 * 1024 && sm > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    configured = sm;
-  }
+  cudaError_t e = ensure_smem((const void*)k_lut, sm);
+  if (e != cudaSuccess) return e;
   k_lut<<<grid, 256, sm, s>>>(Q, nq, ix.d, ix.m, ix.dsub, ix.codebooks, ix.npairs, scale, ws.lut);
   return cudaGetLastError();
 }

@@ -587,17 +587,22 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanAr
   const int nq = a.nq, np = a.np, Z = a.waves;
   for (int q = warp; q < nq; q += nw) {
     const long long S = a.item_off[(long long)q * np], E = a.item_off[(long long)(q + 1) * np];
+    int timed_out = 0;
     if (lane == 0) {
       const unsigned long long t0 = globaltimer_ns();
       for (uint32_t spin = 0; ld_acquire_gpu(a.qdone + q) != (unsigned long long)(E - S); ++spin) {
         __nanosleep(64);
         if ((spin & 1023u) == 1023u && globaltimer_ns() - t0 > 4000000000ull) {  // bounded: never hang
-          atomicOr(status, 2);  // the host wait then times out with an error
+          atomicOr(status, 2);  // reported as VLR_ERR_CUDA by vlr_search / the next call on the handle
+          timed_out = 1;
           break;
         }
       }
     }
-    __syncwarp();
+    // a query whose scan did not complete in time is NOT merged and NOT released: its partial lists may
+    // be incomplete (or left over from an earlier search), so ready[q] stays != epoch and the host wait
+    // (vlr_wait_ready / vlr_poll_ready) times out instead of returning a wrong row
+    if (__shfl_sync(kFull, timed_out, 0)) continue;
     __threadfence();
     int z = (int)(((long long)(q + 1) * Z - 1) / nq);  // q's wave and its group range (k_scan's split)
     z = z < Z - 1 ? z : Z - 1;
@@ -736,15 +741,8 @@ int scan_ctas(const DeviceIndex& ix) {
 
 template <int MP, int NB, int EXP, bool REL = false>
 static cudaError_t launch_scan_e(const ScanArgs& a, int n_cta, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan<MP, NB, EXP, REL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(2 * kLutPairBytes));
-    if (e != cudaSuccess) return e;
-    cudaFuncAttributes fa;  // forces the (lazy) module load now
-    if ((e = cudaFuncGetAttributes(&fa, k_scan<MP, NB, EXP, REL>)) != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = ensure_smem((const void*)k_scan<MP, NB, EXP, REL>, (size_t)(2 * kLutPairBytes));
+  if (e != cudaSuccess) return e;
   if (n_cta == 0) return cudaSuccess;  // configure (and so load) only
   k_scan<MP, NB, EXP, REL><<<n_cta, kScanThreads, a.lut_bytes, s>>>(a);
   return cudaGetLastError();
@@ -794,18 +792,14 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
       const char* e = getenv("VLR_RELEASE_WAVES");
       env_waves = e ? atoi(e) : 0;
     }
-    const int zw = env_waves > 0 ? env_waves : kReleaseWaves;
+    // the partial-list slots are sized for kMaxReleaseWaves waves (capi.cu ensure_ws): clamp the override
+    const int zw = env_waves > 0 ? (env_waves < kMaxReleaseWaves ? env_waves : kMaxReleaseWaves) : kReleaseWaves;
     a.waves = nq < zw ? nq : zw;
     // Both kernels must be loaded before the fork: with lazy module loading, loading a kernel while the
     // spinning merger runs waits for the merger (and the merger waits for the scan).
-    static bool merger_loaded = false;
     cudaError_t e = launch_scan_k(ix, a, 0, s);
     if (e != cudaSuccess) return e;
-    if (!merger_loaded) {
-      cudaFuncAttributes fa;
-      if ((e = cudaFuncGetAttributes(&fa, k_release_merge)) != cudaSuccess) return e;
-      merger_loaded = true;
-    }
+    if ((e = ensure_smem((const void*)k_release_merge, 0)) != cudaSuccess) return e;
     // fork: the merger CTA runs concurrently with the scan on a second stream, joined back before return
     e = cudaEventRecord(rel->fork, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(rel->stream, rel->fork, 0);

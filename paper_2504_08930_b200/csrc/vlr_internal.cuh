@@ -25,8 +25,10 @@ constexpr int kScanThreads = VLR_SCAN_THREADS;  // 16 warps per scan CTA (tuning
 constexpr int kScanWarps = kScanThreads / kWarp;
 constexpr int kCandCap = 8192;     // K2 candidate list capacity per query (overflow -> rescan)
 constexpr int kRefineChunk = 1024; // K3 candidates per exact-refine flush
-constexpr int kReleaseWaves = 8;  // NEXT-4: query waves of the release-mode scan
+constexpr int kReleaseWaves = 8;      // NEXT-4: default query waves of the release-mode scan
+constexpr int kMaxReleaseWaves = 16;  // upper bound (VLR_RELEASE_WAVES is clamped to it; sizes the partial slots)
 constexpr int kMaxNprobe = 2048;   // cap on nprobe' (K3 sort buffer; the paper's operating point)
+constexpr int kMaxWorldProbes = 16384;  // world x nprobe' cap of the sharded coarse stage (K2 stage-2 select)
 constexpr int kLutPairBytes = 256 * 64 * 4;  // one [256 codes][64 sub-spaces] fp32 slab (8-bit codes)
 constexpr int kLutPairBytes4 = 16 * 64 * 4;  // one [16 codes][64 sub-spaces] fp32 slab (4-bit codes)
 
@@ -47,6 +49,18 @@ void set_error(const std::string& msg);
   } while (0)
 
 // ---------------------------------------------------------------- device data
+// one exact coarse candidate exchanged between ranks by the centroid-sharded
+// coarse stage: fp64 key D (O2), cluster id l (-1 = padding, D = +inf)
+struct __align__(16) CoarseEntry {
+  double D;
+  int32_t l;
+  int32_t pad;
+};
+
+// K2 / K3b modes (k_coarse.cu)
+constexpr int kSelFull = 0, kSelStage1 = 1, kSelStage2 = 2;
+constexpr int kRefRoute = 0, kRefLocal = 1, kRefMerge = 2;
+
 struct DeviceIndex {
   int d = 0, d8 = 0, nlist = 0, m = 0, mpad = 0, npairs = 0, dsub = 0;
   int nbits = 8, ksub = 256;   // bits per sub-code (8, or 4: nibble-packed) and codewords per sub-space
@@ -59,6 +73,10 @@ struct DeviceIndex {
   int metric = 0;              // 0 squared L2, 1 inner product (distance = -<q, x>)
   int by_residual = 1;         // 1: codes encode x - c_l
   bool shard_only = false;
+  // centroid-sharded coarse stage (world > 1): this rank filters centroids [c_lo, c_hi)
+  // (whole 128-centroid K1 tiles, dealt contiguously); world == 1: [0, nlist)
+  int c_lo = 0, c_hi = 0;
+  bool coarse_sharded = false;  // the NCCL search runs the sharded coarse stage (VLR_COARSE_REPLICATED=1: off)
   // replicated, coarse quantizer
   float* centroids = nullptr;  // [nlist][d]
   float* cnorm2 = nullptr;     // [nlist] ||c||^2 (fp64 -> fp32); zeros for metric 1 (filter = -2<q,c>)
@@ -94,6 +112,10 @@ struct Workspace {
   int32_t* cand = nullptr;     // [nq][kCandCap]
   int32_t* ncand = nullptr;    // [nq]
   double* exact = nullptr;     // [nq][kCandCap] exact fp64 D of listed candidates (K3a)
+  float* x1 = nullptr;         // [nq][np] sharded coarse stage 1: this rank's np smallest group minima
+  float* x1_all = nullptr;     // [world][nq][np] gathered x1 (rank order)
+  CoarseEntry* x2 = nullptr;   // [nq][np] stage 2: this rank's sorted top-np exact (D, l)
+  CoarseEntry* x2_all = nullptr;  // [world][nq][np] gathered x2
   float* bound = nullptr;      // [nq] candidate bound theta~ + 2 Delta*
   int32_t* probes = nullptr;   // [nq][np]
   float* term1 = nullptr;      // [nq][np] query-dependent constant of probe p (fp64 -> fp32): ||q - c_l||^2
@@ -138,10 +160,17 @@ struct vlr_index {
   cudaStream_t lut_stream = nullptr;
   cudaEvent_t lut_fork = nullptr, lut_join = nullptr;
   int lut_side = -1;  // -1 unset; 0 serial (VLR_LUT_SERIAL=1, A/B timing), 1 forked
+  bool lut_forked = false;  // the current search forked K5 (joined before the scan)
+  int stage = 0, stage_nq = 0, stage_np = 0;  // staged search progress (vlr_coarse_stage1/2, vlr_search_stage3)
   std::string last_err;
 };
 
 namespace vlr {
+
+// Per-(device, kernel) launch configuration: raises the kernel's dynamic shared-memory limit to at
+// least `bytes` on the CURRENT device (the attribute is per device context) and forces its module to be
+// loaded (cudaFuncGetAttributes); cached, thread-safe. Every launcher calls it before a launch.
+cudaError_t ensure_smem(const void* fn, size_t bytes);
 
 // ---------------------------------------------------------------- launchers
 // K0 layout (load time)
@@ -150,16 +179,17 @@ cudaError_t launch_layout(const DeviceIndex& ix, const uint8_t* stage_codes, con
 // stage 0..2 coarse quantizer
 cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, float* qsq, uint16_t* qf16, float* qinv,
                          int32_t* status, cudaStream_t s);
-cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, float* dt, float* gmin,
-                             cudaStream_t s);
+// K1 over centroid tiles [t_lo, t_hi) (128 centroids each): dt columns and gmin groups of those tiles
+cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, int t_lo, int t_hi,
+                             float* dt, float* gmin, cudaStream_t s);
 cudaError_t launch_round_f16(const float* src, int rows, int d, int d8, float scale, uint16_t* dst, cudaStream_t s);
 cudaError_t make_tmap_2d(void* map, const uint16_t* base, int rows, int cols, int box_rows);
 cudaError_t launch_tile_f16(const DeviceIndex& ix, cudaStream_t s);
-cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float band_rel,
+cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float e_dot, int mode,
                           cudaStream_t s);
 cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s);
 cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, int np, uint8_t* miss,
-                          int32_t* probes_out, cudaStream_t s);
+                          int32_t* probes_out, int mode, cudaStream_t s);
 // stage 3..4
 cudaError_t launch_offsets(const Workspace& ws, int nq, int np, cudaStream_t s);
 cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s);

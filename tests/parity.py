@@ -18,10 +18,13 @@ def tol(ref, qn2):
     return REL * np.maximum(np.abs(ref), FLOOR * qn2)
 
 
-def check(index, Q, gpu, orc, hot=None, idmap=None, qsel=None, max_report=5):
+def check(index, Q, gpu, orc, hot=None, idmap=None, qsel=None, max_report=5, ref=None):
     """Compare GPU outputs with oracle outputs on the queries `qsel` (rows of
     Q; default all). gpu/orc: dicts with ids, dist, miss, probes (numpy,
-    row-aligned with qsel). Returns a list of failure strings (empty = pass).
+    row-aligned with qsel). ref: optional precomputed dist_ref of the GPU's
+    valid (id >= 0) entries in row-major order (a multi-rank check assembles it
+    from the ranks that hold the codes). Returns a list of failure strings
+    (empty = pass).
     """
     errs = []
     qsel = np.arange(len(Q)) if qsel is None else np.asarray(qsel)
@@ -47,7 +50,8 @@ def check(index, Q, gpu, orc, hot=None, idmap=None, qsel=None, max_report=5):
     # R2: every returned distance vs dist_ref
     valid = gids >= 0
     rows = np.repeat(qsel[:, None], k, 1)[valid]
-    ref = oracle.dist_ref(index, Q, rows, gids[valid], idmap=idmap)
+    if ref is None:
+        ref = oracle.dist_ref(index, Q, rows, gids[valid], idmap=idmap)
     if np.any(np.isnan(ref)):
         errs.append("R2 GPU returned unknown ids")
     qn2v = np.repeat(qn2[:, None], k, 1)[valid]
@@ -96,3 +100,24 @@ def check(index, Q, gpu, orc, hot=None, idmap=None, qsel=None, max_report=5):
     if np.any(full & (ref > lim)):
         errs.append("R3 GPU returned an id beyond r_k + tol")
     return errs
+
+
+def merge_partials_np(parts, k):
+    """Merge rank-partial oracle results (dicts with ids, dist, kth1; the same
+    probes/miss on every rank) into the result over the union of the ranks'
+    lists: the k smallest by (dist, id), padded (-1, +inf); kth1 = the
+    (k+1)-th smallest of the union of every rank's top-k and (k+1)-th (P:414;
+    the hybrid = monolithic rule S:473)."""
+    nq = parts[0]["ids"].shape[0]
+    out = dict(ids=np.full((nq, k), -1, np.int64), dist=np.full((nq, k), np.inf), kth1=np.full(nq, np.inf),
+               probes=parts[0]["probes"], miss=parts[0]["miss"])
+    big = np.iinfo(np.int64).max
+    for q in range(nq):
+        i = np.concatenate([p["ids"][q] for p in parts])
+        dv = np.concatenate([p["dist"][q] for p in parts])
+        o = np.lexsort((np.where(i < 0, big, i), dv))
+        sel = o[:k]
+        out["ids"][q], out["dist"][q] = i[sel], dv[sel]
+        extra = np.concatenate([dv[o[k:]], [p["kth1"][q] for p in parts]])
+        out["kth1"][q] = extra.min() if len(extra) else np.inf
+    return out

@@ -36,7 +36,7 @@ def test_exports_every_declared_symbol():
 
 
 def test_version():
-    assert vlr.version() == (1, 2)
+    assert vlr.version() == (1, 3)
 
 
 def _tiny(m=2, d=4, L=3):

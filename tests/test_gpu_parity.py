@@ -620,12 +620,17 @@ def test_nccl_exchange_path_single_rank(c1_index, c1_queries, monkeypatch):
     n_plain = h.last_launch_count
     h.close()
     monkeypatch.setenv("VLR_FORCE_EXCHANGE", "1")
+    monkeypatch.setenv("VLR_COARSE_REPLICATED", "1")  # the replicated coarse stage: only the result exchange
     hx = vlr.Index.from_arrays(c1_index, nccl_id=vlr.nccl_unique_id())
     b = gpu_search(hx, c1_queries, c["nprobe"], c["k"])
     assert hx.last_launch_count == n_plain + 1  # + K8
     for key in a:
         assert np.array_equal(a[key], b[key]), key
     hx.close()
+    # and directly against the oracle (rules R1-R4), not only against the plain search
+    o = oracle.search(c1_index, c1_queries, c["nprobe"], c["k"])
+    errs = check(c1_index, c1_queries, b, o, idmap=oracle.IdMap(c1_index))
+    assert not errs, errs
 
 
 @pytest.mark.parametrize("flag,val", [("VLR_FILTER_PERSISTENT", "1"), ("VLR_FILTER_CLUSTER", "2"),

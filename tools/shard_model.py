@@ -1,0 +1,122 @@
+"""Per-rank device time of the sharded search at G ranks, measured on ONE GPU.
+
+The G ranks are G shard-only handles of the same index (each holds its dealt
+hot lists and filters its own 128-centroid tiles). Their staged calls run one
+after another on one stream, so CUDA events around each rank's call measure
+exactly that rank's kernels:
+  stage1 = qprep + K1 (its tiles) + K2 stage 1
+  stage2 = K2 stage 2 + K3a + K3b local
+  stage3 = K3b merge + route + K4b + (LUT join) + K6 scan + K7
+The exchanges (3 all-gathers on NVLink at G > 1) are not measurable on one
+GPU; the line reports them as a separate term. Output: one JSON line.
+
+  python tools/shard_model.py --config C4 --G 8 --batches 10
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--G", type=int, default=8)
+    ap.add_argument("--batches", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--seed", type=int, default=2504_08930)
+    a = ap.parse_args()
+    import datagen
+    import paper_2504_08930_b200 as vlr
+    from paper_2504_08930_b200 import build
+    build.build()
+    c = datagen.CONFIGS[a.config]
+    B, K = c["batch"], c["k"]
+    t = time.time()
+    ix = datagen.make_index(c["N"], c["d"], c["nlist"], c["m"], seed=a.seed, device="cuda")
+    gen_s = time.time() - t
+    pool = datagen.make_queries(c["N"], c["d"], c["nlist"], (a.warmup + a.batches) * B, seed=a.seed, stream=2,
+                                alpha=c["alpha"], device="cuda")
+    Qd = torch.from_numpy(pool).cuda().reshape(-1, B, c["d"])
+    G = a.G
+    hs = [vlr.Index.from_arrays(ix, rank=r, world=G) for r in range(G)]
+    h1 = vlr.Index.from_arrays(ix)
+    for h in hs + [h1]:
+        h.reserve(B, c["nprobe"], K)
+    s = torch.cuda.current_stream()
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(s)
+        return e
+
+    rows = []
+    for b in range(a.warmup + a.batches):
+        Q = Qd[b]
+        e1 = []
+        x1 = []
+        for h in hs:
+            e0 = ev()
+            x1.append(h.coarse_stage1(Q, c["nprobe"], stream=s))
+            e1.append((e0, ev()))
+        x1_all = torch.stack(x1)
+        e2, x2 = [], []
+        for h in hs:
+            e0 = ev()
+            x2.append(h.coarse_stage2(Q, c["nprobe"], x1_all, stream=s))
+            e2.append((e0, ev()))
+        x2_all = torch.stack(x2)
+        e3, parts = [], []
+        for h in hs:
+            h.set_profiling(2)
+            e0 = ev()
+            parts.append(h.search_stage3(Q, c["nprobe"], K, x2_all, stream=s))
+            e3.append((e0, ev()))
+        e0 = ev()
+        mi, md = vlr.merge_partials(torch.stack([p[0] for p in parts]), torch.stack([p[1] for p in parts]), stream=s)
+        em = (e0, ev())
+        torch.cuda.synchronize()
+        scan = [h.stage_times(0)["scan"] for h in hs]
+        for h in hs:
+            h.set_profiling(0)
+        # single-GPU reference on the same batch: bitwise equality + its stage breakdown
+        h1.set_profiling(1)
+        ids1, d1, m1, p1 = h1.search(Q, c["nprobe"], K, sync=True)
+        st1 = h1.stage_times(0)
+        h1.set_profiling(0)
+        same = bool(torch.equal(ids1, mi) and torch.equal(d1, md) and torch.equal(p1, parts[0][3]))
+        if b < a.warmup:
+            continue
+        t1 = [x.elapsed_time(y) for x, y in e1]
+        t2 = [x.elapsed_time(y) for x, y in e2]
+        t3 = [x.elapsed_time(y) for x, y in e3]
+        rows.append(dict(t1=t1, t2=t2, t3=t3, scan=scan, merge=em[0].elapsed_time(em[1]), same=same, single=st1))
+    T1, T2, T3, SC = (np.array([r[k] for r in rows]) for k in ("t1", "t2", "t3", "scan"))
+    nonscan = T1 + T2 + T3 - SC  # [batches, G] ms
+    single = {k: float(np.mean([r["single"][k] for r in rows])) for k in rows[0]["single"]}
+    out = {
+        "tool": "tools/shard_model.py", "config": a.config, "G": G, "batch": B, "nprobe": c["nprobe"], "k": K,
+        "batches": a.batches, "gen_s": round(gen_s, 1),
+        "bitwise_equal_to_single_gpu": all(r["same"] for r in rows),
+        "per_rank_ms": {"stage1_mean": float(T1.mean()), "stage2_mean": float(T2.mean()),
+                        "stage3_minus_scan_mean": float((T3 - SC).mean()), "scan_mean": float(SC.mean()),
+                        "scan_max_rank_mean": float(SC.max(1).mean()),
+                        "nonscan_mean": float(nonscan.mean()), "nonscan_max_rank_mean": float(nonscan.max(1).mean()),
+                        "step_kernels_max_rank_mean": float((T1 + T2 + T3).max(1).mean())},
+        "merge_ms": float(np.mean([r["merge"] for r in rows])),
+        "single_gpu_stage_ms": single,
+        "model": "step(G) = max over ranks of (stage1 + stage2 + stage3) + 3 all-gathers (x1 nq*np*4 B, x2 "
+                 "nq*np*16 B, results nq*k*16 B per rank; NVLink latency, not measurable on one GPU) + K8 merge",
+    }
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
