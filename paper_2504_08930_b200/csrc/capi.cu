@@ -500,9 +500,12 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   LTRY(cudaMemcpyAsync(ix.centroids, D.centroids, sizeof(float) * L * d, cudaMemcpyHostToDevice, s));
   LTRY(cudaMemcpyAsync(ix.cnorm2, cn2.data(), sizeof(float) * L, cudaMemcpyHostToDevice, s));
   LTRY(launch_round_f16(ix.centroids, L, d, ix.d8, std::ldexp(1.0f, ix.c_exp), ix.cf16, s));
-  LTRY(make_tmap_2d(ix.tmapA, ix.cf16, L, ix.d8, 128));
+  LTRY(make_tmap_2d(ix.tmapA, ix.cf16, L, ix.d8, 128, true));
   LTRY(dalloc(&ix.cf16t, (size_t)((L + 127) / 128) * 128 * (size_t)((ix.d8 + 63) / 64) * 64));
   LTRY(launch_tile_f16(ix, s));
+  // the pre-tiled copy as a 2-D [tiles * kblocks * 128][64] tensor (box = one 16 KB tile image, stored
+  // pre-swizzled: no TMA swizzle) for the CTA-pair filter's .cta_group::2 tensor loads
+  LTRY(make_tmap_2d(ix.tmapAt, ix.cf16t, ((L + 127) / 128) * ((ix.d8 + 63) / 64) * 128, 64, 128, false));
   LTRY(cudaMemcpyAsync(ix.codebooks, D.codebooks, sizeof(float) * ncb, cudaMemcpyHostToDevice, s));
   LTRY(cudaMemcpyAsync(ix.owner, owner.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, s));
   LTRY(cudaMemcpyAsync(ix.local, local.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, s));
@@ -982,7 +985,9 @@ static vlr_status staged_begin(vlr_index* h, const float* Q, int32_t nq, int32_t
   if (st != VLR_OK) return st;
   if (nq < 1 || !Q) return fail(VLR_ERR_INVALID_ARG, "staged search: nq >= 1 and queries required");
   VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
-  return ensure_ws(h, nq, *np, k);
+  // sized for any k up front: a reallocation between the stages would drop the LUT and the gathered
+  // buffers of the batch in flight
+  return ensure_ws(h, nq, *np, std::max(k, kMaxK));
 }
 
 vlr_status vlr_coarse_stage1(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, float* d_x1, void* stream) {

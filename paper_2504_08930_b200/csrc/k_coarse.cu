@@ -114,6 +114,7 @@ cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, fl
 //     sets is the single-GPU candidate set.
 constexpr int kSelThreads = 1024;
 constexpr int kSelMaxGroups = 16384;  // groups per rank <= 16384 (nlist <= 512K) for the sorted-minima path
+constexpr int kSelGroupCap = 2048;    // qualifying 32-centroid groups gathered per query (else: full row scan)
 
 // radix select (4 x 8-bit digits) of the want-th smallest (1-based) of n order-preserving keys in shared
 // memory; the whole CTA calls it, the result is CTA-uniform
@@ -253,31 +254,61 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
         if (pos < (unsigned)kCandCap) out[pos] = i;
       }
     };
-    const int n = hi - lo;
-    if ((L & 3) == 0 && (lo & 3) == 0 && (n & 3) == 0) {
-      const float4* r4 = reinterpret_cast<const float4*>(row + lo);
-      constexpr int U = 2;  // loads in flight per thread before any emit (32 regs: 2 CTAs per SM)
-      for (int i0 = 0; i0 < n / 4; i0 += U * blockDim.x) {
-        float4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = i0 + u * blockDim.x + threadIdx.x;
-          v[u] = i < n / 4 ? __ldg(r4 + i) : make_float4(CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = i0 + u * blockDim.x + threadIdx.x;
-          const bool in = i < n / 4;
-          emit(in && v[u].x <= bnd, lo + 4 * i);
-          emit(in && v[u].y <= bnd, lo + 4 * i + 1);
-          emit(in && v[u].z <= bnd, lo + 4 * i + 2);
-          emit(in && v[u].w <= bnd, lo + 4 * i + 3);
-        }
+    // Group-guided compaction: K1 stored gmin = the minimum of the group's 32 stored dt values (the same
+    // fp32 values, rows >= L as +inf), so {l : dt_l <= bnd} is exactly the union, over the groups with
+    // gmin <= bnd, of their members with dt <= bnd. Only those groups' 128-byte dt pieces are read
+    // (~200 of the 2048 groups of a C4 row); more than kSelGroupCap qualifying groups: full row scan.
+    __shared__ int s_grp[kSelGroupCap];
+    __shared__ unsigned s_ng;
+    if (threadIdx.x == 0) s_ng = 0u;
+    __syncthreads();
+    const float* grow = gmin + (size_t)q * ngL + g0;
+    for (int i0 = 0; i0 < ng; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
+      const bool keep = i < ng && grow[i] <= bnd;
+      const unsigned km = __ballot_sync(kFull, keep);
+      if (km == 0u) continue;
+      unsigned base = 0u;
+      if (lane == 0) base = atomicAdd(&s_ng, (unsigned)__popc(km));
+      base = __shfl_sync(kFull, base, 0);
+      const unsigned pos = base + __popc(km & ((1u << lane) - 1u));
+      if (keep && pos < (unsigned)kSelGroupCap) s_grp[pos] = g0 + i;
+    }
+    __syncthreads();
+    const unsigned ngq = s_ng;
+    const int warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    if (ngq <= (unsigned)kSelGroupCap) {
+      for (unsigned j = warp; j < ngq; j += nwarp) {  // warp-uniform loop: one 128-B piece per group
+        const int l = s_grp[j] * 32 + lane;
+        emit(l < hi && row[l] <= bnd, l);
       }
     } else {
-      for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-        const int i = i0 + threadIdx.x;
-        emit(i < n && row[lo + i] <= bnd, lo + i);
+      const int n = hi - lo;
+      if ((L & 3) == 0 && (lo & 3) == 0 && (n & 3) == 0) {
+        const float4* r4 = reinterpret_cast<const float4*>(row + lo);
+        constexpr int U = 2;  // loads in flight per thread before any emit (32 regs: 2 CTAs per SM)
+        for (int i0 = 0; i0 < n / 4; i0 += U * blockDim.x) {
+          float4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * blockDim.x + threadIdx.x;
+            v[u] = i < n / 4 ? __ldg(r4 + i) : make_float4(CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * blockDim.x + threadIdx.x;
+            const bool in = i < n / 4;
+            emit(in && v[u].x <= bnd, lo + 4 * i);
+            emit(in && v[u].y <= bnd, lo + 4 * i + 1);
+            emit(in && v[u].z <= bnd, lo + 4 * i + 2);
+            emit(in && v[u].w <= bnd, lo + 4 * i + 3);
+          }
+        }
+      } else {
+        for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+          const int i = i0 + threadIdx.x;
+          emit(i < n && row[lo + i] <= bnd, lo + i);
+        }
       }
     }
     __syncthreads();

@@ -454,6 +454,186 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------- CTA-pair filter (cta_group::2)
+// The same contraction with M = 256-centroid tiles on a CTA PAIR (a 2-CTA
+// cluster on one TPC): CTA t of the pair holds centroid rows [128t, 128t+128)
+// of the tile (A, K-major) and query rows [t QT/2, (t+1) QT/2) of the batch
+// tile (B, K-major); the leader (rank 0) issues tcgen05.mma.cta_group::2 with
+// M = 256, N = QT, which reads both CTAs' shared memory at the same offsets
+// and leaves each CTA the accumulator of ITS 128 rows x QT columns in its own
+// TMEM. Both CTAs' tensor TMAs (.cta_group::2) complete their bytes on the
+// leader's full barrier (rank-0 address from mapa); the leader's commits are
+// multicast to both CTAs' empty / tfull barriers. Per 128 centroids an SM
+// now ingests A (256 KB at d 1024) + HALF the query tile instead of the whole
+// one: 512 KB instead of 768 KB at QT = 256 (K1). Arithmetic per
+// element is that of k_filter_tc (same operands, fp32 accumulation over K in
+// the tensor core, same epilogue), so the band proof is unchanged.
+__device__ __forceinline__ uint32_t mapa_rank0(uint32_t saddr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+  return r;
+}
+__device__ __forceinline__ void tma_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar_rank0) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(bar_rank0)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_pair(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          s32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+// grid.x = 2 x (pairs of 128-centroid tiles in [t0, t_end)), grid.y = query tiles of QT rows; cluster (2,1,1).
+// tmA: the pre-tiled fp16 centroids (cf16t) as a 2-D [tiles*kblocks*128][64] tensor, box {64, 128},
+// no swizzle (the tiles are stored pre-swizzled); tmB: fp16 queries [nq][d8], box {64, QT/2}, SWIZZLE_128B.
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_filter_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int L, int nq,
+                  int kblocks, int QT, int stages, const float* __restrict__ cn2, const float* __restrict__ qinv,
+                  float c_inv, float* __restrict__ dt, float* __restrict__ gmin, int ngroups, int t0, int t_end) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull;
+  __shared__ uint32_t tmem_base;
+  __shared__ float s_inv[256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();                // 0 = leader
+  const int tile = t0 + (int)blockIdx.x;                // this CTA's 128-centroid tile (pairs: 2p, 2p+1)
+  const int m0 = tile * kTcM;
+  const int q0 = blockIdx.y * QT;
+  const int half = QT / 2;
+  const uint32_t bytesA = kTcM * 128, bytesB = (uint32_t)half * 128;
+  const uint32_t stage_bytes = bytesA + bytesB;
+  uint32_t ncols = 32;
+  while ((int)ncols < QT) ncols <<= 1;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mb_init(&full[s], 1);   // leader: its own arrive.expect_tx (both CTAs' bytes)
+      mb_init(&empty[s], 1);  // the leader's MMA commit, multicast to both CTAs
+    }
+    mb_init(&tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 1) {  // collective over the pair: same warp, same destination offset in both CTAs
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tmem_base)), "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();  // the leader's barriers are initialised before the peer's TMA signals them
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tbase = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full0 = mapa_rank0(s32(&full[0]));  // the leader's full barriers (same layout)
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % stages;
+        const uint32_t ph = (uint32_t)(kb / stages) & 1u;
+        mb_wait(&empty[s], ph ^ 1u);
+        uint8_t* sA = smem + (size_t)s * stage_bytes;
+        uint8_t* sB = sA + bytesA;
+        if (crank == 0) mb_expect_tx(&full[s], 2u * stage_bytes);
+        const uint32_t fb = full0 + (uint32_t)s * 8u;
+        tma_2d_pair(s32(sA), &tmA, 0, (tile * kblocks + kb) * kTcM, fb);
+        tma_2d_pair(s32(sB), &tmB, kb * kTcBK, q0 + (int)crank * half, fb);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && crank == 0) {
+      // instruction descriptor: F32 accum, A/B F16, K-major, N = QT, M = 256
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(QT >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % stages;
+        const uint32_t ph = (uint32_t)(kb / stages) & 1u;
+        mb_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t aaddr = s32(smem + (size_t)s * stage_bytes);
+        const uint32_t baddr = aaddr + bytesA;
+#pragma unroll
+        for (int kk = 0; kk < kTcBK / 16; ++kk)
+          mma_f16_pair(tbase, sw128_desc(aaddr + kk * 32), sw128_desc(baddr + kk * 32), idesc, (kb | kk) != 0 ? 1u : 0u);
+        mma_commit_pair(&empty[s]);  // frees stage s in both CTAs once these MMAs have read it
+      }
+      mma_commit_pair(&tfull);  // both CTAs' accumulators complete
+    }
+    __syncwarp();
+  } else {
+    // epilogue: warps 2..5 -> TMEM lane groups (warp % 4) = this CTA's 128 centroid rows
+    const int lg = warp & 3;
+    const int row = m0 + lg * 32 + lane;
+    const bool live = tile < t_end;  // the pair's second tile past the range end (odd tile count): no stores
+    const float cn = row < L ? cn2[row] : 0.f;
+    for (int j = threadIdx.x - 64; j < QT; j += 128) {
+      const int q = q0 + j;
+      s_inv[j] = q < nq ? qinv[q] * c_inv : 0.f;  // product of powers of two >= 2^-120: exact
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
+    mb_wait(&tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int grp = tile * 4 + lg;
+    for (int c = 0; c < QT; c += 32) {
+      uint32_t v[32];
+      const uint32_t taddr = tbase + ((uint32_t)(lg * 32) << 16) + (uint32_t)c;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr));
+      if (c + 16 < QT) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr + 16u));
+      } else {
+#pragma unroll
+        for (int j = 16; j < 32; ++j) v[j] = __float_as_uint(CUDART_INF_F);
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      float f[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        f[j] = row < L ? cn - 2.f * (__uint_as_float(v[j]) * s_inv[c + j < QT ? c + j : 0]) : CUDART_INF_F;
+        const int q = q0 + c + j;
+        if (live && row < L && q < nq && c + j < QT) dt[(size_t)q * L + row] = f[j];
+      }
+#pragma unroll
+      for (int w = 16; w >= 1; w >>= 1) {
+        const bool upper = (lane & w) != 0;
+#pragma unroll
+        for (int j = 0; j < w; ++j) {
+          const float send = upper ? f[j] : f[j + w];
+          const float keep = upper ? f[j + w] : f[j];
+          f[j] = fminf(keep, __shfl_xor_sync(kFull, send, w));
+        }
+      }
+      const int q = q0 + c + lane;
+      if (live && q < nq && c + lane < QT && grp < ngroups) gmin[(size_t)q * ngroups + grp] = f[0];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();  // the peer's MMAs / commits no longer touch this CTA's smem or barriers
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(ncols));
+  }
+}
+
 // ---------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -471,8 +651,9 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2-D fp16 tensor [rows][cols] (cols = d8, row stride d8*2 B), box {64, box_rows}, SW128
-cudaError_t make_tmap_2d(void* map_, const uint16_t* base, int rows, int cols, int box_rows) {
+// 2-D fp16 tensor [rows][cols] (row stride cols*2 B), box {64, box_rows}, SWIZZLE_128B (swizzle = false:
+// none -- for tiles stored pre-swizzled)
+cudaError_t make_tmap_2d(void* map_, const uint16_t* base, int rows, int cols, int box_rows, bool swizzle) {
   CUtensorMap* map = reinterpret_cast<CUtensorMap*>(map_);
   EncodeTiledFn fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
@@ -481,7 +662,8 @@ cudaError_t make_tmap_2d(void* map_, const uint16_t* base, int rows, int cols, i
   cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<uint16_t*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -520,9 +702,65 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   if (nacc == 1 && !use_persistent)
     for (int c : {4, 2})
       if (c <= cl_env && nN % (8 * c) == 0 && (t_hi - t_lo) % c == 0) { CL = c; break; }
+  // CTA-pair kernel (default; VLR_FILTER_PAIR=0: the one-CTA kernels): the query tile QT <= 256 rows is
+  // halved (multiple of 16) while the grid has fewer than ~2 CTAs per SM, so a shard's few centroid tiles
+  // still fill the GPU (world > 1: each rank filters 1/world of the tiles)
+  static int pair_env = -1;
+  if (pair_env < 0) {
+    const char* pe = getenv("VLR_FILTER_PAIR");
+    pair_env = pe ? atoi(pe) : 1;
+  }
+  if (pair_env && !use_persistent && CL == 1) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = t_hi - t_lo, pairs = (tiles + 1) / 2;
+    int QT = nq <= 256 ? ((nq + 15) / 16) * 16 : 256;
+    static int qt_env = -1;  // VLR_FILTER_QT: fixed query tile (experiments)
+    if (qt_env < 0) {
+      const char* qe = getenv("VLR_FILTER_QT");
+      qt_env = qe ? atoi(qe) : 0;
+    }
+    if (qt_env >= 32 && qt_env <= 256 && qt_env % 32 == 0) QT = qt_env;
+    else
+      while (QT > 32 && (long long)2 * pairs * ((nq + QT - 1) / QT) < 2LL * sms) QT = ((QT / 2 + 15) / 16) * 16;
+    if (QT < 32) QT = 32;  // two halves of >= 16 rows (N multiple of 16, one SW128 atom per half)
+    CUtensorMap tmBp;
+    cudaError_t e = make_tmap_2d(&tmBp, Qh, nq, ix.d8, QT / 2, true);
+    if (e != cudaSuccess) return e;
+    const uint32_t stage_bytes = kTcM * 128 + (uint32_t)(QT / 2) * 128;
+    int stages = (int)((100 * 1024) / stage_bytes);
+    static int st_env = -1;  // VLR_FILTER_STAGES (experiments)
+    if (st_env < 0) {
+      const char* se = getenv("VLR_FILTER_STAGES");
+      st_env = se ? atoi(se) : 0;
+    }
+    if (st_env >= 2) stages = st_env;
+    if (stages > kTcMaxStages) stages = kTcMaxStages;
+    if (stages < 2) stages = 2;
+    const size_t smem = (size_t)stages * stage_bytes + 1024;
+    e = ensure_smem((const void*)k_filter_pair, smem);
+    if (e != cudaSuccess) return e;
+    const int kblocks = (ix.d8 + kTcBK - 1) / kTcBK;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs, (nq + QT - 1) / QT);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_filter_pair, *reinterpret_cast<const CUtensorMap*>(ix.tmapAt), tmBp, ix.nlist,
+                              nq, kblocks, QT, stages, (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin,
+                              (ix.nlist + 31) / 32, t_lo, t_hi);
+  }
   const int box_rows_b = (nN < 256 ? nN : 256) / CL;
   CUtensorMap tmB;
-  cudaError_t e = make_tmap_2d(&tmB, Qh, nq, ix.d8, box_rows_b);
+  cudaError_t e = make_tmap_2d(&tmB, Qh, nq, ix.d8, box_rows_b, true);
   if (e != cudaSuccess) return e;
   const int kblocks = (ix.d8 + kTcBK - 1) / kTcBK;
   if (nacc == 1 && use_persistent) {

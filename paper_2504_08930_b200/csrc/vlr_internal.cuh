@@ -85,6 +85,7 @@ struct DeviceIndex {
   int c_exp = 0;               // power-of-two centroid scale: max |c * 2^c_exp| < 2^14
   float c_inv = 1.f;           // 2^-c_exp
   alignas(64) unsigned char tmapA[128] = {};  // CUtensorMap of cf16 (box 64 x 128, SWIZZLE_128B)
+  alignas(64) unsigned char tmapAt[128] = {}; // CUtensorMap of cf16t as [tiles*kblocks*128][64] (box 64 x 128, pre-swizzled)
   float cmax = 0.f;            // max ||c|| (host), for the filter band
   float* codebooks = nullptr;  // [m][ksub][dsub]
   int32_t* owner = nullptr;    // [nlist] owner rank or -1 (mapping table)
@@ -183,7 +184,7 @@ cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, fl
 cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, int t_lo, int t_hi,
                              float* dt, float* gmin, cudaStream_t s);
 cudaError_t launch_round_f16(const float* src, int rows, int d, int d8, float scale, uint16_t* dst, cudaStream_t s);
-cudaError_t make_tmap_2d(void* map, const uint16_t* base, int rows, int cols, int box_rows);
+cudaError_t make_tmap_2d(void* map, const uint16_t* base, int rows, int cols, int box_rows, bool swizzle);
 cudaError_t launch_tile_f16(const DeviceIndex& ix, cudaStream_t s);
 cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float e_dot, int mode,
                           cudaStream_t s);

@@ -109,8 +109,9 @@ def merge_partials_np(parts, k):
     (k+1)-th smallest of the union of every rank's top-k and (k+1)-th (P:414;
     the hybrid = monolithic rule S:473)."""
     nq = parts[0]["ids"].shape[0]
+    # a probe is a miss iff no rank holds it (each rank's oracle saw only its own lists as resident)
     out = dict(ids=np.full((nq, k), -1, np.int64), dist=np.full((nq, k), np.inf), kth1=np.full(nq, np.inf),
-               probes=parts[0]["probes"], miss=parts[0]["miss"])
+               probes=parts[0]["probes"], miss=np.minimum.reduce([p["miss"] for p in parts]))
     big = np.iinfo(np.int64).max
     for q in range(nq):
         i = np.concatenate([p["ids"][q] for p in parts])
