@@ -224,14 +224,14 @@ def gen_index(c, seed, rank, world, hot=None, gt_queries=None):
     VLR_GEN_CACHE=<dir> reuses arrays saved by an earlier process of the same
     command sequence (never relied on for timing: only generation time)."""
     import datagen
-    sizes = datagen.list_sizes(c["N"], c["nlist"], seed)
+    sizes = datagen.list_sizes(c["N"], c["d"], c["nlist"], seed, device="cuda")
     owned = None
     if world > 1:
         own = datagen.deal_owners(sizes, np.arange(c["nlist"]) if hot is None else hot, world)
         owned = own == rank
     t = time.time()
     cache = os.environ.get("VLR_GEN_CACHE")
-    key = f"{c['N']}_{c['d']}_{c['nlist']}_{c['m']}_{seed}_{world}_{rank}_{'all' if hot is None else len(hot)}"
+    key = f"g2_{c['N']}_{c['d']}_{c['nlist']}_{c['m']}_{seed}_{world}_{rank}_{'all' if hot is None else len(hot)}"
     key += f"_mt{c['metric']}_br{c['by_residual']}_nb{c['nbits']}"
     if gt_queries is not None:
         import hashlib
@@ -266,7 +266,7 @@ def calib_hot(c, seed):
     if c["hot_mass"] >= 1.0:
         return None, None
     ncal = 10_000
-    C = datagen.gen.Generator(c["N"], c["d"], c["nlist"], 1, seed=seed, device="cuda").centroids().cpu().numpy()
+    C = datagen.centroids(c["N"], c["d"], c["nlist"], seed, device="cuda")
     Qc = datagen.make_queries(c["N"], c["d"], c["nlist"], ncal, seed=seed, stream=1, alpha=c["alpha"], device="cuda")
     counts = datagen.access_counts(C, Qc, c["nprobe"], device="cuda", metric=c["metric"])
     return datagen.hot_from_mass(counts, c["hot_mass"]), counts

@@ -19,6 +19,8 @@ from .gen import (  # noqa: F401
     topk_share,
     index_from_parts,
     list_sizes,
+    centroids,
+    layout,
     deal_owners,
     pack_nibbles,
 )

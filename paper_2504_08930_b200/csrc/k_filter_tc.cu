@@ -702,13 +702,13 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   if (nacc == 1 && !use_persistent)
     for (int c : {4, 2})
       if (c <= cl_env && nN % (8 * c) == 0 && (t_hi - t_lo) % c == 0) { CL = c; break; }
-  // CTA-pair kernel (default; VLR_FILTER_PAIR=0: the one-CTA kernels): the query tile QT <= 256 rows is
+  // CTA-pair kernel (VLR_FILTER_PAIR=1): the query tile QT <= 256 rows is
   // halved (multiple of 16) while the grid has fewer than ~2 CTAs per SM, so a shard's few centroid tiles
   // still fill the GPU (world > 1: each rank filters 1/world of the tiles)
   static int pair_env = -1;
   if (pair_env < 0) {
     const char* pe = getenv("VLR_FILTER_PAIR");
-    pair_env = pe ? atoi(pe) : 1;
+    pair_env = pe ? atoi(pe) : 0;  // off by default: measured slower at C4 (tools/k1_bench.py)
   }
   if (pair_env && !use_persistent && CL == 1) {
     int dev = 0, sms = 148;

@@ -202,6 +202,8 @@ def test_nccl_search_stall_times_out_with_error():
         ix = datagen.make_index(4000, 16, 64, 4, seed=1)
         Q = torch.from_numpy(datagen.make_queries(4000, 16, 64, 8, seed=1, stream=2)).cuda()
         h = vlr.Index.from_arrays(ix, device=0, nccl_id=vlr.nccl_unique_id())
+        import os
+        os.environ["VLR_NCCL_TIMEOUT_MS"] = "500"  # after the (1-rank) communicator init: bounds the search
         t = time.time()
         try:
             h.search(Q, 4, 5, sync=True)
@@ -215,7 +217,7 @@ def test_nccl_search_stall_times_out_with_error():
             print("SECOND", e.name)
         torch.cuda.synchronize()
     """
-    r = _run_py(code, {"VLR_FORCE_EXCHANGE": "1", "VLR_FAULT_STALL_US": "3000000", "VLR_NCCL_TIMEOUT_MS": "500"})
+    r = _run_py(code, {"VLR_FORCE_EXCHANGE": "1", "VLR_FAULT_STALL_US": "3000000"})
     assert "ERR NCCL" in r.stdout and "SECOND NCCL" in r.stdout, (r.stdout, r.stderr[-2000:])
     secs = float(r.stdout.split("ERR NCCL")[1].split()[0])
     # detected at the 0.5 s timeout; ncclCommAbort may then wait for the bounded stall to drain

@@ -19,8 +19,8 @@ p.add_argument("--config", default="C4")
 p.add_argument("--nq", type=int, default=256)
 a = p.parse_args()
 c = datagen.CONFIGS[a.config]
-g = datagen.gen.Generator(c["N"], c["d"], c["nlist"], c["m"], device="cuda")
-C = g.centroids()
+g = None
+C = datagen.layout(c["N"], c["d"], c["nlist"], device="cuda")["centroids"]
 C = torch.as_tensor(C, device="cuda", dtype=torch.float32)
 Q = torch.from_numpy(datagen.make_queries(c["N"], c["d"], c["nlist"], a.nq, stream=2, device="cuda")).cuda()
 d = c["d"]
