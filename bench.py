@@ -63,6 +63,9 @@ def parse():
                    help="N > 1 plumbing on ONE shared GPU: gloo process group, shard-only handles, the staged "
                         "sharded search with the exchanges over gloo (host), vlr_merge_partials; timing is not a "
                         "multi-GPU number")
+    p.add_argument("--lat-batches", type=int, default=1000,
+                   help="latency pass: CUDA-graph closed-loop batches per batch size (SURVEY §8(d): >= 1000)")
+    p.add_argument("--sustained-s", type=float, default=10.0, help="sustained pass length (s), batch of the config")
     p.add_argument("--sweep-out", default=None,
                    help="also run the C5 batch x nprobe sweep on the same index and write JSON lines here")
     return p.parse_args()
@@ -91,6 +94,17 @@ def workload_name(c, name):
               ("" if c.get("by_residual", 1) else ", non-residual PQ")
     return (f"{name}: {c['N'] / 1e6:g}M x d{c['d']}, IVF{c['nlist']}, PQ{c['m']}x{c.get('nbits', 8)}, nprobe {c['nprobe']}, "
             f"k {c['k']}, batch {c['batch']}, Zipf alpha {c['alpha']}, {hot}{var}")
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 def f16_peak():
@@ -310,7 +324,7 @@ def run_reference(a):
             "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded clustered embeddings, Zipf queries)",
             "config": {"workload": workload_name(c, a.config), "seed": a.seed, "sample_queries_per_step": S},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                              "sample": f"{S} of the {B} queries of each step's batch, oracle/oracle.c fp64, OpenMP"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gen_s": gen_s}
@@ -487,6 +501,11 @@ def main():
     release = None
     if world == 1 and not a.ncu:
         release = release_leg(a, c, h, Qdev, outs, K)
+    # ---- latency pass: CUDA-graph closed loop of >= 1000 batches per batch size, p50/p99 over
+    # batches; then a sustained run of the config's batch (q/s after the power cap settles)
+    latency = None
+    if world == 1 and not a.ncu and a.lat_batches > 0:
+        latency = latency_leg(a, c, h, pool, K, local)
     # ---- NEXT-2: GPU access profile of a calibration stream -> per-rank work share of the paper's deal vs
     # the traffic-aware deal at G = 2/4/8 (over the timed batches' probes), and a full-shard refresh time
     shards = None
@@ -524,10 +543,14 @@ def main():
         tp, tp_src = f16_peak()
         fl = 2.0 * B * c["nlist"] * c["d"]
         tfs = fl / (cf_ms * 1e-3) / 1e12
-        cbytes = c["nlist"] * c["d"] * 4 + B * c["nlist"] * 4
+        # bytes K1 moves: the pre-tiled fp16 centroid stream (L x d8 x 2, read once per batch) + the fp32 filter
+        # matrix it writes (B x L x 4; most of it is consumed by K2 from L2) + the fp16 queries
+        cbytes = c["nlist"] * ((c["d"] + 7) // 8 * 8) * 2 + B * c["nlist"] * 4 + B * c["d"] * 2
         coarse_roof = {"bound": "tensor", "dtype": "f16 (power-of-two scaled operands, fp32 accumulate)", "achieved": tfs, "peak": tp, "unit": "TFLOP/s",
                        "frac": tfs / tp, "peak_source": tp_src, "flops_per_launch": fl,
                        "ms_per_launch": cf_ms, "hbm_gbs": cbytes / (cf_ms * 1e-3) / 1e9,
+                       "hbm_bytes_per_launch": cbytes,
+                       "hbm_bytes_how": "fp16 centroid tiles (L*d8*2) + fp32 filter writes (B*L*4) + fp16 queries",
                        "kernel": "k_qprep + k_filter_tc (K1)"}
     # ---- residency (P:214 hit rate eta_q = 1 - sum_p miss / nprobe'; rho = resident share of the index)
     hq = np.concatenate(hit)
@@ -572,6 +595,7 @@ def main():
             "residency": residency,
             "e2e": e2e, "clocks": clk, "cpu_baseline": cpu, "parity_sample": par, "recall": recall,
             "release": release,
+            "latency": latency,
             "shards": shards,
             "gen_s": round(gen_s, 1), "load_s": round(load_s, 1),
         }
@@ -622,6 +646,87 @@ def shard_leg(a, c, h, ix, hot, outs, K):
             "refresh_s": reload_s,
             "refresh_how": "vlr_update_hot of this rank's whole shard (host arrays -> new device residency, swap; "
                            "the paper reports <10 s per shard, P:421)"}
+
+
+def latency_leg(a, c, h, pool, K, device):
+    """Per batch size B in (32, 64, 128, 256) (and the config's batch): the search captured ONCE in a CUDA
+    graph (torch.cuda.graph on a side stream; the library's K5 fork/join is captured with it), replayed
+    closed-loop for a.lat_batches batches; each replay's queries are copied into the graph's static input
+    first (inside the replay's event pair: the latency is input-in-HBM to result-in-HBM). CUDA events around
+    every replay -> p50 / p99 / p99.9 / max over >= 1000 batches; q/s = queries / summed device time.
+    Then a sustained loop of the config's batch for a.sustained_s seconds (q/s of the last half, after
+    the power cap settles) and, for the outlier question, the same closed loop with the nvidia-smi sampler
+    running next to it."""
+    import torch
+    out = {"how": __doc_latency__, "by_batch": {}}
+    qd = torch.from_numpy(pool).cuda()
+    nb_pool = len(pool)
+    NP = min(c["nprobe"], c["nlist"])
+    batches = sorted({32, 64, 128, 256, c["batch"]})
+    graphs = {}
+    for B in batches:
+        if B > nb_pool:
+            continue
+        h.reserve(B, NP, K)
+        qin = torch.empty(B, c["d"], device="cuda")
+        o = (torch.empty(B, K, dtype=torch.int64, device="cuda"), torch.empty(B, K, device="cuda"),
+             torch.empty(B, NP, dtype=torch.uint8, device="cuda"), torch.empty(B, NP, dtype=torch.int32, device="cuda"))
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for i in range(3):  # eager warm-up on the capture stream (module loads, workspace)
+                qin.copy_(qd[i * B % (nb_pool - B + 1):][:B])
+                h.search(qin, c["nprobe"], K, out=o, stream=s)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            h.search(qin, c["nprobe"], K, out=o, stream=s)
+        graphs[B] = (g, qin, o, s)
+
+    def loop(B, n, sampler=None):
+        g, qin, o, s = graphs[B]
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        nstart = max(1, nb_pool // B)
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.start()
+            time.sleep(0.3)
+        with torch.cuda.stream(s):
+            for i in range(n):
+                ev[i][0].record(s)
+                j = (i % nstart) * B
+                qin.copy_(qd[j:j + B])
+                g.replay()
+                ev[i][1].record(s)
+        torch.cuda.synchronize()
+        clk = sampler.stop() if sampler else None
+        lat = np.array([x.elapsed_time(y) for x, y in ev])
+        return lat, clk
+
+    for B in graphs:
+        lat, _ = loop(B, a.lat_batches)
+        out["by_batch"][str(B)] = {"batches": len(lat), "qps": float(B * len(lat) / (lat.sum() * 1e-3)),
+                                   "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+                                   "p999_ms": float(np.percentile(lat, 99.9)), "max_ms": float(lat.max()),
+                                   "mean_ms": float(lat.mean())}
+    B = c["batch"]
+    if B in graphs and a.sustained_s > 0:
+        per = max(1e-4, out["by_batch"][str(B)]["mean_ms"] * 1e-3)
+        n = int(a.sustained_s / per)
+        lat, clk = loop(B, n, sampler=Clocks(device))
+        half = lat[len(lat) // 2:]
+        out["sustained"] = {"batch": B, "seconds": float(lat.sum() * 1e-3), "batches": int(n),
+                            "qps_all": float(B * len(lat) / (lat.sum() * 1e-3)),
+                            "qps_last_half": float(B * len(half) / (half.sum() * 1e-3)),
+                            "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+                            "max_ms": float(lat.max()), "clocks": clk,
+                            "outliers_gt_1p5x_median": int((lat > 1.5 * np.median(lat)).sum()),
+                            "how": "same graph closed loop for sustained_s seconds with the nvidia-smi sampler "
+                                   "(-lms 100) running; compare p99/max with by_batch (no sampler)"}
+    return out
+
+
+__doc_latency__ = ("torch CUDA graph of one vlr_search_async per batch size, replayed closed-loop; per replay a "
+                   "D2D copy of that batch's queries into the graph input then the replay, CUDA events around both")
 
 
 def release_leg(a, c, h, Qdev, outs, K):
@@ -779,7 +884,7 @@ def oracle_leg(a, c, ix, hot, pool, outs):
     t = time.time()
     o = oracle.search(ix, first[:S], c["nprobe"], c["k"], hot=hot, nthreads=cores)
     el = time.time() - t
-    cpu = {"value": S / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+    cpu = {"value": S / el, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
            "sample": f"first {S} queries of the first timed batch (same index and queries), oracle/oracle.c fp64"}
     g = outs[0]
     gpu = dict(ids=g[0].cpu().numpy()[:S], dist=g[1].cpu().numpy()[:S], miss=g[2].cpu().numpy()[:S],

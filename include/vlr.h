@@ -47,7 +47,7 @@ typedef enum {
   VLR_ERR_CUDA = 7,            /* any other CUDA runtime error (no device, launch failure, ...) */
   VLR_ERR_NCCL = 8,            /* NCCL error; the communicator is aborted, the handle unusable */
   VLR_ERR_UNSUPPORTED = 9      /* valid but outside this version: nbits not in {4, 8}, metric not in
-                                  {0, 1}, m > 128 (8-bit) / 256 (4-bit), k > 32, nprobe' > 2048 */
+                                  {0, 1}, m > 192 (8-bit) / 384 (4-bit), k > 1024, nprobe' > 2048 */
 } vlr_status;
 
 /*
@@ -66,7 +66,7 @@ typedef enum {
 typedef struct {
   int32_t d;            /* vector dimension, >= 1 */
   int32_t nlist;        /* number of inverted lists / coarse centroids, >= 1 */
-  int32_t m;            /* PQ sub-quantizers, d % m == 0, 1 <= m <= 128 (nbits 8) or 256 (nbits 4) */
+  int32_t m;            /* PQ sub-quantizers, d % m == 0, 1 <= m <= 192 (nbits 8) or 384 (nbits 4) */
   int32_t nbits;        /* bits per sub-code: 8 (256 codewords) or 4 (16 codewords; the paper's 4-bit
                            PQ, reading A4') */
   int32_t metric;       /* 0 = squared L2, 1 = inner product (distance reported as -<q, x>) */
@@ -140,7 +140,10 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
  *  d_queries [nq][d] device fp32.   nq >= 0 (nq == 0 is a no-op).
  *  nprobe >= 1; clamped to nprobe' = min(nprobe, nlist); nprobe' <= 2048
  *  (the paper's operating point), else VLR_ERR_UNSUPPORTED.
- *  1 <= k <= 32.
+ *  1 <= k <= 1024. k <= 32: warp-register top-k fused into the scan; k > 32:
+ *  the scan writes every candidate's distance and a per-query radix select
+ *  keeps the k smallest (same unique result).
+ *  world x nprobe' <= 16384 and (k > 32) world x k <= 8192 when world > 1.
  *  Outputs (device, caller-allocated):
  *   d_ids  [nq][k] int64, d_dist [nq][k] fp32: row q = the k smallest
  *      candidates by (ADC distance, id), ascending; missing slots (-1, +inf).

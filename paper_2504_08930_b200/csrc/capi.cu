@@ -75,7 +75,7 @@ __global__ void k_negative(const int64_t* ids, long long n, int32_t* flag) {
 }
 
 static void free_ws(Workspace& w) {
-  void* ps[] = {w.qnorm, w.qsq, w.qf16, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.x1, w.x1_all, w.x2, w.x2_all, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.qdone, w.lut,
+  void* ps[] = {w.qnorm, w.qsq, w.qf16, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.x1, w.x1_all, w.x2, w.x2_all, w.dump, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.qdone, w.lut,
                 w.pdist, w.pid, w.send, w.recv, w.d_q, w.d_ids, w.d_dist, w.d_miss, w.d_probes, w.status};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -129,8 +129,15 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   VLR_CUDA_TRY(dalloc(&w.qtot, nqs));
   VLR_CUDA_TRY(dalloc(&w.qdone, nqs));
   VLR_CUDA_TRY(dalloc(&w.lut, nqs * ix.npairs * (ix.lut_pair_bytes / 4)));
-  const size_t nslots = ((size_t)w.n_cta * kMaxReleaseWaves + nqs) * kScanWarps * ck;  // slot (c + q + wave * n_cta)
+  // warp partial lists (k <= 32 path only): slot (c + q + wave * n_cta)
+  const size_t nslots = ((size_t)w.n_cta * kMaxReleaseWaves + nqs) * kScanWarps * std::min(ck, kMaxK);
   VLR_CUDA_TRY(dalloc(&w.pdist, nslots));
+  if (ck > kMaxK) {  // large-k candidate buffer: chunks of dump_nq queries x (groups of the np largest lists)
+    const int64_t maxg = ix.top_groups[std::min<size_t>((size_t)cnp, ix.top_groups.size() - 1)];
+    const size_t per_q = (size_t)std::max<int64_t>(maxg, 1) * 32 * sizeof(uint2);
+    w.dump_nq = (int)std::max<size_t>(1, std::min<size_t>((size_t)cnq, kDumpBudget / per_q));
+    VLR_CUDA_TRY(dalloc(&w.dump, (size_t)w.dump_nq * per_q / sizeof(uint2)));
+  }
   VLR_CUDA_TRY(dalloc(&w.pid, nslots));
   if (ix.nccl) {  // exchange buffers (world > 1 with a communicator, or the forced 1-rank exchange)
     VLR_CUDA_TRY(dalloc(reinterpret_cast<Packed**>(&w.send), nqs * ck));
@@ -349,8 +356,8 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   if (D.nbits != 8 && D.nbits != 4) return fail(VLR_ERR_UNSUPPORTED, "nbits must be 8 or 4");
   if (D.metric != 0 && D.metric != 1) return fail(VLR_ERR_UNSUPPORTED, "metric must be 0 (squared L2) or 1 (inner product)");
   if (D.by_residual != 0 && D.by_residual != 1) return fail(VLR_ERR_INVALID_ARG, "by_residual must be 0 or 1");
-  if (D.nbits == 8 && D.m > kMaxM) return fail(VLR_ERR_UNSUPPORTED, "m > 128 (8-bit codes)");
-  if (D.nbits == 4 && D.m > kMaxM4) return fail(VLR_ERR_UNSUPPORTED, "m > 256 (4-bit codes)");
+  if (D.nbits == 8 && D.m > kMaxM) return fail(VLR_ERR_UNSUPPORTED, "m > 192 (8-bit codes)");
+  if (D.nbits == 4 && D.m > kMaxM4) return fail(VLR_ERR_UNSUPPORTED, "m > 384 (4-bit codes)");
   if (!D.centroids || !D.codebooks || !D.list_offsets) return fail(VLR_ERR_INVALID_ARG, "null array");
   if (D.n_hot < 0 || (D.n_hot > 0 && !D.hot)) return fail(VLR_ERR_INVALID_ARG, "bad hot set");
   const int L = D.nlist, d = D.d, m = D.m, dsub = d / m;
@@ -422,7 +429,8 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
   ix.ksub = ksub;
   {
     const char* nib = getenv("VLR_PQ4_NIBBLE");  // 4-bit nibble-slot scan instead of pair tables (experiments)
-    ix.code_bits = (D.nbits == 4 && nib && atoi(nib) == 1) ? 4 : 8;
+    // (nibble slots are instantiated up to 256 sub-spaces; above, pair mode)
+    ix.code_bits = (D.nbits == 4 && D.m <= 256 && nib && atoi(nib) == 1) ? 4 : 8;
   }
   ix.code_m = (D.nbits == 4 && ix.code_bits == 8) ? (m + 1) / 2 : m;  // pair mode: one slot per packed byte
   ix.lut_pair_bytes = (1 << ix.code_bits) * 64 * 4;
@@ -485,6 +493,13 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
     }
   }
   ix.n_local = (int32_t)lglob.size();
+  {  // groups of the i largest local lists, i = 0..n_local (bounds one query's candidates for the large-k path)
+    std::vector<int64_t> gl((size_t)ix.n_local);
+    for (int32_t i = 0; i < ix.n_local; ++i) gl[i] = gbase_h[i + 1] - gbase_h[i];
+    std::sort(gl.begin(), gl.end(), std::greater<int64_t>());
+    ix.top_groups.assign(1, 0);
+    for (int64_t v : gl) ix.top_groups.push_back(ix.top_groups.back() + v);
+  }
   ix.n_vec = vbase_h.back();
   ix.n_groups = gbase_h.back();
   LTRY(dalloc(&ix.centroids, (size_t)L * d));
@@ -637,7 +652,7 @@ void vlr_index_free(vlr_index* h) {
 
 vlr_status vlr_reserve(vlr_index* h, int32_t max_nq, int32_t max_nprobe, int32_t max_k) {
   if (!h || max_nq < 0 || max_nprobe < 1 || max_k < 1) return fail(VLR_ERR_INVALID_ARG, "vlr_reserve: bad args");
-  if (max_k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32");
+  if (max_k > kMaxKLarge) return fail(VLR_ERR_UNSUPPORTED, "k > 1024");
   cudaSetDevice(h->ix.device);
   const int np = std::min(max_nprobe, h->ix.nlist);
   if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 2048");
@@ -748,6 +763,13 @@ static vlr_status phase_c(vlr_index* h, Pipe& p, bool sharded, int64_t* out_ids,
     VLR_CUDA_TRY(launch_lut(p.Q, ix, w, p.nq, p.s)); ++p.n;
   }
   rec(h, 5, p.s);
+  if (p.k > kMaxK) {  // large k: DUMP scan + per-query select, per chunk of queries (k_scan.cu)
+    VLR_CUDA_TRY(launch_scan_large(ix, w, p.nq, p.np, p.k, out_ids, out_dist, packed ? w.send : nullptr, p.s));
+    p.n += 2 * ((p.nq + w.dump_nq - 1) / w.dump_nq);
+    rec(h, 6, p.s);
+    rec(h, 7, p.s);
+    return VLR_OK;
+  }
   if (rel) VLR_CUDA_TRY(cudaMemsetAsync(w.qdone, 0, sizeof(unsigned long long) * p.nq, p.s));
   VLR_CUDA_TRY(launch_scan(ix, w, p.nq, p.np, p.k, p.s, rel)); ++p.n;
   rec(h, 6, p.s);
@@ -761,7 +783,10 @@ static vlr_status phase_c(vlr_index* h, Pipe& p, bool sharded, int64_t* out_ids,
 static vlr_status check_search_args(vlr_index* h, int32_t nq, int32_t nprobe, int32_t k, int* np) {
   if (h->dead) return fail(VLR_ERR_NCCL, "index unusable after an NCCL failure");
   if (nq < 0 || nprobe < 1 || k < 1) return fail(VLR_ERR_INVALID_ARG, "nq < 0, nprobe < 1 or k < 1");
-  if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32 (v1)");
+  if (k > kMaxKLarge) return fail(VLR_ERR_UNSUPPORTED, "k > 1024");
+  if (k > kMaxK && h->ix.world * k > 8192) return fail(VLR_ERR_UNSUPPORTED, "world x k > 8192 (k > 32 merge)");
+  if (k > kMaxK && (uint64_t)h->ix.n_groups * 32 >= (1ull << 32))
+    return fail(VLR_ERR_UNSUPPORTED, "k > 32 needs < 2^32 resident vector slots on a rank");
   *np = std::min(nprobe, h->ix.nlist);
   if (*np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 2048");
   if (h->ix.world * *np > kMaxWorldProbes && h->ix.world > 1)
@@ -847,6 +872,7 @@ vlr_status vlr_search_release_async(vlr_index* h, const float* Q, int32_t nq, in
   if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
   if (h->ix.world > 1 || h->ix.shard_only || h->ix.nccl)
     return fail(VLR_ERR_UNSUPPORTED, "early release needs world == 1 (rows are final only after the exchange)");
+  if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "early release: k > 32");
   if (nq > 0) {
     if (!ready || epoch == 0) return fail(VLR_ERR_INVALID_ARG, "release: null ready flags or epoch 0");
     VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
@@ -932,7 +958,7 @@ static vlr_status search_host_impl(vlr_index* h, const float* hQ, int32_t nq, in
                                    bool sync) {
   if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
   if (nq < 0 || nprobe < 1 || k < 1) return fail(VLR_ERR_INVALID_ARG, "nq < 0, nprobe < 1 or k < 1");
-  if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32 (v1)");
+  if (k > kMaxKLarge) return fail(VLR_ERR_UNSUPPORTED, "k > 1024");
   if (nq == 0) return VLR_OK;
   if (!hQ || !h_ids || !h_dist || !h_miss) return fail(VLR_ERR_INVALID_ARG, "null buffer");
   const int np = std::min(nprobe, h->ix.nlist);
@@ -983,11 +1009,12 @@ static vlr_status staged_begin(vlr_index* h, const float* Q, int32_t nq, int32_t
   if (!h->ix.shard_only) return fail(VLR_ERR_INVALID_ARG, "staged search needs a shard-only handle (world > 1, no communicator)");
   vlr_status st = check_search_args(h, nq, nprobe, k, np);
   if (st != VLR_OK) return st;
+  if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "staged search: k > 32");
   if (nq < 1 || !Q) return fail(VLR_ERR_INVALID_ARG, "staged search: nq >= 1 and queries required");
   VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
   // sized for any k up front: a reallocation between the stages would drop the LUT and the gathered
   // buffers of the batch in flight
-  return ensure_ws(h, nq, *np, std::max(k, kMaxK));
+  return ensure_ws(h, nq, *np, std::max(k, kMaxK));  // k <= 32 only (vlr.h: staged search)
 }
 
 vlr_status vlr_coarse_stage1(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, float* d_x1, void* stream) {
@@ -1057,7 +1084,8 @@ vlr_status vlr_search_stage3(vlr_index* h, const float* Q, int32_t nq, int32_t n
 vlr_status vlr_merge_partials(const int64_t* part_ids, const float* part_dist, int32_t n_shards, int32_t nq, int32_t k,
                               int64_t* out_ids, float* out_dist, void* stream) {
   if (n_shards < 1 || nq < 0 || k < 1) return fail(VLR_ERR_INVALID_ARG, "vlr_merge_partials: bad sizes");
-  if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "k > 32 (v1)");
+  if (k > kMaxKLarge || (k > kMaxK && (int64_t)n_shards * k > 8192))
+    return fail(VLR_ERR_UNSUPPORTED, "k > 1024, or n_shards x k > 8192 for k > 32");
   if (nq == 0) return VLR_OK;
   if (!part_ids || !part_dist || !out_ids || !out_dist) return fail(VLR_ERR_INVALID_ARG, "null buffer");
   VLR_CUDA_TRY(launch_merge_split(part_ids, part_dist, n_shards, nq, k, out_ids, out_dist,

@@ -131,11 +131,7 @@ __device__ unsigned radix_select_kth(const unsigned* skeys, int n, unsigned want
       const unsigned key = i < n ? skeys[i] : 0u;
       const bool act = i < n && (key & mask) == prefix;
       const unsigned bin = (key >> shift) & 255u;
-      const unsigned am = __ballot_sync(kFull, act);
-      if (act) {
-        const unsigned peers = __match_any_sync(am, bin);
-        if (lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned)__popc(peers));
-      }
+      if (act) atomicAdd(&hist[bin], 1u);  // plain shared-memory atomics (no match_any aggregation)
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -466,6 +462,71 @@ __device__ double warp_exact(const double* __restrict__ qs, const float* __restr
   return key_final<MET>(s);
 }
 
+// Two candidates per lane (rows rid0, rid1: two independent in-order fp64
+// chains interleaved, so each chain's 8-cycle DADD latency overlaps the other's
+// work); 64 rows per tile (8 KB per stage). Same per-candidate arithmetic and
+// order as warp_exact -> bit-identical D.
+template <int S, int MET>
+__device__ void warp_exact2(const double* __restrict__ qs, const float* __restrict__ C, int d, int rid0, int rid1,
+                            float* buf, int lane, double& D0, double& D1) {
+  double s0 = 0.0, s1 = 0.0;
+  const int ntile = d >> 5;
+  const float* src[16];
+  uint32_t dst[16];
+  const uint32_t buf_s = (uint32_t)__cvta_generic_to_shared(buf);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {  // (row r of 64, chunk k): rows 0-31 -> rid0 of lane r, 32-63 -> rid1
+    const int idx = i * 32 + lane;
+    const int r = idx >> 3, k = idx & 7;
+    const int rr = r & 31;
+    const int rid = __shfl_sync(kFull, r < 32 ? rid0 : rid1, rr);
+    src[i] = C + (size_t)rid * d + 4 * k;
+    dst[i] = buf_s + (uint32_t)(r * 32 + ((k ^ (r & 7)) << 2)) * 4u;
+  }
+  auto issue = [&](int tile) {
+    if (tile < ntile) {
+      const uint32_t so = (uint32_t)(tile % S) * 8192u;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst[i] + so), "l"(src[i] + tile * 32)
+                     : "memory");
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int t = 0; t < S - 1; ++t) issue(t);
+  for (int tile = 0; tile < ntile; ++tile) {
+    issue(tile + S - 1);
+    cp_async_wait<S - 1>();
+    __syncwarp();
+    const float* row0 = buf + (tile % S) * 2048 + lane * 32;
+    const float* row1 = row0 + 32 * 32;
+    const double2* qt = reinterpret_cast<const double2*>(qs + tile * 32);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float4 v = *reinterpret_cast<const float4*>(row0 + ((k ^ (lane & 7)) << 2));
+      const float4 w = *reinterpret_cast<const float4*>(row1 + ((k ^ (lane & 7)) << 2));
+      const double2 qa = qt[2 * k], qb = qt[2 * k + 1];
+      s0 = key_term<MET>(s0, qa.x, (double)v.x);
+      s1 = key_term<MET>(s1, qa.x, (double)w.x);
+      s0 = key_term<MET>(s0, qa.y, (double)v.y);
+      s1 = key_term<MET>(s1, qa.y, (double)w.y);
+      s0 = key_term<MET>(s0, qb.x, (double)v.z);
+      s1 = key_term<MET>(s1, qb.x, (double)w.z);
+      s0 = key_term<MET>(s0, qb.y, (double)v.w);
+      s1 = key_term<MET>(s1, qb.y, (double)w.w);
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  for (int t = ntile * 32; t < d; ++t) {  // tail dimensions, still in order
+    s0 = key_term<MET>(s0, qs[t], (double)__ldg(C + (size_t)rid0 * d + t));
+    s1 = key_term<MET>(s1, qs[t], (double)__ldg(C + (size_t)rid1 * d + t));
+  }
+  D0 = key_final<MET>(s0);
+  D1 = key_final<MET>(s1);
+}
+
 template <int MET>
 __device__ __forceinline__ double scalar_exact(const double* __restrict__ qs, const float* __restrict__ C, int d,
                                                int row_id) {
@@ -484,7 +545,7 @@ __device__ __forceinline__ double scalar_exact(const double* __restrict__ qs, co
 constexpr int kExactWarps = 4;
 constexpr int kExactStages = 3;
 
-template <int MET, int S, int W>
+template <int MET, int S, int W, int CH = 1>
 __global__ void __launch_bounds__(W * 32) k_exact(const float* __restrict__ Q, const float* __restrict__ C,
                                                   int d, const int32_t* __restrict__ cand,
                                                   const int32_t* __restrict__ ncand,
@@ -492,7 +553,7 @@ __global__ void __launch_bounds__(W * 32) k_exact(const float* __restrict__ Q, c
   extern __shared__ __align__(16) unsigned char sm[];
   const int q = blockIdx.x;
   const int nc = ncand[q];
-  const int g0 = blockIdx.y * W * 32;
+  const int g0 = blockIdx.y * W * 32 * CH;
   if (nc > kCandCap || g0 >= nc) return;
   double* qs = reinterpret_cast<double*>(sm);
   float* tiles = reinterpret_cast<float*>(qs + ((d + 1) & ~1));
@@ -500,27 +561,38 @@ __global__ void __launch_bounds__(W * 32) k_exact(const float* __restrict__ Q, c
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t* lst = cand + (size_t)q * kCandCap;
-  // groups of 32 candidates: this warp takes g = g0 + 32*warp + stride*i
-  const int stride = gridDim.y * W * 32;
-  for (int g = g0 + warp * 32; g < nc; g += stride) {
+  // groups of 32 CH candidates: this warp takes g = g0 + 32 CH warp + stride i
+  const int stride = gridDim.y * W * 32 * CH;
+  for (int g = g0 + warp * 32 * CH; g < nc; g += stride) {
     const int j = g + lane;
     const int rid = lst[j < nc ? j : g];
+    if constexpr (CH == 2) {
+      if ((d & 3) == 0 && g + 32 < nc) {  // a second chain with at least one real candidate
+        const int j1 = j + 32;
+        const int rid1 = lst[j1 < nc ? j1 : g];
+        double D0, D1;
+        warp_exact2<S, MET>(qs, C, d, rid, rid1, tiles + warp * (S * 2048), lane, D0, D1);
+        if (j < nc) exact[(size_t)q * kCandCap + j] = D0;
+        if (j1 < nc) exact[(size_t)q * kCandCap + j1] = D1;
+        continue;
+      }
+    }
     double D;
     if ((d & 3) == 0)
-      D = warp_exact<S, MET>(qs, C, d, rid, tiles + warp * (S * 1024), lane);
+      D = warp_exact<S, MET>(qs, C, d, rid, tiles + warp * (S * 1024 * CH), lane);
     else
       D = scalar_exact<MET>(qs, C, d, rid);
     if (j < nc) exact[(size_t)q * kCandCap + j] = D;
   }
 }
 
-template <int S, int W>
+template <int S, int W, int CH = 1>
 static cudaError_t launch_exact_t(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
-  const size_t sm = (size_t)((ix.d + 1) & ~1) * sizeof(double) + (size_t)W * S * 1024 * sizeof(float);
-  auto fn = ix.metric == 1 ? k_exact<1, S, W> : k_exact<0, S, W>;
+  const size_t sm = (size_t)((ix.d + 1) & ~1) * sizeof(double) + (size_t)W * S * 1024 * CH * sizeof(float);
+  auto fn = ix.metric == 1 ? k_exact<1, S, W, CH> : k_exact<0, S, W, CH>;
   cudaError_t e = ensure_smem((const void*)fn, sm);
   if (e != cudaSuccess) return e;
-  dim3 grid(nq, 1024 / (W * 32));  // 1024 candidates per pass; queries with more loop
+  dim3 grid(nq, 1024 / (W * 32 * CH));  // 1024 candidates per pass; queries with more loop
   fn<<<grid, W * 32, sm, s>>>(Q, ix.centroids, ix.d, ws.cand, ws.ncand, ws.exact);
   return cudaGetLastError();
 }
@@ -539,6 +611,9 @@ cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace&
     case 28: return launch_exact_t<2, 8>(Q, ix, ws, nq, s);
     case 22: return launch_exact_t<2, 2>(Q, ix, ws, nq, s);
     case 42: return launch_exact_t<4, 2>(Q, ix, ws, nq, s);
+    case 32: return launch_exact_t<3, 2, 2>(Q, ix, ws, nq, s);   // "3,2" two chains per lane, 2 warps
+    case 36: return launch_exact_t<3, 4, 2>(Q, ix, ws, nq, s);   // "3,6": two chains per lane, 4 warps
+    case 52: return launch_exact_t<5, 2, 2>(Q, ix, ws, nq, s);   // "5,2": two chains, 5 stages, 2 warps
     default: return launch_exact_t<kExactStages, kExactWarps>(Q, ix, ws, nq, s);
   }
 }
@@ -610,9 +685,10 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
       nbest = min(np, tot);
     }
   } else {
-    for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = (double)Q[(size_t)q * d + t];
     const int nc = ncand[q];
     const bool listed = nc <= kCandCap;
+    if (!listed)  // the query (fp64) is needed only by the rescan path, which computes exact keys here
+      for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = (double)Q[(size_t)q * d + t];
     const int src_len = listed ? nc : hi - lo;
     const float bnd = bound[q];
     const int32_t* lst = cand + (size_t)q * kCandCap;

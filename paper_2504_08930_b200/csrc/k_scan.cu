@@ -30,6 +30,7 @@
 // split once into its even and odd nibbles (w & 0x0F0F0F0F, (w >> 4) &
 // 0x0F0F0F0F) so the same one-PRMT address build applies.
 #include <cfloat>
+#include <climits>
 #include <cstdlib>
 
 #include "vlr_device.cuh"
@@ -66,6 +67,10 @@ struct ScanArgs {
   int64_t* out_ids;           // [nq][k] final rows (device or pinned host)
   float* out_dist;
   int waves;                  // REL: the batch is scanned in this many query waves
+  // large k (k > 32, DUMP scan): every candidate's (dist, position) goes to dump[(g - WL) * 32 + lane] for
+  // the groups g of queries [q_lo, q_hi); k_select_large keeps each query's k smallest
+  int q_lo, q_hi;
+  uint2* dump;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -466,9 +471,10 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32) k_rank_merge(
                      item_off[(long long)(q + 1) * np], pdist, pid, out_ids, out_dist, packed, sm);
 }
 
-template <int MP, int NB, int EXP>
+template <int MP, int NB, int EXP, bool DUMP = false>
 __device__ __forceinline__ void grp_finish(const Grp<MP, NB>& G, const ScanArgs& a, const unsigned char* lutc,
-                                           uint32_t lane4, int lane, float& bd, long long& bid, float& thr) {
+                                           uint32_t lane4, int lane, float& bd, long long& bid, float& thr,
+                                           long long dslot = 0) {
   float s;
   if constexpr (EXP == 1) {  // timing experiment: no LUT gathers (ALU sum of code words)
     uint32_t x = 0;
@@ -479,6 +485,10 @@ __device__ __forceinline__ void grp_finish(const Grp<MP, NB>& G, const ScanArgs&
     s = grp_adc<MP, NB>(G, lutc, lane4);
   }
   const float dist = (G.t1 + G.b) + s;
+  if constexpr (DUMP) {  // large k: every candidate out (padding rows have dist = +inf)
+    a.dump[dslot * 32 + lane] = make_uint2(__float_as_uint(dist), (uint32_t)(G.gaddr * 32 + lane));
+    return;
+  }
   const bool cand = dist <= thr;
   long long my_id = 0;
   if (cand) my_id = __ldg(reinterpret_cast<const long long*>(a.ids) + G.gaddr * 32 + lane);
@@ -621,7 +631,7 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanAr
   }
 }
 
-template <int MP, int NB, int EXP, bool REL = false>
+template <int MP, int NB, int EXP, bool REL = false, bool DUMP = false>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
@@ -650,7 +660,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
   for (int z1 = 0; z1 < Z; ++z1) {
     if constexpr (REL) __syncthreads();  // s_z of the previous wave written
     const int z = REL ? zcur() : z1;
-    const int i_lo = (int)((long long)z * a.nq / Z) * a.np, i_hi = (int)((long long)(z + 1) * a.nq / Z) * a.np;
+    const int i_lo = (REL ? (int)((long long)z * a.nq / Z) : a.q_lo) * a.np;
+    const int i_hi = (REL ? (int)((long long)(z + 1) * a.nq / Z) : a.q_hi) * a.np;
     const long long WL = a.item_off[i_lo], WH = a.item_off[i_hi];
     const long long g0 = WL + (long long)c * (WH - WL) / G, g1 = WL + (long long)(c + 1) * (WH - WL) / G;
     if constexpr (REL) {
@@ -705,17 +716,17 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
         if constexpr (kPfDist > 0)
           if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gn + kPfDist * kScanWarps, itp, lane);
         if (gn < seg_end) grp_load<MP, NB, EXP>(B, a, gn, it, lane);
-        grp_finish<MP, NB, EXP>(A, a, lutc, lane4, lane, bd, bid, thr);
+        grp_finish<MP, NB, EXP, DUMP>(A, a, lutc, lane4, lane, bd, bid, thr, gg - WL);
         if (gn >= seg_end) break;
         const long long gm = gn + kScanWarps;
         if constexpr (kPfDist > 0)
           if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gm + kPfDist * kScanWarps, itp, lane);
         if (gm < seg_end) grp_load<MP, NB, EXP>(A, a, gm, it, lane);
-        grp_finish<MP, NB, EXP>(B, a, lutc, lane4, lane, bd, bid, thr);
+        grp_finish<MP, NB, EXP, DUMP>(B, a, lutc, lane4, lane, bd, bid, thr, gn - WL);
         gg = gm;
       }
       const long long slot = ((long long)(c + q) + (long long)(REL ? zcur() - 1 : 0) * G) * kScanWarps * a.k + warp * a.k;
-      if (lane < a.k) {
+      if (!DUMP && lane < a.k) {
         a.pdist[slot + lane] = bd;
         a.pid[slot + lane] = bid;
         if constexpr (REL) __threadfence();
@@ -739,12 +750,15 @@ int scan_ctas(const DeviceIndex& ix) {
   return sms;  // one persistent CTA per SM (128 KB LUT + 16 warps)
 }
 
-template <int MP, int NB, int EXP, bool REL = false>
+template <int MP, int NB, int EXP, bool REL = false, bool DUMP = false>
 static cudaError_t launch_scan_e(const ScanArgs& a, int n_cta, cudaStream_t s) {
-  cudaError_t e = ensure_smem((const void*)k_scan<MP, NB, EXP, REL>, (size_t)(2 * kLutPairBytes));
+  // the LUT of one query: ceil(MP / 64) slabs of 64 slots (8-bit slots: 64 KB each; MP 192 -> 192 KB)
+  constexpr size_t kLutMax = (size_t)((MP + 63) / 64) * (NB == 8 ? kLutPairBytes : kLutPairBytes4);
+  cudaError_t e = ensure_smem((const void*)k_scan<MP, NB, EXP, REL, DUMP>, kLutMax > 2 * kLutPairBytes ? kLutMax
+                                                                                                  : (size_t)(2 * kLutPairBytes));
   if (e != cudaSuccess) return e;
   if (n_cta == 0) return cudaSuccess;  // configure (and so load) only
-  k_scan<MP, NB, EXP, REL><<<n_cta, kScanThreads, a.lut_bytes, s>>>(a);
+  k_scan<MP, NB, EXP, REL, DUMP><<<n_cta, kScanThreads, a.lut_bytes, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -762,6 +776,7 @@ static int scan_experiment() {
 template <int MP, int NB>
 static cudaError_t launch_scan_t(const ScanArgs& a, int n_cta, cudaStream_t s) {
   if (a.ready) return launch_scan_e<MP, NB, 0, true>(a, n_cta, s);
+  if (a.dump) return launch_scan_e<MP, NB, 0, false, true>(a, n_cta, s);
   if constexpr (MP == 128 && NB == 8) {
     const int x = scan_experiment();
     if (x == 1) return launch_scan_e<MP, NB, 1>(a, n_cta, s);
@@ -777,7 +792,7 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
   if (nq <= 0) return cudaSuccess;
   ScanArgs a{nq, np, k, ix.npairs, (uint32_t)(ix.npairs * ix.lut_pair_bytes), ws.plocal, ws.term1, ws.item_off,
              ix.gbase, ix.codes, ix.bias, ix.ids, ws.lut, ws.pdist, ws.pid,
-             nullptr, nullptr, 0u, nullptr, nullptr, 1};
+             nullptr, nullptr, 0u, nullptr, nullptr, 1, 0, nq, nullptr};
   int G = ws.n_cta;
   if (rel) {
     if ((long long)ws.n_cta * kScanWarps > kMergeMaxLists || ws.n_cta < 2) return cudaErrorInvalidConfiguration;
@@ -831,6 +846,8 @@ static cudaError_t launch_scan_k(const DeviceIndex& ix, const ScanArgs& a, int n
     case 64: return launch_scan_t<64, 8>(a, n_cta, s);
     case 96: return launch_scan_t<96, 8>(a, n_cta, s);
     case 128: return launch_scan_t<128, 8>(a, n_cta, s);
+    case 160: return launch_scan_t<160, 8>(a, n_cta, s);  // 8-bit m <= 160, or 4-bit pair mode m <= 320
+    case 192: return launch_scan_t<192, 8>(a, n_cta, s);  // 8-bit m <= 192, or 4-bit pair mode m <= 384 (PQ384x4)
     default: return cudaErrorInvalidValue;
   }
 }
@@ -847,6 +864,174 @@ cudaError_t launch_rank_merge(const DeviceIndex& ix, const Workspace& ws, int nq
   k_rank_merge<<<nq, nw * 32, 0, s>>>(nq, np, k, ws.n_cta, ws.item_off, ws.pdist, ws.pid, out_ids, out_dist,
                                       reinterpret_cast<Packed*>(out_packed));
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- large k (k > 32)
+// §8(b) allows k up to 1024; the warp-register top-k holds 32. For k > 32 the
+// scan runs in DUMP mode (every candidate's (dist, vector position) written
+// per group, 8 B per vector next to the 132 B of codes and bias it reads)
+// over a chunk of queries, and k_select_large (one CTA per query) keeps the
+// k smallest by (dist, id): a radix select of the k-th distance key over the
+// query's candidates (4 passes of 8 bits), the entries below it, the entries
+// equal to it in ascending id order up to k, then a bitonic sort by
+// (dist, id). Same unique result as the warp top-k path.
+constexpr int kSelLargeThreads = 1024;
+constexpr int kSelLargeEqCap = 3072;  // entries equal to the k-th key held for the id tie-break
+
+__device__ __forceinline__ bool lt_did(float d1, long long i1, float d2, long long i2) {
+  return d1 < d2 || (d1 == d2 && i1 < i2);
+}
+
+__global__ void __launch_bounds__(kSelLargeThreads) k_select_large(
+    int q_lo, int np, int k, const int64_t* __restrict__ item_off, const uint2* __restrict__ dump,
+    const int64_t* __restrict__ ids, int64_t* __restrict__ out_ids, float* __restrict__ out_dist,
+    Packed* __restrict__ packed) {
+  __shared__ unsigned hist[256];
+  __shared__ unsigned s_prefix, s_want, s_cnt, s_neq, s_valid;
+  __shared__ float sd[kMaxKLarge];      // the kk <= 1024 selected entries (bitonic-sorted in place)
+  __shared__ long long sid[kMaxKLarge];
+  __shared__ long long seq[kSelLargeEqCap];
+  const int q = q_lo + blockIdx.x;
+  const long long WL = item_off[(long long)q_lo * np];  // the chunk's first group (the DUMP scan's base)
+  const long long S = (item_off[(long long)q * np] - WL) * 32, E = (item_off[(long long)(q + 1) * np] - WL) * 32;
+  const unsigned kInfKey = 0xFF800000u;  // fkey(+inf)
+  if (threadIdx.x == 0) { s_valid = 0u; s_cnt = 0u; s_neq = 0u; }
+  __syncthreads();
+  unsigned nv = 0;
+  for (long long i = S + threadIdx.x; i < E; i += blockDim.x) nv += fkey(__uint_as_float(dump[i].x)) < kInfKey;
+  atomicAdd(&s_valid, nv);
+  __syncthreads();
+  const unsigned valid = s_valid;
+  const int kk = (int)(valid < (unsigned)k ? valid : (unsigned)k);
+  unsigned theta = kInfKey;
+  if (kk > 0) {  // the kk-th smallest key among the finite ones
+    unsigned prefix = 0u, mask = 0u, want = (unsigned)kk;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
+      __syncthreads();
+      for (long long i = S + threadIdx.x; i < E; i += blockDim.x) {
+        const unsigned key = fkey(__uint_as_float(dump[i].x));
+        if (key < kInfKey && (key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned c = 0;
+        for (int b = 0; b < 256; ++b) {
+          if (c + hist[b] >= want) { s_prefix = prefix | ((unsigned)b << shift); s_want = want - c; break; }
+          c += hist[b];
+        }
+      }
+      __syncthreads();
+      prefix = s_prefix;
+      want = s_want;
+      mask |= 255u << shift;
+      __syncthreads();
+    }
+    theta = prefix;
+  }
+  // entries below theta (fewer than kk of them) and the theta-equal ones (ids, for the tie-break)
+  for (long long i = S + threadIdx.x; i < E; i += blockDim.x) {
+    const uint2 e = dump[i];
+    const unsigned key = fkey(__uint_as_float(e.x));
+    if (kk == 0 || key > theta) continue;
+    const long long id = __ldg(reinterpret_cast<const long long*>(ids) + e.y);
+    if (key < theta) {
+      const unsigned at = atomicAdd(&s_cnt, 1u);
+      sd[at] = __uint_as_float(e.x);
+      sid[at] = id;
+    } else {
+      const unsigned at = atomicAdd(&s_neq, 1u);
+      if (at < (unsigned)kSelLargeEqCap) seq[at] = id;
+    }
+  }
+  __syncthreads();
+  const int nlt = (int)s_cnt;
+  const int neq = (int)s_neq;
+  const int need = kk - nlt;  // theta-equal entries to take, smallest ids first
+  if (need > 0) {
+    if (neq <= kSelLargeEqCap) {
+      // rank of each equal id among the equal ids (ids are unique): the need smallest go in
+      for (int j = threadIdx.x; j < neq; j += blockDim.x) {
+        const long long v = seq[j];
+        int r = 0;
+        for (int t = 0; t < neq; ++t) r += seq[t] < v;
+        if (r < need) {
+          sd[nlt + r] = fkey_inv(theta);
+          sid[nlt + r] = v;
+        }
+      }
+    } else if (threadIdx.x == 0) {  // (pathological ties) repeated minimum over the equal entries
+      long long last = -1;
+      for (int r = 0; r < need; ++r) {
+        long long best = LLONG_MAX;
+        for (long long i = S; i < E; ++i) {
+          const uint2 e = dump[i];
+          if (fkey(__uint_as_float(e.x)) != theta) continue;
+          const long long id = ids[e.y];
+          if (id > last && id < best) best = id;
+        }
+        sd[nlt + r] = fkey_inv(theta);
+        sid[nlt + r] = best;
+        last = best;
+      }
+    }
+  }
+  __syncthreads();
+  int n2 = 1;
+  while (n2 < kk) n2 <<= 1;
+  for (int j = kk + threadIdx.x; j < n2; j += blockDim.x) {
+    sd[j] = CUDART_INF_F;
+    sid[j] = LLONG_MAX;
+  }
+  for (int size = 2; size <= n2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < (n2 >> 1); i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const float da = sd[lo], db = sd[hi];
+        const long long ia = sid[lo], ib = sid[hi];
+        if (up ? lt_did(db, ib, da, ia) : lt_did(da, ia, db, ib)) {
+          sd[lo] = db; sd[hi] = da;
+          sid[lo] = ib; sid[hi] = ia;
+        }
+      }
+    }
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const float dv = j < kk ? sd[j] : CUDART_INF_F;
+    const long long iv = j < kk ? sid[j] : -1;
+    if (packed) {
+      Packed pk;
+      pk.d = dv;
+      pk.pad = 0;
+      pk.id = iv;
+      packed[(size_t)q * k + j] = pk;
+    } else {
+      out_ids[(size_t)q * k + j] = iv;
+      out_dist[(size_t)q * k + j] = dv;
+    }
+  }
+}
+
+// the large-k path of one search: chunks of queries whose candidates fit ws.dump
+cudaError_t launch_scan_large(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, int64_t* out_ids,
+                              float* out_dist, void* out_packed, cudaStream_t s) {
+  if (nq <= 0) return cudaSuccess;
+  const int qc = ws.dump_nq;  // queries per chunk (ensure_ws: chunk x max groups per query <= dump capacity)
+  if (qc < 1) return cudaErrorInvalidConfiguration;
+  for (int q0 = 0; q0 < nq; q0 += qc) {
+    const int q1 = q0 + qc < nq ? q0 + qc : nq;
+    ScanArgs a{nq, np, k, ix.npairs, (uint32_t)(ix.npairs * ix.lut_pair_bytes), ws.plocal, ws.term1, ws.item_off,
+               ix.gbase, ix.codes, ix.bias, ix.ids, ws.lut, ws.pdist, ws.pid,
+               nullptr, nullptr, 0u, nullptr, nullptr, 1, q0, q1, ws.dump};
+    cudaError_t e = launch_scan_k(ix, a, ws.n_cta, s);
+    if (e != cudaSuccess) return e;
+    k_select_large<<<q1 - q0, kSelLargeThreads, 0, s>>>(q0, np, k, ws.item_off, ws.dump, ix.ids, out_ids, out_dist,
+                                                        reinterpret_cast<Packed*>(out_packed));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // ---------------------------------------------------------------- K8 shard merge
@@ -876,9 +1061,73 @@ __global__ void k_merge_parts(int n_shards, int nq, int k, const Packed* __restr
   }
 }
 
+// K8 for k > 32: one CTA per query sorts the n_shards * k gathered entries by
+// (dist, id) in shared memory (bitonic) and keeps the k smallest.
+constexpr int kMergeLargeCap = 8192;  // n_shards * k (checked by the callers)
+__global__ void __launch_bounds__(1024) k_merge_large(int n_shards, int nq, int k, const Packed* __restrict__ packed,
+                                                      const int64_t* __restrict__ pids,
+                                                      const float* __restrict__ pdist, int64_t* __restrict__ out_ids,
+                                                      float* __restrict__ out_dist) {
+  extern __shared__ __align__(16) unsigned char smm[];
+  const int n = n_shards * k;
+  int n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  long long* sid = reinterpret_cast<long long*>(smm);
+  float* sd = reinterpret_cast<float*>(sid + n2);
+  const int q = blockIdx.x;
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    float dv = CUDART_INF_F;
+    long long iv = LLONG_MAX;
+    if (i < n) {
+      const size_t o = ((size_t)(i / k) * nq + q) * k + (i % k);
+      if (packed) { dv = packed[o].d; iv = packed[o].id; }
+      else { dv = pdist[o]; iv = pids[o]; }
+      if (iv < 0) iv = LLONG_MAX;  // padding sorts last
+    }
+    sd[i] = dv;
+    sid[i] = iv;
+  }
+  for (int size = 2; size <= n2; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < (n2 >> 1); i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const float da = sd[lo], db = sd[hi];
+        const long long ia = sid[lo], ib = sid[hi];
+        if (up ? lt_did(db, ib, da, ia) : lt_did(da, ia, db, ib)) {
+          sd[lo] = db; sd[hi] = da;
+          sid[lo] = ib; sid[hi] = ia;
+        }
+      }
+    }
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const bool pad = sid[j] == LLONG_MAX;
+    out_ids[(size_t)q * k + j] = pad ? -1 : sid[j];
+    out_dist[(size_t)q * k + j] = pad ? CUDART_INF_F : sd[j];
+  }
+}
+
+static cudaError_t launch_merge_large(const Packed* packed, const int64_t* pids, const float* pdist, int n_shards,
+                                      int nq, int k, int64_t* out_ids, float* out_dist, cudaStream_t s) {
+  const int n = n_shards * k;
+  if (n > kMergeLargeCap) return cudaErrorInvalidValue;
+  int n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  const size_t sm = (size_t)n2 * (sizeof(long long) + sizeof(float));
+  cudaError_t e = ensure_smem((const void*)k_merge_large, sm);
+  if (e != cudaSuccess) return e;
+  k_merge_large<<<nq, 1024, sm, s>>>(n_shards, nq, k, packed, pids, pdist, out_ids, out_dist);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_merge_packed(const void* parts, int n_shards, int nq, int k, int64_t* out_ids, float* out_dist,
                                 cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
+  if (k > kMaxK)
+    return launch_merge_large(reinterpret_cast<const Packed*>(parts), nullptr, nullptr, n_shards, nq, k, out_ids,
+                              out_dist, s);
   const int wpb = 8;
   k_merge_parts<<<(nq + wpb - 1) / wpb, wpb * 32, 0, s>>>(n_shards, nq, k, reinterpret_cast<const Packed*>(parts),
                                                           nullptr, nullptr, out_ids, out_dist);
@@ -888,6 +1137,7 @@ cudaError_t launch_merge_packed(const void* parts, int n_shards, int nq, int k, 
 cudaError_t launch_merge_split(const int64_t* part_ids, const float* part_dist, int n_shards, int nq, int k,
                                int64_t* out_ids, float* out_dist, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
+  if (k > kMaxK) return launch_merge_large(nullptr, part_ids, part_dist, n_shards, nq, k, out_ids, out_dist, s);
   const int wpb = 8;
   k_merge_parts<<<(nq + wpb - 1) / wpb, wpb * 32, 0, s>>>(n_shards, nq, k, nullptr, part_ids, part_dist, out_ids,
                                                           out_dist);

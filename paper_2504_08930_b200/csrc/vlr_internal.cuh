@@ -16,8 +16,10 @@ namespace vlr {
 // ---------------------------------------------------------------- constants
 constexpr int kWarp = 32;
 constexpr int kMaxK = 32;          // warp-register top-k (one entry per lane)
-constexpr int kMaxM = 128;         // max sub-quantizers, 8-bit codes (padded count of the scan kernel)
-constexpr int kMaxM4 = 256;        // max sub-quantizers, 4-bit codes
+constexpr int kMaxKLarge = 1024;   // k > 32: DUMP scan + per-query radix select (k_select_large), §8(b)
+constexpr size_t kDumpBudget = (size_t)1 << 30;  // bytes of the large-k candidate buffer (queries chunked to fit)
+constexpr int kMaxM = 192;         // max sub-quantizers, 8-bit codes (scan instantiations up to 192 slots)
+constexpr int kMaxM4 = 384;        // max sub-quantizers, 4-bit codes (pair mode: 192 byte slots; PQ384x4)
 #ifndef VLR_SCAN_THREADS
 #define VLR_SCAN_THREADS 512
 #endif
@@ -99,6 +101,7 @@ struct DeviceIndex {
   float* bias = nullptr;       // [n_groups*32] b_i = ||yhat||^2 + 2<c_l, yhat> (+inf for padding)
   int64_t* ids = nullptr;      // [n_groups*32] (-1 for padding)
   int64_t bytes = 0;
+  std::vector<int64_t> top_groups;  // [i] = groups of the i largest local lists (large-k buffer bound)
   void* nccl = nullptr;        // ncclComm_t
 };
 
@@ -129,6 +132,8 @@ struct Workspace {
   float* lut = nullptr;        // [nq][npairs][ksub][64]
   float* pdist = nullptr;      // [(n_cta + nq) * warps * k] scan partials
   int64_t* pid = nullptr;
+  uint2* dump = nullptr;       // large k: [dump_nq x max groups per query x 32] (dist bits, vector position)
+  int dump_nq = 0;             // queries per large-k chunk
   void* send = nullptr;        // [nq][k] 16-byte entries (world > 1)
   void* recv = nullptr;        // [world][nq][k]
   float* h_stage = nullptr;    // pinned staging for vlr_search_host (queries)
@@ -210,6 +215,8 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
                         const Release* rel = nullptr);
 cudaError_t launch_rank_merge(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k,
                               int64_t* out_ids, float* out_dist, void* out_packed, cudaStream_t s);
+cudaError_t launch_scan_large(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, int64_t* out_ids,
+                              float* out_dist, void* out_packed, cudaStream_t s);
 cudaError_t launch_merge_packed(const void* parts, int n_shards, int nq, int k, int64_t* out_ids, float* out_dist,
                                 cudaStream_t s);
 cudaError_t launch_merge_split(const int64_t* part_ids, const float* part_dist, int n_shards, int nq, int k,

@@ -92,8 +92,12 @@ def test_search_argument_validation_without_index():
     assert vlr.STATUS[st] == "INVALID_ARG"
     st = L.vlr_merge_partials(None, None, 0, 1, 1, None, None, None)
     assert vlr.STATUS[st] == "INVALID_ARG"
-    st = L.vlr_merge_partials(None, None, 1, 1, 64, None, None, None)
+    st = L.vlr_merge_partials(None, None, 1, 1, 2000, None, None, None)  # k > 1024
     assert vlr.STATUS[st] == "UNSUPPORTED"
+    st = L.vlr_merge_partials(None, None, 9, 1, 1000, None, None, None)  # n_shards x k > 8192 (k > 32)
+    assert vlr.STATUS[st] == "UNSUPPORTED"
+    st = L.vlr_merge_partials(None, None, 2, 1, 64, None, None, None)  # k 64 valid: null buffers
+    assert vlr.STATUS[st] == "INVALID_ARG"
     st = L.vlr_merge_partials(None, None, 1, 0, 4, None, None, None)
     assert vlr.STATUS[st] == "OK"  # nq == 0 is a no-op
     assert b"" != L.vlr_last_error() or True
