@@ -199,9 +199,15 @@ vlr_status vlr_search_host(vlr_index* idx, const float* h_queries, int32_t nq, i
  * Rows with no resident probe are released first, as padding. Results are
  * bit-identical to vlr_search_async (same distances, same merge code). Not
  * graph-capturable (the epoch is a launch argument).
- * Errors: as vlr_search_async; UNSUPPORTED for world > 1 or shard-only handles
- * (rows there are final only after the exchange); INVALID_ARG for epoch 0,
- * NULL or non-device-accessible ready/ids/dist.
+ * Sharded (world > 1: shard-only handles, or a communicator with the sharded
+ * coarse stage): every rank releases ITS partial rows (its owned probes only;
+ * no result all-gather), and the dispatcher merges the shards' rows per query
+ * with vlr_merge_ready as soon as every shard has released it.
+ * Across processes, put the rows and flags in host memory every rank maps
+ * (e.g. POSIX shared memory registered with cudaHostRegister).
+ * Errors: as vlr_search_async; UNSUPPORTED for k > 32, or a communicator
+ * with VLR_COARSE_REPLICATED=1; INVALID_ARG for epoch 0, NULL or
+ * non-device-accessible ready/ids/dist.
  */
 vlr_status vlr_search_release_async(vlr_index* idx, const float* d_queries, int32_t nq, int32_t nprobe, int32_t k,
                                     int64_t* d_ids, float* d_dist, uint8_t* d_miss, int32_t* d_probes,
@@ -217,6 +223,18 @@ vlr_status vlr_search_release_async(vlr_index* idx, const float* d_queries, int3
  * the returned queries can be read after the call. Host only; no CUDA calls. */
 int32_t vlr_poll_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, uint8_t* seen, int32_t* out_q,
                        int64_t* out_t_ns, int32_t max_out, int64_t timeout_us);
+
+/* The cross-rank dispatcher merge of NEXT-4 (host only): ready[s] [nq] flags
+ * and part_ids[s] / part_dist[s] [nq][k] partial rows of shard s (as released
+ * by vlr_search_release_async on each shard, host-visible). Spins until every
+ * query is released by all n_shards shards or timeout_us passes; each query's
+ * row out_ids/out_dist [nq][k] is written as soon as its last shard released
+ * it: the k smallest (dist, id) of the shards' sorted rows. out_t_ns (may be
+ * NULL) [nq]: CLOCK_MONOTONIC ns when q was merged. Returns the number of
+ * merged queries (nq on success), -1 for bad arguments. */
+int32_t vlr_merge_ready(int32_t n_shards, const uint32_t* const* ready, uint32_t epoch, int32_t nq, int32_t k,
+                        const int64_t* const* part_ids, const float* const* part_dist, int64_t* out_ids,
+                        float* out_dist, int64_t* out_t_ns, int64_t timeout_us);
 
 /* Native dispatcher loop for vlr_search_release_async without per-query
  * callbacks: spins until every q < nq has ready[q] == epoch or timeout_us

@@ -23,7 +23,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "NONFINITE", 4: "UNKN
 # every symbol include/vlr.h declares (checked by tests/test_abi.py)
 EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_search_host_async",
            "vlr_search_release_async", "vlr_coarse_stage1", "vlr_coarse_stage2", "vlr_search_stage3",
-           "vlr_poll_ready", "vlr_wait_ready", "vlr_reserve", "vlr_deal_owners", "vlr_update_hot",
+           "vlr_poll_ready", "vlr_wait_ready", "vlr_merge_ready", "vlr_reserve", "vlr_deal_owners", "vlr_update_hot",
            "vlr_merge_partials", "vlr_access_counts", "vlr_index_info", "vlr_index_owners", "vlr_set_profiling", "vlr_stage_times",
            "vlr_last_launch_count", "vlr_nccl_unique_id", "vlr_index_free", "vlr_last_error", "vlr_version"]
 
@@ -89,6 +89,8 @@ def lib():
         L.vlr_poll_ready.restype = I32
         L.vlr_wait_ready.argtypes = [P, I32, ctypes.c_uint32, P, I64]
         L.vlr_wait_ready.restype = I32
+        L.vlr_merge_ready.argtypes = [I32, P, ctypes.c_uint32, I32, I32, P, P, P, P, P, I64]
+        L.vlr_merge_ready.restype = I32
         L.vlr_last_launch_count.argtypes = [P]
         L.vlr_last_launch_count.restype = I32
         L.vlr_index_free.argtypes = [P]
@@ -311,6 +313,25 @@ class Index:
         t_ready.t0 = t0
         return ids, dist, miss, prb, t_ready
 
+    def search_release_launch(self, Q, nprobe: int, k: int, stream=None):
+        """vlr_search_release_async without waiting: returns (ids, dist, miss,
+        probes, ready, epoch) with ids/dist/ready pinned CPU tensors (the rows
+        and flags the dispatcher reads; on a sharded handle: THIS shard's
+        partial rows, merged across shards with merge_ready)."""
+        import torch
+        assert Q.is_cuda and Q.dtype == torch.float32 and Q.is_contiguous()
+        nq, npr = int(Q.shape[0]), min(nprobe, self.nlist)
+        ids = torch.empty(nq, k, dtype=torch.int64, pin_memory=True)
+        dist = torch.empty(nq, k, dtype=torch.float32, pin_memory=True)
+        miss = torch.empty(nq, npr, dtype=torch.uint8, device=Q.device)
+        prb = torch.empty(nq, npr, dtype=torch.int32, device=Q.device)
+        ready = torch.zeros(nq, dtype=torch.int32, pin_memory=True)
+        self._epoch = (getattr(self, "_epoch", 0) % 0x7FFFFFFF) + 1
+        _check(lib().vlr_search_release_async(self._h, Q.data_ptr(), nq, nprobe, k, ids.data_ptr(), dist.data_ptr(),
+                                              miss.data_ptr(), prb.data_ptr(), ready.data_ptr(), self._epoch,
+                                              _stream_handle(stream)))
+        return ids, dist, miss, prb, ready, self._epoch
+
     def search_host(self, Q: np.ndarray, nprobe: int, k: int, out=None, stream=None):
         """vlr_search_host: host buffers in and out (copies inside the call)."""
         Q = np.ascontiguousarray(Q, dtype=np.float32)
@@ -411,6 +432,30 @@ def deal_owners(list_offsets, hot, world: int, counts=None) -> np.ndarray:
     _check(lib().vlr_deal_owners(offs.ctypes.data, int(offs.size - 1), cnt.ctypes.data if cnt is not None else None,
                                  _ptr(hotv), int(hotv.size), int(world), _ptr(out)))
     return out
+
+
+def merge_ready(readys, epochs, part_ids, part_dist, timeout_s: float = 30.0):
+    """vlr_merge_ready: the cross-shard dispatcher merge of released partial
+    rows (pinned CPU tensors from search_release_launch on each shard; every
+    shard's flags must use one epoch). Returns (ids, dist, t_merged_ns)."""
+    import torch
+    S = len(readys)
+    assert len(set(int(e) for e in epochs)) == 1, "one epoch for every shard"
+    nq, k = part_ids[0].shape
+    P = ctypes.c_void_p
+    rr = (P * S)(*[r.data_ptr() for r in readys])
+    pi = (P * S)(*[t.data_ptr() for t in part_ids])
+    pd = (P * S)(*[t.data_ptr() for t in part_dist])
+    ids = np.empty((nq, k), np.int64)
+    dist = np.empty((nq, k), np.float32)
+    t = np.zeros(nq, np.int64)
+    n = lib().vlr_merge_ready(S, ctypes.cast(rr, P), int(epochs[0]), nq, k, ctypes.cast(pi, P), ctypes.cast(pd, P),
+                              ids.ctypes.data, dist.ctypes.data, t.ctypes.data, int(timeout_s * 1e6))
+    if n < 0:
+        raise VlrError(1, "vlr_merge_ready: bad arguments")
+    if n < nq:
+        raise VlrError(7, f"merge_ready: {nq - n} queries not released by every shard within {timeout_s} s")
+    return torch.from_numpy(ids), torch.from_numpy(dist), t
 
 
 def merge_partials(part_ids, part_dist, stream=None):

@@ -1,6 +1,7 @@
 // capi.cu -- the C ABI of libvlr.so (include/vlr.h): index residency, the
 // search pipeline (stream-ordered launches of K1..K8), NCCL exchange.
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -57,6 +58,26 @@ static vlr_status fail(vlr_status st, const std::string& msg) {
 // accumulation over d terms in the tensor core bounded conservatively by
 // d * 2^-23 (order and rounding mode unspecified).
 static float filter_edot(int d) { return 2.0f * 4.8828125e-4f + 2.3841858e-7f + 1.01f * (float)d * 1.1920929e-7f; }
+
+// NVTX ranges per pipeline stage (host-side enqueue spans; with nsys/ncu
+// --nvtx they label the K-stages). On when VLR_NVTX=1 or profiling is on.
+static bool nvtx_on(const vlr_index* h) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("VLR_NVTX");
+    env = (e && e[0] == '1') ? 1 : 0;
+  }
+  return env == 1 || h->profiling != 0;
+}
+struct NvtxRange {
+  bool on;
+  NvtxRange(const vlr_index* h, const char* name) : on(nvtx_on(h)) {
+    if (on) nvtxRangePushA(name);
+  }
+  ~NvtxRange() {
+    if (on) nvtxRangePop();
+  }
+};
 
 template <class T>
 static cudaError_t dalloc(T** p, size_t n) {
@@ -239,6 +260,7 @@ static ncclResult_t nccl_settle_init(ncclComm_t* comm, int world, ncclUniqueId u
 
 static vlr_status nccl_allgather(vlr_index* h, const void* send, void* recv, size_t bytes, cudaStream_t s,
                                  const char* what) {
+  NvtxRange nv(h, what);
   ncclComm_t comm = reinterpret_cast<ncclComm_t>(h->ix.nccl);
   bool to = false;
   ncclResult_t r = nccl_settle(comm, ncclAllGather(send, recv, bytes, ncclUint8, comm, s), nccl_timeout_ms(), &to);
@@ -717,6 +739,7 @@ static vlr_status lut_fork(vlr_index* h, Pipe& p) {
 }
 
 static vlr_status phase_a(vlr_index* h, Pipe& p, bool sharded, uint8_t* out_miss, int32_t* out_probes) {
+  NvtxRange nv(h, sharded ? "vlr coarse stage 1 (qprep, K1, K2s1)" : "vlr coarse (qprep, K1, K2, K3a, K3b)");
   DeviceIndex& ix = h->ix;
   Workspace& w = h->ws;
   VLR_CUDA_TRY(cudaMemsetAsync(w.status, 0, sizeof(int32_t), p.s));
@@ -738,6 +761,7 @@ static vlr_status phase_a(vlr_index* h, Pipe& p, bool sharded, uint8_t* out_miss
 }
 
 static vlr_status phase_b(vlr_index* h, Pipe& p) {
+  NvtxRange nv(h, "vlr coarse stage 2 (K2s2, K3a, K3b local)");
   DeviceIndex& ix = h->ix;
   Workspace& w = h->ws;
   VLR_CUDA_TRY(launch_select(ix, w, p.nq, p.np, filter_edot(ix.d), kSelStage2, p.s)); ++p.n;
@@ -749,6 +773,7 @@ static vlr_status phase_b(vlr_index* h, Pipe& p) {
 
 static vlr_status phase_c(vlr_index* h, Pipe& p, bool sharded, int64_t* out_ids, float* out_dist, uint8_t* out_miss,
                           int32_t* out_probes, const Release* rel, bool packed) {
+  NvtxRange nv(h, rel ? "vlr route + release scan (K4b, K6 REL, merger)" : "vlr route + scan + merge (K4b, K6, K7)");
   DeviceIndex& ix = h->ix;
   Workspace& w = h->ws;
   if (sharded) {
@@ -829,8 +854,9 @@ static vlr_status search_locked(vlr_index* h, const float* Q, int32_t nq, int32_
     if ((st = nccl_allgather(h, w.x2, w.x2_all, sizeof(CoarseEntry) * nq * np, s, "coarse stage 2")) != VLR_OK)
       return st;
   }
-  if ((st = phase_c(h, p, sharded, out_ids, out_dist, out_miss, out_probes, rel, exchange)) != VLR_OK) return st;
-  if (exchange) {
+  if ((st = phase_c(h, p, sharded, out_ids, out_dist, out_miss, out_probes, rel, exchange && !rel)) != VLR_OK)
+    return st;
+  if (exchange && !rel) {  // release mode: each rank releases its partial rows; vlr_merge_ready merges them
     if ((st = nccl_allgather(h, w.send, w.recv, (size_t)nq * k * sizeof(Packed), s, "results")) != VLR_OK) return st;
     VLR_CUDA_TRY(launch_merge_packed(w.recv, ix.world, nq, k, out_ids, out_dist, s)); ++p.n;
   }
@@ -870,8 +896,8 @@ vlr_status vlr_search_release_async(vlr_index* h, const float* Q, int32_t nq, in
                                     int64_t* out_ids, float* out_dist, uint8_t* out_miss, int32_t* out_probes,
                                     uint32_t* ready, uint32_t epoch, void* stream) {
   if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
-  if (h->ix.world > 1 || h->ix.shard_only || h->ix.nccl)
-    return fail(VLR_ERR_UNSUPPORTED, "early release needs world == 1 (rows are final only after the exchange)");
+  if (h->ix.nccl && !h->ix.coarse_sharded)
+    return fail(VLR_ERR_UNSUPPORTED, "early release with a communicator needs the sharded coarse stage");
   if (k > kMaxK) return fail(VLR_ERR_UNSUPPORTED, "early release: k > 32");
   if (nq > 0) {
     if (!ready || epoch == 0) return fail(VLR_ERR_INVALID_ARG, "release: null ready flags or epoch 0");
@@ -942,6 +968,67 @@ int32_t vlr_wait_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, int64_
       break;
   }
   std::atomic_thread_fence(std::memory_order_acquire);
+  return n;
+}
+
+// The dispatcher side of NEXT-4 across ranks ("Each GPU worker sets
+// a completion flag ... the dispatcher merges"): polls the n_shards flag arrays;
+// query q is final once every shard has released it (ready[s][q] == epoch);
+// its final row is the k smallest (dist, id) of the shards' partial rows (k-way
+// merge of sorted rows, padding (-1, +inf) last). Host only.
+int32_t vlr_merge_ready(int32_t n_shards, const uint32_t* const* ready, uint32_t epoch, int32_t nq, int32_t k,
+                        const int64_t* const* part_ids, const float* const* part_dist, int64_t* out_ids,
+                        float* out_dist, int64_t* out_t_ns, int64_t timeout_us) {
+  if (n_shards < 1 || !ready || !part_ids || !part_dist || !out_ids || !out_dist || nq < 0 || k < 1) return -1;
+  for (int32_t r = 0; r < n_shards; ++r)
+    if (!ready[r] || !part_ids[r] || !part_dist[r]) return -1;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<uint8_t> done((size_t)nq, 0);
+  std::vector<int32_t> pos((size_t)n_shards);
+  int32_t n = 0, lo = 0;
+  while (n < nq) {
+    bool any = false;
+    for (int32_t q = lo; q < nq; ++q) {
+      if (done[q]) continue;
+      bool all = true;
+      for (int32_t r = 0; r < n_shards && all; ++r) all = reinterpret_cast<const volatile uint32_t*>(ready[r])[q] == epoch;
+      if (!all) continue;
+      std::atomic_thread_fence(std::memory_order_acquire);  // the rows were written before the flags
+      std::fill(pos.begin(), pos.end(), 0);
+      for (int32_t j = 0; j < k; ++j) {
+        int32_t best = -1;
+        float bd = 0.f;
+        int64_t bi = 0;
+        for (int32_t r = 0; r < n_shards; ++r) {
+          if (pos[r] >= k) continue;
+          const int64_t id = part_ids[r][(size_t)q * k + pos[r]];
+          if (id < 0) continue;  // padding: the rest of this row is padding
+          const float dv = part_dist[r][(size_t)q * k + pos[r]];
+          if (best < 0 || dv < bd || (dv == bd && id < bi)) { best = r; bd = dv; bi = id; }
+        }
+        if (best < 0) {
+          out_ids[(size_t)q * k + j] = -1;
+          out_dist[(size_t)q * k + j] = std::numeric_limits<float>::infinity();
+        } else {
+          out_ids[(size_t)q * k + j] = bi;
+          out_dist[(size_t)q * k + j] = bd;
+          ++pos[best];
+        }
+      }
+      done[q] = 1;
+      any = true;
+      ++n;
+      if (out_t_ns) {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        out_t_ns[q] = (int64_t)ts.tv_sec * 1000000000LL + ts.tv_nsec;
+      }
+    }
+    while (lo < nq && done[lo]) ++lo;
+    if (!any && std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count() >=
+                    timeout_us)
+      break;
+  }
   return n;
 }
 

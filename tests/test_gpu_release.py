@@ -118,7 +118,37 @@ def test_release_errors(c1_index, c1_queries):
     assert L.vlr_search_release_async(*args, pageable.ctypes.data, 5, s) == 1  # not device-accessible
     assert L.vlr_search_release_async(*args, None, 5, s) == 1
     h.close()
-    hs = vlr.Index.from_arrays(c1_index, rank=0, world=2)  # shard-only handle
-    args = (hs._h, Qd.data_ptr(), 4, 16, 10, ids.data_ptr(), dist.data_ptr(), miss.data_ptr(), None)
-    assert L.vlr_search_release_async(*args, ready.data_ptr(), 5, s) == 9  # UNSUPPORTED
-    hs.close()
+    torch.cuda.synchronize()
+    args = (h._h, Qd.data_ptr(), 4, 16, 40, ids.data_ptr(), dist.data_ptr(), miss.data_ptr(), None)
+    h = vlr.Index.from_arrays(c1_index)
+    args = (h._h,) + args[1:]
+    assert L.vlr_search_release_async(*args, ready.data_ptr(), 5, s) == 9  # UNSUPPORTED: k > 32
+    h.close()
+
+
+def test_release_sharded_dispatcher_merge(c1_index, c1_queries):
+    """NEXT-4 at world > 1: G shard-only handles each release their
+    partial rows (own probes only) with completion flags; the host dispatcher
+    (vlr_merge_ready) merges a query as soon as every shard released it. The
+    merged rows equal the single-GPU search bitwise; shards launched on their
+    own streams run concurrently."""
+    c = datagen.CONFIGS["C1"]
+    Qd = torch.from_numpy(c1_queries).cuda()
+    h1 = vlr.Index.from_arrays(c1_index)
+    ref = h1.search(Qd, c["nprobe"], c["k"], sync=True)
+    h1.close()
+    for G in (2, 3):
+        hs = [vlr.Index.from_arrays(c1_index, rank=r, world=G) for r in range(G)]
+        for h in hs:  # identical epochs across shards (first release on each handle)
+            h._epoch = 100
+        streams = [torch.cuda.Stream() for _ in range(G)]
+        outs = [h.search_release_launch(Qd, c["nprobe"], c["k"], stream=s) for h, s in zip(hs, streams)]
+        ids, dist, t = vlr.merge_ready([o[4] for o in outs], [o[5] for o in outs], [o[0] for o in outs],
+                                       [o[1] for o in outs])
+        torch.cuda.synchronize()
+        assert torch.equal(ids, ref[0].cpu()) and torch.equal(dist, ref[1].cpu()), G
+        for o in outs[1:]:
+            assert torch.equal(o[2], outs[0][2]) and torch.equal(o[3], outs[0][3])
+        assert (t > 0).all()
+        for h in hs:
+            h.close()
