@@ -96,7 +96,7 @@ __global__ void k_negative(const int64_t* ids, long long n, int32_t* flag) {
 }
 
 static void free_ws(Workspace& w) {
-  void* ps[] = {w.qnorm, w.qsq, w.qf16, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.x1, w.x1_all, w.x2, w.x2_all, w.dump, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.qdone, w.lut,
+  void* ps[] = {w.qnorm, w.qsq, w.qf16, w.qf16t, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.x1, w.x1_all, w.x2, w.x2_all, w.dump, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.qdone, w.lut,
                 w.pdist, w.pid, w.send, w.recv, w.d_q, w.d_ids, w.d_dist, w.d_miss, w.d_probes, w.status};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -129,6 +129,7 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   VLR_CUDA_TRY(dalloc(&w.qnorm, nqs));
   VLR_CUDA_TRY(dalloc(&w.qsq, nqs));
   VLR_CUDA_TRY(dalloc(&w.qf16, nqs * ix.d8));
+  VLR_CUDA_TRY(dalloc(&w.qf16t, (size_t)((cnq + 511) / 512 * 512) * ((ix.d8 + 63) / 64 * 64)));
   VLR_CUDA_TRY(dalloc(&w.qinv, nqs));
   VLR_CUDA_TRY(dalloc(&w.dt, nqs * ix.nlist));
   VLR_CUDA_TRY(dalloc(&w.gmin, nqs * ((ix.nlist + 31) / 32)));
@@ -744,10 +745,12 @@ static vlr_status phase_a(vlr_index* h, Pipe& p, bool sharded, uint8_t* out_miss
   Workspace& w = h->ws;
   VLR_CUDA_TRY(cudaMemsetAsync(w.status, 0, sizeof(int32_t), p.s));
   rec(h, 0, p.s);
-  VLR_CUDA_TRY(launch_qprep(p.Q, p.nq, ix.d, ix.d8, w.qnorm, w.qsq, w.qf16, w.qinv, w.status, p.s)); ++p.n;
+  const int bt = filter_btile_rows(p.nq);
+  VLR_CUDA_TRY(launch_qprep(p.Q, p.nq, ix.d, ix.d8, w.qnorm, w.qsq, w.qf16, w.qinv, w.status, bt ? w.qf16t : nullptr,
+                            bt, p.s)); ++p.n;
   const int t_lo = sharded ? ix.c_lo / 128 : 0;
   const int t_hi = sharded ? (ix.c_hi + 127) / 128 : (ix.nlist + 127) / 128;
-  VLR_CUDA_TRY(launch_filter_tc(w.qf16, w.qinv, p.nq, ix, t_lo, t_hi, w.dt, w.gmin, p.s)); ++p.n;
+  VLR_CUDA_TRY(launch_filter_tc(w.qf16, w.qinv, p.nq, ix, t_lo, t_hi, w.dt, w.gmin, bt ? w.qf16t : nullptr, p.s)); ++p.n;
   vlr_status st = lut_fork(h, p);
   if (st != VLR_OK) return st;
   rec(h, 1, p.s);

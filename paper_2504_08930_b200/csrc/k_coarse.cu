@@ -27,9 +27,21 @@ namespace vlr {
 // fp16(q 2^e_q) with 2^e_q the power of two putting max |q_t| 2^e_q in
 // [2^13, 2^14) (exponent clamped to [-60, 60]; DESIGN.md §5 bounds the
 // subnormal flush that clamping can cause).
-__global__ void k_qprep(const float* __restrict__ Q, int d, int d8, float* __restrict__ qnorm, float* __restrict__ qsq,
-                        uint16_t* __restrict__ qf16, float* __restrict__ qinv, int32_t* status) {
+// qf16t (optional): the same fp16 operand pre-tiled for K1's B loads: [qtile of QT rows][kblock of 64][QT rows]
+// [64 cols], each 128-B row's 16-B chunks XOR-swizzled by (row & 7) (the SW128 K-major image), so a K1 stage's
+// B tile is ONE contiguous bulk copy; rows of the last tile past nq are zero (CTAs q >= nq write only those).
+__global__ void k_qprep(const float* __restrict__ Q, int nq, int d, int d8, float* __restrict__ qnorm,
+                        float* __restrict__ qsq, uint16_t* __restrict__ qf16, float* __restrict__ qinv, int32_t* status,
+                        uint16_t* __restrict__ qf16t, int QT) {
   const int q = blockIdx.x;
+  if (q >= nq) {  // zero padding rows of the tiled operand
+    const int qt = q / QT, r = q % QT, kbn = (d8 + 63) / 64;
+    for (int t = threadIdx.x; t < kbn * 64; t += blockDim.x) {
+      const int kb = t >> 6, col = t & 63;
+      qf16t[((size_t)(qt * kbn + kb) * QT + r) * 64 + (((col >> 3) ^ (r & 7)) << 3) + (col & 7)] = 0;
+    }
+    return;
+  }
   const float* row = Q + (size_t)q * d;
   double s = 0.0;
   float mx = 0.f;
@@ -77,16 +89,23 @@ __global__ void k_qprep(const float* __restrict__ Q, int d, int d8, float* __res
   }
   __syncthreads();
   const float sc = s_scale;
-  for (int t = threadIdx.x; t < d8; t += blockDim.x) {
+  const int kbn = (d8 + 63) / 64;
+  for (int t = threadIdx.x; t < (qf16t ? kbn * 64 : d8); t += blockDim.x) {
     const float v = t < d ? row[t] * sc : 0.f;
-    qf16[(size_t)q * d8 + t] = __half_as_ushort(__float2half_rn(v));
+    const uint16_t h = __half_as_ushort(__float2half_rn(v));
+    if (t < d8) qf16[(size_t)q * d8 + t] = h;
+    if (qf16t) {
+      const int qt = q / QT, r = q % QT, kb = t >> 6, col = t & 63;
+      qf16t[((size_t)(qt * kbn + kb) * QT + r) * 64 + (((col >> 3) ^ (r & 7)) << 3) + (col & 7)] = h;
+    }
   }
 }
 
 cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, float* qsq, uint16_t* qf16, float* qinv,
-                         int32_t* status, cudaStream_t s) {
+                         int32_t* status, uint16_t* qf16t, int QT, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  k_qprep<<<nq, 256, 0, s>>>(Q, d, d8, qnorm, qsq, qf16, qinv, status);
+  const int grid = qf16t ? (nq + QT - 1) / QT * QT : nq;
+  k_qprep<<<grid, 256, 0, s>>>(Q, nq, d, d8, qnorm, qsq, qf16, qinv, status, qf16t, QT);
   return cudaGetLastError();
 }
 

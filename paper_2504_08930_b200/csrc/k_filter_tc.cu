@@ -87,6 +87,12 @@ __device__ __forceinline__ void bulk_g2s_16k(void* dst, const void* src, uint64_
                "l"(src), "r"(s32(bar))
                : "memory");
 }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   s32(dst)),
+               "l"(src), "r"(bytes), "r"(s32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
@@ -130,7 +136,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     k_filter_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int L, int nq,
                 int kblocks, int nN, int nacc, int stages, const float* __restrict__ cn2,
                 const float* __restrict__ qinv, float c_inv, float* __restrict__ dt, float* __restrict__ gmin,
-                int ngroups, const uint16_t* __restrict__ At, int t0) {
+                int ngroups, const uint16_t* __restrict__ At, int t0, const uint16_t* __restrict__ Bt) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull;
@@ -194,6 +200,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if constexpr (CL > 1) {  // nacc == 1: this CTA's 1/CL of the query rows, to every cluster CTA
           const int rq = nN / CL;
           tma_2d_mc(sB + (size_t)crank * rq * 128, &tmB, kb * kTcBK, q0 + (int)crank * rq, &full[s], kMask);
+        } else if (Bt) {  // pre-tiled query operand (k_qprep): the stage's whole B tile in one bulk copy
+          bulk_g2s(sB, Bt + ((size_t)blockIdx.y * kblocks + kb) * (size_t)(nacc * nN) * kTcBK, bytesB, &full[s]);
         } else {
           for (int r = 0; r < nacc * nN; r += 256) {
             tma_2d(sB + (size_t)r * 128, &tmB, kb * kTcBK, q0 + r, &full[s]);
@@ -668,8 +676,38 @@ cudaError_t make_tmap_2d(void* map_, const uint16_t* base, int rows, int cols, i
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+static int btiled_env() {
+  static int v = -1;  // VLR_FILTER_BTILED=0: K1's B through the 2-D tensor map of the row-major queries
+  if (v < 0) {
+    const char* e = getenv("VLR_FILTER_BTILED");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+static int pair_env_get() {
+  static int v = -1;  // VLR_FILTER_PAIR=1: the CTA-pair kernel (off by default: measured slower at C4)
+  if (v < 0) {
+    const char* e = getenv("VLR_FILTER_PAIR");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+static int persistent_env_get() {
+  static int v = -1;  // VLR_FILTER_PERSISTENT=1: the persistent double-buffered kernel (experiment)
+  if (v < 0) {
+    const char* e = getenv("VLR_FILTER_PERSISTENT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+int filter_btile_rows(int nq) {
+  if (!btiled_env() || pair_env_get() || persistent_env_get()) return 0;
+  return nq <= 256 ? ((nq + 15) / 16) * 16 : 512;  // = nN * nacc of the one-CTA kernel
+}
+
 cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, int t_lo, int t_hi,
-                             float* dt, float* gmin, cudaStream_t s) {
+                             float* dt, float* gmin, const uint16_t* Qt, cudaStream_t s) {
   if (nq <= 0 || t_hi <= t_lo) return cudaSuccess;
   const int ntiles_all = (ix.nlist + kTcM - 1) / kTcM;
   const bool full_range = t_lo == 0 && t_hi == ntiles_all;
@@ -684,11 +722,7 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   // VLR_FILTER_PERSISTENT=1: the persistent double-buffered kernel for batches <= 256 (experiment; measured
   // 0.102 ms vs 0.060 ms for the one-tile-per-CTA kernel at C4, batch 256: latency-bound at 1 CTA per SM,
   // DRAM 20% / L2 16% of peak, profiles/k1_persistent_r01.md). Off by default.
-  static int persistent = -1;
-  if (persistent < 0) {
-    const char* e = getenv("VLR_FILTER_PERSISTENT");
-    persistent = e ? atoi(e) : 0;
-  }
+  const int persistent = persistent_env_get();
   // B multicast cluster size (VLR_FILTER_CLUSTER, default kTcCluster): CL CTAs on adjacent centroid tiles
   // each load 1/CL of the query tile and multicast it to the others (rows per slice a multiple of 8 = one
   // SW128 atom). One accumulator (nq <= 256) only.
@@ -705,11 +739,7 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   // CTA-pair kernel (VLR_FILTER_PAIR=1): the query tile QT <= 256 rows is
   // halved (multiple of 16) while the grid has fewer than ~2 CTAs per SM, so a shard's few centroid tiles
   // still fill the GPU (world > 1: each rank filters 1/world of the tiles)
-  static int pair_env = -1;
-  if (pair_env < 0) {
-    const char* pe = getenv("VLR_FILTER_PAIR");
-    pair_env = pe ? atoi(pe) : 0;  // off by default: measured slower at C4 (tools/k1_bench.py)
-  }
+  const int pair_env = pair_env_get();
   if (pair_env && !use_persistent && CL == 1) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -802,7 +832,7 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   const uint16_t* At = (tiled && ix.cf16t) ? ix.cf16t : nullptr;
   if (CL == 1) {
     k_filter_tc<1><<<grid, kTcThreads, smem, s>>>(tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages, ix.cnorm2, qinv,
-                                                  ix.c_inv, dt, gmin, ngroups, At, t_lo);
+                                                  ix.c_inv, dt, gmin, ngroups, At, t_lo, Qt);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -819,9 +849,11 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   cfg.numAttrs = 1;
   if (CL == 4)
     return cudaLaunchKernelEx(&cfg, k_filter_tc<4>, tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages,
-                              (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups, At, t_lo);
+                              (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups, At, t_lo,
+                              (const uint16_t*)nullptr);
   return cudaLaunchKernelEx(&cfg, k_filter_tc<2>, tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages,
-                            (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups, At, t_lo);
+                            (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups, At, t_lo,
+                            (const uint16_t*)nullptr);
 }
 
 // fp16(c * scale) (round to nearest even) into a d8-padded copy; scale is a power of two

@@ -631,6 +631,10 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanAr
   }
 }
 
+#ifdef VLR_SCAN_TRACE
+// timing variant (tools/scan_trace.py): per CTA start, end, LUT-wait ns, segments, smid, groups
+__device__ unsigned long long g_scan_trace[1024][6];
+#endif
 template <int MP, int NB, int EXP, bool REL = false, bool DUMP = false>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -649,6 +653,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
   const uint32_t lane4 = (uint32_t)lane << 2;
   const unsigned char* lutc = smem;
   uint32_t phase = 0;
+#ifdef VLR_SCAN_TRACE
+  unsigned long long tr_start = globaltimer_ns(), tr_lut = 0, tr_seg = 0, tr_grp = 0;
+#endif
   // REL: the wave index lives in shared memory and is re-read where needed, so
   // no register is held across the scan loop for it (the MP = 128 loop needs
   // all 128 registers)
@@ -697,8 +704,16 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
       if constexpr (REL) {  // segment length through shared memory: nothing extra stays live across the scan loop
         if (threadIdx.x == 0) s_ng = seg_end - g;
       }
+#ifdef VLR_SCAN_TRACE
+      const unsigned long long tw0 = globaltimer_ns();
+#endif
       mbar_wait(&mbar, phase);
       phase ^= 1u;
+#ifdef VLR_SCAN_TRACE
+      tr_lut += globaltimer_ns() - tw0;
+      ++tr_seg;
+      tr_grp += (unsigned long long)(seg_end - g);
+#endif
 
       float bd = CUDART_INF_F, thr = CUDART_INF_F;
       long long bid = -1;
@@ -740,7 +755,26 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
       }
     }
   }
+#ifdef VLR_SCAN_TRACE
+  if (threadIdx.x == 0 && c < 1024) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_scan_trace[c][0] = tr_start;
+    g_scan_trace[c][1] = globaltimer_ns();
+    g_scan_trace[c][2] = tr_lut;
+    g_scan_trace[c][3] = tr_seg;
+    g_scan_trace[c][4] = smid;
+    g_scan_trace[c][5] = tr_grp;
+  }
+#endif
 }
+
+#ifdef VLR_SCAN_TRACE
+extern "C" int vlr_debug_scan_trace(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_scan_trace, sizeof(unsigned long long) * 6 * (n < 1024 ? n : 1024)) == cudaSuccess
+             ? 0 : -1;
+}
+#endif
 
 int scan_ctas(const DeviceIndex& ix) {
   (void)ix;

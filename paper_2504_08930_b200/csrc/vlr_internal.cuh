@@ -110,6 +110,7 @@ struct Workspace {
   float* qnorm = nullptr;      // [nq] ||q|| (fp32, rounded up; filter band)
   float* qsq = nullptr;        // [nq] ||q||^2 (fp64 sum -> fp32; term1 of L2 with by_residual = 0)
   uint16_t* qf16 = nullptr;    // [nq][d8] fp16(q * 2^e_q) (RN), zero-padded (filter operand B)
+  uint16_t* qf16t = nullptr;   // the same pre-tiled for one-copy B loads (k_qprep): [ceil(nq/512)*512][kb*64]
   float* qinv = nullptr;       // [nq] 2^-e_q
   float* dt = nullptr;         // [nq][nlist] filter distances ||c||^2 - 2<q,c>
   float* gmin = nullptr;       // [nq][ceil(nlist/32)] min of dt over each 32-centroid group
@@ -184,10 +185,13 @@ cudaError_t launch_layout(const DeviceIndex& ix, const uint8_t* stage_codes, con
                           const int64_t* vbase, const int32_t* lglob, cudaStream_t s);
 // stage 0..2 coarse quantizer
 cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, float* qsq, uint16_t* qf16, float* qinv,
-                         int32_t* status, cudaStream_t s);
+                         int32_t* status, uint16_t* qf16t, int QT, cudaStream_t s);
+// K1's query tile (rows of B per CTA): the pre-tiled operand written by qprep uses it; 0 = K1 reads the
+// row-major fp16 queries through a tensor map (VLR_FILTER_BTILED=0, or the pair / persistent kernels)
+int filter_btile_rows(int nq);
 // K1 over centroid tiles [t_lo, t_hi) (128 centroids each): dt columns and gmin groups of those tiles
 cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, int t_lo, int t_hi,
-                             float* dt, float* gmin, cudaStream_t s);
+                             float* dt, float* gmin, const uint16_t* Qt, cudaStream_t s);
 cudaError_t launch_round_f16(const float* src, int rows, int d, int d8, float scale, uint16_t* dst, cudaStream_t s);
 cudaError_t make_tmap_2d(void* map, const uint16_t* base, int rows, int cols, int box_rows, bool swizzle);
 cudaError_t launch_tile_f16(const DeviceIndex& ix, cudaStream_t s);

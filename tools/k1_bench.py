@@ -47,7 +47,7 @@ def child(a):
             h.search(Q[i], c["nprobe"], c["k"], sync=True)
     torch.cuda.synchronize()
     h.set_profiling(1)
-    ts = []
+    ts, sel, ref = [], [], []
     probes = None
     for i in range(5, 5 + a.iters):
         if a.world > 1:  # stage 1 only (qprep + K1 + K2 stage 1): events 0 -> 1 are qprep + K1
@@ -61,7 +61,10 @@ def child(a):
             probes = x1 if probes is None else probes
         else:
             out = h.search(Q[i], c["nprobe"], c["k"], sync=True)
-            ts.append(h.stage_times(0)["coarse_filter"])
+            st = h.stage_times(0)
+            ts.append(st["coarse_filter"])
+            sel.append(st["select"])
+            ref.append(st["refine"])
             if probes is None:
                 probes = out[3]
     import hashlib
@@ -70,12 +73,19 @@ def child(a):
                       "world": a.world, "ms_mean": float(np.mean(ts)), "ms_min": float(np.min(ts)),
                       "ms_median": float(np.median(ts)),
                       "what": "stage1 (qprep + K1 + K2 stage 1)" if a.world > 1 else "qprep + K1",
+                      "select_ms": float(np.mean(sel)) if sel else None,
+                      "refine_ms (K3a+K3b)": float(np.mean(ref)) if ref else None,
                       "probes_md5": dig}), flush=True)
 
 
 VARIANTS = {
     "pair": {"VLR_FILTER_PAIR": "1"},
     "single": {"VLR_FILTER_PAIR": "0"},
+    "single_tmapB": {"VLR_FILTER_PAIR": "0", "VLR_FILTER_BTILED": "0"},
+    "exact_3_2x2": {"VLR_EXACT_CFG": "3,2"},
+    "exact_3_4x2": {"VLR_EXACT_CFG": "3,6"},
+    "exact_5_2x2": {"VLR_EXACT_CFG": "5,2"},
+    "exact_4_4": {"VLR_EXACT_CFG": "4,4"},
     "single_cl2": {"VLR_FILTER_PAIR": "0", "VLR_FILTER_CLUSTER": "2"},
     "pair_qt128": {"VLR_FILTER_PAIR": "1", "VLR_FILTER_QT": "128"},
     "pair_qt64": {"VLR_FILTER_PAIR": "1", "VLR_FILTER_QT": "64"},
