@@ -63,6 +63,10 @@ def parse():
                    help="N > 1 plumbing on ONE shared GPU: gloo process group, shard-only handles, the staged "
                         "sharded search with the exchanges over gloo (host), vlr_merge_partials; timing is not a "
                         "multi-GPU number")
+    p.add_argument("--exchange", default="p2p", choices=["p2p", "nccl", "staged"],
+                   help="N > 1 transport: p2p = the NVLink peer-exchange kernels (vlr_p2p_*; default), nccl = "
+                        "ncclAllGather on the search stream, staged = the staged C-ABI with the caller's transport "
+                        "(dry run only)")
     p.add_argument("--lat-batches", type=int, default=1000,
                    help="latency pass: CUDA-graph closed-loop batches per batch size (SURVEY §8(d): >= 1000)")
     p.add_argument("--sustained-s", type=float, default=10.0, help="sustained pass length (s), batch of the config")
@@ -379,6 +383,17 @@ def main():
     # ---- queries (test stream), resident in HBM
     Qdev = torch.from_numpy(pool).cuda().reshape(a.warmup + a.steps, B, c["d"])
     h.reserve(B, NP, K)
+    xchg = a.exchange if world > 1 else "none"
+    if dry and xchg == "nccl":
+        xchg = "p2p"  # NCCL refuses two ranks on one device
+    if xchg == "p2p":  # inboxes IPC-mapped across the ranks: exchanges inside the kernels, no NCCL calls
+        if dry:
+            mine = h.p2p_export()
+            handles = all_objects(mine, world)
+            h.p2p_connect(handles)
+        else:
+            h.p2p_setup()
+        barrier(world)
     outs = [(torch.empty(B, K, dtype=torch.int64, device="cuda"), torch.empty(B, K, device="cuda"),
              torch.empty(B, NP, dtype=torch.uint8, device="cuda"), torch.empty(B, NP, dtype=torch.int32, device="cuda"))
             for _ in range(a.steps)]
@@ -387,7 +402,7 @@ def main():
     def step(Q, out):
         """one batch search: the collective NCCL search, or (dry run) the staged sharded search with the
         exchanges over gloo and the partial top-k merged by vlr_merge_partials"""
-        if not dry:
+        if xchg != "staged":
             h.search(Q, c["nprobe"], K, out=out, stream=stream)
             return
         ids, dd, miss, prb = h.search_staged(Q, c["nprobe"], K, lambda t: gather_stack(t, world), stream=stream)
@@ -575,8 +590,10 @@ def main():
                        "nprobe": c["nprobe"], "k": K, "batch": B, "alpha": c["alpha"], "hot_mass": c["hot_mass"],
                        "seed": a.seed,
                        "parallelism": (f"hot-list shards x{world}, centroid-sharded coarse stage, "
-                                       + ("exchanges over gloo through host memory, all ranks on ONE GPU (dry run)"
-                                          if dry else "NCCL all-gathers + GPU merge-select")) if world > 1
+                                       + {"p2p": "NVLink peer-exchange kernels (IPC-mapped inboxes, epoch flags)",
+                                          "nccl": "NCCL all-gathers + GPU merge-select",
+                                          "staged": "staged C-ABI, exchanges over gloo through host memory"}[xchg]
+                                       + (", all ranks on ONE GPU (dry run)" if dry else "")) if world > 1
                                       else "one GPU",
                        "l2": "inputs larger than L2 (index %.1f GB/GPU, %.2f GB scanned per batch)" % (
                            info["bytes_on_device"] / 1e9, float(step_bytes.mean()) / 1e9)},

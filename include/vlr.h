@@ -284,6 +284,27 @@ vlr_status vlr_search_stage3(vlr_index* idx, const float* d_queries, int32_t nq,
                              const void* d_x2_all, int64_t* d_ids, float* d_dist, uint8_t* d_miss,
                              int32_t* d_probes, void* stream);
 
+/*
+ * NVLink peer exchange: the three exchanges of the collective
+ * search (coarse stage 1, coarse stage 2, results) without NCCL calls. Each
+ * rank owns an inbox (device memory, IPC-exported); the producer kernels (K2
+ * stage 1, K3b local, K7) store their slabs straight into every rank's inbox
+ * over NVLink and the last CTA raises a per-rank flag (system-scope release);
+ * the consumer kernels (K2 stage 2, K3b merge, K8) wait for all flags
+ * (acquire, bounded: a missing peer sets status bit 2 -> VLR_ERR_CUDA, no
+ * hang). Searches after connect are COLLECTIVE on every rank and return the
+ * FINAL rows (shard-only handles too); batches up to the caps reserved before
+ * the export (vlr_reserve; k <= 32), no early release.
+ *  vlr_p2p_export(idx, out64): allocates the inbox, writes its 64-byte IPC handle.
+ *  vlr_p2p_connect(idx, handles): handles [world][64] in rank order (exchanged
+ *    by the caller, e.g. torch.distributed); opens every peer's inbox.
+ *  vlr_p2p_setup(idx): export + all-gather of the handles over the handle's
+ *    NCCL communicator + connect (collective).
+ */
+vlr_status vlr_p2p_export(vlr_index* idx, void* handle_out);
+vlr_status vlr_p2p_connect(vlr_index* idx, const void* handles);
+vlr_status vlr_p2p_setup(vlr_index* idx);
+
 /* Pre-size the per-handle workspace for batches up to (max_nq, max_nprobe, max_k)
  * so that later searches allocate nothing (required before graph capture). */
 vlr_status vlr_reserve(vlr_index* idx, int32_t max_nq, int32_t max_nprobe, int32_t max_k);

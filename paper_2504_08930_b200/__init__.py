@@ -23,7 +23,8 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "NONFINITE", 4: "UNKN
 # every symbol include/vlr.h declares (checked by tests/test_abi.py)
 EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_search_host_async",
            "vlr_search_release_async", "vlr_coarse_stage1", "vlr_coarse_stage2", "vlr_search_stage3",
-           "vlr_poll_ready", "vlr_wait_ready", "vlr_merge_ready", "vlr_reserve", "vlr_deal_owners", "vlr_update_hot",
+           "vlr_poll_ready", "vlr_wait_ready", "vlr_merge_ready", "vlr_p2p_export", "vlr_p2p_connect",
+           "vlr_p2p_setup", "vlr_reserve", "vlr_deal_owners", "vlr_update_hot",
            "vlr_merge_partials", "vlr_access_counts", "vlr_index_info", "vlr_index_owners", "vlr_set_profiling", "vlr_stage_times",
            "vlr_last_launch_count", "vlr_nccl_unique_id", "vlr_index_free", "vlr_last_error", "vlr_version"]
 
@@ -68,6 +69,9 @@ def lib():
             "vlr_search_host_async": [P, P, I32, I32, I32, P, P, P, P, P],
             "vlr_search_release_async": [P, P, I32, I32, I32, P, P, P, P, P, ctypes.c_uint32, P],
             "vlr_coarse_stage1": [P, P, I32, I32, P, P],
+            "vlr_p2p_export": [P, P],
+            "vlr_p2p_connect": [P, P],
+            "vlr_p2p_setup": [P],
             "vlr_coarse_stage2": [P, P, I32, I32, P, P, P],
             "vlr_search_stage3": [P, P, I32, I32, I32, P, P, P, P, P, P],
             "vlr_reserve": [P, I32, I32, I32],
@@ -357,6 +361,22 @@ class Index:
         """vlr_search_host_async on raw pinned host pointers (no synchronisation)."""
         _check(lib().vlr_search_host_async(self._h, q_ptr, nq, nprobe, k, ids_ptr, dist_ptr, miss_ptr, probes_ptr,
                                            _stream_handle(stream)))
+
+    def p2p_export(self) -> bytes:
+        """vlr_p2p_export: allocate this rank's inbox (after reserve) -> its 64-byte IPC handle."""
+        buf = ctypes.create_string_buffer(64)
+        _check(lib().vlr_p2p_export(self._h, ctypes.cast(buf, ctypes.c_void_p)))
+        return buf.raw
+
+    def p2p_connect(self, handles):
+        """vlr_p2p_connect: every rank's handle in rank order; searches become collective."""
+        blob = b"".join(bytes(hh) for hh in handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        _check(lib().vlr_p2p_connect(self._h, ctypes.cast(buf, ctypes.c_void_p)))
+
+    def p2p_setup(self):
+        """vlr_p2p_setup: export + NCCL all-gather of the handles + connect (collective)."""
+        _check(lib().vlr_p2p_setup(self._h))
 
     def reserve(self, max_nq: int, max_nprobe: int, max_k: int):
         _check(lib().vlr_reserve(self._h, max_nq, max_nprobe, max_k))

@@ -116,6 +116,7 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   Workspace& w = h->ws;
   const DeviceIndex& ix = h->ix;
   if (w.status && nq <= w.cap_nq && np <= w.cap_np && k <= w.cap_k) return VLR_OK;
+  if (h->p2p.on) return fail(VLR_ERR_UNSUPPORTED, "peer exchange connected: batch beyond the reserved workspace");
   const int cnq = std::max(nq, w.cap_nq), cnp = std::max(np, w.cap_np), ck = std::max(k, w.cap_k);
   int32_t status_keep = 0;
   if (w.h_status) status_keep = *w.h_status;
@@ -655,6 +656,15 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
 #undef LTRY
 }
 
+static void p2p_close(vlr_index* h) {
+  auto& L = h->p2p;
+  for (int g = 0; g < L.G; ++g)
+    if (L.peer[g] && L.peer[g] != L.inbox) cudaIpcCloseMemHandle(L.peer[g]);
+  if (L.inbox) cudaFree(L.inbox);
+  if (L.ctr) cudaFree(L.ctr);
+  L = vlr_index::PeerLink{};
+}
+
 void vlr_index_free(vlr_index* h) {
   if (!h) return;
   cudaSetDevice(h->ix.device);
@@ -668,6 +678,7 @@ void vlr_index_free(vlr_index* h) {
   if (h->lut_fork) cudaEventDestroy(h->lut_fork);
   if (h->lut_join) cudaEventDestroy(h->lut_join);
   if (h->lut_stream) cudaStreamDestroy(h->lut_stream);
+  p2p_close(h);
   free_ws(h->ws);
   free_index(h->ix);
   delete h;
@@ -685,13 +696,15 @@ vlr_status vlr_reserve(vlr_index* h, int32_t max_nq, int32_t max_nprobe, int32_t
 
 // device status word (mirrored to pinned host memory at the end of every search):
 // bit 0 = a non-finite query (qprep), bit 1 = the NEXT-4 merger's bounded wait
-// expired (those queries were neither merged nor released). Reported and cleared
-// by the first call that sees it.
+// expired (those queries were neither merged nor released), bit 2 = a peer
+// exchange wait expired. Reported and cleared by the first call that sees it.
 static vlr_status take_status(Workspace& w, const char* when) {
   const int32_t st = *w.h_status;
   if (!st) return VLR_OK;
   *w.h_status = 0;
   if (st & 1) return fail(VLR_ERR_NONFINITE, std::string("non-finite query") + when);
+  if (st & 4) return fail(VLR_ERR_CUDA, std::string("peer exchange: a rank's slab did not arrive within the bound "
+                                                    "(a peer stopped?); the results are invalid") + when);
   return fail(VLR_ERR_CUDA, std::string("release merger timed out waiting for the scan; the affected queries "
                                         "were not released") + when);
 }
@@ -700,6 +713,37 @@ static inline void rec(vlr_index* h, int i, cudaStream_t s) {
   // mode 1: every stage boundary; mode 2: only around the scan (events 5, 6)
   if (h->profiling == 1 || (h->profiling == 2 && (i == 5 || i == 6)))
     cudaEventRecord(h->ev[h->nsearch % vlr_index::kRing][i], s);
+}
+
+// ---------------------------------------------------------------- NVLink peer exchange plumbing
+// Exchange kinds: 0 = coarse stage 1 (x1, fp32 [nq][np] per rank), 1 = coarse
+// stage 2 (x2, 16-B entries [nq][np]), 2 = results (16-B entries [nq][k]).
+static PeerOut peer_out(const vlr_index* h, int kind) {
+  PeerOut o{};
+  const auto& L = h->p2p;
+  const size_t off = kind == 0 ? L.off_x1 : kind == 1 ? L.off_x2 : L.off_res;
+  for (int g = 0; g < L.G; ++g) {
+    o.base[g] = static_cast<char*>(L.peer[g]) + off;
+    o.flag[g] = reinterpret_cast<uint32_t*>(static_cast<char*>(L.peer[g]) + L.off_flags) + kind * L.G;
+  }
+  o.G = L.G;
+  o.rank = h->ix.rank;
+  o.epoch = L.epoch;
+  o.ctr = L.ctr + kind;
+  return o;
+}
+static PeerIn peer_in(vlr_index* h, int kind) {
+  PeerIn i{};
+  const auto& L = h->p2p;
+  i.flags = reinterpret_cast<const uint32_t*>(static_cast<char*>(L.inbox) + L.off_flags) + kind * L.G;
+  i.G = L.G;
+  i.epoch = L.epoch;
+  i.status = h->ws.status;
+  return i;
+}
+static void* inbox_region(vlr_index* h, int kind) {
+  const auto& L = h->p2p;
+  return static_cast<char*>(L.inbox) + (kind == 0 ? L.off_x1 : kind == 1 ? L.off_x2 : L.off_res);
 }
 
 // ---------------------------------------------------------------- the search pipeline
@@ -745,15 +789,20 @@ static vlr_status phase_a(vlr_index* h, Pipe& p, bool sharded, uint8_t* out_miss
   Workspace& w = h->ws;
   VLR_CUDA_TRY(cudaMemsetAsync(w.status, 0, sizeof(int32_t), p.s));
   rec(h, 0, p.s);
-  const int bt = filter_btile_rows(p.nq);
-  VLR_CUDA_TRY(launch_qprep(p.Q, p.nq, ix.d, ix.d8, w.qnorm, w.qsq, w.qf16, w.qinv, w.status, bt ? w.qf16t : nullptr,
-                            bt, p.s)); ++p.n;
   const int t_lo = sharded ? ix.c_lo / 128 : 0;
   const int t_hi = sharded ? (ix.c_hi + 127) / 128 : (ix.nlist + 127) / 128;
+  const int bt = filter_btile_rows(p.nq, t_hi - t_lo);
+  VLR_CUDA_TRY(launch_qprep(p.Q, p.nq, ix.d, ix.d8, w.qnorm, w.qsq, w.qf16, w.qinv, w.status, bt ? w.qf16t : nullptr,
+                            bt, p.s)); ++p.n;
   VLR_CUDA_TRY(launch_filter_tc(w.qf16, w.qinv, p.nq, ix, t_lo, t_hi, w.dt, w.gmin, bt ? w.qf16t : nullptr, p.s)); ++p.n;
   vlr_status st = lut_fork(h, p);
   if (st != VLR_OK) return st;
   rec(h, 1, p.s);
+  if (sharded && h->p2p.on) {
+    const PeerOut po = peer_out(h, 0);
+    VLR_CUDA_TRY(launch_select(ix, w, p.nq, p.np, filter_edot(ix.d), kSelStage1, p.s, &po)); ++p.n;
+    return VLR_OK;
+  }
   VLR_CUDA_TRY(launch_select(ix, w, p.nq, p.np, filter_edot(ix.d), sharded ? kSelStage1 : kSelFull, p.s)); ++p.n;
   if (sharded) return VLR_OK;
   rec(h, 2, p.s);
@@ -767,10 +816,19 @@ static vlr_status phase_b(vlr_index* h, Pipe& p) {
   NvtxRange nv(h, "vlr coarse stage 2 (K2s2, K3a, K3b local)");
   DeviceIndex& ix = h->ix;
   Workspace& w = h->ws;
-  VLR_CUDA_TRY(launch_select(ix, w, p.nq, p.np, filter_edot(ix.d), kSelStage2, p.s)); ++p.n;
+  const bool pp = h->p2p.on;
+  PeerIn pi;
+  PeerOut po;
+  Workspace wv = w;  // the gathered buffers are the inbox regions under the peer exchange
+  if (pp) {
+    pi = peer_in(h, 0);
+    po = peer_out(h, 1);
+    wv.x1_all = static_cast<float*>(inbox_region(h, 0));
+  }
+  VLR_CUDA_TRY(launch_select(ix, wv, p.nq, p.np, filter_edot(ix.d), kSelStage2, p.s, nullptr, pp ? &pi : nullptr)); ++p.n;
   rec(h, 2, p.s);
   VLR_CUDA_TRY(launch_exact(p.Q, ix, w, p.nq, p.s)); ++p.n;
-  VLR_CUDA_TRY(launch_refine(p.Q, ix, w, p.nq, p.np, nullptr, nullptr, kRefLocal, p.s)); ++p.n;
+  VLR_CUDA_TRY(launch_refine(p.Q, ix, w, p.nq, p.np, nullptr, nullptr, kRefLocal, p.s, pp ? &po : nullptr)); ++p.n;
   return VLR_OK;
 }
 
@@ -780,7 +838,14 @@ static vlr_status phase_c(vlr_index* h, Pipe& p, bool sharded, int64_t* out_ids,
   DeviceIndex& ix = h->ix;
   Workspace& w = h->ws;
   if (sharded) {
-    VLR_CUDA_TRY(launch_refine(p.Q, ix, w, p.nq, p.np, out_miss, out_probes, kRefMerge, p.s)); ++p.n;
+    if (h->p2p.on) {
+      const PeerIn pi = peer_in(h, 1);
+      Workspace wv = w;
+      wv.x2_all = static_cast<CoarseEntry*>(inbox_region(h, 1));
+      VLR_CUDA_TRY(launch_refine(p.Q, ix, wv, p.nq, p.np, out_miss, out_probes, kRefMerge, p.s, nullptr, &pi)); ++p.n;
+    } else {
+      VLR_CUDA_TRY(launch_refine(p.Q, ix, w, p.nq, p.np, out_miss, out_probes, kRefMerge, p.s)); ++p.n;
+    }
     rec(h, 3, p.s);
   }
   VLR_CUDA_TRY(launch_offsets(w, p.nq, p.np, p.s)); ++p.n;
@@ -802,7 +867,12 @@ static vlr_status phase_c(vlr_index* h, Pipe& p, bool sharded, int64_t* out_ids,
   VLR_CUDA_TRY(launch_scan(ix, w, p.nq, p.np, p.k, p.s, rel)); ++p.n;
   rec(h, 6, p.s);
   if (!rel) {  // release mode: the scan merged and released every row itself
-    VLR_CUDA_TRY(launch_rank_merge(ix, w, p.nq, p.np, p.k, out_ids, out_dist, packed ? w.send : nullptr, p.s)); ++p.n;
+    if (h->p2p.on && packed) {
+      const PeerOut po = peer_out(h, 2);
+      VLR_CUDA_TRY(launch_rank_merge(ix, w, p.nq, p.np, p.k, out_ids, out_dist, nullptr, p.s, &po)); ++p.n;
+    } else {
+      VLR_CUDA_TRY(launch_rank_merge(ix, w, p.nq, p.np, p.k, out_ids, out_dist, packed ? w.send : nullptr, p.s)); ++p.n;
+    }
   }
   rec(h, 7, p.s);
   return VLR_OK;
@@ -840,26 +910,38 @@ static vlr_status search_locked(vlr_index* h, const float* Q, int32_t nq, int32_
   Workspace& w = h->ws;
   st = take_status(w, " (detected in a previous search on this handle)");
   if (st != VLR_OK) return st;
-  const bool exchange = ix.nccl != nullptr;
-  if (exchange) {  // an error of an earlier asynchronous search on this communicator
+  const bool p2p = h->p2p.on;  // NVLink peer exchange: collective over the ranks' inboxes, no NCCL calls
+  const bool exchange = ix.nccl != nullptr || p2p;
+  if (ix.nccl && !p2p) {  // an error of an earlier asynchronous search on this communicator
     ncclResult_t as = ncclSuccess;
     if (ncclCommGetAsyncError(reinterpret_cast<ncclComm_t>(ix.nccl), &as) != ncclSuccess ||
         (as != ncclSuccess && as != ncclInProgress))
       return nccl_dead(h, std::string("NCCL asynchronous error of an earlier search: ") + ncclGetErrorString(as));
   }
-  const bool sharded = exchange && ix.coarse_sharded;
+  if (p2p) {
+    if (nq > h->p2p.cap_nq || np > h->p2p.cap_np || k > h->p2p.cap_k || k > kMaxK)
+      return fail(VLR_ERR_UNSUPPORTED, "peer exchange: batch beyond the caps reserved at vlr_p2p_export (or k > 32)");
+    if (rel) return fail(VLR_ERR_UNSUPPORTED, "peer exchange: early release is on the NCCL / shard-only paths");
+    if (++h->p2p.epoch == 0) ++h->p2p.epoch;  // every rank runs the same searches: epochs agree
+  }
+  const bool sharded = p2p || (ix.nccl && ix.coarse_sharded);
   Pipe p{Q, nq, np, k, s};
   if ((st = phase_a(h, p, sharded, out_miss, out_probes)) != VLR_OK) return st;
   if (exchange) VLR_CUDA_TRY(fault_stall(s));
-  if (sharded) {
+  if (sharded && !p2p) {
     if ((st = nccl_allgather(h, w.x1, w.x1_all, sizeof(float) * nq * np, s, "coarse stage 1")) != VLR_OK) return st;
     if ((st = phase_b(h, p)) != VLR_OK) return st;
     if ((st = nccl_allgather(h, w.x2, w.x2_all, sizeof(CoarseEntry) * nq * np, s, "coarse stage 2")) != VLR_OK)
       return st;
+  } else if (p2p) {
+    if ((st = phase_b(h, p)) != VLR_OK) return st;
   }
   if ((st = phase_c(h, p, sharded, out_ids, out_dist, out_miss, out_probes, rel, exchange && !rel)) != VLR_OK)
     return st;
-  if (exchange && !rel) {  // release mode: each rank releases its partial rows; vlr_merge_ready merges them
+  if (p2p) {
+    const PeerIn pi = peer_in(h, 2);
+    VLR_CUDA_TRY(launch_merge_packed(inbox_region(h, 2), h->p2p.G, nq, k, out_ids, out_dist, s, &pi)); ++p.n;
+  } else if (exchange && !rel) {  // release mode: each rank releases its partial rows; vlr_merge_ready merges them
     if ((st = nccl_allgather(h, w.send, w.recv, (size_t)nq * k * sizeof(Packed), s, "results")) != VLR_OK) return st;
     VLR_CUDA_TRY(launch_merge_packed(w.recv, ix.world, nq, k, out_ids, out_dist, s)); ++p.n;
   }
@@ -1169,6 +1251,92 @@ vlr_status vlr_search_stage3(vlr_index* h, const float* Q, int32_t nq, int32_t n
   h->launches += p.n;
   if (h->profiling) h->prof_mode[h->nsearch++ % vlr_index::kRing] = h->profiling;
   return VLR_OK;
+}
+
+// ---------------------------------------------------------------- NVLink peer exchange (setup)
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+vlr_status vlr_p2p_export(vlr_index* h, void* handle_out) {
+  if (!h || !handle_out) return fail(VLR_ERR_INVALID_ARG, "vlr_p2p_export: null argument");
+  std::lock_guard<std::mutex> lock(h->mu);
+  const DeviceIndex& ix = h->ix;
+  if (ix.world < 2 || ix.world > kMaxWorld) return fail(VLR_ERR_UNSUPPORTED, "peer exchange needs 2 <= world <= 8");
+  Workspace& w = h->ws;
+  if (!w.status) return fail(VLR_ERR_INVALID_ARG, "vlr_p2p_export: call vlr_reserve first (the inbox is sized by it)");
+  VLR_CUDA_TRY(cudaSetDevice(ix.device));
+  p2p_close(h);
+  auto& L = h->p2p;
+  L.G = ix.world;
+  L.cap_nq = w.cap_nq;
+  L.cap_np = w.cap_np;
+  L.cap_k = std::min(w.cap_k, kMaxK);
+  const size_t G = (size_t)L.G, nq = (size_t)L.cap_nq, np = (size_t)L.cap_np, k = (size_t)L.cap_k;
+  L.off_x1 = 0;
+  L.off_x2 = align256(L.off_x1 + G * nq * np * sizeof(float));
+  L.off_res = align256(L.off_x2 + G * nq * np * sizeof(CoarseEntry));
+  L.off_flags = align256(L.off_res + G * nq * k * sizeof(Packed));
+  L.bytes = align256(L.off_flags + 3 * G * sizeof(uint32_t));
+  VLR_CUDA_TRY(cudaMalloc(&L.inbox, L.bytes));
+  VLR_CUDA_TRY(cudaMemset(L.inbox, 0, L.bytes));
+  VLR_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&L.ctr), 3 * sizeof(int)));
+  VLR_CUDA_TRY(cudaMemset(L.ctr, 0, 3 * sizeof(int)));
+  cudaIpcMemHandle_t mh;
+  VLR_CUDA_TRY(cudaIpcGetMemHandle(&mh, L.inbox));
+  static_assert(sizeof(mh) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle_out, &mh, sizeof(mh));
+  return VLR_OK;
+}
+
+vlr_status vlr_p2p_connect(vlr_index* h, const void* handles) {
+  if (!h || !handles) return fail(VLR_ERR_INVALID_ARG, "vlr_p2p_connect: null argument");
+  std::lock_guard<std::mutex> lock(h->mu);
+  auto& L = h->p2p;
+  if (!L.inbox) return fail(VLR_ERR_INVALID_ARG, "vlr_p2p_connect: vlr_p2p_export first");
+  VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
+  for (int g = 0; g < L.G; ++g) {
+    if (g == h->ix.rank) {
+      L.peer[g] = L.inbox;
+      continue;
+    }
+    cudaIpcMemHandle_t mh;
+    std::memcpy(&mh, static_cast<const char*>(handles) + 64 * g, 64);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (int r = 0; r < g; ++r)
+        if (L.peer[r] && L.peer[r] != L.inbox) cudaIpcCloseMemHandle(L.peer[r]);
+      std::fill(L.peer, L.peer + kMaxWorld, nullptr);
+      return fail(VLR_ERR_CUDA, std::string("cudaIpcOpenMemHandle of rank ") + std::to_string(g) + ": " +
+                                     cudaGetErrorString(e));
+    }
+    L.peer[g] = p;
+  }
+  L.on = true;
+  L.epoch = 0;
+  return VLR_OK;
+}
+
+vlr_status vlr_p2p_setup(vlr_index* h) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  if (!h->ix.nccl) return fail(VLR_ERR_INVALID_ARG, "vlr_p2p_setup needs a communicator (else export / connect)");
+  std::vector<char> mine(64), all(64 * (size_t)h->ix.world);
+  vlr_status st = vlr_p2p_export(h, mine.data());
+  if (st != VLR_OK) return st;
+  // the handles travel over the communicator: a device copy, one all-gather
+  char* d = nullptr;
+  VLR_CUDA_TRY(cudaMalloc(&d, all.size() + 64));
+  VLR_CUDA_TRY(cudaMemcpy(d, mine.data(), 64, cudaMemcpyHostToDevice));
+  cudaStream_t s = nullptr;
+  VLR_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  st = nccl_allgather(h, d, d + 64, 64, s, "peer-exchange handles");
+  if (st == VLR_OK) st = wait_stream(h, s);
+  cudaStreamDestroy(s);
+  if (st == VLR_OK) {
+    VLR_CUDA_TRY(cudaMemcpy(all.data(), d + 64, all.size(), cudaMemcpyDeviceToHost));
+  }
+  cudaFree(d);
+  if (st != VLR_OK) return st;
+  return vlr_p2p_connect(h, all.data());
 }
 
 vlr_status vlr_merge_partials(const int64_t* part_ids, const float* part_dist, int32_t n_shards, int32_t nq, int32_t k,

@@ -14,6 +14,7 @@
 //            sum in dimension order); the filter then holds -2<q, c>
 //            (||c||^2 = 0 in K1), the same key scaled by 2.
 #include <cfloat>
+#include <cstdio>
 
 #include <cuda_fp16.h>
 
@@ -192,7 +193,8 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
                                                         float e_dot, float e_abs, const float* __restrict__ qinv,
                                                         float c_inv, const float* __restrict__ x1_all,
                                                         float* __restrict__ x1, int32_t* __restrict__ cand,
-                                                        int32_t* __restrict__ ncand, float* __restrict__ bound_out) {
+                                                        int32_t* __restrict__ ncand, float* __restrict__ bound_out,
+                                                        PeerOut pout, PeerIn pin) {
   extern __shared__ unsigned skeys[];
   __shared__ unsigned s_cnt;
   const int q = blockIdx.x;
@@ -202,6 +204,7 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
   const int g0 = lo / 32, ng = (hi + 31) / 32 - g0;  // this rank's groups
   float theta = CUDART_INF_F;
   if constexpr (MODE == kSelStage2) {
+    peer_wait(pin);  // NVLink peer exchange: every rank's x1 slab has landed in this rank's inbox
     const int n = world * np;  // <= kSelMaxGroups (checked at launch)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int r = i / np, j = i - r * np;
@@ -217,14 +220,20 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
     }
   }
   if constexpr (MODE == kSelStage1) {
-    // x1 row: the np smallest group minima of this range as a multiset
+    // x1 row: the np smallest group minima of this range as a multiset (P2P: into every rank's inbox)
     float* out = x1 + (size_t)q * np;
+    const long long slab = (long long)nq * np;
+    auto put = [&](int i, float v) {
+      if (pout.G) peer_store(pout, slab, (long long)q * np + i, v);
+      else out[i] = v;
+    };
     if (threadIdx.x == 0) s_cnt = 0u;
     __syncthreads();
     // fewer than np groups: all of them, +inf padding (theta' stays exact). More than kSelMaxGroups: the
     // first np (any np genuine group minima give an np-th smallest >= theta~, a valid but looser bound)
     if (ng < np || ng > kSelMaxGroups) {
-      for (int i = threadIdx.x; i < np; i += blockDim.x) out[i] = i < ng ? gmin[(size_t)q * ngL + g0 + i] : CUDART_INF_F;
+      for (int i = threadIdx.x; i < np; i += blockDim.x) put(i, i < ng ? gmin[(size_t)q * ngL + g0 + i] : CUDART_INF_F);
+      peer_signal(pout);
       return;
     }
     for (int i0 = 0; i0 < ng; i0 += blockDim.x) {
@@ -235,10 +244,11 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
       unsigned base = 0u;
       if (lane == 0) base = atomicAdd(&s_cnt, (unsigned)__popc(km));
       base = __shfl_sync(kFull, base, 0);
-      if (keep) out[base + __popc(km & ((1u << lane) - 1u))] = fkey_inv(skeys[i]);
+      if (keep) put(base + __popc(km & ((1u << lane) - 1u)), fkey_inv(skeys[i]));
     }
     __syncthreads();
-    for (int i = (int)s_cnt + threadIdx.x; i < np; i += blockDim.x) out[i] = theta;  // fewer than np are < theta
+    for (int i = (int)s_cnt + threadIdx.x; i < np; i += blockDim.x) put(i, theta);  // fewer than np are < theta
+    peer_signal(pout);
     return;
   } else {
     const float qn = qnorm[q];
@@ -333,7 +343,9 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
 
 // mode: kSelFull (single GPU / replicated coarse), kSelStage1 (-> ws.x1), kSelStage2 (ws.x1_all -> candidates)
 cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float e_dot, int mode,
-                          cudaStream_t s) {
+                          cudaStream_t s, const PeerOut* po, const PeerIn* pi) {
+  const PeerOut pout = po ? *po : PeerOut{};
+  const PeerIn pin = pi ? *pi : PeerIn{};
   if (nq <= 0) return cudaSuccess;
   const int lo = mode == kSelFull ? 0 : ix.c_lo, hi = mode == kSelFull ? ix.nlist : ix.c_hi;
   const int ng = (hi + 31) / 32 - lo / 32;
@@ -349,7 +361,7 @@ cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, in
   if (e != cudaSuccess) return e;
   const float e_abs = sqrtf((float)ix.d) * 2.9802322e-8f * 1.00049f * 1.0001f;  // sqrt(d) 2^-25 (1 + 2^-11), rounded up
 #define VLR_SEL_ARGS ws.dt, ws.gmin, ix.nlist, lo, hi, np, ix.world, ws.qnorm, ix.cmax, e_dot, e_abs, ws.qinv, \
-                     ix.c_inv, ws.x1_all, ws.x1, ws.cand, ws.ncand, ws.bound
+                     ix.c_inv, ws.x1_all, ws.x1, ws.cand, ws.ncand, ws.bound, pout, pin
   if (mode == kSelStage1) k_select<kSelStage1><<<nq, kSelThreads, sm, s>>>(VLR_SEL_ARGS);
   else if (mode == kSelStage2) k_select<kSelStage2><<<nq, kSelThreads, sm, s>>>(VLR_SEL_ARGS);
   else k_select<kSelFull><<<nq, kSelThreads, sm, s>>>(VLR_SEL_ARGS);
@@ -618,21 +630,36 @@ static cudaError_t launch_exact_t(const float* Q, const DeviceIndex& ix, const W
 
 cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  static int cfg = -1;
-  if (cfg < 0) {
+  // VLR_EXACT_CFG="S,W[,CH]" (stages, warps, chains per lane) overrides the product choice: (3, 4, 1) on one
+  // GPU (~200 candidates per query: throughput regime, profiles/k3a_sweep_r01.txt), (16, 1, 1) with the
+  // sharded coarse stage at world >= 4 (~25 candidates per query and rank: one warp per query, latency
+  // regime -> half a candidate row of loads in flight per warp)
+  static int env_s = -1, env_w = 0, env_c = 1;
+  if (env_s < 0) {
+    env_s = 0;
     const char* e = getenv("VLR_EXACT_CFG");
-    cfg = 34;
-    if (e && e[0] && e[1] == ',' && e[2]) cfg = (e[0] - '0') * 10 + (e[2] - '0');
+    if (e && e[0]) {
+      int s_ = 0, w_ = 0, c_ = 1;
+      const int n = sscanf(e, "%d,%d,%d", &s_, &w_, &c_);
+      if (n >= 2) { env_s = s_; env_w = w_; env_c = n >= 3 ? c_ : 1; }
+    }
   }
+  int S = 3, W = 4, CH = 1;
+  if (ix.world >= 4 && (ix.nccl || ix.shard_only) && ix.d <= 1024) { S = 16; W = 1; }
+  if (env_s > 0) { S = env_s; W = env_w; CH = env_c; }
+  const int cfg = S * 100 + W * 10 + CH;
   switch (cfg) {
-    case 24: return launch_exact_t<2, 4>(Q, ix, ws, nq, s);
-    case 44: return launch_exact_t<4, 4>(Q, ix, ws, nq, s);
-    case 28: return launch_exact_t<2, 8>(Q, ix, ws, nq, s);
-    case 22: return launch_exact_t<2, 2>(Q, ix, ws, nq, s);
-    case 42: return launch_exact_t<4, 2>(Q, ix, ws, nq, s);
-    case 32: return launch_exact_t<3, 2, 2>(Q, ix, ws, nq, s);   // "3,2" two chains per lane, 2 warps
-    case 36: return launch_exact_t<3, 4, 2>(Q, ix, ws, nq, s);   // "3,6": two chains per lane, 4 warps
-    case 52: return launch_exact_t<5, 2, 2>(Q, ix, ws, nq, s);   // "5,2": two chains, 5 stages, 2 warps
+    case 241: return launch_exact_t<2, 4>(Q, ix, ws, nq, s);
+    case 441: return launch_exact_t<4, 4>(Q, ix, ws, nq, s);
+    case 281: return launch_exact_t<2, 8>(Q, ix, ws, nq, s);
+    case 221: return launch_exact_t<2, 2>(Q, ix, ws, nq, s);
+    case 421: return launch_exact_t<4, 2>(Q, ix, ws, nq, s);
+    case 322: return launch_exact_t<3, 2, 2>(Q, ix, ws, nq, s);
+    case 342: return launch_exact_t<3, 4, 2>(Q, ix, ws, nq, s);
+    case 522: return launch_exact_t<5, 2, 2>(Q, ix, ws, nq, s);
+    case 1611: return launch_exact_t<16, 1>(Q, ix, ws, nq, s);
+    case 3211: return launch_exact_t<32, 1>(Q, ix, ws, nq, s);
+    case 821: return launch_exact_t<8, 2>(Q, ix, ws, nq, s);
     default: return launch_exact_t<kExactStages, kExactWarps>(Q, ix, ws, nq, s);
   }
 }
@@ -664,7 +691,7 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
                                                            int32_t* __restrict__ probes_out,
                                                            int32_t* __restrict__ plocal,
                                                            int64_t* __restrict__ item_local,
-                                                           int64_t* __restrict__ qtot) {
+                                                           int64_t* __restrict__ qtot, PeerOut pout, PeerIn pin) {
   extern __shared__ __align__(16) unsigned char sm[];
   float* tiles = reinterpret_cast<float*>(sm);                        // [kRescanWarps][2][32][32]
   double* key = reinterpret_cast<double*>(tiles + kRescanWarps * 2048);  // [scap]
@@ -677,6 +704,7 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int nbest = 0;
   if constexpr (MODE == kRefMerge) {
+    peer_wait(pin);  // NVLink peer exchange: every rank's x2 slab has landed in this rank's inbox
     // G sorted lists of np entries; padding (+inf, -1) is skipped
     const int src_len = world * np;
     for (int pos = 0; pos < src_len; pos += kRefineChunk) {
@@ -778,8 +806,10 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
       e.D = p < nbest ? key[p] : CUDART_INF;
       e.l = p < nbest ? id[p] : -1;
       e.pad = 0;
-      x2[(size_t)q * np + p] = e;
+      if (pout.G) peer_store(pout, (long long)nq * np, (long long)q * np + p, e);
+      else x2[(size_t)q * np + p] = e;
     }
+    peer_signal(pout);
     return;
   } else {
     // ---- router epilogue (K4 fused): mask, owned work items
@@ -850,8 +880,10 @@ static const void* refine_fn(int mode) {
 
 // mode kRefRoute / kRefLocal (-> ws.x2) / kRefMerge (ws.x2_all -> probes, route)
 cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, int np, uint8_t* miss,
-                          int32_t* probes_out, int mode, cudaStream_t s) {
+                          int32_t* probes_out, int mode, cudaStream_t s, const PeerOut* po, const PeerIn* pi) {
   if (nq <= 0) return cudaSuccess;
+  const PeerOut pout = po ? *po : PeerOut{};
+  const PeerIn pin = pi ? *pi : PeerIn{};
   // kRefMerge sorts chunks of up to kRefineChunk entries with the running np best, as the other modes
   const int scap = sort_cap(np);
   const size_t sm = refine_smem(ix.d, scap);
@@ -864,7 +896,7 @@ cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace
                   (void*)&ws.dt, (void*)&ws.cand, (void*)&ws.ncand, (void*)&ws.bound, (void*)&ws.exact,
                   (void*)&ws.x2, (void*)&ws.x2_all, (void*)&ws.probes, (void*)&ws.term1, (void*)&ix.rank,
                   (void*)&ix.owner, (void*)&ix.local, (void*)&ix.gbase, (void*)&miss, (void*)&probes_out,
-                  (void*)&ws.plocal, (void*)&ws.item_local, (void*)&ws.qtot};
+                  (void*)&ws.plocal, (void*)&ws.item_local, (void*)&ws.qtot, (void*)&pout, (void*)&pin};
   return cudaLaunchKernel(fn, dim3(nq), dim3(kRefineThreads), args, sm, s);
 }
 

@@ -701,9 +701,26 @@ static int persistent_env_get() {
   return v;
 }
 
-int filter_btile_rows(int nq) {
+static int num_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+// query rows per CTA (nN) of the one-CTA kernel for nq <= 256: the batch rounded up to 16, halved while the
+// grid (tiles x query tiles) has fewer than 2 CTAs per SM -- a rank of the sharded coarse stage filters only
+// 1/world of the tiles (C4, world 8: 64 tiles -> nN 64, 256 CTAs)
+static int filter_nn(int nq, int tiles) {
+  int nN = ((nq + 15) / 16) * 16;
+  const int sms = num_sms();
+  while (nN > 32 && (long long)tiles * ((nq + nN - 1) / nN) < 2LL * sms) nN = ((nN / 2 + 15) / 16) * 16;
+  return nN;
+}
+
+int filter_btile_rows(int nq, int tiles) {
   if (!btiled_env() || pair_env_get() || persistent_env_get()) return 0;
-  return nq <= 256 ? ((nq + 15) / 16) * 16 : 512;  // = nN * nacc of the one-CTA kernel
+  return nq <= 256 ? filter_nn(nq, tiles) : 512;  // = nN * nacc of the one-CTA kernel
 }
 
 cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, int t_lo, int t_hi,
@@ -714,7 +731,7 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   int nacc, nN;
   if (nq <= 256) {
     nacc = 1;
-    nN = ((nq + 15) / 16) * 16;
+    nN = filter_nn(nq, t_hi - t_lo);
   } else {
     nacc = 2;
     nN = 256;

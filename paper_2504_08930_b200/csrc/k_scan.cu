@@ -306,7 +306,7 @@ template <bool CG>
 __device__ __forceinline__ void merge_query(
     int q, int k, int n_cta, long long WL, long long WH, long long zoff, long long S, long long E,
     const float* pdist, const int64_t* pid, int64_t* out_ids, float* out_dist, Packed* __restrict__ packed,
-    MergeSmem& sm) {
+    MergeSmem& sm, const PeerOut* pout = nullptr, int nq = 0) {
   float* s_d = sm.s_d;
   long long* s_id = sm.s_id;
   float& s_t0 = sm.s_t0;
@@ -447,7 +447,13 @@ __device__ __forceinline__ void merge_query(
     thr = __shfl_sync(kFull, bd, k - 1);
   }
   if (lane < k) {
-    if (packed) {
+    if (pout && pout->G) {  // NVLink peer exchange: this rank's partial row into every rank's inbox
+      Packed p;
+      p.d = bd;
+      p.pad = 0;
+      p.id = bid;
+      peer_store(*pout, (long long)nq * k, (long long)q * k + lane, p);
+    } else if (packed) {
       Packed p;
       p.d = bd;
       p.pad = 0;
@@ -464,11 +470,21 @@ __device__ __forceinline__ void merge_query(
 __global__ void __launch_bounds__(kMergeMaxWarps * 32) k_rank_merge(
     int nq, int np, int k, int n_cta, const int64_t* __restrict__ item_off, const float* __restrict__ pdist,
     const int64_t* __restrict__ pid, int64_t* __restrict__ out_ids, float* __restrict__ out_dist,
-    Packed* __restrict__ packed) {
+    Packed* __restrict__ packed, PeerOut pout) {
   __shared__ MergeSmem sm;
   const int q = blockIdx.x;
   merge_query<false>(q, k, n_cta, 0, item_off[(long long)nq * np], 0, item_off[(long long)q * np],
-                     item_off[(long long)(q + 1) * np], pdist, pid, out_ids, out_dist, packed, sm);
+                     item_off[(long long)(q + 1) * np], pdist, pid, out_ids, out_dist, packed, sm, &pout, nq);
+  // merge_query returns warps > 0 early (after phase B): the CTA's arrival is by warp 0
+  if (pout.G && (threadIdx.x >> 5) == 0) {
+    __threadfence_system();
+    __syncwarp();
+    if (threadIdx.x == 0 && (unsigned)atomicAdd(pout.ctr, 1) == gridDim.x - 1) {
+      *pout.ctr = 0;
+      __threadfence_system();
+      for (int g = 0; g < pout.G; ++g) st_release_sys_u32(pout.flag[g] + pout.rank, pout.epoch);
+    }
+  }
 }
 
 template <int MP, int NB, int EXP, bool DUMP = false>
@@ -887,7 +903,8 @@ static cudaError_t launch_scan_k(const DeviceIndex& ix, const ScanArgs& a, int n
 }
 
 cudaError_t launch_rank_merge(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, int64_t* out_ids,
-                              float* out_dist, void* out_packed, cudaStream_t s) {
+                              float* out_dist, void* out_packed, cudaStream_t s, const PeerOut* po) {
+  const PeerOut pout = po ? *po : PeerOut{};
   (void)ix;
   if (nq <= 0) return cudaSuccess;
   // expected lists per query: (scan CTAs spanned) x warps
@@ -896,7 +913,7 @@ cudaError_t launch_rank_merge(const DeviceIndex& ix, const Workspace& ws, int nq
   while (nw < kMergeMaxWarps && (long long)nw * 128 < lists) nw <<= 1;
   if ((long long)ws.n_cta * kScanWarps > kMergeMaxLists) return cudaErrorInvalidConfiguration;
   k_rank_merge<<<nq, nw * 32, 0, s>>>(nq, np, k, ws.n_cta, ws.item_off, ws.pdist, ws.pid, out_ids, out_dist,
-                                      reinterpret_cast<Packed*>(out_packed));
+                                      reinterpret_cast<Packed*>(out_packed), pout);
   return cudaGetLastError();
 }
 
@@ -1072,7 +1089,8 @@ cudaError_t launch_scan_large(const DeviceIndex& ix, const Workspace& ws, int nq
 // parts [S][nq][k]: top-k of the union per query.
 __global__ void k_merge_parts(int n_shards, int nq, int k, const Packed* __restrict__ packed,
                               const int64_t* __restrict__ pids, const float* __restrict__ pdist,
-                              int64_t* __restrict__ out_ids, float* __restrict__ out_dist) {
+                              int64_t* __restrict__ out_ids, float* __restrict__ out_dist, PeerIn pin) {
+  peer_wait(pin);  // NVLink peer exchange: every rank's partial rows have landed in this rank's inbox
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
@@ -1157,14 +1175,15 @@ static cudaError_t launch_merge_large(const Packed* packed, const int64_t* pids,
 }
 
 cudaError_t launch_merge_packed(const void* parts, int n_shards, int nq, int k, int64_t* out_ids, float* out_dist,
-                                cudaStream_t s) {
+                                cudaStream_t s, const PeerIn* pi) {
+  const PeerIn pin = pi ? *pi : PeerIn{};
   if (nq <= 0) return cudaSuccess;
   if (k > kMaxK)
     return launch_merge_large(reinterpret_cast<const Packed*>(parts), nullptr, nullptr, n_shards, nq, k, out_ids,
                               out_dist, s);
   const int wpb = 8;
   k_merge_parts<<<(nq + wpb - 1) / wpb, wpb * 32, 0, s>>>(n_shards, nq, k, reinterpret_cast<const Packed*>(parts),
-                                                          nullptr, nullptr, out_ids, out_dist);
+                                                          nullptr, nullptr, out_ids, out_dist, pin);
   return cudaGetLastError();
 }
 
@@ -1174,7 +1193,7 @@ cudaError_t launch_merge_split(const int64_t* part_ids, const float* part_dist, 
   if (k > kMaxK) return launch_merge_large(nullptr, part_ids, part_dist, n_shards, nq, k, out_ids, out_dist, s);
   const int wpb = 8;
   k_merge_parts<<<(nq + wpb - 1) / wpb, wpb * 32, 0, s>>>(n_shards, nq, k, nullptr, part_ids, part_dist, out_ids,
-                                                          out_dist);
+                                                          out_dist, PeerIn{});
   return cudaGetLastError();
 }
 

@@ -170,6 +170,77 @@ __device__ __forceinline__ float fkey_inv(unsigned k) {
   return __uint_as_float(u);
 }
 
+// ---------------------------------------------------------------- NVLink peer exchange
+// ("P2P exchange"): a producer kernel stores its slab of an
+// exchanged buffer straight into every rank's inbox (IPC-mapped peer device
+// memory over NVLink; the own inbox for the own rank), and its LAST CTA to
+// finish raises flag[kind][rank] = epoch in every rank's inbox (system-scope
+// release after a system fence); a consumer kernel's first thread waits until
+// all world flags of its kind carry the search's epoch (acquire), bounded.
+constexpr int kMaxWorld = 8;
+struct PeerOut {
+  void* base[kMaxWorld];       // per rank: the inbox region of this exchange kind ([world][slab] layout)
+  uint32_t* flag[kMaxWorld];   // per rank: that rank's flags of this kind ([world], written at [my rank])
+  int G, rank;                 // G = 0: no peer exchange (write the local buffer)
+  uint32_t epoch;
+  int* ctr;                    // CTA-completion counter (local, 0 between launches)
+};
+struct PeerIn {
+  const uint32_t* flags;       // own inbox flags of this kind ([world])
+  int G;                       // 0: nothing to wait for
+  uint32_t epoch;
+  int32_t* status;             // bit 2 (value 4): a peer did not arrive within the bound
+};
+
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// element o of this rank's slab (slab elements per rank) into every rank's inbox
+template <class T>
+__device__ __forceinline__ void peer_store(const PeerOut& p, long long slab, long long o, const T& v) {
+  for (int g = 0; g < p.G; ++g) reinterpret_cast<T*>(p.base[g])[(long long)p.rank * slab + o] = v;
+}
+
+// every thread of every CTA calls it once, after its stores
+__device__ __forceinline__ void peer_signal(const PeerOut& p) {
+  if (p.G == 0) return;
+  __threadfence_system();  // each thread's own peer stores, before the CTA barrier
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned total = gridDim.x * gridDim.y * gridDim.z;
+    if ((unsigned)atomicAdd(p.ctr, 1) == total - 1) {  // the last CTA: every CTA's stores are fenced
+      *p.ctr = 0;
+      __threadfence_system();
+      for (int g = 0; g < p.G; ++g) st_release_sys_u32(p.flag[g] + p.rank, p.epoch);
+    }
+  }
+}
+
+// prologue of a consumer kernel: all ranks' slabs of this kind have arrived
+__device__ __forceinline__ void peer_wait(const PeerIn& w) {
+  if (w.G == 0) return;
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer_ns();
+    for (int r = 0; r < w.G; ++r) {
+      for (uint32_t spin = 0; ld_acquire_sys_u32(w.flags + r) != w.epoch; ++spin) {
+        __nanosleep(64);
+        if ((spin & 1023u) == 1023u && globaltimer_ns() - t0 > 4000000000ull) {  // bounded: never hang
+          atomicOr(w.status, 4);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // 16-byte packed result entry used by the cross-GPU exchange
 struct __align__(16) Packed {
   float d;

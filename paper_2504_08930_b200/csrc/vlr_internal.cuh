@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "vlr.h"
+#include "vlr_device.cuh"
 
 namespace vlr {
 
@@ -159,6 +160,16 @@ struct vlr_index {
   int64_t nsearch = 0;       // searches recorded while profiling
   int launches = 0;
   bool dead = false;  // NCCL failure
+  // NVLink peer exchange (vlr_p2p_*): every rank's inbox IPC-mapped here
+  struct PeerLink {
+    bool on = false;
+    int cap_nq = 0, cap_np = 0, cap_k = 0, G = 0;
+    void* inbox = nullptr;                    // own inbox (cudaMalloc base, exported with cudaIpcGetMemHandle)
+    size_t bytes = 0, off_x1 = 0, off_x2 = 0, off_res = 0, off_flags = 0;
+    void* peer[vlr::kMaxWorld] = {};          // every rank's inbox base (own = inbox; others IPC-opened)
+    int* ctr = nullptr;                       // [3] CTA-completion counters
+    uint32_t epoch = 0;
+  } p2p;
   std::mutex mu;  // held while a search is enqueued and while vlr_update_hot swaps the residency
   cudaStream_t rel_stream = nullptr;  // NEXT-4 merger stream + fork/join events (created on first use)
   cudaEvent_t rel_fork = nullptr, rel_join = nullptr;
@@ -188,7 +199,7 @@ cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, fl
                          int32_t* status, uint16_t* qf16t, int QT, cudaStream_t s);
 // K1's query tile (rows of B per CTA): the pre-tiled operand written by qprep uses it; 0 = K1 reads the
 // row-major fp16 queries through a tensor map (VLR_FILTER_BTILED=0, or the pair / persistent kernels)
-int filter_btile_rows(int nq);
+int filter_btile_rows(int nq, int tiles);
 // K1 over centroid tiles [t_lo, t_hi) (128 centroids each): dt columns and gmin groups of those tiles
 cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, const DeviceIndex& ix, int t_lo, int t_hi,
                              float* dt, float* gmin, const uint16_t* Qt, cudaStream_t s);
@@ -196,10 +207,11 @@ cudaError_t launch_round_f16(const float* src, int rows, int d, int d8, float sc
 cudaError_t make_tmap_2d(void* map, const uint16_t* base, int rows, int cols, int box_rows, bool swizzle);
 cudaError_t launch_tile_f16(const DeviceIndex& ix, cudaStream_t s);
 cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, int np, float e_dot, int mode,
-                          cudaStream_t s);
+                          cudaStream_t s, const PeerOut* po = nullptr, const PeerIn* pi = nullptr);
 cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s);
 cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, int np, uint8_t* miss,
-                          int32_t* probes_out, int mode, cudaStream_t s);
+                          int32_t* probes_out, int mode, cudaStream_t s, const PeerOut* po = nullptr,
+                          const PeerIn* pi = nullptr);
 // stage 3..4
 cudaError_t launch_offsets(const Workspace& ws, int nq, int np, cudaStream_t s);
 cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s);
@@ -218,11 +230,12 @@ struct Release {               // NEXT-4 early per-query release (vlr_search_rel
 cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s,
                         const Release* rel = nullptr);
 cudaError_t launch_rank_merge(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k,
-                              int64_t* out_ids, float* out_dist, void* out_packed, cudaStream_t s);
+                              int64_t* out_ids, float* out_dist, void* out_packed, cudaStream_t s,
+                              const PeerOut* po = nullptr);
 cudaError_t launch_scan_large(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, int64_t* out_ids,
                               float* out_dist, void* out_packed, cudaStream_t s);
 cudaError_t launch_merge_packed(const void* parts, int n_shards, int nq, int k, int64_t* out_ids, float* out_dist,
-                                cudaStream_t s);
+                                cudaStream_t s, const PeerIn* pi = nullptr);
 cudaError_t launch_merge_split(const int64_t* part_ids, const float* part_dist, int n_shards, int nq, int k,
                                int64_t* out_ids, float* out_dist, cudaStream_t s);
 

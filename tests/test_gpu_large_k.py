@@ -101,7 +101,7 @@ def test_large_k_limits(big_nlist):
     h.close()
 
 
-@pytest.mark.parametrize("d,m,nbits", [(768, 384, 4), (768, 320, 4), (384, 192, 8), (320, 160, 8)])
+@pytest.mark.parametrize("d,m,nbits", [(768, 384, 4), (640, 320, 4), (384, 192, 8), (320, 160, 8)])
 def test_wide_pq_parity(d, m, nbits):
     """the paper's inferred index format PQ384x4 at 768-d (~205 B/vector, SURVEY reading A4; pair
     slots: 192 bytes) and the other widened scan instantiations (160 / 192 byte slots)"""

@@ -85,3 +85,67 @@ def test_two_process_staged_search_one_gpu():
     for rank, bit, errs in res:
         assert not errs, (rank, errs)
         assert bit, f"rank {rank}: staged two-process result differs from the single-GPU search"
+
+
+def _p2p_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        import datagen
+        import oracle
+        import paper_2504_08930_b200 as vlr
+        from parity import check
+        c = datagen.CONFIGS["C1"]
+        ix = datagen.make_index(c["N"], c["d"], c["nlist"], c["m"])
+        Q = datagen.make_queries(c["N"], c["d"], c["nlist"], c["batch"], stream=2, alpha=c["alpha"])
+        Qd = torch.from_numpy(Q).cuda()
+        h = vlr.Index.from_arrays(ix, rank=rank, world=world, device=0)
+        h.reserve(c["batch"], c["nprobe"], c["k"])
+        mine = h.p2p_export()
+        handles = [None] * world
+        dist.all_gather_object(handles, mine)
+        h.p2p_connect(handles)
+        dist.barrier()
+        outs = []
+        for it in range(3):  # collective searches over the peer inboxes (epochs advance together)
+            outs.append(h.search(Qd, c["nprobe"], c["k"], sync=True))
+        got = dict(ids=outs[-1][0].cpu().numpy(), dist=outs[-1][1].cpu().numpy(), miss=outs[-1][2].cpu().numpy(),
+                   probes=outs[-1][3].cpu().numpy())
+        dist.barrier()
+        h.close()
+        h1 = vlr.Index.from_arrays(ix, device=0)
+        ref = h1.search(Qd, c["nprobe"], c["k"], sync=True)
+        h1.close()
+        bit = all(np.array_equal(got[key], r.cpu().numpy()) for key, r in zip(("ids", "dist", "miss", "probes"), ref))
+        bit = bit and all(torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1]) for o in outs)
+        o = oracle.search(ix, Q, c["nprobe"], c["k"], nthreads=2)
+        errs = check(ix, Q, got, o, idmap=oracle.IdMap(ix))
+        out_q.put((rank, bit, errs[:3]))
+    except Exception as e:
+        out_q.put((rank, False, [repr(e)]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_process_nvlink_peer_exchange_one_gpu():
+    """The peer-exchange transport (vlr_p2p_export / connect): two processes on
+    one GPU map each other's inboxes with CUDA IPC; every search is collective,
+    the producer kernels store their slabs into both inboxes and raise epoch
+    flags, the consumers wait on them. Final rows equal the single-GPU search
+    bitwise on both ranks, over repeated searches (epochs), and pass R1-R4."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, bit, errs in res:
+        assert not errs, (rank, errs)
+        assert bit, f"rank {rank}: peer-exchange result differs from the single-GPU search"

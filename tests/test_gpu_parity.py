@@ -635,8 +635,9 @@ def test_nccl_exchange_path_single_rank(c1_index, c1_queries, monkeypatch):
 
 @pytest.mark.parametrize("flag,val", [("VLR_FILTER_PERSISTENT", "1"), ("VLR_FILTER_CLUSTER", "2"),
                                       ("VLR_FILTER_CLUSTER", "4"), ("VLR_FILTER_PAIR", "1"), ("VLR_EXACT_CFG", "4,4"),
-                                      ("VLR_EXACT_CFG", "2,8"), ("VLR_EXACT_CFG", "2,2"), ("VLR_EXACT_CFG", "3,2"),
-                                      ("VLR_EXACT_CFG", "3,6"), ("VLR_EXACT_CFG", "5,2"), ("VLR_FILTER_BTILED", "0")])
+                                      ("VLR_EXACT_CFG", "2,8"), ("VLR_EXACT_CFG", "2,2"), ("VLR_EXACT_CFG", "3,2,2"),
+                                      ("VLR_EXACT_CFG", "3,4,2"), ("VLR_EXACT_CFG", "5,2,2"), ("VLR_EXACT_CFG", "16,1"),
+                                      ("VLR_EXACT_CFG", "32,1"), ("VLR_FILTER_BTILED", "0")])
 def test_filter_variant_parity(flag, val):
     """K1 experiment kernels (persistent k_filter_tc_p; query-tile multicast
     over 2- or 4-CTA clusters; the CTA-pair cta_group::2 kernel) and K3a (stages, warps) configurations other

@@ -82,10 +82,12 @@ VARIANTS = {
     "pair": {"VLR_FILTER_PAIR": "1"},
     "single": {"VLR_FILTER_PAIR": "0"},
     "single_tmapB": {"VLR_FILTER_PAIR": "0", "VLR_FILTER_BTILED": "0"},
-    "exact_3_2x2": {"VLR_EXACT_CFG": "3,2"},
-    "exact_3_4x2": {"VLR_EXACT_CFG": "3,6"},
-    "exact_5_2x2": {"VLR_EXACT_CFG": "5,2"},
+    "exact_3_2x2": {"VLR_EXACT_CFG": "3,2,2"},
+    "exact_3_4x2": {"VLR_EXACT_CFG": "3,4,2"},
+    "exact_5_2x2": {"VLR_EXACT_CFG": "5,2,2"},
     "exact_4_4": {"VLR_EXACT_CFG": "4,4"},
+    "exact_16_1": {"VLR_EXACT_CFG": "16,1"},
+    "exact_8_2": {"VLR_EXACT_CFG": "8,2"},
     "single_cl2": {"VLR_FILTER_PAIR": "0", "VLR_FILTER_CLUSTER": "2"},
     "pair_qt128": {"VLR_FILTER_PAIR": "1", "VLR_FILTER_QT": "128"},
     "pair_qt64": {"VLR_FILTER_PAIR": "1", "VLR_FILTER_QT": "64"},
