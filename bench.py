@@ -249,21 +249,22 @@ def gen_index(c, seed, rank, world, hot=None, gt_queries=None):
         owned = own == rank
     t = time.time()
     cache = os.environ.get("VLR_GEN_CACHE")
-    key = f"g2_{c['N']}_{c['d']}_{c['nlist']}_{c['m']}_{seed}_{world}_{rank}_{'all' if hot is None else len(hot)}"
+    key = f"g3_{c['N']}_{c['d']}_{c['nlist']}_{c['m']}_{seed}_{world}_{rank}_{'all' if hot is None else len(hot)}"
     key += f"_mt{c['metric']}_br{c['by_residual']}_nb{c['nbits']}"
     if gt_queries is not None:
         import hashlib
         key += f"_gt{len(gt_queries)}_{hashlib.md5(gt_queries.tobytes()).hexdigest()[:10]}"
-    names = ["centroids", "codebooks", "list_offsets", "ids", "codes"] + (["gt_ids"] if gt_queries is not None else [])
+    names = ["centroids", "codebooks", "list_offsets", "ids", "codes"] + (["gt_ids", "gt_dist"] if gt_queries is not None
+                                                                          else [])
     if cache:
         path = os.path.join(cache, key)
         if os.path.exists(os.path.join(path, "done")):
             f = {n: np.ascontiguousarray(np.load(os.path.join(path, n + ".npy"), mmap_mode="r")) for n in names}
-            gt = f.pop("gt_ids", None)
+            gt, gtd = f.pop("gt_ids", None), f.pop("gt_dist", None)
             ix = datagen.IndexArrays(d=c["d"], nlist=c["nlist"], m=c["m"], seed=seed, metric=c["metric"],
                                      by_residual=c["by_residual"], nbits=c["nbits"], **f)
             if gt is not None:
-                ix.gt_ids = gt
+                ix.gt_ids, ix.gt_dist = gt, gtd
             return ix, time.time() - t
     ix = datagen.make_index(c["N"], c["d"], c["nlist"], c["m"], seed=seed, device="cuda", owned=owned,
                             gt_queries=gt_queries, metric=c["metric"], by_residual=c["by_residual"],

@@ -13,6 +13,7 @@
 //            metric (NEXT-3): D = -sum_t q_t c_t (products exact in fp64, the
 //            sum in dimension order); the filter then holds -2<q, c>
 //            (||c||^2 = 0 in K1), the same key scaled by 2.
+#include <algorithm>
 #include <cfloat>
 #include <cstdio>
 
@@ -135,6 +136,7 @@ cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, fl
 constexpr int kSelThreads = 1024;
 constexpr int kSelMaxGroups = 16384;  // groups per rank <= 16384 (nlist <= 512K) for the sorted-minima path
 constexpr int kSelGroupCap = 2048;    // qualifying 32-centroid groups gathered per query (else: full row scan)
+constexpr int kSelGather = 8192;      // filter values gathered per query in shared memory (the theta~ select)
 
 // radix select (4 x 8-bit digits) of the want-th smallest (1-based) of n order-preserving keys in shared
 // memory; the whole CTA calls it, the result is CTA-uniform
@@ -195,13 +197,15 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
                                                         float* __restrict__ x1, int32_t* __restrict__ cand,
                                                         int32_t* __restrict__ ncand, float* __restrict__ bound_out,
                                                         PeerOut pout, PeerIn pin) {
-  extern __shared__ unsigned skeys[];
-  __shared__ unsigned s_cnt;
+  extern __shared__ unsigned skeys[];  // >= max(keys of the theta' select, 2 kSelGather) words
+  __shared__ unsigned s_cnt, s_ng, s_ovf;
+  __shared__ int s_grp[kSelGroupCap];
   const int q = blockIdx.x;
   const int nq = gridDim.x;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int ngL = (L + 31) / 32;               // groups of all L centroids (gmin row stride)
-  const int g0 = lo / 32, ng = (hi + 31) / 32 - g0;  // this rank's groups
+  const int g0 = lo / 32, ng = hi > lo ? (hi + 31) / 32 - g0 : 0;  // this rank's groups
+  // ---- theta': an upper bound of theta~ (the np-th smallest filter value)
   float theta = CUDART_INF_F;
   if constexpr (MODE == kSelStage2) {
     peer_wait(pin);  // NVLink peer exchange: every rank's x1 slab has landed in this rank's inbox
@@ -219,54 +223,112 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
       theta = fkey_inv(radix_select_kth(skeys, ng, (unsigned)np));
     }
   }
+  const float qn = qnorm[q];
+  const float u = 5.9604645e-8f;  // 2^-24
+  // fp16 subnormal flush of the scaled operands (absolute):
+  // A = sqrt(d) 2^-25 (||q|| c_inv + c_max q_inv)(1 + 2^-11) + d 2^-50 c_inv q_inv,
+  // e_abs = sqrt(d) 2^-25 (1 + 2^-11), d 2^-50 = e_abs^2 / (1 + 2^-11)^2 <= e_abs^2
+  const float qi = qinv[q];
+  const float abs_dot = e_abs * (qn * c_inv + cmax * qi) + e_abs * e_abs * (c_inv * qi) + 1.2e-38f;
+  const float delta = 2.0f * (2.0f * (e_dot + 2.0f * u) * qn * cmax + 4.0f * u * (cmax * cmax + qn * qn) +
+                              2.0f * abs_dot);
+  // ---- gather every filter value <= lim of this range into shared memory, (key, centroid) pairs:
+  // stage 1 gathers below theta' (the np smallest values of the range are among them), the others
+  // below theta' + 2 Delta* (a superset of the candidate set). K1 stored gmin = the minimum of the
+  // group's 32 stored values (+inf past L), so only groups with gmin <= lim are read (one 128-B piece).
+  const float lim = MODE == kSelStage1 ? theta : theta + 2.0f * delta;
+  unsigned* sk = skeys;                 // [kSelGather] keys
+  unsigned* sid = skeys + kSelGather;   // [kSelGather] centroid ids
+  __syncthreads();  // skeys (the theta' select) consumed
+  if (threadIdx.x == 0) { s_cnt = 0u; s_ng = 0u; s_ovf = 0u; }
+  __syncthreads();
+  const float* grow = gmin + (size_t)q * ngL + g0;
+  for (int i0 = 0; i0 < ng; i0 += blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    const bool keep = i < ng && grow[i] <= lim;
+    const unsigned km = __ballot_sync(kFull, keep);
+    if (km == 0u) continue;
+    unsigned base = 0u;
+    if (lane == 0) base = atomicAdd(&s_ng, (unsigned)__popc(km));
+    base = __shfl_sync(kFull, base, 0);
+    const unsigned pos = base + __popc(km & ((1u << lane) - 1u));
+    if (keep && pos < (unsigned)kSelGroupCap) s_grp[pos] = g0 + i;
+  }
+  __syncthreads();
+  const unsigned ngq = s_ng;
+  const float* row = dt + (size_t)q * L;
+  if (ngq <= (unsigned)kSelGroupCap) {
+    for (unsigned j = warp; j < ngq; j += nwarp) {  // warp-uniform: one 128-B piece per group
+      const int l = s_grp[j] * 32 + lane;
+      const float v = l < hi ? row[l] : CUDART_INF_F;
+      const bool keep = v <= lim;
+      const unsigned km = __ballot_sync(kFull, keep);
+      if (km == 0u) continue;
+      unsigned base = 0u;
+      if (lane == 0) base = atomicAdd(&s_cnt, (unsigned)__popc(km));
+      base = __shfl_sync(kFull, base, 0);
+      const unsigned pos = base + __popc(km & ((1u << lane) - 1u));
+      if (keep && pos < (unsigned)kSelGather) {
+        sk[pos] = fkey(v);
+        sid[pos] = (unsigned)l;
+      }
+    }
+  } else if (threadIdx.x == 0) {
+    s_ovf = 1u;
+  }
+  __syncthreads();
+  const unsigned n_g = s_cnt;
+  const bool ok = !s_ovf && n_g <= (unsigned)kSelGather;
   if constexpr (MODE == kSelStage1) {
-    // x1 row: the np smallest group minima of this range as a multiset (P2P: into every rank's inbox)
+    // x1 row: the np smallest filter values of this range as a multiset (exchanged; the union's np-th
+    // smallest is the global theta~). P2P: straight into every rank's inbox.
     float* out = x1 + (size_t)q * np;
     const long long slab = (long long)nq * np;
     auto put = [&](int i, float v) {
       if (pout.G) peer_store(pout, slab, (long long)q * np + i, v);
       else out[i] = v;
     };
-    if (threadIdx.x == 0) s_cnt = 0u;
-    __syncthreads();
-    // fewer than np groups: all of them, +inf padding (theta' stays exact). More than kSelMaxGroups: the
-    // first np (any np genuine group minima give an np-th smallest >= theta~, a valid but looser bound)
-    if (ng < np || ng > kSelMaxGroups) {
-      for (int i = threadIdx.x; i < np; i += blockDim.x) put(i, i < ng ? gmin[(size_t)q * ngL + g0 + i] : CUDART_INF_F);
-      peer_signal(pout);
-      return;
+    if (ok) {
+      if (n_g >= (unsigned)np) {
+        const unsigned kth = radix_select_kth(sk, (int)n_g, (unsigned)np);
+        if (threadIdx.x == 0) s_cnt = 0u;
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < n_g; i += blockDim.x)
+          if (sk[i] < kth) put((int)atomicAdd(&s_cnt, 1u), fkey_inv(sk[i]));  // fewer than np are below
+        __syncthreads();
+        for (int i = (int)s_cnt + threadIdx.x; i < np; i += blockDim.x) put(i, fkey_inv(kth));
+      } else {  // the whole range holds fewer than np values (theta' = +inf): all of them, +inf padding
+        for (int i = threadIdx.x; i < np; i += blockDim.x) put(i, i < (int)n_g ? fkey_inv(sk[i]) : CUDART_INF_F);
+      }
+    } else {
+      // too many values below theta' for the gather: the np smallest GROUP MINIMA (any np genuine filter
+      // values give an np-th smallest >= theta~: a valid, looser bound), or every group minimum
+      if (threadIdx.x == 0) s_cnt = 0u;
+      __syncthreads();
+      if (ng < np || ng > kSelMaxGroups) {
+        for (int i = threadIdx.x; i < np; i += blockDim.x) put(i, i < ng ? grow[i] : CUDART_INF_F);
+      } else {
+        for (int i = threadIdx.x; i < ng; i += blockDim.x)
+          if (grow[i] < theta) put((int)atomicAdd(&s_cnt, 1u), grow[i]);
+        __syncthreads();
+        for (int i = (int)s_cnt + threadIdx.x; i < np; i += blockDim.x) put(i, theta);
+      }
     }
-    for (int i0 = 0; i0 < ng; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      const bool keep = i < ng && skeys[i] < fkey(theta);
-      const unsigned km = __ballot_sync(kFull, keep);
-      if (km == 0u) continue;
-      unsigned base = 0u;
-      if (lane == 0) base = atomicAdd(&s_cnt, (unsigned)__popc(km));
-      base = __shfl_sync(kFull, base, 0);
-      if (keep) put(base + __popc(km & ((1u << lane) - 1u)), fkey_inv(skeys[i]));
-    }
-    __syncthreads();
-    for (int i = (int)s_cnt + threadIdx.x; i < np; i += blockDim.x) put(i, theta);  // fewer than np are < theta
     peer_signal(pout);
     return;
   } else {
-    const float qn = qnorm[q];
-    const float u = 5.9604645e-8f;  // 2^-24
-    // fp16 subnormal flush of the scaled operands (absolute):
-    // A = sqrt(d) 2^-25 (||q|| c_inv + c_max q_inv)(1 + 2^-11) + d 2^-50 c_inv q_inv,
-    // e_abs = sqrt(d) 2^-25 (1 + 2^-11), d 2^-50 = e_abs^2 / (1 + 2^-11)^2 <= e_abs^2
-    const float qi = qinv[q];
-    const float abs_dot = e_abs * (qn * c_inv + cmax * qi) + e_abs * e_abs * (c_inv * qi) + 1.2e-38f;
-    const float delta = 2.0f * (2.0f * (e_dot + 2.0f * u) * qn * cmax + 4.0f * u * (cmax * cmax + qn * qn) +
-                                2.0f * abs_dot);
-    const float bnd = theta + 2.0f * delta;
+    // single GPU: tighten theta' to theta~ itself, the np-th smallest gathered value (every value below
+    // theta' + 2 Delta* is in the gather, and theta~ <= theta'); stage 2 already holds the global theta~
+    float th = theta;
+    if constexpr (MODE == kSelFull) {
+      if (ok && n_g >= (unsigned)np) th = fkey_inv(radix_select_kth(sk, (int)n_g, (unsigned)np));
+    }
+    const float bnd = th + 2.0f * delta;
     if (threadIdx.x == 0) {
       s_cnt = 0u;
       bound_out[q] = bnd;
     }
     __syncthreads();
-    const float* row = dt + (size_t)q * L;
     int32_t* out = cand + (size_t)q * kCandCap;
     auto emit = [&](bool keep, int i) {
       const unsigned km = __ballot_sync(kFull, keep);
@@ -279,54 +341,32 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
         if (pos < (unsigned)kCandCap) out[pos] = i;
       }
     };
-    // Group-guided compaction: K1 stored gmin = the minimum of the group's 32 stored dt values (the same
-    // fp32 values, rows >= L as +inf), so {l : dt_l <= bnd} is exactly the union, over the groups with
-    // gmin <= bnd, of their members with dt <= bnd. Only those groups' 128-byte dt pieces are read
-    // (~200 of the 2048 groups of a C4 row); more than kSelGroupCap qualifying groups: full row scan.
-    __shared__ int s_grp[kSelGroupCap];
-    __shared__ unsigned s_ng;
-    if (threadIdx.x == 0) s_ng = 0u;
-    __syncthreads();
-    const float* grow = gmin + (size_t)q * ngL + g0;
-    for (int i0 = 0; i0 < ng; i0 += blockDim.x) {
-      const int i = i0 + threadIdx.x;
-      const bool keep = i < ng && grow[i] <= bnd;
-      const unsigned km = __ballot_sync(kFull, keep);
-      if (km == 0u) continue;
-      unsigned base = 0u;
-      if (lane == 0) base = atomicAdd(&s_ng, (unsigned)__popc(km));
-      base = __shfl_sync(kFull, base, 0);
-      const unsigned pos = base + __popc(km & ((1u << lane) - 1u));
-      if (keep && pos < (unsigned)kSelGroupCap) s_grp[pos] = g0 + i;
-    }
-    __syncthreads();
-    const unsigned ngq = s_ng;
-    const int warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    if (ngq <= (unsigned)kSelGroupCap) {
-      for (unsigned j = warp; j < ngq; j += nwarp) {  // warp-uniform loop: one 128-B piece per group
-        const int l = s_grp[j] * 32 + lane;
-        emit(l < hi && row[l] <= bnd, l);
+    if (ok) {
+      const unsigned kb = fkey(bnd);
+      for (unsigned i0 = 0; i0 < n_g; i0 += blockDim.x) {
+        const unsigned i = i0 + threadIdx.x;
+        emit(i < n_g && sk[i] <= kb, i < n_g ? (int)sid[i] : 0);
       }
     } else {
       const int n = hi - lo;
       if ((L & 3) == 0 && (lo & 3) == 0 && (n & 3) == 0) {
         const float4* r4 = reinterpret_cast<const float4*>(row + lo);
-        constexpr int U = 2;  // loads in flight per thread before any emit (32 regs: 2 CTAs per SM)
+        constexpr int U = 2;  // loads in flight per thread before any emit
         for (int i0 = 0; i0 < n / 4; i0 += U * blockDim.x) {
           float4 v[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int i = i0 + u * blockDim.x + threadIdx.x;
-            v[u] = i < n / 4 ? __ldg(r4 + i) : make_float4(CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F);
+          for (int uu = 0; uu < U; ++uu) {
+            const int i = i0 + uu * blockDim.x + threadIdx.x;
+            v[uu] = i < n / 4 ? __ldg(r4 + i) : make_float4(CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F);
           }
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int i = i0 + u * blockDim.x + threadIdx.x;
+          for (int uu = 0; uu < U; ++uu) {
+            const int i = i0 + uu * blockDim.x + threadIdx.x;
             const bool in = i < n / 4;
-            emit(in && v[u].x <= bnd, lo + 4 * i);
-            emit(in && v[u].y <= bnd, lo + 4 * i + 1);
-            emit(in && v[u].z <= bnd, lo + 4 * i + 2);
-            emit(in && v[u].w <= bnd, lo + 4 * i + 3);
+            emit(in && v[uu].x <= bnd, lo + 4 * i);
+            emit(in && v[uu].y <= bnd, lo + 4 * i + 1);
+            emit(in && v[uu].z <= bnd, lo + 4 * i + 2);
+            emit(in && v[uu].w <= bnd, lo + 4 * i + 3);
           }
         }
       } else {
@@ -354,7 +394,7 @@ cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, in
     n_keys = (size_t)ix.world * np;
     if (n_keys > (size_t)kSelMaxGroups) return cudaErrorInvalidValue;  // world * nprobe' <= 16384
   }
-  const size_t sm = n_keys * sizeof(unsigned);
+  const size_t sm = std::max(n_keys, (size_t)2 * kSelGather) * sizeof(unsigned);
   const void* fn = mode == kSelStage1 ? (const void*)k_select<kSelStage1>
                    : mode == kSelStage2 ? (const void*)k_select<kSelStage2> : (const void*)k_select<kSelFull>;
   cudaError_t e = ensure_smem(fn, sm);

@@ -811,6 +811,11 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   if (e != cudaSuccess) return e;
   const int kblocks = (ix.d8 + kTcBK - 1) / kTcBK;
   if (nacc == 1 && use_persistent) {
+    nN = ((nq + 15) / 16) * 16;  // one accumulator holds the whole batch (no query tiles)
+    CUtensorMap tmBp;
+    e = make_tmap_2d(&tmBp, Qh, nq, ix.d8, nN, true);
+    if (e != cudaSuccess) return e;
+    tmB = tmBp;
     const uint32_t sb = kTcM * 128 + (uint32_t)(nN * 128);
     int stages = (int)((200 * 1024) / sb);
     if (stages > kTcMaxStages) stages = kTcMaxStages;

@@ -127,13 +127,33 @@ struct Grp {
   long long gaddr;
 };
 
+// Advance the item cursor to the item holding group gg (item_off[it] <= gg <
+// item_off[it + 1]). Non-owned probes are empty items (0 groups): at world 8
+// about 7 of 8 consecutive items are empty, so a one-by-one walk costs a chain
+// of dependent L2 loads at every item boundary. The warp probes 32 items per
+// step (one load, a ballot); gg is warp-uniform, so the loop is too.
+__device__ __forceinline__ void advance_item(const ScanArgs& a, long long gg, long long& it, int lane) {
+  if (a.item_off[it + 1] > gg) return;
+  const long long n_items = (long long)a.nq * a.np;  // item_off has n_items + 1 entries
+  for (;;) {
+    const long long j = it + 1 + lane;  // candidate: the first item whose end exceeds gg
+    const bool past = j >= n_items || a.item_off[j + 1] > gg;
+    const unsigned m = __ballot_sync(kFull, past);
+    if (m) {
+      it += 1 + (__ffs(m) - 1);
+      return;
+    }
+    it += 32;
+  }
+}
+
 // L2 prefetch of a whole group's codes: each lane prefetches one 128-B line
 // (LSU prefetch, no data return; a 4 KB TMA bulk prefetch per group costs
 // ~0.3 us of TMA issue time, tools/tma_issue.cu): keeps DRAM requests in
 // flight beyond the register double buffer (K6).
 template <int MP, int NB>
 __device__ __forceinline__ void grp_prefetch(const ScanArgs& a, long long gg, long long& it, int lane) {
-  while (a.item_off[it + 1] <= gg) ++it;
+  advance_item(a, gg, it, lane);
   const long long gaddr = a.gbase[a.plocal[it]] + (gg - a.item_off[it]);
   if (lane < MP * NB / 32)  // 128-byte lines of the group
     asm volatile("prefetch.global.L2 [%0];" ::"l"(a.codes + gaddr * (4 * MP * NB) + lane * 128) : "memory");
@@ -142,7 +162,7 @@ __device__ __forceinline__ void grp_prefetch(const ScanArgs& a, long long gg, lo
 template <int MP, int NB, int EXP = 0>
 __device__ __forceinline__ void grp_load(Grp<MP, NB>& G, const ScanArgs& a, long long gg, long long& it, int lane) {
   constexpr int kChunks = MP * NB / 128;
-  while (a.item_off[it + 1] <= gg) ++it;
+  advance_item(a, gg, it, lane);
   const int loc = a.plocal[it];
   G.gaddr = a.gbase[loc] + (gg - a.item_off[it]);
   G.t1 = a.term1[it];
@@ -692,19 +712,28 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
       if (threadIdx.x == 0) s_z = z + 1;
     }
     if (g0 >= g1) continue;  // CTA-uniform
-    __syncthreads();  // s_it of the previous wave consumed
-    if (threadIdx.x == 0) {
-      // item containing group g0: last i with item_off[i] <= g0
+    // item containing group g0: the last i with item_off[i] <= g0, by a CTA-parallel search (each round
+    // samples kScanThreads positions: 2 dependent loads for up to 256K items, where a one-thread binary
+    // search costs ~15 dependent L2 round trips -- paid at every wave start of the release scan)
+    {
       int lo = i_lo, hi = i_hi;  // item_off[lo] <= g0 < item_off[hi]
       while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (a.item_off[mid] <= g0) lo = mid; else hi = mid;
+        const int step = (hi - lo + kScanThreads - 1) / kScanThreads;
+        const int i = lo + (int)threadIdx.x * step;
+        __syncthreads();  // s_it of the previous round / wave consumed
+        if (threadIdx.x == 0) s_it = lo;
+        __syncthreads();
+        if (threadIdx.x > 0 && i < hi && a.item_off[i] <= g0) atomicMax(reinterpret_cast<long long*>(&s_it), (long long)i);
+        __syncthreads();
+        lo = (int)s_it;
+        hi = lo + step < hi ? lo + step : hi;
       }
-      s_it = lo;
+      __syncthreads();
+      if (threadIdx.x == 0) s_it = lo;
+      __syncthreads();
     }
-    __syncthreads();
     long long it0 = s_it;
-    while (a.item_off[it0 + 1] <= g0) ++it0;
+    advance_item(a, g0, it0, lane);
     long long g = g0;
     while (g < g1) {
       const int q = (int)(it0 / a.np);
@@ -767,7 +796,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
       g = seg_end;
       if (g < g1) {
         it0 = (long long)(q + 1) * a.np;
-        while (a.item_off[it0 + 1] <= g) ++it0;
+        advance_item(a, g, it0, lane);
       }
     }
   }
