@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
   __syncthreads();
   const unsigned n_g = s_cnt;
   const bool ok = !s_ovf && n_g <= (unsigned)kSelGather;
+  __syncthreads();  // every thread has read n_g / ok before s_cnt is reused below
   if constexpr (MODE == kSelStage1) {
     // x1 row: the np smallest filter values of this range as a multiset (exchanged; the union's np-th
     // smallest is the global theta~). P2P: straight into every rank's inbox.
