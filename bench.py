@@ -70,12 +70,22 @@ def parse():
     p.add_argument("--lat-batches", type=int, default=1000,
                    help="latency pass: CUDA-graph closed-loop batches per batch size (SURVEY §8(d): >= 1000)")
     p.add_argument("--sustained-s", type=float, default=10.0, help="sustained pass length (s), batch of the config")
+    p.add_argument("--pipeline", type=int, default=1, choices=[0, 1],
+                   help="1: cross-batch pipelining (vlr_set_pipeline: two workspace slots, batches alternate over "
+                        "two streams, batch i+1's coarse stage beside batch i's scan); 0: one stream")
+    p.add_argument("--scan-reserve", type=int, default=-1,
+                   help="SMs the scan leaves to the other stream's coarse stage when pipelining (-1: default)")
     p.add_argument("--sweep-out", default=None,
                    help="also run the C5 batch x nprobe sweep on the same index and write JSON lines here")
     return p.parse_args()
 
 
 # ---------------------------------------------------------------- helpers
+def default_reserve(world):
+    """SMs the scan leaves to the next batch's coarse stage when pipelining (tools/overlap_probe.py)."""
+    return 8 if world == 1 else 16
+
+
 def cfg_of(a):
     import datagen
     c = dict(datagen.CONFIGS[a.config])
@@ -383,10 +393,16 @@ def main():
     info = h.info()
     # ---- queries (test stream), resident in HBM
     Qdev = torch.from_numpy(pool).cuda().reshape(a.warmup + a.steps, B, c["d"])
-    h.reserve(B, NP, K)
     xchg = a.exchange if world > 1 else "none"
     if dry and xchg == "nccl":
         xchg = "p2p"  # NCCL refuses two ranks on one device
+    # cross-batch pipelining: not for the staged dry-run transport (host-synchronous gloo
+    # exchanges) nor NCCL (the communicator serialises its collectives across streams)
+    pipe = bool(a.pipeline) and xchg in ("none", "p2p")
+    reserve = a.scan_reserve if a.scan_reserve >= 0 else default_reserve(world)
+    if pipe:
+        h.set_pipeline(2, reserve)
+    h.reserve(B, NP, K)
     if xchg == "p2p":  # inboxes IPC-mapped across the ranks: exchanges inside the kernels, no NCCL calls
         if dry:
             mine = h.p2p_export()
@@ -399,8 +415,9 @@ def main():
              torch.empty(B, NP, dtype=torch.uint8, device="cuda"), torch.empty(B, NP, dtype=torch.int32, device="cuda"))
             for _ in range(a.steps)]
     stream = torch.cuda.current_stream()
+    streams = [stream, torch.cuda.Stream()] if pipe else [stream, stream]
 
-    def step(Q, out):
+    def step(Q, out, stream=stream):
         """one batch search: the collective NCCL search, or (dry run) the staged sharded search with the
         exchanges over gloo and the partial top-k merged by vlr_merge_partials"""
         if xchg != "staged":
@@ -414,28 +431,52 @@ def main():
         out[3].copy_(prb)
 
     for i in range(a.warmup):
-        step(Qdev[i], outs[0])
+        step(Qdev[i], outs[i % 2], streams[i % 2])
     torch.cuda.synchronize()
-    h.set_profiling(2)  # timed region: only the two events around the scan (roofline), nothing else
     launches = h.last_launch_count
     clocks = Clocks(local)
     if not a.ncu and not a.no_clocks:
         clocks.start()
         time.sleep(0.3)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(world)
     torch.cuda.synchronize()
+    # ---- the timed region: K batches back to back (pipelined: alternating over two streams, two workspace
+    # slots; each batch's whole hot path runs inside the region), device-timed from the first launch to
+    # the completion of the last batch on both streams
     e0.record(stream)
+    streams[1].wait_event(e0)
     for i in range(a.steps):
-        ev[i][0].record(stream)
-        step(Qdev[a.warmup + i], outs[i])
-        ev[i][1].record(stream)
+        step(Qdev[a.warmup + i], outs[i], streams[i % 2])
+    stream.wait_stream(streams[1])
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
     clk = clocks.stop() if not a.ncu and not a.no_clocks else None
     ms_total = allmax(e0.elapsed_time(e1), world)
+    # ---- serial pass on one stream with the scan on every SM (reserve 0): per-batch latency (launch ->
+    # completion, no queueing behind another batch) and the scan kernel's own duration for the roofline
+    # (CUDA events around the scan on its launch stream; in the pipelined region the scan of batch i+1
+    # starts on SMs while batch i's still runs, so its event interval is not its duration)
+    if pipe:
+        h.set_pipeline(2, 0)
+    for i in range(2):
+        step(Qdev[i], outs[0])
+    torch.cuda.synchronize()
+    h.set_profiling(2)  # only the two events around the scan
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    es0, es1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    es0.record(stream)
+    for i in range(a.steps):
+        ev[i][0].record(stream)
+        step(Qdev[a.warmup + i], outs[i])
+        ev[i][1].record(stream)
+    es1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms_serial = allmax(es0.elapsed_time(es1), world)
     lat = np.array([s.elapsed_time(e) for s, e in ev])
     nrec = min(a.steps, 64)
     scan_ms = np.array([h.stage_times(back=j)["scan"] for j in range(nrec)][::-1])  # oldest first
@@ -483,6 +524,8 @@ def main():
         hid = torch.empty(B, K, dtype=torch.int64).pin_memory()
         hd = torch.empty(B, K, dtype=torch.float32).pin_memory()
         hm = torch.empty(B, NP, dtype=torch.uint8).pin_memory()
+        if pipe:
+            h.set_pipeline(2, reserve)
         for i in range(min(3, ne)):
             h.search_host_ptr(hq[i].data_ptr(), B, c["nprobe"], K, hid.data_ptr(), hd.data_ptr(), hm.data_ptr(), None)
         barrier(world)
@@ -490,8 +533,9 @@ def main():
         for i in range(ne):
             h.search_host_ptr(hq[i].data_ptr(), B, c["nprobe"], K, hid.data_ptr(), hd.data_ptr(), hm.data_ptr(), None)
         el_block = allmax(time.perf_counter() - t, world)
-        # serving pipeline: vlr_search_host_async back to back on one stream (each step's H2D, search and
-        # D2H enqueued; one synchronisation at the end), per-step output buffers
+        # serving pipeline: vlr_search_host_async back to back (pipelined: alternating over two streams,
+        # two workspace slots; each step's H2D, search and D2H enqueued; one synchronisation at the end),
+        # per-step output buffers
         pid_ = torch.empty(ne, B, K, dtype=torch.int64).pin_memory()
         pdd_ = torch.empty(ne, B, K, dtype=torch.float32).pin_memory()
         pmm_ = torch.empty(ne, B, NP, dtype=torch.uint8).pin_memory()
@@ -500,17 +544,21 @@ def main():
         t = time.perf_counter()
         for i in range(ne):
             h.search_host_ptr_async(hq[i].data_ptr(), B, c["nprobe"], K, pid_[i].data_ptr(), pdd_[i].data_ptr(),
-                                    pmm_[i].data_ptr(), None)
-        torch.cuda.current_stream().synchronize()
+                                    pmm_[i].data_ptr(), None, stream=streams[i % 2])
+        torch.cuda.synchronize()
         el = allmax(time.perf_counter() - t, world)
         e2e_same = bool(torch.equal(pid_[ne - 1], hid) and torch.equal(pdd_[ne - 1], hd))
-        e2e = {"value": ne * B / el_block, "unit": UNIT, "h2d_bytes_per_step": B * c["d"] * 4,
+        e2e = {"value": ne * B / el, "unit": UNIT, "h2d_bytes_per_step": B * c["d"] * 4,
                "d2h_bytes_per_step": B * K * 12 + B * NP,
-               "how": "vlr_search_host (synchronous) per step: pinned host queries in, ids/dist/miss out",
-               "pipelined_value": ne * B / el,
-               "pipelined_how": "vlr_search_host_async per step back to back on one stream, wall clock to the final "
-                                "synchronisation (runs right after the blocking pass: sustained load, power-capped)",
-               "pipelined_equal_to_blocking": e2e_same}
+               "how": ("vlr_search_host_async per step (pinned host queries in, ids/dist/miss out), "
+                       + ("alternating over two streams with two workspace slots (pipelined)" if pipe
+                          else "back to back on one stream")
+                       + "; wall clock from the first call to the final synchronisation"),
+               "blocking_value": ne * B / el_block,
+               "blocking_how": "vlr_search_host (synchronous: H2D, search, D2H, stream sync) per step",
+               "async_equal_to_blocking": e2e_same}
+        if pipe:
+            h.set_pipeline(2, 0)
     # ---- NEXT-4 early per-query release (the paper's dispatcher ablation, Fig. 14):
     # host-observed latency of each query from launch to its release flag, against the same batches
     # searched with the batch barrier (launch -> stream sync). Untimed by the headline metric.
@@ -601,6 +649,10 @@ def main():
             "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
             "lat_ms_top5": [round(float(x), 4) for x in np.sort(lat)[::-1][:5]],
             "gpu_launches": int(launches * a.steps),
+            "pipeline": {"on": pipe, "slots": 2 if pipe else 1, "scan_reserve_sms": reserve if pipe else 0,
+                         "serial_value": a.steps * B / (ms_serial * 1e-3), "serial_ms_per_step": ms_serial / a.steps,
+                         "how": "timed region: batches alternate over two streams (vlr_set_pipeline(2, R)); "
+                                "serial pass: one stream, R = 0 (p50/p99 and the scan roofline come from it)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "k_scan (K6 ADC scan)", "peak_source": peak_src,
                          "bytes_per_launch": float(bytes_rec.mean()), "ms_per_launch": float(scan_ms.mean())},

@@ -305,9 +305,27 @@ vlr_status vlr_p2p_export(vlr_index* idx, void* handle_out);
 vlr_status vlr_p2p_connect(vlr_index* idx, const void* handles);
 vlr_status vlr_p2p_setup(vlr_index* idx);
 
-/* Pre-size the per-handle workspace for batches up to (max_nq, max_nprobe, max_k)
- * so that later searches allocate nothing (required before graph capture). */
+/* Pre-size the per-handle workspace (every slot, see vlr_set_pipeline) for
+ * batches up to (max_nq, max_nprobe, max_k) so that later searches allocate
+ * nothing (required before graph capture). */
 vlr_status vlr_reserve(vlr_index* idx, int32_t max_nq, int32_t max_nprobe, int32_t max_k);
+
+/*
+ * Cross-batch pipelining. slots = 1 (default) or 2 workspace
+ * slots; search number i on the handle uses slot i % slots. With 2 slots a
+ * search first makes its stream wait (event) for the previous search of its
+ * slot, so searches enqueued on two different streams overlap on the device:
+ * batch i+1's coarse stage (K1-K5) runs beside batch i's scan. Searches on
+ * one stream stay ordered; results are bitwise those of slots = 1.
+ * scan_reserve_sms in [0, SMs - 2]: SMs the scan's persistent grid leaves
+ * free for the other stream's coarse stage (0 = one scan CTA per SM).
+ * With the peer exchange every rank must use the same slot count (set
+ * before vlr_p2p_export; UNSUPPORTED after) and issue the same searches in
+ * the same order. Not under stream capture (a captured search uses its slot
+ * without the event). Memory: one workspace per slot. INVALID_ARG for bad
+ * values. Initial scan reserve: env VLR_SCAN_RESERVE (else 0).
+ */
+vlr_status vlr_set_pipeline(vlr_index* idx, int32_t slots, int32_t scan_reserve_sms);
 
 /*
  * Merge S shard-partial results (shard-only mode) into the final top-k:

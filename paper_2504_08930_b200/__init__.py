@@ -24,7 +24,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "DIM_MISMATCH", 3: "NONFINITE", 4: "UNKN
 EXPORTS = ["vlr_load_index", "vlr_search_async", "vlr_search", "vlr_search_host", "vlr_search_host_async",
            "vlr_search_release_async", "vlr_coarse_stage1", "vlr_coarse_stage2", "vlr_search_stage3",
            "vlr_poll_ready", "vlr_wait_ready", "vlr_merge_ready", "vlr_p2p_export", "vlr_p2p_connect",
-           "vlr_p2p_setup", "vlr_reserve", "vlr_deal_owners", "vlr_update_hot",
+           "vlr_p2p_setup", "vlr_reserve", "vlr_set_pipeline", "vlr_deal_owners", "vlr_update_hot",
            "vlr_merge_partials", "vlr_access_counts", "vlr_index_info", "vlr_index_owners", "vlr_set_profiling", "vlr_stage_times",
            "vlr_last_launch_count", "vlr_nccl_unique_id", "vlr_index_free", "vlr_last_error", "vlr_version"]
 
@@ -75,6 +75,7 @@ def lib():
             "vlr_coarse_stage2": [P, P, I32, I32, P, P, P],
             "vlr_search_stage3": [P, P, I32, I32, I32, P, P, P, P, P, P],
             "vlr_reserve": [P, I32, I32, I32],
+            "vlr_set_pipeline": [P, I32, I32],
             "vlr_deal_owners": [P, I32, P, P, I32, I32, P],
             "vlr_update_hot": [P, P],
             "vlr_merge_partials": [P, P, I32, I32, I32, P, P, P],
@@ -380,6 +381,11 @@ class Index:
 
     def reserve(self, max_nq: int, max_nprobe: int, max_k: int):
         _check(lib().vlr_reserve(self._h, max_nq, max_nprobe, max_k))
+
+    def set_pipeline(self, slots: int = 2, scan_reserve_sms: int = 0):
+        """vlr_set_pipeline: workspace slots for searches in flight on different streams, and the SMs
+        the scan leaves to the other stream's coarse stage."""
+        _check(lib().vlr_set_pipeline(self._h, slots, scan_reserve_sms))
 
     def access_counts(self, probes, counts=None, stream=None):
         """vlr_access_counts: accumulate per-cluster probe counts (torch int32

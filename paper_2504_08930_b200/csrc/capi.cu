@@ -112,8 +112,8 @@ static void free_index(DeviceIndex& ix) {
   ix = DeviceIndex{};
 }
 
-static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
-  Workspace& w = h->ws;
+static vlr_status ensure_ws(vlr_index* h, int slot, int nq, int np, int k) {
+  Workspace& w = h->wsl[slot];
   const DeviceIndex& ix = h->ix;
   if (w.status && nq <= w.cap_nq && np <= w.cap_np && k <= w.cap_k) return VLR_OK;
   if (h->p2p.on) return fail(VLR_ERR_UNSUPPORTED, "peer exchange connected: batch beyond the reserved workspace");
@@ -125,7 +125,8 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   w.cap_nq = cnq;
   w.cap_np = cnp;
   w.cap_k = ck;
-  w.n_cta = scan_ctas(ix);
+  w.n_cta_cap = scan_ctas(ix);
+  w.n_cta = w.n_cta_cap;
   const size_t nqs = (size_t)cnq;
   VLR_CUDA_TRY(dalloc(&w.qnorm, nqs));
   VLR_CUDA_TRY(dalloc(&w.qsq, nqs));
@@ -153,7 +154,7 @@ static vlr_status ensure_ws(vlr_index* h, int nq, int np, int k) {
   VLR_CUDA_TRY(dalloc(&w.qdone, nqs));
   VLR_CUDA_TRY(dalloc(&w.lut, nqs * ix.npairs * (ix.lut_pair_bytes / 4)));
   // warp partial lists (k <= 32 path only): slot (c + q + wave * n_cta)
-  const size_t nslots = ((size_t)w.n_cta * kMaxReleaseWaves + nqs) * kScanWarps * std::min(ck, kMaxK);
+  const size_t nslots = ((size_t)w.n_cta_cap * kMaxReleaseWaves + nqs) * kScanWarps * std::min(ck, kMaxK);
   VLR_CUDA_TRY(dalloc(&w.pdist, nslots));
   if (ck > kMaxK) {  // large-k candidate buffer: chunks of dump_nq queries x (groups of the np largest lists)
     const int64_t maxg = ix.top_groups[std::min<size_t>((size_t)cnp, ix.top_groups.size() - 1)];
@@ -355,7 +356,7 @@ vlr_status vlr_update_hot(vlr_index* h, const vlr_index_desc* desc) {
     n->ix.coarse_sharded = old.coarse_sharded;
     old.nccl = nullptr;
     if (n->ix.mpad != old.mpad || n->ix.npairs != old.npairs || n->ix.lut_pair_bytes != old.lut_pair_bytes) {
-      free_ws(h->ws);  // scan/LUT shapes changed (e.g. a different 4-bit mode): size the workspace again
+      for (auto& w : h->wsl) free_ws(w);  // scan/LUT shapes changed (e.g. a different 4-bit mode): size again
     }
     h->ix = n->ix;
     n->ix = old;  // freed with the temporary handle
@@ -651,6 +652,11 @@ vlr_status vlr_load_index(const vlr_index_desc* desc, const vlr_comm_desc* comm,
     const char* rep_env = getenv("VLR_COARSE_REPLICATED");
     ix.coarse_sharded = ix.nccl != nullptr && !(rep_env && atoi(rep_env) == 1);
   }
+  {
+    // VLR_SCAN_RESERVE=n: the scan's persistent grid leaves n SMs free (experiments; vlr_set_pipeline)
+    const char* rs = getenv("VLR_SCAN_RESERVE");
+    if (rs) h->scan_reserve = std::max(0, std::min(atoi(rs), scan_ctas(ix) - 2));
+  }
   *out = h;
   return VLR_OK;
 #undef LTRY
@@ -672,14 +678,15 @@ void vlr_index_free(vlr_index* h) {
   for (auto& row : h->ev)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
-  if (h->rel_fork) cudaEventDestroy(h->rel_fork);
-  if (h->rel_join) cudaEventDestroy(h->rel_join);
-  if (h->rel_stream) cudaStreamDestroy(h->rel_stream);
-  if (h->lut_fork) cudaEventDestroy(h->lut_fork);
-  if (h->lut_join) cudaEventDestroy(h->lut_join);
-  if (h->lut_stream) cudaStreamDestroy(h->lut_stream);
+  for (auto& r : h->res) {
+    cudaEvent_t evs[] = {r.done, r.lut_fork, r.lut_join, r.rel_fork, r.rel_join};
+    for (cudaEvent_t e : evs)
+      if (e) cudaEventDestroy(e);
+    if (r.lut_stream) cudaStreamDestroy(r.lut_stream);
+    if (r.rel_stream) cudaStreamDestroy(r.rel_stream);
+  }
   p2p_close(h);
-  free_ws(h->ws);
+  for (auto& w : h->wsl) free_ws(w);
   free_index(h->ix);
   delete h;
 }
@@ -691,7 +698,34 @@ vlr_status vlr_reserve(vlr_index* h, int32_t max_nq, int32_t max_nprobe, int32_t
   const int np = std::min(max_nprobe, h->ix.nlist);
   if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 2048");
   std::lock_guard<std::mutex> lock(h->mu);
-  return ensure_ws(h, std::max(max_nq, 1), np, max_k);
+  for (int b = 0; b < h->nslots; ++b) {
+    const vlr_status st = ensure_ws(h, b, std::max(max_nq, 1), np, max_k);
+    if (st != VLR_OK) return st;
+  }
+  return VLR_OK;
+}
+
+vlr_status vlr_set_pipeline(vlr_index* h, int32_t slots, int32_t scan_reserve_sms) {
+  if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
+  if (slots < 1 || slots > vlr_index::kSlots) return fail(VLR_ERR_INVALID_ARG, "slots must be 1 or 2");
+  std::lock_guard<std::mutex> lock(h->mu);
+  int sms = 0;
+  VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
+  VLR_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->ix.device));
+  if (scan_reserve_sms < 0 || scan_reserve_sms > sms - 2)
+    return fail(VLR_ERR_INVALID_ARG, "scan_reserve_sms must be in [0, SMs - 2]");
+  if (h->p2p.inbox && slots != h->p2p.nslots)
+    return fail(VLR_ERR_UNSUPPORTED, "the peer-exchange inbox was exported for another slot count");
+  if (slots > h->nslots && h->wsl[0].status) {  // size the new slots like slot 0
+    const Workspace& w0 = h->wsl[0];
+    for (int b = h->nslots; b < slots; ++b) {
+      const vlr_status st = ensure_ws(h, b, w0.cap_nq, w0.cap_np, w0.cap_k);
+      if (st != VLR_OK) return st;
+    }
+  }
+  h->nslots = slots;
+  h->scan_reserve = scan_reserve_sms;
+  return VLR_OK;
 }
 
 // device status word (mirrored to pinned host memory at the end of every search):
@@ -718,32 +752,37 @@ static inline void rec(vlr_index* h, int i, cudaStream_t s) {
 // ---------------------------------------------------------------- NVLink peer exchange plumbing
 // Exchange kinds: 0 = coarse stage 1 (x1, fp32 [nq][np] per rank), 1 = coarse
 // stage 2 (x2, 16-B entries [nq][np]), 2 = results (16-B entries [nq][k]).
-static PeerOut peer_out(const vlr_index* h, int kind) {
+// Each workspace slot has its own inbox region (flags included) and counters: two searches in flight
+// (cross-batch pipelining) never share one.
+static PeerOut peer_out(const vlr_index* h, int kind, int slot) {
   PeerOut o{};
   const auto& L = h->p2p;
-  const size_t off = kind == 0 ? L.off_x1 : kind == 1 ? L.off_x2 : L.off_res;
+  const size_t so = L.slot_bytes * (size_t)slot;
+  const size_t off = so + (kind == 0 ? L.off_x1 : kind == 1 ? L.off_x2 : L.off_res);
   for (int g = 0; g < L.G; ++g) {
     o.base[g] = static_cast<char*>(L.peer[g]) + off;
-    o.flag[g] = reinterpret_cast<uint32_t*>(static_cast<char*>(L.peer[g]) + L.off_flags) + kind * L.G;
+    o.flag[g] = reinterpret_cast<uint32_t*>(static_cast<char*>(L.peer[g]) + so + L.off_flags) + kind * L.G;
   }
   o.G = L.G;
   o.rank = h->ix.rank;
   o.epoch = L.epoch;
-  o.ctr = L.ctr + kind;
+  o.ctr = L.ctr + 3 * slot + kind;
   return o;
 }
-static PeerIn peer_in(vlr_index* h, int kind) {
+static PeerIn peer_in(vlr_index* h, int kind, int slot) {
   PeerIn i{};
   const auto& L = h->p2p;
-  i.flags = reinterpret_cast<const uint32_t*>(static_cast<char*>(L.inbox) + L.off_flags) + kind * L.G;
+  const size_t so = L.slot_bytes * (size_t)slot;
+  i.flags = reinterpret_cast<const uint32_t*>(static_cast<char*>(L.inbox) + so + L.off_flags) + kind * L.G;
   i.G = L.G;
   i.epoch = L.epoch;
-  i.status = h->ws.status;
+  i.status = h->wsl[slot].status;
   return i;
 }
-static void* inbox_region(vlr_index* h, int kind) {
+static void* inbox_region(vlr_index* h, int kind, int slot) {
   const auto& L = h->p2p;
-  return static_cast<char*>(L.inbox) + (kind == 0 ? L.off_x1 : kind == 1 ? L.off_x2 : L.off_res);
+  return static_cast<char*>(L.inbox) + L.slot_bytes * (size_t)slot +
+         (kind == 0 ? L.off_x1 : kind == 1 ? L.off_x2 : L.off_res);
 }
 
 // ---------------------------------------------------------------- the search pipeline
@@ -758,7 +797,10 @@ struct Pipe {
   const float* Q;
   int nq, np, k;
   cudaStream_t s;
+  int slot = 0;
+  Workspace* w = nullptr;  // the slot's workspace
   int n = 0;  // launches
+  bool lut_forked = false;  // this search forked K5 (joined before the scan)
 };
 
 static vlr_status lut_fork(vlr_index* h, Pipe& p) {
@@ -766,27 +808,28 @@ static vlr_status lut_fork(vlr_index* h, Pipe& p) {
     const char* e = getenv("VLR_LUT_SERIAL");
     h->lut_side = (e && e[0] == '1') ? 0 : 1;
   }
-  h->lut_forked = h->lut_side == 1 && h->profiling != 1;  // per-stage profiling keeps stages serial
-  if (!h->lut_forked) return VLR_OK;
-  if (!h->lut_stream) {
-    VLR_CUDA_TRY(cudaStreamCreateWithFlags(&h->lut_stream, cudaStreamNonBlocking));
-    VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->lut_fork, cudaEventDisableTiming));
-    VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->lut_join, cudaEventDisableTiming));
+  p.lut_forked = h->lut_side == 1 && h->profiling != 1;  // per-stage profiling keeps stages serial
+  if (!p.lut_forked) return VLR_OK;
+  auto& r = h->res[p.slot];
+  if (!r.lut_stream) {
+    VLR_CUDA_TRY(cudaStreamCreateWithFlags(&r.lut_stream, cudaStreamNonBlocking));
+    VLR_CUDA_TRY(cudaEventCreateWithFlags(&r.lut_fork, cudaEventDisableTiming));
+    VLR_CUDA_TRY(cudaEventCreateWithFlags(&r.lut_join, cudaEventDisableTiming));
   }
   // forked after K1 so K5's CTAs do not take SM slots from the filter's waves;
-  // everything before the fork on s (incl. the previous search's scan, which
-  // read w.lut) is ordered before K5
-  VLR_CUDA_TRY(cudaEventRecord(h->lut_fork, p.s));
-  VLR_CUDA_TRY(cudaStreamWaitEvent(h->lut_stream, h->lut_fork, 0));
-  VLR_CUDA_TRY(launch_lut(p.Q, h->ix, h->ws, p.nq, h->lut_stream)); ++p.n;
-  VLR_CUDA_TRY(cudaEventRecord(h->lut_join, h->lut_stream));
+  // everything before the fork on s (incl. the previous search of this slot, whose
+  // scan read w.lut) is ordered before K5
+  VLR_CUDA_TRY(cudaEventRecord(r.lut_fork, p.s));
+  VLR_CUDA_TRY(cudaStreamWaitEvent(r.lut_stream, r.lut_fork, 0));
+  VLR_CUDA_TRY(launch_lut(p.Q, h->ix, *p.w, p.nq, r.lut_stream)); ++p.n;
+  VLR_CUDA_TRY(cudaEventRecord(r.lut_join, r.lut_stream));
   return VLR_OK;
 }
 
 static vlr_status phase_a(vlr_index* h, Pipe& p, bool sharded, uint8_t* out_miss, int32_t* out_probes) {
   NvtxRange nv(h, sharded ? "vlr coarse stage 1 (qprep, K1, K2s1)" : "vlr coarse (qprep, K1, K2, K3a, K3b)");
   DeviceIndex& ix = h->ix;
-  Workspace& w = h->ws;
+  Workspace& w = *p.w;
   VLR_CUDA_TRY(cudaMemsetAsync(w.status, 0, sizeof(int32_t), p.s));
   rec(h, 0, p.s);
   const int t_lo = sharded ? ix.c_lo / 128 : 0;
@@ -799,7 +842,7 @@ static vlr_status phase_a(vlr_index* h, Pipe& p, bool sharded, uint8_t* out_miss
   if (st != VLR_OK) return st;
   rec(h, 1, p.s);
   if (sharded && h->p2p.on) {
-    const PeerOut po = peer_out(h, 0);
+    const PeerOut po = peer_out(h, 0, p.slot);
     VLR_CUDA_TRY(launch_select(ix, w, p.nq, p.np, filter_edot(ix.d), kSelStage1, p.s, &po)); ++p.n;
     return VLR_OK;
   }
@@ -815,15 +858,15 @@ static vlr_status phase_a(vlr_index* h, Pipe& p, bool sharded, uint8_t* out_miss
 static vlr_status phase_b(vlr_index* h, Pipe& p) {
   NvtxRange nv(h, "vlr coarse stage 2 (K2s2, K3a, K3b local)");
   DeviceIndex& ix = h->ix;
-  Workspace& w = h->ws;
+  Workspace& w = *p.w;
   const bool pp = h->p2p.on;
   PeerIn pi;
   PeerOut po;
   Workspace wv = w;  // the gathered buffers are the inbox regions under the peer exchange
   if (pp) {
-    pi = peer_in(h, 0);
-    po = peer_out(h, 1);
-    wv.x1_all = static_cast<float*>(inbox_region(h, 0));
+    pi = peer_in(h, 0, p.slot);
+    po = peer_out(h, 1, p.slot);
+    wv.x1_all = static_cast<float*>(inbox_region(h, 0, p.slot));
   }
   VLR_CUDA_TRY(launch_select(ix, wv, p.nq, p.np, filter_edot(ix.d), kSelStage2, p.s, nullptr, pp ? &pi : nullptr)); ++p.n;
   rec(h, 2, p.s);
@@ -836,12 +879,12 @@ static vlr_status phase_c(vlr_index* h, Pipe& p, bool sharded, int64_t* out_ids,
                           int32_t* out_probes, const Release* rel, bool packed) {
   NvtxRange nv(h, rel ? "vlr route + release scan (K4b, K6 REL, merger)" : "vlr route + scan + merge (K4b, K6, K7)");
   DeviceIndex& ix = h->ix;
-  Workspace& w = h->ws;
+  Workspace& w = *p.w;
   if (sharded) {
     if (h->p2p.on) {
-      const PeerIn pi = peer_in(h, 1);
+      const PeerIn pi = peer_in(h, 1, p.slot);
       Workspace wv = w;
-      wv.x2_all = static_cast<CoarseEntry*>(inbox_region(h, 1));
+      wv.x2_all = static_cast<CoarseEntry*>(inbox_region(h, 1, p.slot));
       VLR_CUDA_TRY(launch_refine(p.Q, ix, wv, p.nq, p.np, out_miss, out_probes, kRefMerge, p.s, nullptr, &pi)); ++p.n;
     } else {
       VLR_CUDA_TRY(launch_refine(p.Q, ix, w, p.nq, p.np, out_miss, out_probes, kRefMerge, p.s)); ++p.n;
@@ -850,8 +893,8 @@ static vlr_status phase_c(vlr_index* h, Pipe& p, bool sharded, int64_t* out_ids,
   }
   VLR_CUDA_TRY(launch_offsets(w, p.nq, p.np, p.s)); ++p.n;
   rec(h, 4, p.s);
-  if (h->lut_forked) {
-    VLR_CUDA_TRY(cudaStreamWaitEvent(p.s, h->lut_join, 0));
+  if (p.lut_forked) {
+    VLR_CUDA_TRY(cudaStreamWaitEvent(p.s, h->res[p.slot].lut_join, 0));
   } else {
     VLR_CUDA_TRY(launch_lut(p.Q, ix, w, p.nq, p.s)); ++p.n;
   }
@@ -868,7 +911,7 @@ static vlr_status phase_c(vlr_index* h, Pipe& p, bool sharded, int64_t* out_ids,
   rec(h, 6, p.s);
   if (!rel) {  // release mode: the scan merged and released every row itself
     if (h->p2p.on && packed) {
-      const PeerOut po = peer_out(h, 2);
+      const PeerOut po = peer_out(h, 2, p.slot);
       VLR_CUDA_TRY(launch_rank_merge(ix, w, p.nq, p.np, p.k, out_ids, out_dist, nullptr, p.s, &po)); ++p.n;
     } else {
       VLR_CUDA_TRY(launch_rank_merge(ix, w, p.nq, p.np, p.k, out_ids, out_dist, packed ? w.send : nullptr, p.s)); ++p.n;
@@ -892,10 +935,43 @@ static vlr_status check_search_args(vlr_index* h, int32_t nq, int32_t nprobe, in
   return VLR_OK;
 }
 
-// enqueue one search; the caller holds h->mu (the workspace and the residency are per handle)
+// Workspace slot of the next search: slot = seq % nslots. With more than one slot the
+// stream first waits for the slot's previous search (event), so searches on different streams can
+// overlap while none writes a slot another search still reads. Not under stream capture (the graph's
+// replays are ordered by the capturing stream). The caller holds h->mu.
+static bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+static vlr_status acquire_slot(vlr_index* h, int nq, int np, int k, cudaStream_t s, int* slot) {
+  const int b = h->nslots > 1 ? (int)(h->seq % (uint64_t)h->nslots) : 0;
+  vlr_status st = ensure_ws(h, b, nq, np, k);
+  if (st != VLR_OK) return st;
+  auto& r = h->res[b];
+  if (h->nslots > 1 && r.pending && !capturing(s)) {
+    VLR_CUDA_TRY(cudaStreamWaitEvent(s, r.done, 0));
+    r.pending = false;
+  }
+  Workspace& w = h->wsl[b];
+  w.n_cta = std::max(2, w.n_cta_cap - h->scan_reserve);
+  ++h->seq;
+  *slot = b;
+  return VLR_OK;
+}
+static vlr_status release_slot(vlr_index* h, int b, cudaStream_t s) {
+  if (h->nslots < 2 || capturing(s)) return VLR_OK;
+  auto& r = h->res[b];
+  if (!r.done) VLR_CUDA_TRY(cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming));
+  VLR_CUDA_TRY(cudaEventRecord(r.done, s));
+  r.pending = true;
+  return VLR_OK;
+}
+
+// enqueue one search; the caller holds h->mu (the workspace slots and the residency are per handle).
+// slot_in >= 0: the caller acquired that slot (vlr_search_host stages its queries there first).
 static vlr_status search_locked(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
                                 float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream,
-                                const Release* rel) {
+                                const Release* rel_in, int slot_in = -1, int* slot_out = nullptr) {
   int np = 0;
   vlr_status st = check_search_args(h, nq, nprobe, k, &np);
   if (st != VLR_OK) return st;
@@ -905,12 +981,18 @@ static vlr_status search_locked(vlr_index* h, const float* Q, int32_t nq, int32_
   if (!Q || !out_ids || !out_dist || !out_miss) return fail(VLR_ERR_INVALID_ARG, "null buffer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   VLR_CUDA_TRY(cudaSetDevice(ix.device));
-  st = ensure_ws(h, nq, np, k);
-  if (st != VLR_OK) return st;
-  Workspace& w = h->ws;
+  const bool p2p = h->p2p.on;  // NVLink peer exchange: collective over the ranks' inboxes, no NCCL calls
+  if (p2p) {
+    if (nq > h->p2p.cap_nq || np > h->p2p.cap_np || k > h->p2p.cap_k || k > kMaxK)
+      return fail(VLR_ERR_UNSUPPORTED, "peer exchange: batch beyond the caps reserved at vlr_p2p_export (or k > 32)");
+    if (rel_in) return fail(VLR_ERR_UNSUPPORTED, "peer exchange: early release is on the NCCL / shard-only paths");
+  }
+  int slot = slot_in;
+  if (slot < 0 && (st = acquire_slot(h, nq, np, k, s, &slot)) != VLR_OK) return st;
+  if (slot_out) *slot_out = slot;
+  Workspace& w = h->wsl[slot];
   st = take_status(w, " (detected in a previous search on this handle)");
   if (st != VLR_OK) return st;
-  const bool p2p = h->p2p.on;  // NVLink peer exchange: collective over the ranks' inboxes, no NCCL calls
   const bool exchange = ix.nccl != nullptr || p2p;
   if (ix.nccl && !p2p) {  // an error of an earlier asynchronous search on this communicator
     ncclResult_t as = ncclSuccess;
@@ -918,14 +1000,26 @@ static vlr_status search_locked(vlr_index* h, const float* Q, int32_t nq, int32_
         (as != ncclSuccess && as != ncclInProgress))
       return nccl_dead(h, std::string("NCCL asynchronous error of an earlier search: ") + ncclGetErrorString(as));
   }
-  if (p2p) {
-    if (nq > h->p2p.cap_nq || np > h->p2p.cap_np || k > h->p2p.cap_k || k > kMaxK)
-      return fail(VLR_ERR_UNSUPPORTED, "peer exchange: batch beyond the caps reserved at vlr_p2p_export (or k > 32)");
-    if (rel) return fail(VLR_ERR_UNSUPPORTED, "peer exchange: early release is on the NCCL / shard-only paths");
-    if (++h->p2p.epoch == 0) ++h->p2p.epoch;  // every rank runs the same searches: epochs agree
+  if (p2p && ++h->p2p.epoch == 0) ++h->p2p.epoch;  // every rank runs the same searches: epochs agree
+  Release relv{};
+  const Release* rel = nullptr;
+  if (rel_in) {  // the merger runs on the slot's own stream
+    auto& r = h->res[slot];
+    if (!r.rel_stream) {
+      VLR_CUDA_TRY(cudaStreamCreateWithFlags(&r.rel_stream, cudaStreamNonBlocking));
+      VLR_CUDA_TRY(cudaEventCreateWithFlags(&r.rel_fork, cudaEventDisableTiming));
+      VLR_CUDA_TRY(cudaEventCreateWithFlags(&r.rel_join, cudaEventDisableTiming));
+    }
+    relv = *rel_in;
+    relv.stream = r.rel_stream;
+    relv.fork = r.rel_fork;
+    relv.join = r.rel_join;
+    rel = &relv;
   }
   const bool sharded = p2p || (ix.nccl && ix.coarse_sharded);
   Pipe p{Q, nq, np, k, s};
+  p.slot = slot;
+  p.w = &w;
   if ((st = phase_a(h, p, sharded, out_miss, out_probes)) != VLR_OK) return st;
   if (exchange) VLR_CUDA_TRY(fault_stall(s));
   if (sharded && !p2p) {
@@ -939,8 +1033,8 @@ static vlr_status search_locked(vlr_index* h, const float* Q, int32_t nq, int32_
   if ((st = phase_c(h, p, sharded, out_ids, out_dist, out_miss, out_probes, rel, exchange && !rel)) != VLR_OK)
     return st;
   if (p2p) {
-    const PeerIn pi = peer_in(h, 2);
-    VLR_CUDA_TRY(launch_merge_packed(inbox_region(h, 2), h->p2p.G, nq, k, out_ids, out_dist, s, &pi)); ++p.n;
+    const PeerIn pi = peer_in(h, 2, slot);
+    VLR_CUDA_TRY(launch_merge_packed(inbox_region(h, 2, slot), h->p2p.G, nq, k, out_ids, out_dist, s, &pi)); ++p.n;
   } else if (exchange && !rel) {  // release mode: each rank releases its partial rows; vlr_merge_ready merges them
     if ((st = nccl_allgather(h, w.send, w.recv, (size_t)nq * k * sizeof(Packed), s, "results")) != VLR_OK) return st;
     VLR_CUDA_TRY(launch_merge_packed(w.recv, ix.world, nq, k, out_ids, out_dist, s)); ++p.n;
@@ -949,15 +1043,16 @@ static vlr_status search_locked(vlr_index* h, const float* Q, int32_t nq, int32_
   VLR_CUDA_TRY(cudaMemcpyAsync(w.h_status, w.status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   h->launches = p.n;
   if (h->profiling) h->prof_mode[h->nsearch++ % vlr_index::kRing] = h->profiling;
+  if (slot_in < 0) return release_slot(h, slot, s);
   return VLR_OK;
 }
 
 static vlr_status search_impl(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
                               float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream,
-                              const Release* rel) {
+                              const Release* rel, int* slot_out = nullptr) {
   if (!h) return fail(VLR_ERR_INVALID_ARG, "null index");
   std::lock_guard<std::mutex> lock(h->mu);
-  return search_locked(h, Q, nq, nprobe, k, out_ids, out_dist, out_miss, out_probes, stream, rel);
+  return search_locked(h, Q, nq, nprobe, k, out_ids, out_dist, out_miss, out_probes, stream, rel, -1, slot_out);
 }
 
 vlr_status vlr_search_async(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
@@ -991,13 +1086,7 @@ vlr_status vlr_search_release_async(vlr_index* h, const float* Q, int32_t nq, in
         !device_accessible(out_dist))
       return fail(VLR_ERR_INVALID_ARG, "release: ready/ids/dist must be device or pinned (mapped) host memory");
   }
-  if (!h->rel_stream) {
-    VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
-    VLR_CUDA_TRY(cudaStreamCreateWithFlags(&h->rel_stream, cudaStreamNonBlocking));
-    VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->rel_fork, cudaEventDisableTiming));
-    VLR_CUDA_TRY(cudaEventCreateWithFlags(&h->rel_join, cudaEventDisableTiming));
-  }
-  const Release rel{ready, epoch, out_ids, out_dist, h->rel_stream, h->rel_fork, h->rel_join};
+  const Release rel{ready, epoch, out_ids, out_dist, nullptr, nullptr, nullptr};  // stream: the slot's
   return search_impl(h, Q, nq, nprobe, k, out_ids, out_dist, out_miss, out_probes, stream, &rel);
 }
 
@@ -1119,10 +1208,11 @@ int32_t vlr_merge_ready(int32_t n_shards, const uint32_t* const* ready, uint32_t
 
 vlr_status vlr_search(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, int32_t k, int64_t* out_ids,
                       float* out_dist, uint8_t* out_miss, int32_t* out_probes, void* stream) {
-  vlr_status st = vlr_search_async(h, Q, nq, nprobe, k, out_ids, out_dist, out_miss, out_probes, stream);
+  int slot = 0;
+  vlr_status st = search_impl(h, Q, nq, nprobe, k, out_ids, out_dist, out_miss, out_probes, stream, nullptr, &slot);
   if (st != VLR_OK || nq == 0) return st;
   if ((st = wait_stream(h, reinterpret_cast<cudaStream_t>(stream))) != VLR_OK) return st;
-  return take_status(h->ws, "");
+  return take_status(h->wsl[slot], "");
 }
 
 static vlr_status search_host_impl(vlr_index* h, const float* hQ, int32_t nq, int32_t nprobe, int32_t k,
@@ -1137,24 +1227,27 @@ static vlr_status search_host_impl(vlr_index* h, const float* hQ, int32_t nq, in
   if (np > kMaxNprobe) return fail(VLR_ERR_UNSUPPORTED, "nprobe' > 2048");
   VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int slot = 0;
   {
     // the staging buffers belong to the handle's workspace, which ensure_ws may reallocate and
     // vlr_update_hot may free: size, stage and enqueue under the handle's mutex
     std::lock_guard<std::mutex> lock(h->mu);
-    vlr_status st = ensure_ws(h, nq, np, k);
+    vlr_status st = check_search_args(h, nq, nprobe, k, &slot);  // (validates before a slot is taken)
     if (st != VLR_OK) return st;
-    Workspace& w = h->ws;
+    if ((st = acquire_slot(h, nq, np, k, s, &slot)) != VLR_OK) return st;
+    Workspace& w = h->wsl[slot];
     VLR_CUDA_TRY(cudaMemcpyAsync(w.d_q, hQ, sizeof(float) * nq * h->ix.d, cudaMemcpyHostToDevice, s));
     st = search_locked(h, w.d_q, nq, nprobe, k, w.d_ids, w.d_dist, w.d_miss, h_probes ? w.d_probes : nullptr, stream,
-                       nullptr);
+                       nullptr, slot);
     if (st != VLR_OK) return st;
     VLR_CUDA_TRY(cudaMemcpyAsync(h_ids, w.d_ids, sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, s));
     VLR_CUDA_TRY(cudaMemcpyAsync(h_dist, w.d_dist, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, s));
     VLR_CUDA_TRY(cudaMemcpyAsync(h_miss, w.d_miss, (size_t)nq * np, cudaMemcpyDeviceToHost, s));
     if (h_probes)
       VLR_CUDA_TRY(cudaMemcpyAsync(h_probes, w.d_probes, sizeof(int32_t) * nq * np, cudaMemcpyDeviceToHost, s));
+    if ((st = release_slot(h, slot, s)) != VLR_OK) return st;
   }
-  Workspace& w = h->ws;
+  Workspace& w = h->wsl[slot];
   if (!sync) return VLR_OK;  // results land when `stream` reaches this point; status: next call
   vlr_status st = wait_stream(h, s);
   if (st != VLR_OK) return st;
@@ -1186,7 +1279,7 @@ static vlr_status staged_begin(vlr_index* h, const float* Q, int32_t nq, int32_t
   VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
   // sized for any k up front: a reallocation between the stages would drop the LUT and the gathered
   // buffers of the batch in flight
-  return ensure_ws(h, nq, *np, std::max(k, kMaxK));  // k <= 32 only (vlr.h: staged search)
+  return ensure_ws(h, h->stage_slot, nq, *np, std::max(k, kMaxK));  // k <= 32 only (vlr.h: staged search)
 }
 
 vlr_status vlr_coarse_stage1(vlr_index* h, const float* Q, int32_t nq, int32_t nprobe, float* d_x1, void* stream) {
@@ -1196,11 +1289,17 @@ vlr_status vlr_coarse_stage1(vlr_index* h, const float* Q, int32_t nq, int32_t n
   vlr_status st = staged_begin(h, Q, nq, nprobe, 1, &np);
   if (st != VLR_OK) return st;
   if (!d_x1) return fail(VLR_ERR_INVALID_ARG, "null x1");
-  if ((st = take_status(h->ws, " (detected in a previous search on this handle)")) != VLR_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int slot = 0;  // the batch keeps this workspace slot through stage 3
+  if ((st = acquire_slot(h, nq, np, kMaxK, s, &slot)) != VLR_OK) return st;
+  h->stage_slot = slot;
+  Workspace& w = h->wsl[slot];
+  if ((st = take_status(w, " (detected in a previous search on this handle)")) != VLR_OK) return st;
   Pipe p{Q, nq, np, 1, s};
+  p.slot = slot;
+  p.w = &w;
   if ((st = phase_a(h, p, true, nullptr, nullptr)) != VLR_OK) return st;
-  VLR_CUDA_TRY(cudaMemcpyAsync(d_x1, h->ws.x1, sizeof(float) * nq * np, cudaMemcpyDeviceToDevice, s));
+  VLR_CUDA_TRY(cudaMemcpyAsync(d_x1, w.x1, sizeof(float) * nq * np, cudaMemcpyDeviceToDevice, s));
   h->stage = 1;
   h->stage_nq = nq;
   h->stage_np = np;
@@ -1219,9 +1318,11 @@ vlr_status vlr_coarse_stage2(vlr_index* h, const float* Q, int32_t nq, int32_t n
   if (h->stage != 1 || h->stage_nq != nq || h->stage_np != np)
     return fail(VLR_ERR_INVALID_ARG, "vlr_coarse_stage2 must follow vlr_coarse_stage1 of the same batch");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  Workspace& w = h->ws;
+  Workspace& w = h->wsl[h->stage_slot];
   VLR_CUDA_TRY(cudaMemcpyAsync(w.x1_all, d_x1_all, sizeof(float) * nq * np * h->ix.world, cudaMemcpyDeviceToDevice, s));
   Pipe p{Q, nq, np, 1, s};
+  p.slot = h->stage_slot;
+  p.w = &w;
   if ((st = phase_b(h, p)) != VLR_OK) return st;
   VLR_CUDA_TRY(cudaMemcpyAsync(d_x2, w.x2, sizeof(CoarseEntry) * nq * np, cudaMemcpyDeviceToDevice, s));
   h->stage = 2;
@@ -1240,13 +1341,16 @@ vlr_status vlr_search_stage3(vlr_index* h, const float* Q, int32_t nq, int32_t n
   if (h->stage != 2 || h->stage_nq != nq || h->stage_np != np)
     return fail(VLR_ERR_INVALID_ARG, "vlr_search_stage3 must follow vlr_coarse_stage2 of the same batch");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  Workspace& w = h->ws;
+  Workspace& w = h->wsl[h->stage_slot];
   VLR_CUDA_TRY(cudaMemcpyAsync(w.x2_all, d_x2_all, sizeof(CoarseEntry) * nq * np * h->ix.world,
                                cudaMemcpyDeviceToDevice, s));
   Pipe p{Q, nq, np, k, s};
+  p.slot = h->stage_slot;
+  p.w = &w;
   if ((st = phase_c(h, p, true, d_ids, d_dist, d_miss, d_probes, nullptr, false)) != VLR_OK) return st;
   rec(h, 8, s);
   VLR_CUDA_TRY(cudaMemcpyAsync(w.h_status, w.status, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if ((st = release_slot(h, h->stage_slot, s)) != VLR_OK) return st;
   h->stage = 0;
   h->launches += p.n;
   if (h->profiling) h->prof_mode[h->nsearch++ % vlr_index::kRing] = h->profiling;
@@ -1261,12 +1365,15 @@ vlr_status vlr_p2p_export(vlr_index* h, void* handle_out) {
   std::lock_guard<std::mutex> lock(h->mu);
   const DeviceIndex& ix = h->ix;
   if (ix.world < 2 || ix.world > kMaxWorld) return fail(VLR_ERR_UNSUPPORTED, "peer exchange needs 2 <= world <= 8");
-  Workspace& w = h->ws;
-  if (!w.status) return fail(VLR_ERR_INVALID_ARG, "vlr_p2p_export: call vlr_reserve first (the inbox is sized by it)");
+  Workspace& w = h->wsl[0];
+  for (int b = 0; b < h->nslots; ++b)
+    if (!h->wsl[b].status)
+      return fail(VLR_ERR_INVALID_ARG, "vlr_p2p_export: call vlr_reserve first (the inbox is sized by it)");
   VLR_CUDA_TRY(cudaSetDevice(ix.device));
   p2p_close(h);
   auto& L = h->p2p;
   L.G = ix.world;
+  L.nslots = h->nslots;
   L.cap_nq = w.cap_nq;
   L.cap_np = w.cap_np;
   L.cap_k = std::min(w.cap_k, kMaxK);
@@ -1275,11 +1382,12 @@ vlr_status vlr_p2p_export(vlr_index* h, void* handle_out) {
   L.off_x2 = align256(L.off_x1 + G * nq * np * sizeof(float));
   L.off_res = align256(L.off_x2 + G * nq * np * sizeof(CoarseEntry));
   L.off_flags = align256(L.off_res + G * nq * k * sizeof(Packed));
-  L.bytes = align256(L.off_flags + 3 * G * sizeof(uint32_t));
+  L.slot_bytes = align256(L.off_flags + 3 * G * sizeof(uint32_t));
+  L.bytes = L.slot_bytes * (size_t)L.nslots;
   VLR_CUDA_TRY(cudaMalloc(&L.inbox, L.bytes));
   VLR_CUDA_TRY(cudaMemset(L.inbox, 0, L.bytes));
-  VLR_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&L.ctr), 3 * sizeof(int)));
-  VLR_CUDA_TRY(cudaMemset(L.ctr, 0, 3 * sizeof(int)));
+  VLR_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&L.ctr), 3 * L.nslots * sizeof(int)));
+  VLR_CUDA_TRY(cudaMemset(L.ctr, 0, 3 * L.nslots * sizeof(int)));
   cudaIpcMemHandle_t mh;
   VLR_CUDA_TRY(cudaIpcGetMemHandle(&mh, L.inbox));
   static_assert(sizeof(mh) == 64, "cudaIpcMemHandle_t is 64 bytes");

@@ -619,42 +619,48 @@ constexpr int kExactStages = 3;
 
 template <int MET, int S, int W, int CH = 1>
 __global__ void __launch_bounds__(W * 32) k_exact(const float* __restrict__ Q, const float* __restrict__ C,
-                                                  int d, const int32_t* __restrict__ cand,
+                                                  int d, int nq, int ny, const int32_t* __restrict__ cand,
                                                   const int32_t* __restrict__ ncand,
                                                   double* __restrict__ exact) {
   extern __shared__ __align__(16) unsigned char sm[];
-  const int q = blockIdx.x;
-  const int nc = ncand[q];
-  const int g0 = blockIdx.y * W * 32 * CH;
-  if (nc > kCandCap || g0 >= nc) return;
   double* qs = reinterpret_cast<double*>(sm);
   float* tiles = reinterpret_cast<float*>(qs + ((d + 1) & ~1));
-  for (int t = threadIdx.x; t < d; t += blockDim.x) qs[t] = (double)Q[(size_t)q * d + t];
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int32_t* lst = cand + (size_t)q * kCandCap;
-  // groups of 32 CH candidates: this warp takes g = g0 + 32 CH warp + stride i
-  const int stride = gridDim.y * W * 32 * CH;
-  for (int g = g0 + warp * 32 * CH; g < nc; g += stride) {
-    const int j = g + lane;
-    const int rid = lst[j < nc ? j : g];
-    if constexpr (CH == 2) {
-      if ((d & 3) == 0 && g + 32 < nc) {  // a second chain with at least one real candidate
-        const int j1 = j + 32;
-        const int rid1 = lst[j1 < nc ? j1 : g];
-        double D0, D1;
-        warp_exact2<S, MET>(qs, C, d, rid, rid1, tiles + warp * (S * 2048), lane, D0, D1);
-        if (j < nc) exact[(size_t)q * kCandCap + j] = D0;
-        if (j1 < nc) exact[(size_t)q * kCandCap + j1] = D1;
-        continue;
+  // persistent over tasks (q, y) = candidate block y of query q, y-major (every query's first block
+  // first): a task past the query's candidate count costs one L2 read here instead of a CTA launch
+  // (the grid of empty CTAs dominated at world 8, where a rank holds ~20 candidates per query)
+  for (int t = blockIdx.x; t < nq * ny; t += gridDim.x) {
+    const int q = t % nq, y = t / nq;
+    const int nc = ncand[q];
+    const int g0 = y * W * 32 * CH;
+    if (nc > kCandCap || g0 >= nc) continue;  // CTA-uniform
+    __syncthreads();  // qs of the previous task consumed
+    for (int i = threadIdx.x; i < d; i += blockDim.x) qs[i] = (double)Q[(size_t)q * d + i];
+    __syncthreads();
+    const int32_t* lst = cand + (size_t)q * kCandCap;
+    // groups of 32 CH candidates: this warp takes g = g0 + 32 CH warp + stride i
+    const int stride = ny * W * 32 * CH;
+    for (int g = g0 + warp * 32 * CH; g < nc; g += stride) {
+      const int j = g + lane;
+      const int rid = lst[j < nc ? j : g];
+      if constexpr (CH == 2) {
+        if ((d & 3) == 0 && g + 32 < nc) {  // a second chain with at least one real candidate
+          const int j1 = j + 32;
+          const int rid1 = lst[j1 < nc ? j1 : g];
+          double D0, D1;
+          warp_exact2<S, MET>(qs, C, d, rid, rid1, tiles + warp * (S * 2048), lane, D0, D1);
+          if (j < nc) exact[(size_t)q * kCandCap + j] = D0;
+          if (j1 < nc) exact[(size_t)q * kCandCap + j1] = D1;
+          continue;
+        }
       }
+      double D;
+      if ((d & 3) == 0)
+        D = warp_exact<S, MET>(qs, C, d, rid, tiles + warp * (S * 1024 * CH), lane);
+      else
+        D = scalar_exact<MET>(qs, C, d, rid);
+      if (j < nc) exact[(size_t)q * kCandCap + j] = D;
     }
-    double D;
-    if ((d & 3) == 0)
-      D = warp_exact<S, MET>(qs, C, d, rid, tiles + warp * (S * 1024 * CH), lane);
-    else
-      D = scalar_exact<MET>(qs, C, d, rid);
-    if (j < nc) exact[(size_t)q * kCandCap + j] = D;
   }
 }
 
@@ -664,8 +670,14 @@ static cudaError_t launch_exact_t(const float* Q, const DeviceIndex& ix, const W
   auto fn = ix.metric == 1 ? k_exact<1, S, W, CH> : k_exact<0, S, W, CH>;
   cudaError_t e = ensure_smem((const void*)fn, sm);
   if (e != cudaSuccess) return e;
-  dim3 grid(nq, 1024 / (W * 32 * CH));  // 1024 candidates per pass; queries with more loop
-  fn<<<grid, W * 32, sm, s>>>(Q, ix.centroids, ix.d, ws.cand, ws.ncand, ws.exact);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, W * 32, sm)) != cudaSuccess) return e;
+  const int ny = 1024 / (W * 32 * CH);  // 1024 candidates per pass over a query's list; more loop
+  const int tasks = nq * ny;
+  const int grid = std::max(1, std::min(tasks, sms * std::max(per_sm, 1)));
+  fn<<<grid, W * 32, sm, s>>>(Q, ix.centroids, ix.d, nq, ny, ws.cand, ws.ncand, ws.exact);
   return cudaGetLastError();
 }
 

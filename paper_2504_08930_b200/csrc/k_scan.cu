@@ -826,7 +826,7 @@ int scan_ctas(const DeviceIndex& ix) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms;  // one persistent CTA per SM (128 KB LUT + 16 warps)
+  return sms;  // at most one persistent CTA per SM (128 KB LUT + 16 warps); capi.cu may leave SMs free
 }
 
 template <int MP, int NB, int EXP, bool REL = false, bool DUMP = false>

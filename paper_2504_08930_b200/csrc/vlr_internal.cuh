@@ -107,7 +107,9 @@ struct DeviceIndex {
 };
 
 struct Workspace {
-  int cap_nq = 0, cap_np = 0, cap_k = 0, n_cta = 0;
+  int cap_nq = 0, cap_np = 0, cap_k = 0;
+  int n_cta_cap = 0;           // SM count: the partial-list slots are sized for a grid this large
+  int n_cta = 0;               // the current search's scan grid (n_cta_cap - the handle's scan reserve)
   float* qnorm = nullptr;      // [nq] ||q|| (fp32, rounded up; filter band)
   float* qsq = nullptr;        // [nq] ||q||^2 (fp64 sum -> fp32; term1 of L2 with by_residual = 0)
   uint16_t* qf16 = nullptr;    // [nq][d8] fp16(q * 2^e_q) (RN), zero-padded (filter operand B)
@@ -152,7 +154,26 @@ struct Workspace {
 
 struct vlr_index {
   vlr::DeviceIndex ix;
-  vlr::Workspace ws;
+  // Workspace slots (cross-batch pipelining): search number i uses slot i % nslots; a
+  // search waits (stream event) for the previous user of its slot before it writes the slot, so two
+  // searches enqueued on different streams overlap on the device (batch i+1's coarse stage beside batch
+  // i's scan). nslots = 1 (default): one workspace, every search is ordered by its stream alone.
+  static constexpr int kSlots = 2;
+  vlr::Workspace wsl[kSlots];
+  struct SlotRes {
+    cudaEvent_t done = nullptr;   // recorded at the end of the slot's last search
+    bool pending = false;         // `done` was recorded and not yet waited for by a later user
+    // K5 side stream: the LUT depends only on Q (residual decomposition), so it runs beside
+    // K2-K4 (latency-bound, few CTAs) and joins before the scan
+    cudaStream_t lut_stream = nullptr;
+    cudaEvent_t lut_fork = nullptr, lut_join = nullptr;
+    // NEXT-4 merger stream + fork/join events (created on first use)
+    cudaStream_t rel_stream = nullptr;
+    cudaEvent_t rel_fork = nullptr, rel_join = nullptr;
+  } res[kSlots];
+  int nslots = 1;
+  int scan_reserve = 0;      // SMs the scan's persistent grid leaves free (vlr_set_pipeline)
+  uint64_t seq = 0;          // searches started (slot = seq % nslots)
   int profiling = 0;  // 0 off, 1 every stage, 2 scan only
   static constexpr int kRing = 64;
   cudaEvent_t ev[kRing][9] = {};
@@ -160,26 +181,20 @@ struct vlr_index {
   int64_t nsearch = 0;       // searches recorded while profiling
   int launches = 0;
   bool dead = false;  // NCCL failure
-  // NVLink peer exchange (vlr_p2p_*): every rank's inbox IPC-mapped here
+  // NVLink peer exchange (vlr_p2p_*): every rank's inbox IPC-mapped here; one region per
+  // workspace slot (two searches in flight exchange through different regions)
   struct PeerLink {
     bool on = false;
-    int cap_nq = 0, cap_np = 0, cap_k = 0, G = 0;
+    int cap_nq = 0, cap_np = 0, cap_k = 0, G = 0, nslots = 1;
     void* inbox = nullptr;                    // own inbox (cudaMalloc base, exported with cudaIpcGetMemHandle)
-    size_t bytes = 0, off_x1 = 0, off_x2 = 0, off_res = 0, off_flags = 0;
+    size_t bytes = 0, slot_bytes = 0, off_x1 = 0, off_x2 = 0, off_res = 0, off_flags = 0;  // offsets within a slot
     void* peer[vlr::kMaxWorld] = {};          // every rank's inbox base (own = inbox; others IPC-opened)
-    int* ctr = nullptr;                       // [3] CTA-completion counters
+    int* ctr = nullptr;                       // [nslots][3] CTA-completion counters
     uint32_t epoch = 0;
   } p2p;
   std::mutex mu;  // held while a search is enqueued and while vlr_update_hot swaps the residency
-  cudaStream_t rel_stream = nullptr;  // NEXT-4 merger stream + fork/join events (created on first use)
-  cudaEvent_t rel_fork = nullptr, rel_join = nullptr;
-  // K5 side stream: the LUT depends only on Q (residual decomposition),
-  // so it runs beside K2-K4 (latency-bound, few CTAs) and joins before the scan
-  cudaStream_t lut_stream = nullptr;
-  cudaEvent_t lut_fork = nullptr, lut_join = nullptr;
   int lut_side = -1;  // -1 unset; 0 serial (VLR_LUT_SERIAL=1, A/B timing), 1 forked
-  bool lut_forked = false;  // the current search forked K5 (joined before the scan)
-  int stage = 0, stage_nq = 0, stage_np = 0;  // staged search progress (vlr_coarse_stage1/2, vlr_search_stage3)
+  int stage = 0, stage_nq = 0, stage_np = 0, stage_slot = 0;  // staged search progress (vlr_coarse_stage1/2, vlr_search_stage3)
   std::string last_err;
 };
 
@@ -224,8 +239,8 @@ struct Release {               // NEXT-4 early per-query release (vlr_search_rel
   uint32_t epoch;
   int64_t* out_ids;
   float* out_dist;
-  cudaStream_t stream;         // the merger CTA's stream (forked from / joined to the search stream)
-  cudaEvent_t fork, join;
+  cudaStream_t stream;         // the merger CTA's stream (forked from / joined to the search stream; set per
+  cudaEvent_t fork, join;      // workspace slot by the search)
 };
 cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int np, int k, cudaStream_t s,
                         const Release* rel = nullptr);

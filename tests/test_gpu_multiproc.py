@@ -87,7 +87,7 @@ def test_two_process_staged_search_one_gpu():
         assert bit, f"rank {rank}: staged two-process result differs from the single-GPU search"
 
 
-def _p2p_worker(rank, world, port, out_q):
+def _p2p_worker(rank, world, port, out_q, pipelined=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -102,6 +102,8 @@ def _p2p_worker(rank, world, port, out_q):
         Q = datagen.make_queries(c["N"], c["d"], c["nlist"], c["batch"], stream=2, alpha=c["alpha"])
         Qd = torch.from_numpy(Q).cuda()
         h = vlr.Index.from_arrays(ix, rank=rank, world=world, device=0)
+        if pipelined:  # two workspace slots = two inbox regions; searches alternate over two streams
+            h.set_pipeline(2, 8)
         h.reserve(c["batch"], c["nprobe"], c["k"])
         mine = h.p2p_export()
         handles = [None] * world
@@ -109,8 +111,14 @@ def _p2p_worker(rank, world, port, out_q):
         h.p2p_connect(handles)
         dist.barrier()
         outs = []
-        for it in range(3):  # collective searches over the peer inboxes (epochs advance together)
-            outs.append(h.search(Qd, c["nprobe"], c["k"], sync=True))
+        if pipelined:
+            ss = [torch.cuda.Stream(), torch.cuda.Stream()]
+            for it in range(6):  # slots 0,1,0,1,...: batch i+1 enqueued before batch i completes
+                outs.append(h.search(Qd, c["nprobe"], c["k"], stream=ss[it % 2]))
+            torch.cuda.synchronize()
+        else:
+            for it in range(3):  # collective searches over the peer inboxes (epochs advance together)
+                outs.append(h.search(Qd, c["nprobe"], c["k"], sync=True))
         got = dict(ids=outs[-1][0].cpu().numpy(), dist=outs[-1][1].cpu().numpy(), miss=outs[-1][2].cpu().numpy(),
                    probes=outs[-1][3].cpu().numpy())
         dist.barrier()
@@ -127,6 +135,32 @@ def _p2p_worker(rank, world, port, out_q):
         out_q.put((rank, False, [repr(e)]))
     finally:
         dist.destroy_process_group()
+
+
+def _run_p2p(pipelined):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q, pipelined)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def test_two_process_peer_exchange_pipelined_one_gpu():
+    """Cross-batch pipelining over the peer exchange (vlr_set_pipeline(2, 8)): six
+    collective searches alternate over two streams per rank, so batch i+1's coarse
+    stage and its stage-1/2 exchanges run while batch i is still in flight; each
+    slot exchanges through its own inbox region. Every row equals the single-GPU
+    search bitwise and passes R1-R4."""
+    for rank, bit, errs in _run_p2p(True):
+        assert not errs, (rank, errs)
+        assert bit, f"rank {rank}: pipelined peer-exchange result differs from the single-GPU search"
 
 
 def test_two_process_nvlink_peer_exchange_one_gpu():

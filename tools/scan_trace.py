@@ -23,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C4")
     ap.add_argument("--G", default="1,8", help="shard counts (rank 0's shard traced)")
+    ap.add_argument("--release", action="store_true", help="trace the NEXT-4 release scan (REL waves) too")
     a = ap.parse_args()
     import datagen
     import paper_2504_08930_b200 as vlr
@@ -35,17 +36,24 @@ def main():
     for G in [int(x) for x in a.G.split(",")]:
         h = vlr.Index.from_arrays(ix) if G == 1 else vlr.Index.from_arrays(ix, rank=0, world=G)
         print(json.dumps(trace(h, c, Q, L, a.config, G)), flush=True)
+        if a.release:
+            print(json.dumps(trace(h, c, Q, L, a.config, G, release=True)), flush=True)
         h.close()
 
 
-def trace(h, c, Q, L, config, G):
-    out = {"config": config, "G": G, "runs": []}
+def trace(h, c, Q, L, config, G, release=False):
+    out = {"config": config, "G": G, "release": release, "runs": []}
     for it in range(6):
         h.set_profiling(2)
-        h.search(Q, c["nprobe"], c["k"], sync=True)
+        if release:
+            h.search_release(Q, c["nprobe"], c["k"])
+            torch.cuda.synchronize()
+        else:
+            h.search(Q, c["nprobe"], c["k"], sync=True)
         scan_ms = h.stage_times(0)["scan"]
-        t = np.zeros((148, 6), np.uint64)
-        assert L.vlr_debug_scan_trace(t.ctypes.data, 148) == 0
+        n = 147 if release else 148  # the release scan leaves one SM to the merger CTA
+        t = np.zeros((n, 6), np.uint64)
+        assert L.vlr_debug_scan_trace(t.ctypes.data, n) == 0
         t = t.astype(np.int64)
         t0 = t[:, 0].min()
         st, en = (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3

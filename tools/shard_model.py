@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--seed", type=int, default=2504_08930)
     ap.add_argument("--backlog-cycles", type=int, default=10_000_000)
+    ap.add_argument("--pipe-reserve", default="0,8,16,24,32",
+                    help="scan reserves for the pipelined single-rank pass ('' = skip)")
     a = ap.parse_args()
     import datagen
     import paper_2504_08930_b200 as vlr
@@ -61,6 +63,7 @@ def main():
         return e
 
     rows = []
+    xs = []  # per batch: (x1_all, x2_all), replayed by the pipelined single-rank pass
     for b in range(a.warmup + a.batches):
         Q = Qd[b]
         # backlog the stream (~5 ms spin) so every launch of the batch is queued before the first event
@@ -79,6 +82,7 @@ def main():
             x2.append(h.coarse_stage2(Q, c["nprobe"], x1_all, stream=s))
             e2.append((e0, ev()))
         x2_all = torch.stack(x2)
+        xs.append((x1_all, x2_all))
         e3, parts = [], []
         for h in hs:
             h.set_profiling(2)
@@ -121,7 +125,50 @@ def main():
         "model": "step(G) = max over ranks of (stage1 + stage2 + stage3) + 3 all-gathers (x1 nq*np*4 B, x2 "
                  "nq*np*16 B, results nq*k*16 B per rank; NVLink latency, not measurable on one GPU) + K8 merge",
     }
+    if a.pipe_reserve:
+        out["pipelined_rank"] = pipelined_rank(a, c, hs, Qd, xs, int(np.argmax((T1 + T2 + T3).mean(0))))
     print(json.dumps(out), flush=True)
+
+
+def pipelined_rank(a, c, hs, Qd, xs, r):
+    """One rank's step with cross-batch pipelining (vlr_set_pipeline(2, R)): rank r's staged calls of
+    consecutive batches alternate over two streams; the exchanges are replaced by the gathered x1_all /
+    x2_all the serial pass produced (zero-latency transport), so the loop holds exactly rank r's kernels
+    (+ two small D2D copies of the gathered slabs per batch). Device ms per batch from CUDA events around
+    the whole loop; R = SMs the scan leaves to the other stream's coarse stage."""
+    B, K = c["batch"], c["k"]
+    h = hs[r]
+    n = a.warmup + a.batches
+    ss = [torch.cuda.Stream(), torch.cuda.Stream()]
+
+    def loop(alt):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(ss[0]):
+            torch.cuda._sleep(2 * a.backlog_cycles)  # backlog: the whole loop is enqueued before e0 fires
+        e0.record(ss[0])
+        ss[1].wait_event(e0)
+        for b in range(n):
+            st = ss[b % 2] if alt else ss[0]
+            h.coarse_stage1(Qd[b], c["nprobe"], stream=st)
+            h.coarse_stage2(Qd[b], c["nprobe"], xs[b][0], stream=st)
+            h.search_stage3(Qd[b], c["nprobe"], K, xs[b][1], stream=st)
+        ss[0].wait_stream(ss[1])
+        e1.record(ss[0])
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n
+
+    res = {"rank": r}
+    h.set_pipeline(1, 0)
+    loop(False)
+    res["serial_ms"] = min(loop(False) for _ in range(3))
+    for R in [int(x) for x in a.pipe_reserve.split(",")]:
+        h.set_pipeline(2, R)
+        loop(True)
+        res[f"pipelined_R{R}_ms"] = min(loop(True) for _ in range(3))
+    h.set_pipeline(1, 0)
+    res["how"] = pipelined_rank.__doc__.split("\n")[0]
+    return res
 
 
 if __name__ == "__main__":
