@@ -70,9 +70,10 @@ def parse():
     p.add_argument("--lat-batches", type=int, default=1000,
                    help="latency pass: CUDA-graph closed-loop batches per batch size (SURVEY §8(d): >= 1000)")
     p.add_argument("--sustained-s", type=float, default=10.0, help="sustained pass length (s), batch of the config")
-    p.add_argument("--pipeline", type=int, default=1, choices=[0, 1],
+    p.add_argument("--pipeline", type=int, default=-1, choices=[-1, 0, 1],
                    help="1: cross-batch pipelining (vlr_set_pipeline: two workspace slots, batches alternate over "
-                        "two streams, batch i+1's coarse stage beside batch i's scan); 0: one stream")
+                        "two streams, batch i+1's coarse stage beside batch i's scan); 0: one stream; -1 (default): "
+                        "on at N > 1 only (one GPU: no gain measured, DESIGN.md §5b)")
     p.add_argument("--scan-reserve", type=int, default=-1,
                    help="SMs the scan leaves to the other stream's coarse stage when pipelining (-1: default)")
     p.add_argument("--sweep-out", default=None,
@@ -398,7 +399,7 @@ def main():
         xchg = "p2p"  # NCCL refuses two ranks on one device
     # cross-batch pipelining: not for the staged dry-run transport (host-synchronous gloo
     # exchanges) nor NCCL (the communicator serialises its collectives across streams)
-    pipe = bool(a.pipeline) and xchg in ("none", "p2p")
+    pipe = (a.pipeline == 1 or (a.pipeline < 0 and world > 1)) and xchg in ("none", "p2p")
     reserve = a.scan_reserve if a.scan_reserve >= 0 else default_reserve(world)
     if pipe:
         h.set_pipeline(2, reserve)

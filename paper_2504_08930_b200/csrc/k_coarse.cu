@@ -431,6 +431,8 @@ static int sort_cap(int np) {
   return c;
 }
 constexpr int kRefinePer = (kMaxNprobe + kRefineThreads - 1) / kRefineThreads;  // router items per thread
+static_assert(kRescanWarps * 2048 * sizeof(float) >= kMaxNprobe * (sizeof(double) + sizeof(int)),
+              "kRefMerge's rank-merge output lives in the rescan tiles");
 
 __device__ __forceinline__ bool key_less(double a, int ia, double b, int ib) {
   return a < b || (a == b && ia < ib);
@@ -683,10 +685,10 @@ static cudaError_t launch_exact_t(const float* Q, const DeviceIndex& ix, const W
 
 cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
-  // VLR_EXACT_CFG="S,W[,CH]" (stages, warps, chains per lane) overrides the product choice: (3, 4, 1) on one
-  // GPU (~200 candidates per query: throughput regime, profiles/k3a_sweep_r01.txt), (16, 1, 1) with the
-  // sharded coarse stage at world >= 4 (~25 candidates per query and rank: one warp per query, latency
-  // regime -> half a candidate row of loads in flight per warp)
+  // VLR_EXACT_CFG="S,W[,CH]" (stages, warps, chains per lane) overrides the product choice (3, 4, 1)
+  // (profiles/k3a_sweep_r01.txt). The sharded coarse stage uses it too: a rank's candidates are not ~1/G of
+  // every query's but concentrate on the queries whose neighbourhood lies in its centroid range (ids are
+  // not random), so one warp per query (the former (16, 1) latency choice) serialised up to ~5 passes
   static int env_s = -1, env_w = 0, env_c = 1;
   if (env_s < 0) {
     env_s = 0;
@@ -698,7 +700,6 @@ cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace&
     }
   }
   int S = 3, W = 4, CH = 1;
-  if (ix.world >= 4 && (ix.nccl || ix.shard_only) && ix.d <= 1024) { S = 16; W = 1; }
   if (env_s > 0) { S = env_s; W = env_w; CH = env_c; }
   const int cfg = S * 100 + W * 10 + CH;
   switch (cfg) {
@@ -760,7 +761,55 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
     peer_wait(pin);  // NVLink peer exchange: every rank's x2 slab has landed in this rank's inbox
     // G sorted lists of np entries; padding (+inf, -1) is skipped
     const int src_len = world * np;
-    for (int pos = 0; pos < src_len; pos += kRefineChunk) {
+    if (src_len <= scap) {
+      // merge by rank (one pass, no sort): every list is sorted by (D, l) and the ids are distinct across
+      // lists (disjoint centroid ranges), so an entry's position in the union is its index in its own list
+      // plus, for every other list, the number of its entries that precede it (binary search in shared
+      // memory). Entries of position < np are the global top np, in order -- the same unique sequence the
+      // bitonic path produces. Padding is staged as (+inf, INT_MAX): after every real entry.
+      for (int i = threadIdx.x; i < src_len; i += blockDim.x) {
+        const int r = i / np, j = i - r * np;
+        const CoarseEntry e = x2_all[((size_t)r * nq + q) * np + j];
+        key[i] = e.l >= 0 ? e.D : CUDART_INF;
+        id[i] = e.l >= 0 ? e.l : 0x7fffffff;
+      }
+      if (threadIdx.x == 0) s_cnt = 0;
+      __syncthreads();
+      double* okey = reinterpret_cast<double*>(tiles);  // [np] (the rescan tiles are unused in this mode)
+      int* oid = reinterpret_cast<int*>(okey + np);      // [np]
+      for (int i = threadIdx.x; i < src_len; i += blockDim.x) {
+        const int r = i / np, j = i - r * np;
+        const double D = key[i];
+        const int l = id[i];
+        if (l == 0x7fffffff) continue;
+        atomicAdd(&s_cnt, 1);
+        int rk = j;
+        for (int r2 = 0; r2 < world && rk < np; ++r2) {
+          if (r2 == r) continue;
+          const double* k2 = key + r2 * np;
+          const int* i2 = id + r2 * np;
+          int lo2 = 0, hi2 = np;
+          while (lo2 < hi2) {
+            const int m = (lo2 + hi2) >> 1;
+            if (key_less(k2[m], i2[m], D, l)) lo2 = m + 1;
+            else hi2 = m;
+          }
+          rk += lo2;
+        }
+        if (rk < np) {
+          okey[rk] = D;
+          oid[rk] = l;
+        }
+      }
+      __syncthreads();
+      nbest = min(np, s_cnt);
+      for (int p = threadIdx.x; p < nbest; p += blockDim.x) {
+        key[p] = okey[p];
+        id[p] = oid[p];
+      }
+      __syncthreads();
+    }
+    for (int pos = 0; src_len > scap && pos < src_len; pos += kRefineChunk) {
       if (threadIdx.x == 0) s_cnt = 0;
       __syncthreads();
       const int take = min(kRefineChunk, src_len - pos);

@@ -713,6 +713,12 @@ static int num_sms() {
 // 1/world of the tiles (C4, world 8: 64 tiles -> nN 64, 256 CTAs)
 static int filter_nn(int nq, int tiles) {
   int nN = ((nq + 15) / 16) * 16;
+  static int env_nn = -1;  // VLR_FILTER_NN: fixed query tile (multiple of 16, <= 256; timing experiments)
+  if (env_nn < 0) {
+    const char* e = getenv("VLR_FILTER_NN");
+    env_nn = e ? atoi(e) : 0;
+  }
+  if (env_nn >= 16 && env_nn % 16 == 0) return std::min(nN, std::min(env_nn, 256));
   const int sms = num_sms();
   while (nN > 32 && (long long)tiles * ((nq + nN - 1) / nN) < 2LL * sms) nN = ((nN / 2 + 15) / 16) * 16;
   return nN;

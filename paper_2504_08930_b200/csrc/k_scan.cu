@@ -560,9 +560,9 @@ __device__ __forceinline__ void rel_segment_done(const ScanArgs& a, int q, long 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -636,9 +636,11 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanAr
     int timed_out = 0;
     if (lane == 0) {
       const unsigned long long t0 = globaltimer_ns();
-      for (uint32_t spin = 0; ld_acquire_gpu(a.qdone + q) != (unsigned long long)(E - S); ++spin) {
-        __nanosleep(64);
-        if ((spin & 1023u) == 1023u && globaltimer_ns() - t0 > 4000000000ull) {  // bounded: never hang
+      // relaxed polling with a short sleep (an acquire load per iteration invalidates L1 each time); the
+      // acquire is the fence after the loop
+      for (uint32_t spin = 0; ld_relaxed_gpu(a.qdone + q) != (unsigned long long)(E - S); ++spin) {
+        __nanosleep(256);
+        if ((spin & 255u) == 255u && globaltimer_ns() - t0 > 4000000000ull) {  // bounded: never hang
           atomicOr(status, 2);  // reported as VLR_ERR_CUDA by vlr_search / the next call on the handle
           timed_out = 1;
           break;
@@ -786,10 +788,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
         gg = gm;
       }
       const long long slot = ((long long)(c + q) + (long long)(REL ? zcur() - 1 : 0) * G) * kScanWarps * a.k + warp * a.k;
-      if (!DUMP && lane < a.k) {
+      if (!DUMP && lane < a.k) {  // REL: released by thread 0's fence after the barrier (rel_segment_done)
         a.pdist[slot + lane] = bd;
         a.pid[slot + lane] = bid;
-        if constexpr (REL) __threadfence();
       }
       __syncthreads();  // every warp is done with this LUT
       if constexpr (REL) rel_segment_done(a, q, s_ng);

@@ -200,6 +200,13 @@ __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// polling load: relaxed (no L1 invalidation per iteration, as ld.acquire costs); the waiter issues one
+// acquire fence after it has seen the flag
+__device__ __forceinline__ uint32_t ld_relaxed_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // element o of this rank's slab (slab elements per rank) into every rank's inbox
 template <class T>
@@ -210,7 +217,8 @@ __device__ __forceinline__ void peer_store(const PeerOut& p, long long slab, lon
 // every thread of every CTA calls it once, after its stores
 __device__ __forceinline__ void peer_signal(const PeerOut& p) {
   if (p.G == 0) return;
-  __threadfence_system();  // each thread's own peer stores, before the CTA barrier
+  // the barrier orders every thread's peer stores before thread 0's system-scope fence (fences are
+  // cumulative), so one fence per CTA releases them all (a fence per thread cost a MEMBAR.SYS each)
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
@@ -229,14 +237,17 @@ __device__ __forceinline__ void peer_wait(const PeerIn& w) {
   if (threadIdx.x == 0) {
     const unsigned long long t0 = globaltimer_ns();
     for (int r = 0; r < w.G; ++r) {
-      for (uint32_t spin = 0; ld_acquire_sys_u32(w.flags + r) != w.epoch; ++spin) {
-        __nanosleep(64);
-        if ((spin & 1023u) == 1023u && globaltimer_ns() - t0 > 4000000000ull) {  // bounded: never hang
+      unsigned ns = 32;
+      for (uint32_t spin = 0; ld_relaxed_sys_u32(w.flags + r) != w.epoch; ++spin) {
+        __nanosleep(ns);
+        ns = ns < 512 ? 2 * ns : 512;  // back off: many CTAs of a consumer kernel poll at once
+        if ((spin & 255u) == 255u && globaltimer_ns() - t0 > 4000000000ull) {  // bounded: never hang
           atomicOr(w.status, 4);
           break;
         }
       }
     }
+    __threadfence_system();  // acquire: the slabs after the flags (then the barrier extends it to the CTA)
   }
   __syncthreads();
 }

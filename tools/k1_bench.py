@@ -93,6 +93,10 @@ VARIANTS = {
     "pair_qt64": {"VLR_FILTER_PAIR": "1", "VLR_FILTER_QT": "64"},
     "pair_st4": {"VLR_FILTER_PAIR": "1", "VLR_FILTER_STAGES": "4"},
     "pair_st2": {"VLR_FILTER_PAIR": "1", "VLR_FILTER_STAGES": "2"},
+    "single_nn32": {"VLR_FILTER_PAIR": "0", "VLR_FILTER_NN": "32"},
+    "single_nn64": {"VLR_FILTER_PAIR": "0", "VLR_FILTER_NN": "64"},
+    "single_nn128": {"VLR_FILTER_PAIR": "0", "VLR_FILTER_NN": "128"},
+    "single_nn256": {"VLR_FILTER_PAIR": "0", "VLR_FILTER_NN": "256"},
 }
 
 
