@@ -153,7 +153,10 @@ __device__ unsigned radix_select_kth(const unsigned* skeys, int n, unsigned want
       const unsigned key = i < n ? skeys[i] : 0u;
       const bool act = i < n && (key & mask) == prefix;
       const unsigned bin = (key >> shift) & 255u;
-      if (act) atomicAdd(&hist[bin], 1u);  // plain shared-memory atomics (no match_any aggregation)
+      // warp-aggregated: the keys are order-preserving bit patterns of nearby fp32 values, so most lanes
+      // of a warp share the leading digit's bin; one atomic per distinct bin instead of one per lane
+      const unsigned peers = __match_any_sync(kFull, act ? bin : 256u);
+      if (act && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned)__popc(peers));
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -433,6 +436,7 @@ static int sort_cap(int np) {
 constexpr int kRefinePer = (kMaxNprobe + kRefineThreads - 1) / kRefineThreads;  // router items per thread
 static_assert(kRescanWarps * 2048 * sizeof(float) >= kMaxNprobe * (sizeof(double) + sizeof(int)),
               "kRefMerge's rank-merge output lives in the rescan tiles");
+constexpr int kRankSortMax = 512;  // K3b selects by rank (O(n^2 / threads)) up to this many candidates
 
 __device__ __forceinline__ bool key_less(double a, int ia, double b, int ib) {
   return a < b || (a == b && ia < ib);
@@ -891,6 +895,32 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
         }
       }
       const int tot = nbest + cnt;
+      if (listed && nbest == 0 && pos >= src_len && tot <= kRankSortMax) {
+        // the whole (short) candidate list at once: select the np best by rank (each entry counts the
+        // entries before it in (D, l) order; ids are distinct, so ranks are distinct) instead of a bitonic
+        // sort -- no barrier per stage. Same unique order.
+        __syncthreads();
+        double* okey = reinterpret_cast<double*>(tiles);  // [np] (the rescan tiles are unused when listed)
+        int* oid = reinterpret_cast<int*>(okey + np);
+        for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+          const double D = key[i];
+          const int l = id[i];
+          int rk = 0;
+          for (int j = 0; j < tot; ++j) rk += key_less(key[j], id[j], D, l) ? 1 : 0;
+          if (rk < np) {
+            okey[rk] = D;
+            oid[rk] = l;
+          }
+        }
+        __syncthreads();
+        nbest = min(np, tot);
+        for (int p = threadIdx.x; p < nbest; p += blockDim.x) {
+          key[p] = okey[p];
+          id[p] = oid[p];
+        }
+        __syncthreads();
+        break;
+      }
       int n2 = 1;
       while (n2 < tot) n2 <<= 1;
       for (int j = tot + threadIdx.x; j < n2; j += blockDim.x) {

@@ -720,7 +720,10 @@ static int filter_nn(int nq, int tiles) {
   }
   if (env_nn >= 16 && env_nn % 16 == 0) return std::min(nN, std::min(env_nn, 256));
   const int sms = num_sms();
-  while (nN > 32 && (long long)tiles * ((nq + nN - 1) / nN) < 2LL * sms) nN = ((nN / 2 + 15) / 16) * 16;
+  // halve the query tile while the grid has fewer CTAs than SMs: each halving re-reads every centroid tile
+  // once more, so stop at one CTA per SM (measured at world 8, 64 tiles: nN 64/128 -> stage 1 0.070 ms,
+  // nN 32 (the former "2 per SM" rule) 0.081 ms; tools/k1_bench.py, profiles/r02/k1_bench_w8_l.jsonl)
+  while (nN > 32 && (long long)tiles * ((nq + nN - 1) / nN) < (long long)sms) nN = ((nN / 2 + 15) / 16) * 16;
   return nN;
 }
 

@@ -899,7 +899,14 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
     e = cudaEventRecord(rel->fork, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(rel->stream, rel->fork, 0);
     if (e != cudaSuccess) return e;
-    k_release_merge<<<1, kMergeMaxWarps * 32, 0, rel->stream>>>(a, G, ws.status);
+    static int rel_exp = -1;  // VLR_REL_EXPERIMENT=1: the merger exits at once (timing experiment: nothing
+    if (rel_exp < 0) {        // is released, the host waits time out)
+      const char* e = getenv("VLR_REL_EXPERIMENT");
+      rel_exp = e ? atoi(e) : 0;
+    }
+    ScanArgs am = a;
+    if (rel_exp == 1) am.nq = 0;
+    k_release_merge<<<1, kMergeMaxWarps * 32, 0, rel->stream>>>(am, G, ws.status);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     e = launch_scan_k(ix, a, G, s);
     if (e == cudaSuccess) e = cudaEventRecord(rel->join, rel->stream);

@@ -3,7 +3,8 @@
 Runs every search path once, small: the plain search (K1 one-CTA filter,
 K2, K3a/K3b, K4b, K5 on its side stream, K6, K7), the early-release search
 (NEXT-4: REL scan + resident merger CTA, rows in pinned host memory), the
-staged sharded coarse stage (G = 2 shard-only handles), the large-k path
+staged sharded coarse stage (G = 2 shard-only handles; K3b merges by rank), the large-k path,
+the pipelined search (two workspace slots on two streams)
 (DUMP scan + k_select_large + large merge), a 4-bit index, and -- selected by
 the environment of the run -- the K1 variants (VLR_FILTER_CLUSTER,
 VLR_FILTER_PAIR, VLR_FILTER_PERSISTENT). Exits non-zero if a result differs
@@ -37,6 +38,12 @@ def main():
     big = h.search(Q, 64, 100, sync=True)
     ref64 = h.search(Q, 64, 10, sync=True)
     ok &= torch.equal(big[0][:, :10], ref64[0]) and torch.equal(big[1][:, :10], ref64[1])
+    # cross-batch pipelining: two workspace slots, searches alternating over two streams, scan reserve
+    h.set_pipeline(2, 8)
+    ss = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [h.search(Q, 16, 10, stream=ss[i % 2]) for i in range(4)]
+    torch.cuda.synchronize()
+    ok &= all(torch.equal(o[0], a[0]) and torch.equal(o[1], a[1]) for o in outs)
     h.close()
     # sharded coarse stage, 2 shard-only handles, exchanges by stacking
     hs = [vlr.Index.from_arrays(ix, rank=r, world=2) for r in range(2)]

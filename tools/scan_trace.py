@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--G", default="1,8", help="shard counts (rank 0's shard traced)")
     ap.add_argument("--release", action="store_true", help="trace the NEXT-4 release scan (REL waves) too")
+    ap.add_argument("--release-nowait", action="store_true",
+                    help="launch the release search without waiting for the flags (VLR_REL_EXPERIMENT=1 runs)")
     a = ap.parse_args()
     import datagen
     import paper_2504_08930_b200 as vlr
@@ -37,15 +39,19 @@ def main():
         h = vlr.Index.from_arrays(ix) if G == 1 else vlr.Index.from_arrays(ix, rank=0, world=G)
         print(json.dumps(trace(h, c, Q, L, a.config, G)), flush=True)
         if a.release:
-            print(json.dumps(trace(h, c, Q, L, a.config, G, release=True)), flush=True)
+            print(json.dumps(trace(h, c, Q, L, a.config, G, release=True, nowait=a.release_nowait)), flush=True)
         h.close()
 
 
-def trace(h, c, Q, L, config, G, release=False):
-    out = {"config": config, "G": G, "release": release, "runs": []}
+def trace(h, c, Q, L, config, G, release=False, nowait=False):
+    out = {"config": config, "G": G, "release": release, "env": {k: v for k, v in os.environ.items()
+                                                                  if k.startswith("VLR_")}, "runs": []}
     for it in range(6):
         h.set_profiling(2)
-        if release:
+        if release and nowait:
+            h.search_release_launch(Q, c["nprobe"], c["k"])
+            torch.cuda.synchronize()
+        elif release:
             h.search_release(Q, c["nprobe"], c["k"])
             torch.cuda.synchronize()
         else:
