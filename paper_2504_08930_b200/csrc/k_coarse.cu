@@ -153,10 +153,9 @@ __device__ unsigned radix_select_kth(const unsigned* skeys, int n, unsigned want
       const unsigned key = i < n ? skeys[i] : 0u;
       const bool act = i < n && (key & mask) == prefix;
       const unsigned bin = (key >> shift) & 255u;
-      // warp-aggregated: the keys are order-preserving bit patterns of nearby fp32 values, so most lanes
-      // of a warp share the leading digit's bin; one atomic per distinct bin instead of one per lane
-      const unsigned peers = __match_any_sync(kFull, act ? bin : 256u);
-      if (act && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned)__popc(peers));
+      // plain shared-memory atomics: a match_any-aggregated variant measured slower (K2 stage 1 at world 8
+      // 8.4 -> 21.5 us, profiles/r02/launches_shard_g8_m.csv)
+      if (act) atomicAdd(&hist[bin], 1u);
     }
     __syncthreads();
     if (threadIdx.x < 32) {
