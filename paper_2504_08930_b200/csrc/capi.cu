@@ -46,6 +46,15 @@ cudaError_t ensure_smem(const void* fn, size_t bytes) {
   return cudaSuccess;
 }
 
+bool pdl_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VLR_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static vlr_status fail(vlr_status st, const std::string& msg) {
   g_err = msg;
   return st;
@@ -891,11 +900,11 @@ static vlr_status phase_c(vlr_index* h, Pipe& p, bool sharded, int64_t* out_ids,
     }
     rec(h, 3, p.s);
   }
-  VLR_CUDA_TRY(launch_offsets(w, p.nq, p.np, p.s)); ++p.n;
+  // the forked LUT joins before K4b, so that K4b -> K6 stays a programmatic (PDL) pair
+  if (p.lut_forked) VLR_CUDA_TRY(cudaStreamWaitEvent(p.s, h->res[p.slot].lut_join, 0));
+  VLR_CUDA_TRY(launch_offsets(ix, w, p.nq, p.np, p.s)); ++p.n;
   rec(h, 4, p.s);
-  if (p.lut_forked) {
-    VLR_CUDA_TRY(cudaStreamWaitEvent(p.s, h->res[p.slot].lut_join, 0));
-  } else {
+  if (!p.lut_forked) {
     VLR_CUDA_TRY(launch_lut(p.Q, ix, w, p.nq, p.s)); ++p.n;
   }
   rec(h, 5, p.s);

@@ -35,6 +35,7 @@ namespace vlr {
 __global__ void k_qprep(const float* __restrict__ Q, int nq, int d, int d8, float* __restrict__ qnorm,
                         float* __restrict__ qsq, uint16_t* __restrict__ qf16, float* __restrict__ qinv, int32_t* status,
                         uint16_t* __restrict__ qf16t, int QT) {
+  pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
   const int q = blockIdx.x;
   if (q >= nq) {  // zero padding rows of the tiled operand
     const int qt = q / QT, r = q % QT, kbn = (d8 + 63) / 64;
@@ -107,8 +108,7 @@ cudaError_t launch_qprep(const float* Q, int nq, int d, int d8, float* qnorm, fl
                          int32_t* status, uint16_t* qf16t, int QT, cudaStream_t s) {
   if (nq <= 0) return cudaSuccess;
   const int grid = qf16t ? (nq + QT - 1) / QT * QT : nq;
-  k_qprep<<<grid, 256, 0, s>>>(Q, nq, d, d8, qnorm, qsq, qf16, qinv, status, qf16t, QT);
-  return cudaGetLastError();
+  return launch_pdl(k_qprep, dim3(grid), dim3(256), 0, s, Q, nq, d, d8, qnorm, qsq, qf16, qinv, status, qf16t, QT);
 }
 
 // ----------------------------------------------------------------- K2 select
@@ -199,6 +199,7 @@ __global__ void __launch_bounds__(kSelThreads, 2) k_select(const float* __restri
                                                         float* __restrict__ x1, int32_t* __restrict__ cand,
                                                         int32_t* __restrict__ ncand, float* __restrict__ bound_out,
                                                         PeerOut pout, PeerIn pin) {
+  pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
   extern __shared__ unsigned skeys[];  // >= max(keys of the theta' select, 2 kSelGather) words
   __shared__ unsigned s_cnt, s_ng, s_ovf;
   __shared__ int s_grp[kSelGroupCap];
@@ -405,11 +406,10 @@ cudaError_t launch_select(const DeviceIndex& ix, const Workspace& ws, int nq, in
   const float e_abs = sqrtf((float)ix.d) * 2.9802322e-8f * 1.00049f * 1.0001f;  // sqrt(d) 2^-25 (1 + 2^-11), rounded up
 #define VLR_SEL_ARGS ws.dt, ws.gmin, ix.nlist, lo, hi, np, ix.world, ws.qnorm, ix.cmax, e_dot, e_abs, ws.qinv, \
                      ix.c_inv, ws.x1_all, ws.x1, ws.cand, ws.ncand, ws.bound, pout, pin
-  if (mode == kSelStage1) k_select<kSelStage1><<<nq, kSelThreads, sm, s>>>(VLR_SEL_ARGS);
-  else if (mode == kSelStage2) k_select<kSelStage2><<<nq, kSelThreads, sm, s>>>(VLR_SEL_ARGS);
-  else k_select<kSelFull><<<nq, kSelThreads, sm, s>>>(VLR_SEL_ARGS);
+  if (mode == kSelStage1) return launch_pdl(k_select<kSelStage1>, dim3(nq), dim3(kSelThreads), sm, s, VLR_SEL_ARGS);
+  if (mode == kSelStage2) return launch_pdl(k_select<kSelStage2>, dim3(nq), dim3(kSelThreads), sm, s, VLR_SEL_ARGS);
+  return launch_pdl(k_select<kSelFull>, dim3(nq), dim3(kSelThreads), sm, s, VLR_SEL_ARGS);
 #undef VLR_SEL_ARGS
-  return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------- K3 refine
@@ -627,6 +627,7 @@ __global__ void __launch_bounds__(W * 32) k_exact(const float* __restrict__ Q, c
                                                   int d, int nq, int ny, const int32_t* __restrict__ cand,
                                                   const int32_t* __restrict__ ncand,
                                                   double* __restrict__ exact) {
+  pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
   extern __shared__ __align__(16) unsigned char sm[];
   double* qs = reinterpret_cast<double*>(sm);
   float* tiles = reinterpret_cast<float*>(qs + ((d + 1) & ~1));
@@ -682,8 +683,8 @@ static cudaError_t launch_exact_t(const float* Q, const DeviceIndex& ix, const W
   const int ny = 1024 / (W * 32 * CH);  // 1024 candidates per pass over a query's list; more loop
   const int tasks = nq * ny;
   const int grid = std::max(1, std::min(tasks, sms * std::max(per_sm, 1)));
-  fn<<<grid, W * 32, sm, s>>>(Q, ix.centroids, ix.d, nq, ny, ws.cand, ws.ncand, ws.exact);
-  return cudaGetLastError();
+  return launch_pdl(fn, dim3(grid), dim3(W * 32), sm, s, Q, (const float*)ix.centroids, ix.d, nq, ny,
+                    (const int32_t*)ws.cand, (const int32_t*)ws.ncand, ws.exact);
 }
 
 cudaError_t launch_exact(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s) {
@@ -749,6 +750,7 @@ __global__ void __launch_bounds__(kRefineThreads) k_refine(const float* __restri
                                                            int32_t* __restrict__ plocal,
                                                            int64_t* __restrict__ item_local,
                                                            int64_t* __restrict__ qtot, PeerOut pout, PeerIn pin) {
+  pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
   extern __shared__ __align__(16) unsigned char sm[];
   float* tiles = reinterpret_cast<float*>(sm);                        // [kRescanWarps][2][32][32]
   double* key = reinterpret_cast<double*>(tiles + kRescanWarps * 2048);  // [scap]
@@ -1028,7 +1030,7 @@ cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace
                   (void*)&ws.x2, (void*)&ws.x2_all, (void*)&ws.probes, (void*)&ws.term1, (void*)&ix.rank,
                   (void*)&ix.owner, (void*)&ix.local, (void*)&ix.gbase, (void*)&miss, (void*)&probes_out,
                   (void*)&ws.plocal, (void*)&ws.item_local, (void*)&ws.qtot, (void*)&pout, (void*)&pin};
-  return cudaLaunchKernel(fn, dim3(nq), dim3(kRefineThreads), args, sm, s);
+  return launch_pdl_c(fn, dim3(nq), dim3(kRefineThreads), sm, s, args);
 }
 
 }  // namespace vlr

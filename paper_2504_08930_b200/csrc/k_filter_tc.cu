@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 int kblocks, int nN, int nacc, int stages, const float* __restrict__ cn2,
                 const float* __restrict__ qinv, float c_inv, float* __restrict__ dt, float* __restrict__ gmin,
                 int ngroups, const uint16_t* __restrict__ At, int t0, const uint16_t* __restrict__ Bt) {
+  pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[kTcMaxStages], empty[kTcMaxStages], tfull;
@@ -862,9 +863,8 @@ cudaError_t launch_filter_tc(const uint16_t* Qh, const float* qinv, int nq, cons
   }
   const uint16_t* At = (tiled && ix.cf16t) ? ix.cf16t : nullptr;
   if (CL == 1) {
-    k_filter_tc<1><<<grid, kTcThreads, smem, s>>>(tmA, tmB, ix.nlist, nq, kblocks, nN, nacc, stages, ix.cnorm2, qinv,
-                                                  ix.c_inv, dt, gmin, ngroups, At, t_lo, Qt);
-    return cudaGetLastError();
+    return launch_pdl(k_filter_tc<1>, grid, dim3(kTcThreads), smem, s, tmA, tmB, ix.nlist, nq, kblocks, nN, nacc,
+                      stages, (const float*)ix.cnorm2, qinv, ix.c_inv, dt, gmin, ngroups, At, t_lo, Qt);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;

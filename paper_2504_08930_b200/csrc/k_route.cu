@@ -27,6 +27,7 @@ constexpr int kOffThreads = 256;
 __global__ void __launch_bounds__(kOffThreads) k_offsets(int nq, int np, const int64_t* __restrict__ qtot,
                                                          const int64_t* __restrict__ item_local,
                                                          int64_t* __restrict__ item_off) {
+  pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
   extern __shared__ long long qbase[];  // [nq + 1]
   __shared__ long long wsum[kOffThreads / 32];
   __shared__ long long carry;
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(kOffThreads) k_offsets(int nq, int np, const i
   if (blockIdx.x == 0 && threadIdx.x == 0) item_off[n] = qbase[nq];
 }
 
-cudaError_t launch_offsets(const Workspace& ws, int nq, int np, cudaStream_t s) {
+cudaError_t launch_offsets(const DeviceIndex& ix, const Workspace& ws, int nq, int np, cudaStream_t s) {
   const long long n = (long long)nq * np;
   long long blocks = (n + kOffThreads - 1) / kOffThreads;
   if (blocks > 148 * 4) blocks = 148 * 4;
@@ -71,8 +72,9 @@ cudaError_t launch_offsets(const Workspace& ws, int nq, int np, cudaStream_t s) 
   const size_t sm = (size_t)(nq + 1) * sizeof(long long);
   cudaError_t e = ensure_smem((const void*)k_offsets, sm);
   if (e != cudaSuccess) return e;
-  k_offsets<<<(int)blocks, kOffThreads, sm, s>>>(nq, np, ws.qtot, ws.item_local, ws.item_off);
-  return cudaGetLastError();
+  (void)ix;
+  return launch_pdl(k_offsets, dim3((int)blocks), dim3(kOffThreads), sm, s, nq, np, ws.qtot, ws.item_local,
+                    ws.item_off);
 }
 
 // ----------------------------------------------------------------- K5 LUT

@@ -162,6 +162,9 @@ __device__ __forceinline__ void grp_prefetch(const ScanArgs& a, long long gg, lo
 template <int MP, int NB, int EXP = 0>
 __device__ __forceinline__ void grp_load(Grp<MP, NB>& G, const ScanArgs& a, long long gg, long long& it, int lane) {
   constexpr int kChunks = MP * NB / 128;
+  // the item cursor's loads (item_off, plocal, gbase, term1) hit L1; a per-group metadata array written by
+  // K4b (one 8-byte word per group) measured slower: its first touch per line is an L2 round trip on the
+  // path to the code loads (scan 1.53 -> 1.81 ms at C4, profiles/r02/scan_trace_gmeta_n_slower.jsonl)
   advance_item(a, gg, it, lane);
   const int loc = a.plocal[it];
   G.gaddr = a.gbase[loc] + (gg - a.item_off[it]);
@@ -491,6 +494,7 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32) k_rank_merge(
     int nq, int np, int k, int n_cta, const int64_t* __restrict__ item_off, const float* __restrict__ pdist,
     const int64_t* __restrict__ pid, int64_t* __restrict__ out_ids, float* __restrict__ out_dist,
     Packed* __restrict__ packed, PeerOut pout) {
+  pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
   __shared__ MergeSmem sm;
   const int q = blockIdx.x;
   merge_query<false>(q, k, n_cta, 0, item_off[(long long)nq * np], 0, item_off[(long long)q * np],
@@ -625,47 +629,69 @@ __device__ __forceinline__ void warp_merge_query(const ScanArgs& a, int q, int G
   }
 }
 
-// the resident merger CTA: warp w merges and releases queries w, w + nw, ...
-// in order, each as soon as the scan has finished it (qdone[q] == its groups);
-// G = the scan's grid size
+// the resident merger CTA: warp w owns queries w, w + nw, ... and merges and releases each one as soon as
+// the scan has finished it (qdone[q] == its groups), in whatever order they complete (the scan's CTAs walk
+// their queries in alternating directions, so completion is not in query order); G = the scan's grid size
 __global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanArgs a, int G, int32_t* status) {
+  extern __shared__ unsigned char s_rel[];  // [nq] 1 = released
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nq = a.nq, np = a.np, Z = a.waves;
-  for (int q = warp; q < nq; q += nw) {
-    const long long S = a.item_off[(long long)q * np], E = a.item_off[(long long)(q + 1) * np];
-    int timed_out = 0;
-    if (lane == 0) {
-      const unsigned long long t0 = globaltimer_ns();
-      // relaxed polling with a short sleep (an acquire load per iteration invalidates L1 each time); the
-      // acquire is the fence after the loop
-      for (uint32_t spin = 0; ld_relaxed_gpu(a.qdone + q) != (unsigned long long)(E - S); ++spin) {
-        __nanosleep(256);
-        if ((spin & 255u) == 255u && globaltimer_ns() - t0 > 4000000000ull) {  // bounded: never hang
-          atomicOr(status, 2);  // reported as VLR_ERR_CUDA by vlr_search / the next call on the handle
-          timed_out = 1;
-          break;
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) s_rel[q] = 0;
+  __syncthreads();
+  const int mine = warp < nq ? (nq - warp + nw - 1) / nw : 0;
+  int left = mine;
+  const unsigned long long t0 = globaltimer_ns();
+  while (left > 0) {
+    bool any = false;
+    for (int j0 = 0; j0 < mine; j0 += 32) {
+      // lane i polls query warp + nw (j0 + i) (relaxed load; the acquire is the fence before the merge)
+      const int j = j0 + lane;
+      const int qq = warp + nw * j;
+      bool ready = false;
+      if (j < mine && !s_rel[qq]) {
+        const long long S = a.item_off[(long long)qq * np], E = a.item_off[(long long)(qq + 1) * np];
+        ready = ld_relaxed_gpu(a.qdone + qq) == (unsigned long long)(E - S);
+      }
+      unsigned m = __ballot_sync(kFull, ready);
+      while (m) {
+        const int r = __ffs(m) - 1;
+        m &= m - 1;
+        const int q = warp + nw * (j0 + r);
+        __threadfence();  // acquire: q's partial lists after its completed count
+        const long long S = a.item_off[(long long)q * np], E = a.item_off[(long long)(q + 1) * np];
+        int z = (int)(((long long)(q + 1) * Z - 1) / nq);  // q's wave and its group range (k_scan's split)
+        z = z < Z - 1 ? z : Z - 1;
+        const long long WL = a.item_off[(long long)((long long)z * nq / Z) * np];
+        const long long WH = a.item_off[(long long)((long long)(z + 1) * nq / Z) * np];
+        float bd;
+        long long bid;
+        warp_merge_query(a, q, G, WL, WH, (long long)z * G, S, E, lane, bd, bid);
+        if (lane < a.k) {
+          a.out_ids[(size_t)q * a.k + lane] = bid;
+          a.out_dist[(size_t)q * a.k + lane] = bd;
         }
+        __threadfence_system();  // row q (possibly in pinned host memory) before its flag
+        __syncwarp();
+        if (lane == 0) {
+          st_release_sys(a.ready + q, a.epoch);
+          s_rel[q] = 1;
+        }
+        __syncwarp();
+        --left;
+        any = true;
       }
     }
-    // a query whose scan did not complete in time is NOT merged and NOT released: its partial lists may
-    // be incomplete (or left over from an earlier search), so ready[q] stays != epoch and the host wait
-    // (vlr_wait_ready / vlr_poll_ready) times out instead of returning a wrong row
-    if (__shfl_sync(kFull, timed_out, 0)) continue;
-    __threadfence();
-    int z = (int)(((long long)(q + 1) * Z - 1) / nq);  // q's wave and its group range (k_scan's split)
-    z = z < Z - 1 ? z : Z - 1;
-    const long long WL = a.item_off[(long long)((long long)z * nq / Z) * np];
-    const long long WH = a.item_off[(long long)((long long)(z + 1) * nq / Z) * np];
-    float bd;
-    long long bid;
-    warp_merge_query(a, q, G, WL, WH, (long long)z * G, S, E, lane, bd, bid);
-    if (lane < a.k) {
-      a.out_ids[(size_t)q * a.k + lane] = bid;
-      a.out_dist[(size_t)q * a.k + lane] = bd;
+    if (!any) {
+      __nanosleep(256);
+      // bounded: a query whose scan did not complete in time is NOT merged and NOT released (its partial
+      // lists may be incomplete or left over from an earlier search): ready[q] stays != epoch, the host
+      // wait (vlr_wait_ready / vlr_poll_ready) times out instead of returning a wrong row, and status bit 1
+      // is reported as VLR_ERR_CUDA by vlr_search / the next call on the handle
+      if (globaltimer_ns() - t0 > 4000000000ull) {
+        if (lane == 0) atomicOr(status, 2);
+        break;
+      }
     }
-    __threadfence_system();  // row q (possibly in pinned host memory) before its flag
-    __syncwarp();
-    if (lane == 0) st_release_sys(a.ready + q, a.epoch);
   }
 }
 
@@ -675,11 +701,13 @@ __device__ unsigned long long g_scan_trace[1024][6];
 #endif
 template <int MP, int NB, int EXP, bool REL = false, bool DUMP = false>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
+  pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ long long s_it;
   __shared__ long long s_ng;
-  __shared__ int s_z;
+  __shared__ int s_z, s_qa, s_qb;
+  __shared__ long long s_g0, s_g1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = gridDim.x, c = blockIdx.x;
   const int Z = REL ? a.waves : 1;
@@ -734,13 +762,32 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
       if (threadIdx.x == 0) s_it = lo;
       __syncthreads();
     }
-    long long it0 = s_it;
-    advance_item(a, g0, it0, lane);
-    long long g = g0;
-    while (g < g1) {
-      const int q = (int)(it0 / a.np);
-      const long long qend = a.item_off[(long long)(q + 1) * a.np];
-      const long long seg_end = qend < g1 ? qend : g1;
+    // the CTA's queries: q_a (holding group g0) .. q_b (holding group g1 - 1), kept in shared memory (no
+    // registers live across the scan loop); one segment per query
+    {
+      long long it0 = s_it;
+      advance_item(a, g0, it0, lane);
+      if (threadIdx.x == 0) {
+        int qb = (int)(it0 / a.np);
+        s_qa = qb;
+        while (a.item_off[(long long)(qb + 1) * a.np] < g1) ++qb;
+        s_qb = qb;
+        s_g0 = g0;
+        s_g1 = g1;
+      }
+      __syncthreads();
+    }
+    auto vol_i = [](const int& x) { return *reinterpret_cast<const volatile int*>(&x); };
+    auto vol_l = [](const long long& x) { return *reinterpret_cast<const volatile long long*>(&x); };
+    for (int si = 0; si <= vol_i(s_qb) - vol_i(s_qa); ++si) {
+      // NEXT-4 (REL): even CTAs walk their queries backward, odd CTAs forward, so the query shared by CTAs
+      // 2j and 2j+1 is scanned first by both and completes early; otherwise forward
+      const int q = (REL && (c & 1) == 0) ? vol_i(s_qb) - si : vol_i(s_qa) + si;
+      const long long qstart = a.item_off[(long long)q * a.np], qend = a.item_off[(long long)(q + 1) * a.np];
+      const long long cg0 = vol_l(s_g0), cg1 = vol_l(s_g1);
+      const long long g = qstart > cg0 ? qstart : cg0;
+      const long long seg_end = qend < cg1 ? qend : cg1;
+      if (g >= seg_end) continue;  // a query without owned groups (CTA-uniform)
       if (threadIdx.x == 0) {
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&mbar, lut_bytes);
@@ -764,10 +811,11 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
 
       float bd = CUDART_INF_F, thr = CUDART_INF_F;
       long long bid = -1;
-      long long it = it0;
       long long gg = g + warp;
+      // item cursors of the loads and of the L2 prefetch (kPfDist groups of this warp ahead), from an item
+      // at or before the segment's first (the item holding g0, or q's first item)
+      long long it = g == cg0 ? vol_l(s_it) : (long long)q * a.np, itp = it;
       Grp<MP, NB> A, B;
-      long long itp = it0;  // prefetch cursor: kPfDist groups (of this warp) ahead of the loads
       if (gg < seg_end) {
         for (int p = 1; p <= kPfDist; ++p)
           if (gg + p * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gg + p * kScanWarps, itp, lane);
@@ -794,11 +842,6 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
       }
       __syncthreads();  // every warp is done with this LUT
       if constexpr (REL) rel_segment_done(a, q, s_ng);
-      g = seg_end;
-      if (g < g1) {
-        it0 = (long long)(q + 1) * a.np;
-        advance_item(a, g, it0, lane);
-      }
     }
   }
 #ifdef VLR_SCAN_TRACE
@@ -838,8 +881,7 @@ static cudaError_t launch_scan_e(const ScanArgs& a, int n_cta, cudaStream_t s) {
                                                                                                   : (size_t)(2 * kLutPairBytes));
   if (e != cudaSuccess) return e;
   if (n_cta == 0) return cudaSuccess;  // configure (and so load) only
-  k_scan<MP, NB, EXP, REL, DUMP><<<n_cta, kScanThreads, a.lut_bytes, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k_scan<MP, NB, EXP, REL, DUMP>, dim3(n_cta), dim3(kScanThreads), (size_t)a.lut_bytes, s, a);
 }
 
 // VLR_SCAN_EXPERIMENT=1|2 (timing experiments only; results are wrong):
@@ -894,7 +936,7 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
     // spinning merger runs waits for the merger (and the merger waits for the scan).
     cudaError_t e = launch_scan_k(ix, a, 0, s);
     if (e != cudaSuccess) return e;
-    if ((e = ensure_smem((const void*)k_release_merge, 0)) != cudaSuccess) return e;
+    if ((e = ensure_smem((const void*)k_release_merge, (size_t)a.nq)) != cudaSuccess) return e;
     // fork: the merger CTA runs concurrently with the scan on a second stream, joined back before return
     e = cudaEventRecord(rel->fork, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(rel->stream, rel->fork, 0);
@@ -906,7 +948,7 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
     }
     ScanArgs am = a;
     if (rel_exp == 1) am.nq = 0;
-    k_release_merge<<<1, kMergeMaxWarps * 32, 0, rel->stream>>>(am, G, ws.status);
+    k_release_merge<<<1, kMergeMaxWarps * 32, (size_t)a.nq, rel->stream>>>(am, G, ws.status);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     e = launch_scan_k(ix, a, G, s);
     if (e == cudaSuccess) e = cudaEventRecord(rel->join, rel->stream);
@@ -949,9 +991,8 @@ cudaError_t launch_rank_merge(const DeviceIndex& ix, const Workspace& ws, int nq
   int nw = 1;
   while (nw < kMergeMaxWarps && (long long)nw * 128 < lists) nw <<= 1;
   if ((long long)ws.n_cta * kScanWarps > kMergeMaxLists) return cudaErrorInvalidConfiguration;
-  k_rank_merge<<<nq, nw * 32, 0, s>>>(nq, np, k, ws.n_cta, ws.item_off, ws.pdist, ws.pid, out_ids, out_dist,
-                                      reinterpret_cast<Packed*>(out_packed), pout);
-  return cudaGetLastError();
+  return launch_pdl(k_rank_merge, dim3(nq), dim3(nw * 32), 0, s, nq, np, k, ws.n_cta, ws.item_off, ws.pdist, ws.pid,
+                    out_ids, out_dist, reinterpret_cast<Packed*>(out_packed), pout);
 }
 
 // ---------------------------------------------------------------- large k (k > 32)
@@ -974,6 +1015,7 @@ __global__ void __launch_bounds__(kSelLargeThreads) k_select_large(
     int q_lo, int np, int k, const int64_t* __restrict__ item_off, const uint2* __restrict__ dump,
     const int64_t* __restrict__ ids, int64_t* __restrict__ out_ids, float* __restrict__ out_dist,
     Packed* __restrict__ packed) {
+  pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
   __shared__ unsigned hist[256];
   __shared__ unsigned s_prefix, s_want, s_cnt, s_neq, s_valid;
   __shared__ float sd[kMaxKLarge];      // the kk <= 1024 selected entries (bitonic-sorted in place)
@@ -1115,9 +1157,9 @@ cudaError_t launch_scan_large(const DeviceIndex& ix, const Workspace& ws, int nq
                nullptr, nullptr, 0u, nullptr, nullptr, 1, q0, q1, ws.dump};
     cudaError_t e = launch_scan_k(ix, a, ws.n_cta, s);
     if (e != cudaSuccess) return e;
-    k_select_large<<<q1 - q0, kSelLargeThreads, 0, s>>>(q0, np, k, ws.item_off, ws.dump, ix.ids, out_ids, out_dist,
-                                                        reinterpret_cast<Packed*>(out_packed));
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    e = launch_pdl(k_select_large, dim3(q1 - q0), dim3(kSelLargeThreads), 0, s, q0, np, k, ws.item_off, ws.dump,
+                   ix.ids, out_ids, out_dist, reinterpret_cast<Packed*>(out_packed));
+    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
@@ -1127,6 +1169,7 @@ cudaError_t launch_scan_large(const DeviceIndex& ix, const Workspace& ws, int nq
 __global__ void k_merge_parts(int n_shards, int nq, int k, const Packed* __restrict__ packed,
                               const int64_t* __restrict__ pids, const float* __restrict__ pdist,
                               int64_t* __restrict__ out_ids, float* __restrict__ out_dist, PeerIn pin) {
+  pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
   peer_wait(pin);  // NVLink peer exchange: every rank's partial rows have landed in this rank's inbox
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1157,6 +1200,7 @@ __global__ void __launch_bounds__(1024) k_merge_large(int n_shards, int nq, int 
                                                       const int64_t* __restrict__ pids,
                                                       const float* __restrict__ pdist, int64_t* __restrict__ out_ids,
                                                       float* __restrict__ out_dist) {
+  pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
   extern __shared__ __align__(16) unsigned char smm[];
   const int n = n_shards * k;
   int n2 = 1;
@@ -1207,8 +1251,7 @@ static cudaError_t launch_merge_large(const Packed* packed, const int64_t* pids,
   const size_t sm = (size_t)n2 * (sizeof(long long) + sizeof(float));
   cudaError_t e = ensure_smem((const void*)k_merge_large, sm);
   if (e != cudaSuccess) return e;
-  k_merge_large<<<nq, 1024, sm, s>>>(n_shards, nq, k, packed, pids, pdist, out_ids, out_dist);
-  return cudaGetLastError();
+  return launch_pdl(k_merge_large, dim3(nq), dim3(1024), sm, s, n_shards, nq, k, packed, pids, pdist, out_ids, out_dist);
 }
 
 cudaError_t launch_merge_packed(const void* parts, int n_shards, int nq, int k, int64_t* out_ids, float* out_dist,
@@ -1219,9 +1262,8 @@ cudaError_t launch_merge_packed(const void* parts, int n_shards, int nq, int k, 
     return launch_merge_large(reinterpret_cast<const Packed*>(parts), nullptr, nullptr, n_shards, nq, k, out_ids,
                               out_dist, s);
   const int wpb = 8;
-  k_merge_parts<<<(nq + wpb - 1) / wpb, wpb * 32, 0, s>>>(n_shards, nq, k, reinterpret_cast<const Packed*>(parts),
-                                                          nullptr, nullptr, out_ids, out_dist, pin);
-  return cudaGetLastError();
+  return launch_pdl(k_merge_parts, dim3((nq + wpb - 1) / wpb), dim3(wpb * 32), 0, s, n_shards, nq, k,
+                    reinterpret_cast<const Packed*>(parts), nullptr, nullptr, out_ids, out_dist, pin);
 }
 
 cudaError_t launch_merge_split(const int64_t* part_ids, const float* part_dist, int n_shards, int nq, int k,
@@ -1229,9 +1271,8 @@ cudaError_t launch_merge_split(const int64_t* part_ids, const float* part_dist, 
   if (nq <= 0) return cudaSuccess;
   if (k > kMaxK) return launch_merge_large(nullptr, part_ids, part_dist, n_shards, nq, k, out_ids, out_dist, s);
   const int wpb = 8;
-  k_merge_parts<<<(nq + wpb - 1) / wpb, wpb * 32, 0, s>>>(n_shards, nq, k, nullptr, part_ids, part_dist, out_ids,
-                                                          out_dist, PeerIn{});
-  return cudaGetLastError();
+  return launch_pdl(k_merge_parts, dim3((nq + wpb - 1) / wpb), dim3(wpb * 32), 0, s, n_shards, nq, k, nullptr,
+                    part_ids, part_dist, out_ids, out_dist, PeerIn{});
 }
 
 }  // namespace vlr

@@ -208,6 +208,16 @@ __device__ __forceinline__ uint32_t ld_relaxed_sys_u32(const uint32_t* p) {
   return v;
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic-serialization attribute
+// (launch_pdl) may start while the previous kernel of its stream is still running; griddepcontrol.wait
+// blocks until that kernel has completed and its memory is visible, launch_dependents lets the next
+// kernel start launching. Every chained kernel calls this first, before any early return (so that a
+// kernel can never complete before its predecessor). A no-op for a normal launch.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // element o of this rank's slab (slab elements per rank) into every rank's inbox
 template <class T>
 __device__ __forceinline__ void peer_store(const PeerOut& p, long long slab, long long o, const T& v) {

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <mutex>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -28,7 +29,8 @@ constexpr int kScanThreads = VLR_SCAN_THREADS;  // 16 warps per scan CTA (tuning
 constexpr int kScanWarps = kScanThreads / kWarp;
 constexpr int kCandCap = 8192;     // K2 candidate list capacity per query (overflow -> rescan)
 constexpr int kRefineChunk = 1024; // K3 candidates per exact-refine flush
-constexpr int kReleaseWaves = 8;      // NEXT-4: default query waves of the release-mode scan
+constexpr int kReleaseWaves = 1;      // NEXT-4: default query waves of the release-mode scan (the
+                                      // alternating segment order replaces waves, VLR_RELEASE_WAVES keeps them)
 constexpr int kMaxReleaseWaves = 16;  // upper bound (VLR_RELEASE_WAVES is clamped to it; sizes the partial slots)
 constexpr int kMaxNprobe = 2048;   // cap on nprobe' (K3 sort buffer; the paper's operating point)
 constexpr int kMaxWorldProbes = 16384;  // world x nprobe' cap of the sharded coarse stage (K2 stage-2 select)
@@ -200,6 +202,40 @@ struct vlr_index {
 
 namespace vlr {
 
+// ---------------------------------------------------------------- launches with programmatic dependence
+// The search chain (qprep, K1, K2, K3a, K3b, K4b, K6, K7, K8) is launched with the programmatic stream
+// serialization attribute: a kernel's CTAs launch while its predecessor finishes, and wait at
+// griddepcontrol.wait (pdl_entry, vlr_device.cuh) for its completion -- the launch latency between two
+// dependent kernels overlaps the predecessor's tail. VLR_PDL=0: ordinary launches (A/B timing).
+bool pdl_on();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+inline cudaError_t launch_pdl_c(const void* kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, void** args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelExC(&cfg, kernel, args);
+}
+
 // Per-(device, kernel) launch configuration: raises the kernel's dynamic shared-memory limit to at
 // least `bytes` on the CURRENT device (the attribute is per device context) and forces its module to be
 // loaded (cudaFuncGetAttributes); cached, thread-safe. Every launcher calls it before a launch.
@@ -228,7 +264,7 @@ cudaError_t launch_refine(const float* Q, const DeviceIndex& ix, const Workspace
                           int32_t* probes_out, int mode, cudaStream_t s, const PeerOut* po = nullptr,
                           const PeerIn* pi = nullptr);
 // stage 3..4
-cudaError_t launch_offsets(const Workspace& ws, int nq, int np, cudaStream_t s);
+cudaError_t launch_offsets(const DeviceIndex& ix, const Workspace& ws, int nq, int np, cudaStream_t s);
 cudaError_t launch_lut(const float* Q, const DeviceIndex& ix, const Workspace& ws, int nq, cudaStream_t s);
 cudaError_t launch_access_hist(const int32_t* probes, long long n, int nlist, unsigned long long* counts,
                                cudaStream_t s);
