@@ -76,6 +76,9 @@ def parse():
                         "on at N > 1 only (one GPU: no gain measured, DESIGN.md §5b)")
     p.add_argument("--scan-reserve", type=int, default=-1,
                    help="SMs the scan leaves to the other stream's coarse stage when pipelining (-1: default)")
+    p.add_argument("--deal", default="paper", choices=["paper", "traffic"],
+                   help="N > 1 hot-list deal: the paper's size round-robin (P:339, default) or the traffic-aware "
+                        "LPT deal on size x access count of the calibration stream (NEXT-2, vlr_deal_owners)")
     p.add_argument("--sweep-out", default=None,
                    help="also run the C5 batch x nprobe sweep on the same index and write JSON lines here")
     return p.parse_args()
@@ -248,7 +251,7 @@ def barrier(world):
         dist.barrier()
 
 
-def gen_index(c, seed, rank, world, hot=None, gt_queries=None):
+def gen_index(c, seed, rank, world, hot=None, gt_queries=None, owner_table=None):
     """Generate this rank's shard of the synthetic index on the GPU (TOOLING).
     VLR_GEN_CACHE=<dir> reuses arrays saved by an earlier process of the same
     command sequence (never relied on for timing: only generation time)."""
@@ -256,11 +259,15 @@ def gen_index(c, seed, rank, world, hot=None, gt_queries=None):
     sizes = datagen.list_sizes(c["N"], c["d"], c["nlist"], seed, device="cuda")
     owned = None
     if world > 1:
-        own = datagen.deal_owners(sizes, np.arange(c["nlist"]) if hot is None else hot, world)
+        own = owner_table if owner_table is not None else datagen.deal_owners(
+            sizes, np.arange(c["nlist"]) if hot is None else hot, world)
         owned = own == rank
     t = time.time()
     cache = os.environ.get("VLR_GEN_CACHE")
     key = f"g3_{c['N']}_{c['d']}_{c['nlist']}_{c['m']}_{seed}_{world}_{rank}_{'all' if hot is None else len(hot)}"
+    if owner_table is not None:
+        import hashlib
+        key += f"_own{hashlib.md5(np.ascontiguousarray(owner_table).tobytes()).hexdigest()[:10]}"
     key += f"_mt{c['metric']}_br{c['by_residual']}_nb{c['nbits']}"
     if gt_queries is not None:
         import hashlib
@@ -378,7 +385,22 @@ def main():
     # ground truth of the first timed batch, accumulated while the vectors are generated (N > 1: each rank
     # over its own lists, merged below)
     gtq = pool[a.warmup * B:(a.warmup + 1) * B] if not a.ncu else None
-    ix, gen_s = gen_index(c, a.seed, rank, world, hot=hot, gt_queries=gtq)
+    # hot-list deal (N > 1): the paper's round-robin by size, or the traffic-aware LPT deal on the calibration
+    # stream's access counts (owner per cluster; -1 = cold)
+    owner_table, hot_owner = None, None
+    if world > 1 and a.deal == "traffic":
+        sizes0 = datagen.list_sizes(c["N"], c["d"], c["nlist"], a.seed, device="cuda")
+        offs0 = np.concatenate([[0], np.cumsum(sizes0)]).astype(np.int64)
+        if counts is None:
+            C0 = datagen.centroids(c["N"], c["d"], c["nlist"], a.seed, device="cuda")
+            Qc0 = datagen.make_queries(c["N"], c["d"], c["nlist"], 10_000, seed=a.seed, stream=1, alpha=c["alpha"],
+                                       device="cuda")
+            counts = datagen.access_counts(C0, Qc0, c["nprobe"], device="cuda")
+        hot_ids = np.arange(c["nlist"], dtype=np.int32) if hot is None else np.asarray(hot, np.int32)
+        hot_owner = vlr.deal_owners(offs0, hot_ids, world, counts=counts)
+        owner_table = np.full(c["nlist"], -1, np.int32)
+        owner_table[hot_ids] = hot_owner
+    ix, gen_s = gen_index(c, a.seed, rank, world, hot=hot, gt_queries=gtq, owner_table=owner_table)
     nccl_id = None
     if world > 1 and not dry:
         import torch.distributed as dist
@@ -386,10 +408,11 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     t1 = time.time()
-    h = vlr.Index.from_arrays(ix, hot=hot, rank=rank, world=world, device=local, nccl_id=nccl_id)
+    h = vlr.Index.from_arrays(ix, hot=hot, hot_owner=hot_owner, rank=rank, world=world, device=local, nccl_id=nccl_id)
     load_s = time.time() - t1
     owners = h.owners()
-    exp_own = datagen.deal_owners(ix.list_sizes, np.arange(c["nlist"]) if hot is None else hot, world)
+    exp_own = owner_table if owner_table is not None else datagen.deal_owners(
+        ix.list_sizes, np.arange(c["nlist"]) if hot is None else hot, world)
     assert np.array_equal(owners, exp_own), "owner table differs from the documented deal"
     info = h.info()
     # ---- queries (test stream), resident in HBM
@@ -640,7 +663,9 @@ def main():
             "config": {"workload": workload_name(c, a.config), "N": c["N"], "d": c["d"], "nlist": c["nlist"], "m": c["m"],
                        "nprobe": c["nprobe"], "k": K, "batch": B, "alpha": c["alpha"], "hot_mass": c["hot_mass"],
                        "seed": a.seed,
-                       "parallelism": (f"hot-list shards x{world}, centroid-sharded coarse stage, "
+                       "parallelism": (f"hot-list shards x{world} ("
+                                       + ("size round-robin deal, P:339" if a.deal == "paper"
+                                          else "traffic-aware LPT deal") + "), centroid-sharded coarse stage, "
                                        + {"p2p": "NVLink peer-exchange kernels (IPC-mapped inboxes, epoch flags)",
                                           "nccl": "NCCL all-gathers + GPU merge-select",
                                           "staged": "staged C-ABI, exchanges over gloo through host memory"}[xchg]
@@ -779,7 +804,8 @@ def latency_leg(a, c, h, pool, K, device):
         out["by_batch"][str(B)] = {"batches": len(lat), "qps": float(B * len(lat) / (lat.sum() * 1e-3)),
                                    "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
                                    "p999_ms": float(np.percentile(lat, 99.9)), "max_ms": float(lat.max()),
-                                   "mean_ms": float(lat.mean())}
+                                   "mean_ms": float(lat.mean()),
+                                   "outlier_at_batch": [int(i) for i in np.nonzero(lat > 1.5 * np.median(lat))[0][:32]]}
     B = c["batch"]
     if B in graphs and a.sustained_s > 0:
         per = max(1e-4, out["by_batch"][str(B)]["mean_ms"] * 1e-3)
@@ -792,6 +818,10 @@ def latency_leg(a, c, h, pool, K, device):
                             "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
                             "max_ms": float(lat.max()), "clocks": clk,
                             "outliers_gt_1p5x_median": int((lat > 1.5 * np.median(lat)).sum()),
+                            # when they happen (device time since the loop start, s) and how long they are:
+                            # periodic outliers point at power / clock management, not at the search
+                            "outlier_at_s": [round(float(t), 4) for t in (np.cumsum(lat) * 1e-3)[lat > 1.5 * np.median(lat)][:32]],
+                            "outlier_ms": [round(float(x), 3) for x in lat[lat > 1.5 * np.median(lat)][:32]],
                             "how": "same graph closed loop for sustained_s seconds with the nvidia-smi sampler "
                                    "(-lms 100) running; compare p99/max with by_batch (no sampler)"}
     return out

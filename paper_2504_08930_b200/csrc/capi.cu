@@ -46,13 +46,15 @@ cudaError_t ensure_smem(const void* fn, size_t bytes) {
   return cudaSuccess;
 }
 
+static thread_local bool g_pdl_search = true;
+void pdl_for_search(bool allow) { g_pdl_search = allow; }
 bool pdl_on() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("VLR_PDL");
     v = (e && e[0] == '0') ? 0 : 1;
   }
-  return v == 1;
+  return v == 1 && g_pdl_search;
 }
 
 static vlr_status fail(vlr_status st, const std::string& msg) {
@@ -998,6 +1000,7 @@ static vlr_status search_locked(vlr_index* h, const float* Q, int32_t nq, int32_
   }
   int slot = slot_in;
   if (slot < 0 && (st = acquire_slot(h, nq, np, k, s, &slot)) != VLR_OK) return st;
+  pdl_for_search(h->nslots == 1);
   if (slot_out) *slot_out = slot;
   Workspace& w = h->wsl[slot];
   st = take_status(w, " (detected in a previous search on this handle)");
@@ -1288,6 +1291,7 @@ static vlr_status staged_begin(vlr_index* h, const float* Q, int32_t nq, int32_t
   VLR_CUDA_TRY(cudaSetDevice(h->ix.device));
   // sized for any k up front: a reallocation between the stages would drop the LUT and the gathered
   // buffers of the batch in flight
+  pdl_for_search(h->nslots == 1);
   return ensure_ws(h, h->stage_slot, nq, *np, std::max(k, kMaxK));  // k <= 32 only (vlr.h: staged search)
 }
 

@@ -629,13 +629,46 @@ __device__ __forceinline__ void warp_merge_query(const ScanArgs& a, int q, int G
   }
 }
 
+// qdone[q] bit 63 = "claimed": the merger (during the scan) and k_release_rest (after it) both claim a query
+// with an atomicOr before merging it, so exactly one of them releases it (the scan's group counts stay
+// below 2^63)
+constexpr unsigned long long kClaim = 1ull << 63;
+__device__ __forceinline__ bool rel_claim(const ScanArgs& a, int q, int lane) {
+  unsigned long long old = 0;
+  if (lane == 0) old = atomicOr(a.qdone + q, kClaim);
+  return (__shfl_sync(kFull, old, 0) & kClaim) == 0;
+}
+
+// merge query q's partial lists, write its row and raise its flag (one warp; q is complete and claimed)
+__device__ __forceinline__ void release_query(const ScanArgs& a, int q, int G, int lane) {
+  const int nq = a.nq, np = a.np, Z = a.waves;
+  __threadfence();  // acquire: q's partial lists after its completed count
+  const long long S = a.item_off[(long long)q * np], E = a.item_off[(long long)(q + 1) * np];
+  int z = (int)(((long long)(q + 1) * Z - 1) / nq);  // q's wave and its group range (k_scan's split)
+  z = z < Z - 1 ? z : Z - 1;
+  const long long WL = a.item_off[(long long)((long long)z * nq / Z) * np];
+  const long long WH = a.item_off[(long long)((long long)(z + 1) * nq / Z) * np];
+  float bd;
+  long long bid;
+  warp_merge_query(a, q, G, WL, WH, (long long)z * G, S, E, lane, bd, bid);
+  if (lane < a.k) {
+    a.out_ids[(size_t)q * a.k + lane] = bid;
+    a.out_dist[(size_t)q * a.k + lane] = bd;
+  }
+  __threadfence_system();  // row q (possibly in pinned host memory) before its flag
+  __syncwarp();
+  if (lane == 0) st_release_sys(a.ready + q, a.epoch);
+  __syncwarp();
+}
+
 // the resident merger CTA: warp w owns queries w, w + nw, ... and merges and releases each one as soon as
 // the scan has finished it (qdone[q] == its groups), in whatever order they complete (the scan's CTAs walk
-// their queries in alternating directions, so completion is not in query order); G = the scan's grid size
+// their queries in alternating directions, so completion is not in query order); G = the scan's grid size.
+// The queries still unreleased when the scan ends are taken by k_release_rest (all SMs, one warp each).
 __global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanArgs a, int G, int32_t* status) {
-  extern __shared__ unsigned char s_rel[];  // [nq] 1 = released
+  extern __shared__ unsigned char s_rel[];  // [nq] 1 = released here or claimed by k_release_rest
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nq = a.nq, np = a.np, Z = a.waves;
+  const int nq = a.nq, np = a.np;
   for (int q = threadIdx.x; q < nq; q += blockDim.x) s_rel[q] = 0;
   __syncthreads();
   const int mine = warp < nq ? (nq - warp + nw - 1) / nw : 0;
@@ -644,38 +677,22 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanAr
   while (left > 0) {
     bool any = false;
     for (int j0 = 0; j0 < mine; j0 += 32) {
-      // lane i polls query warp + nw (j0 + i) (relaxed load; the acquire is the fence before the merge)
+      // lane i polls query warp + nw (j0 + i) (relaxed load; the acquire is the fence in release_query)
       const int j = j0 + lane;
       const int qq = warp + nw * j;
       bool ready = false;
       if (j < mine && !s_rel[qq]) {
         const long long S = a.item_off[(long long)qq * np], E = a.item_off[(long long)(qq + 1) * np];
-        ready = ld_relaxed_gpu(a.qdone + qq) == (unsigned long long)(E - S);
+        const unsigned long long v = ld_relaxed_gpu(a.qdone + qq);
+        ready = (v & kClaim) != 0 || v == (unsigned long long)(E - S);
       }
       unsigned m = __ballot_sync(kFull, ready);
       while (m) {
         const int r = __ffs(m) - 1;
         m &= m - 1;
         const int q = warp + nw * (j0 + r);
-        __threadfence();  // acquire: q's partial lists after its completed count
-        const long long S = a.item_off[(long long)q * np], E = a.item_off[(long long)(q + 1) * np];
-        int z = (int)(((long long)(q + 1) * Z - 1) / nq);  // q's wave and its group range (k_scan's split)
-        z = z < Z - 1 ? z : Z - 1;
-        const long long WL = a.item_off[(long long)((long long)z * nq / Z) * np];
-        const long long WH = a.item_off[(long long)((long long)(z + 1) * nq / Z) * np];
-        float bd;
-        long long bid;
-        warp_merge_query(a, q, G, WL, WH, (long long)z * G, S, E, lane, bd, bid);
-        if (lane < a.k) {
-          a.out_ids[(size_t)q * a.k + lane] = bid;
-          a.out_dist[(size_t)q * a.k + lane] = bd;
-        }
-        __threadfence_system();  // row q (possibly in pinned host memory) before its flag
-        __syncwarp();
-        if (lane == 0) {
-          st_release_sys(a.ready + q, a.epoch);
-          s_rel[q] = 1;
-        }
+        if (rel_claim(a, q, lane)) release_query(a, q, G, lane);
+        if (lane == 0) s_rel[q] = 1;
         __syncwarp();
         --left;
         any = true;
@@ -693,6 +710,17 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanAr
       }
     }
   }
+}
+
+// after the release scan (stream order: every partial list is final): one warp per query claims and
+// releases the queries the merger has not taken yet -- the queries completing at the very end of the scan
+// are released in parallel over the GPU instead of 16 at a time by the merger's warps
+__global__ void __launch_bounds__(512) k_release_rest(ScanArgs a, int G) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= a.nq) return;
+  if ((ld_relaxed_gpu(a.qdone + q) & kClaim) != 0) return;  // released (or being released) by the merger
+  if (rel_claim(a, q, lane)) release_query(a, q, G, lane);
 }
 
 #ifdef VLR_SCAN_TRACE
@@ -937,6 +965,7 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
     cudaError_t e = launch_scan_k(ix, a, 0, s);
     if (e != cudaSuccess) return e;
     if ((e = ensure_smem((const void*)k_release_merge, (size_t)a.nq)) != cudaSuccess) return e;
+    if ((e = ensure_smem((const void*)k_release_rest, 0)) != cudaSuccess) return e;
     // fork: the merger CTA runs concurrently with the scan on a second stream, joined back before return
     e = cudaEventRecord(rel->fork, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(rel->stream, rel->fork, 0);
@@ -951,6 +980,10 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
     k_release_merge<<<1, kMergeMaxWarps * 32, (size_t)a.nq, rel->stream>>>(am, G, ws.status);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     e = launch_scan_k(ix, a, G, s);
+    if (e == cudaSuccess && rel_exp != 1) {  // the stragglers, in parallel (claims settle merger vs rest)
+      k_release_rest<<<(a.nq + 15) / 16, 512, 0, s>>>(a, G);
+      e = cudaGetLastError();
+    }
     if (e == cudaSuccess) e = cudaEventRecord(rel->join, rel->stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, rel->join, 0);
     return e;

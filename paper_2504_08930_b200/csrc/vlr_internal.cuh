@@ -207,7 +207,10 @@ namespace vlr {
 // serialization attribute: a kernel's CTAs launch while its predecessor finishes, and wait at
 // griddepcontrol.wait (pdl_entry, vlr_device.cuh) for its completion -- the launch latency between two
 // dependent kernels overlaps the predecessor's tail. VLR_PDL=0: ordinary launches (A/B timing).
-bool pdl_on();
+bool pdl_on();  // VLR_PDL != 0 and the current search allows it (pdl_for_search)
+// PDL is used only without cross-batch pipelining: an early-launched CTA waiting at griddepcontrol.wait
+// holds SM slots the other stream's batch would use (measured at G = 8, pipelined: 0.369 -> 0.403 ms)
+void pdl_for_search(bool allow);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
   cudaLaunchConfig_t cfg = {};

@@ -35,6 +35,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--seed", type=int, default=2504_08930)
     ap.add_argument("--backlog-cycles", type=int, default=10_000_000)
+    ap.add_argument("--deal", default="paper", choices=["paper", "traffic"],
+                    help="hot-list deal: the paper's size round-robin (P:339) or the traffic-aware LPT deal on "
+                         "size x access count of a 4096-query calibration stream (stream 1, disjoint; NEXT-2)")
     ap.add_argument("--pipe-reserve", default="0,8,16,24,32",
                     help="scan reserves for the pipelined single-rank pass ('' = skip)")
     a = ap.parse_args()
@@ -51,7 +54,13 @@ def main():
                                 alpha=c["alpha"], device="cuda")
     Qd = torch.from_numpy(pool).cuda().reshape(-1, B, c["d"])
     G = a.G
-    hs = [vlr.Index.from_arrays(ix, rank=r, world=G) for r in range(G)]
+    owners = None
+    if a.deal == "traffic":
+        Qc = datagen.make_queries(c["N"], c["d"], c["nlist"], 4096, seed=a.seed, stream=1, alpha=c["alpha"],
+                                  device="cuda")
+        cnt = datagen.access_counts(ix.centroids, Qc, c["nprobe"], device="cuda")
+        owners = vlr.deal_owners(ix.list_offsets, np.arange(c["nlist"], dtype=np.int32), G, counts=cnt)
+    hs = [vlr.Index.from_arrays(ix, rank=r, world=G, hot_owner=owners) for r in range(G)]
     h1 = vlr.Index.from_arrays(ix)
     for h in hs + [h1]:
         h.reserve(B, c["nprobe"], K)
@@ -112,7 +121,7 @@ def main():
     nonscan = T1 + T2 + T3 - SC  # [batches, G] ms
     single = {k: float(np.mean([r["single"][k] for r in rows])) for k in rows[0]["single"]}
     out = {
-        "tool": "tools/shard_model.py", "config": a.config, "G": G, "batch": B, "nprobe": c["nprobe"], "k": K,
+        "tool": "tools/shard_model.py", "config": a.config, "G": G, "deal": a.deal, "batch": B, "nprobe": c["nprobe"], "k": K,
         "batches": a.batches, "gen_s": round(gen_s, 1),
         "bitwise_equal_to_single_gpu": all(r["same"] for r in rows),
         "per_rank_ms": {"stage1_mean": float(T1.mean()), "stage2_mean": float(T2.mean()),
