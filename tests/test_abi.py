@@ -100,6 +100,8 @@ def test_search_argument_validation_without_index():
     assert vlr.STATUS[st] == "INVALID_ARG"
     st = L.vlr_merge_partials(None, None, 1, 0, 4, None, None, None)
     assert vlr.STATUS[st] == "OK"  # nq == 0 is a no-op
+    st = L.vlr_set_pipeline(None, 2, 0)  # cross-batch pipelining on a null handle
+    assert vlr.STATUS[st] == "INVALID_ARG"
     assert b"" != L.vlr_last_error() or True
 
 
