@@ -71,6 +71,7 @@ struct ScanArgs {
   // the groups g of queries [q_lo, q_hi); k_select_large keeps each query's k smallest
   int q_lo, q_hi;
   uint2* dump;
+  int alt;                    // 1: even CTAs walk their queries backward (all scans; REL always)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -808,9 +809,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
     auto vol_i = [](const int& x) { return *reinterpret_cast<const volatile int*>(&x); };
     auto vol_l = [](const long long& x) { return *reinterpret_cast<const volatile long long*>(&x); };
     for (int si = 0; si <= vol_i(s_qb) - vol_i(s_qa); ++si) {
-      // NEXT-4 (REL): even CTAs walk their queries backward, odd CTAs forward, so the query shared by CTAs
-      // 2j and 2j+1 is scanned first by both and completes early; otherwise forward
-      const int q = (REL && (c & 1) == 0) ? vol_i(s_qb) - si : vol_i(s_qa) + si;
+      // even CTAs walk their queries backward, odd CTAs forward: for NEXT-4 (REL) the query shared by CTAs
+      // 2j and 2j+1 is scanned first by both and completes early; VLR_SCAN_ALT (default on)
+      // applies the same order to every scan (plain: measured per group no slower)
+      const int q = ((REL || a.alt) && (c & 1) == 0) ? vol_i(s_qb) - si : vol_i(s_qa) + si;
       const long long qstart = a.item_off[(long long)q * a.np], qend = a.item_off[(long long)(q + 1) * a.np];
       const long long cg0 = vol_l(s_g0), cg1 = vol_l(s_g1);
       const long long g = qstart > cg0 ? qstart : cg0;
@@ -893,6 +895,16 @@ extern "C" int vlr_debug_scan_trace(unsigned long long* out, int n) {
 }
 #endif
 
+// VLR_SCAN_ALT=0: every CTA of the plain / large-k scan walks its queries forward (A/B timing)
+static int scan_alt() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("VLR_SCAN_ALT");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+
 int scan_ctas(const DeviceIndex& ix) {
   (void)ix;
   int dev = 0, sms = 148;
@@ -942,7 +954,7 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
   if (nq <= 0) return cudaSuccess;
   ScanArgs a{nq, np, k, ix.npairs, (uint32_t)(ix.npairs * ix.lut_pair_bytes), ws.plocal, ws.term1, ws.item_off,
              ix.gbase, ix.codes, ix.bias, ix.ids, ws.lut, ws.pdist, ws.pid,
-             nullptr, nullptr, 0u, nullptr, nullptr, 1, 0, nq, nullptr};
+             nullptr, nullptr, 0u, nullptr, nullptr, 1, 0, nq, nullptr, scan_alt()};
   int G = ws.n_cta;
   if (rel) {
     if ((long long)ws.n_cta * kScanWarps > kMergeMaxLists || ws.n_cta < 2) return cudaErrorInvalidConfiguration;
@@ -1187,7 +1199,7 @@ cudaError_t launch_scan_large(const DeviceIndex& ix, const Workspace& ws, int nq
     const int q1 = q0 + qc < nq ? q0 + qc : nq;
     ScanArgs a{nq, np, k, ix.npairs, (uint32_t)(ix.npairs * ix.lut_pair_bytes), ws.plocal, ws.term1, ws.item_off,
                ix.gbase, ix.codes, ix.bias, ix.ids, ws.lut, ws.pdist, ws.pid,
-               nullptr, nullptr, 0u, nullptr, nullptr, 1, q0, q1, ws.dump};
+               nullptr, nullptr, 0u, nullptr, nullptr, 1, q0, q1, ws.dump, scan_alt()};
     cudaError_t e = launch_scan_k(ix, a, ws.n_cta, s);
     if (e != cudaSuccess) return e;
     e = launch_pdl(k_select_large, dim3(q1 - q0), dim3(kSelLargeThreads), 0, s, q0, np, k, ws.item_off, ws.dump,
