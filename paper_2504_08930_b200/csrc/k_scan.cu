@@ -810,8 +810,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
     auto vol_l = [](const long long& x) { return *reinterpret_cast<const volatile long long*>(&x); };
     for (int si = 0; si <= vol_i(s_qb) - vol_i(s_qa); ++si) {
       // even CTAs walk their queries backward, odd CTAs forward: for NEXT-4 (REL) the query shared by CTAs
-      // 2j and 2j+1 is scanned first by both and completes early; VLR_SCAN_ALT (default on)
-      // applies the same order to every scan (plain: measured per group no slower)
+      // 2j and 2j+1 is scanned first by both and completes early; VLR_SCAN_ALT=1 applies
+      // the same order to every scan
       const int q = ((REL || a.alt) && (c & 1) == 0) ? vol_i(s_qb) - si : vol_i(s_qa) + si;
       const long long qstart = a.item_off[(long long)q * a.np], qend = a.item_off[(long long)(q + 1) * a.np];
       const long long cg0 = vol_l(s_g0), cg1 = vol_l(s_g1);
@@ -895,12 +895,13 @@ extern "C" int vlr_debug_scan_trace(unsigned long long* out, int n) {
 }
 #endif
 
-// VLR_SCAN_ALT=0: every CTA of the plain / large-k scan walks its queries forward (A/B timing)
+// VLR_SCAN_ALT=1: the plain / large-k scan alternates the segment order too (measured neutral at C4:
+// 1.536-1.540 ms either way, profiles/r02/scan_trace_alt*_s.jsonl; default off)
 static int scan_alt() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("VLR_SCAN_ALT");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v;
 }

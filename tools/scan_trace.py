@@ -57,7 +57,8 @@ def trace(h, c, Q, L, config, G, release=False, nowait=False):
         else:
             h.search(Q, c["nprobe"], c["k"], sync=True)
         scan_ms = h.stage_times(0)["scan"]
-        n = 147 if release else 148  # the release scan leaves one SM to the merger CTA
+        # the scan's grid: SMs - VLR_SCAN_RESERVE, and the release scan leaves one more SM to the merger CTA
+        n = 148 - int(os.environ.get("VLR_SCAN_RESERVE", "0")) - (1 if release else 0)
         t = np.zeros((n, 6), np.uint64)
         assert L.vlr_debug_scan_trace(t.ctypes.data, n) == 0
         t = t.astype(np.int64)
