@@ -548,13 +548,14 @@ def main():
         hid = torch.empty(B, K, dtype=torch.int64).pin_memory()
         hd = torch.empty(B, K, dtype=torch.float32).pin_memory()
         hm = torch.empty(B, NP, dtype=torch.uint8).pin_memory()
-        # the serving pipeline below alternates two streams with two workspace slots whenever the transport
-        # allows (one GPU, or the peer exchange), so batch i+1's H2D copy (copy engine) overlaps batch i's
-        # kernels; the scan reserve is the timed region's (0 on one GPU)
-        e2e_pipe = xchg in ("none", "p2p")
+        # the serving pipeline below alternates two streams with two workspace slots when the timed region
+        # does (N > 1); on one GPU it stays on one stream: two slots there measured slower (127-136k vs
+        # 139-143k q/s, profiles/r02/bench_c4_{o,p}.json vs bench_c4_m.json: the next batch's kernels start
+        # inside the persistent scan's tail and its static split loses balance)
+        e2e_pipe = pipe
         e2e_streams = [stream, torch.cuda.Stream()] if e2e_pipe else [stream, stream]
         if e2e_pipe:
-            h.set_pipeline(2, reserve if pipe else 0)
+            h.set_pipeline(2, reserve)
         for i in range(min(3, ne)):
             h.search_host_ptr(hq[i].data_ptr(), B, c["nprobe"], K, hid.data_ptr(), hd.data_ptr(), hm.data_ptr(), None)
         barrier(world)
