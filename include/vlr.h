@@ -182,11 +182,14 @@ vlr_status vlr_search_host(vlr_index* idx, const float* h_queries, int32_t nq, i
  * NEXT-4: early per-query release -- the GPU analog of the paper's dynamic
  * dispatcher (P:408-414 [§IV.C]: "GPU ... completion flags", "per-query
  * callback" so a finished query does not wait for its batch; Fig. 14).
- * Same search and outputs as vlr_search_async, but the batch is scanned in
- * query waves on all SMs but one, and a resident merger CTA (on the remaining
- * SM, forked onto a second stream and joined back to `stream`) merges each
- * query's partial lists as soon as the scan has finished the query, then
- * raises ready[q] = epoch (no separate K7 launch after the scan).
+ * Same search and outputs as vlr_search_async, but the scan runs on all SMs
+ * but one with even CTAs walking their queries backward (so queries complete
+ * throughout the scan), and a resident merger CTA (on the
+ * remaining SM, forked onto a second stream and joined back to `stream`)
+ * merges each query's partial lists as soon as the scan has finished the
+ * query, in completion order, then raises ready[q] = epoch; the queries still
+ * unreleased when the scan ends are merged by a follow-up kernel over all SMs
+ * (no separate K7 launch).
  *   ready [nq] uint32: flags, device-accessible -- device memory or pinned
  *      host memory (cudaHostAlloc / cudaMallocHost, used through its UVA
  *      pointer); the caller sets them != epoch before the call.
