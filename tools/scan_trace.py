@@ -24,12 +24,13 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--G", default="1,8", help="shard counts (rank 0's shard traced)")
     ap.add_argument("--release", action="store_true", help="trace the NEXT-4 release scan (REL waves) too")
+    ap.add_argument("--lib", default="scantrace", help="variant under tools/_variants/ (built with VLR_SCAN_TRACE=1)")
     ap.add_argument("--release-nowait", action="store_true",
                     help="launch the release search without waiting for the flags (VLR_REL_EXPERIMENT=1 runs)")
     a = ap.parse_args()
     import datagen
     import paper_2504_08930_b200 as vlr
-    vlr.LIB_PATH = os.path.join(ROOT, "tools", "_variants", "scantrace", "libvlr.so")
+    vlr.LIB_PATH = os.path.join(ROOT, "tools", "_variants", a.lib, "libvlr.so")
     c = datagen.CONFIGS[a.config]
     ix = datagen.make_index(c["N"], c["d"], c["nlist"], c["m"], device="cuda")
     Q = torch.from_numpy(datagen.make_queries(c["N"], c["d"], c["nlist"], c["batch"], stream=2, device="cuda")).cuda()
@@ -43,8 +44,13 @@ def main():
         h.close()
 
 
+def vlr_lib_path():
+    import paper_2504_08930_b200 as vlr
+    return vlr.LIB_PATH
+
+
 def trace(h, c, Q, L, config, G, release=False, nowait=False):
-    out = {"config": config, "G": G, "release": release, "env": {k: v for k, v in os.environ.items()
+    out = {"config": config, "G": G, "release": release, "lib": os.path.basename(os.path.dirname(vlr_lib_path())), "env": {k: v for k, v in os.environ.items()
                                                                   if k.startswith("VLR_")}, "runs": []}
     for it in range(6):
         h.set_profiling(2)
