@@ -160,41 +160,18 @@ __device__ __forceinline__ void grp_prefetch(const ScanArgs& a, long long gg, lo
     asm volatile("prefetch.global.L2 [%0];" ::"l"(a.codes + gaddr * (4 * MP * NB) + lane * 128) : "memory");
 }
 
-#ifndef VLR_SCAN_ICACHE
-#define VLR_SCAN_ICACHE 0
-#endif
-// per-warp cache of the current item of the loads (VLR_SCAN_ICACHE=1): consecutive groups of a warp
-// mostly fall in the same item (a probed list), so the item's end, group-address offset and term1 are
-// reused and the item cursor's five L1 loads are paid only at item boundaries
-struct ItemCache {
-  long long end = -1, delta = 0;
-  float t1 = 0.f;
-};
-
 template <int MP, int NB, int EXP = 0>
-__device__ __forceinline__ void grp_load(Grp<MP, NB>& G, const ScanArgs& a, long long gg, long long& it,
-                                         ItemCache& ic, int lane) {
+__device__ __forceinline__ void grp_load(Grp<MP, NB>& G, const ScanArgs& a, long long gg, long long& it, int lane) {
   constexpr int kChunks = MP * NB / 128;
   // the item cursor's loads (item_off, plocal, gbase, term1) hit L1; a per-group metadata array written by
   // K4b (one 8-byte word per group) measured slower: its first touch per line is an L2 round trip on the
-  // path to the code loads (scan 1.53 -> 1.81 ms at C4, profiles/r02/scan_trace_gmeta_n_slower.jsonl)
-#if VLR_SCAN_ICACHE
-  if (gg >= ic.end) {  // warp-uniform
-    advance_item(a, gg, it, lane);
-    const long long ib = a.item_off[it];
-    ic.end = a.item_off[it + 1];
-    ic.delta = a.gbase[a.plocal[it]] - ib;
-    ic.t1 = a.term1[it];
-  }
-  G.gaddr = gg + ic.delta;
-  G.t1 = ic.t1;
-#else
-  (void)ic;
+  // path to the code loads (scan 1.53 -> 1.81 ms at C4, profiles/r02/scan_trace_gmeta_n_slower.jsonl); a
+  // per-warp cache of the current item (end, address offset, term1; loads only at item boundaries) measured
+  // slower too (1.543 -> 1.577 ms, 8 B of spills at 128 registers; profiles/r02/scan_trace_icache_v.jsonl)
   advance_item(a, gg, it, lane);
   const int loc = a.plocal[it];
   G.gaddr = a.gbase[loc] + (gg - a.item_off[it]);
   G.t1 = a.term1[it];
-#endif
   const uint4* src = reinterpret_cast<const uint4*>(a.codes) + G.gaddr * (32 * kChunks) + lane;
 #pragma unroll
   for (int c = 0; c < kChunks; ++c) {
@@ -870,24 +847,23 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
       // item cursors of the loads and of the L2 prefetch (kPfDist groups of this warp ahead), from an item
       // at or before the segment's first (the item holding g0, or q's first item)
       long long it = g == cg0 ? vol_l(s_it) : (long long)q * a.np, itp = it;
-      ItemCache ic;
       Grp<MP, NB> A, B;
       if (gg < seg_end) {
         for (int p = 1; p <= kPfDist; ++p)
           if (gg + p * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gg + p * kScanWarps, itp, lane);
-        grp_load<MP, NB, EXP>(A, a, gg, it, ic, lane);
+        grp_load<MP, NB, EXP>(A, a, gg, it, lane);
       }
       while (gg < seg_end) {
         const long long gn = gg + kScanWarps;
         if constexpr (kPfDist > 0)
           if (gn + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gn + kPfDist * kScanWarps, itp, lane);
-        if (gn < seg_end) grp_load<MP, NB, EXP>(B, a, gn, it, ic, lane);
+        if (gn < seg_end) grp_load<MP, NB, EXP>(B, a, gn, it, lane);
         grp_finish<MP, NB, EXP, DUMP>(A, a, lutc, lane4, lane, bd, bid, thr, gg - WL);
         if (gn >= seg_end) break;
         const long long gm = gn + kScanWarps;
         if constexpr (kPfDist > 0)
           if (gm + kPfDist * kScanWarps < seg_end) grp_prefetch<MP, NB>(a, gm + kPfDist * kScanWarps, itp, lane);
-        if (gm < seg_end) grp_load<MP, NB, EXP>(A, a, gm, it, ic, lane);
+        if (gm < seg_end) grp_load<MP, NB, EXP>(A, a, gm, it, lane);
         grp_finish<MP, NB, EXP, DUMP>(B, a, lutc, lane4, lane, bd, bid, thr, gn - WL);
         gg = gm;
       }
