@@ -636,6 +636,12 @@ __device__ __forceinline__ void warp_merge_query(const ScanArgs& a, int q, int G
 // with an atomicOr before merging it, so exactly one of them releases it (the scan's group counts stay
 // below 2^63)
 constexpr unsigned long long kClaim = 1ull << 63;
+#ifdef VLR_SCAN_TRACE
+// timing variant: per query the globaltimer ns of its flag store and who released it (1 merger, 2 rest);
+// [0] = first k_release_rest CTA start, [1] = merger end
+__device__ unsigned long long g_rel_trace[4096][2];
+__device__ unsigned long long g_rel_misc[2];
+#endif
 __device__ __forceinline__ bool rel_claim(const ScanArgs& a, int q, int lane) {
   unsigned long long old = 0;
   if (lane == 0) old = atomicOr(a.qdone + q, kClaim);
@@ -643,7 +649,7 @@ __device__ __forceinline__ bool rel_claim(const ScanArgs& a, int q, int lane) {
 }
 
 // merge query q's partial lists, write its row and raise its flag (one warp; q is complete and claimed)
-__device__ __forceinline__ void release_query(const ScanArgs& a, int q, int G, int lane) {
+__device__ __forceinline__ void release_query(const ScanArgs& a, int q, int G, int lane, int who = 0) {
   const int nq = a.nq, np = a.np, Z = a.waves;
   __threadfence();  // acquire: q's partial lists after its completed count
   const long long S = a.item_off[(long long)q * np], E = a.item_off[(long long)(q + 1) * np];
@@ -661,6 +667,14 @@ __device__ __forceinline__ void release_query(const ScanArgs& a, int q, int G, i
   __threadfence_system();  // row q (possibly in pinned host memory) before its flag
   __syncwarp();
   if (lane == 0) st_release_sys(a.ready + q, a.epoch);
+#ifdef VLR_SCAN_TRACE
+  if (lane == 0 && q < 4096) {
+    g_rel_trace[q][0] = globaltimer_ns();
+    g_rel_trace[q][1] = (unsigned long long)who;
+  }
+#else
+  (void)who;
+#endif
   __syncwarp();
 }
 
@@ -694,7 +708,7 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanAr
         const int r = __ffs(m) - 1;
         m &= m - 1;
         const int q = warp + nw * (j0 + r);
-        if (rel_claim(a, q, lane)) release_query(a, q, G, lane);
+        if (rel_claim(a, q, lane)) release_query(a, q, G, lane, 1);
         if (lane == 0) s_rel[q] = 1;
         __syncwarp();
         --left;
@@ -713,6 +727,10 @@ __global__ void __launch_bounds__(kMergeMaxWarps * 32, 1) k_release_merge(ScanAr
       }
     }
   }
+#ifdef VLR_SCAN_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) g_rel_misc[1] = globaltimer_ns();
+#endif
 }
 
 // after the release scan (stream order: every partial list is final): one warp per query claims and
@@ -722,8 +740,11 @@ __global__ void __launch_bounds__(512) k_release_rest(ScanArgs a, int G) {
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= a.nq) return;
+#ifdef VLR_SCAN_TRACE
+  if (threadIdx.x == 0) atomicMin(&g_rel_misc[0], globaltimer_ns());
+#endif
   if ((ld_relaxed_gpu(a.qdone + q) & kClaim) != 0) return;  // released (or being released) by the merger
-  if (rel_claim(a, q, lane)) release_query(a, q, G, lane);
+  if (rel_claim(a, q, lane)) release_query(a, q, G, lane, 2);
 }
 
 #ifdef VLR_SCAN_TRACE
@@ -891,6 +912,13 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
 }
 
 #ifdef VLR_SCAN_TRACE
+extern "C" int vlr_debug_rel_trace(unsigned long long* out, int n, unsigned long long* misc) {
+  const unsigned long long init[2] = {~0ull, 0ull};
+  if (!out) return cudaMemcpyToSymbol(g_rel_misc, init, sizeof(init)) == cudaSuccess ? 0 : -1;  // reset
+  if (cudaMemcpyFromSymbol(out, g_rel_trace, sizeof(unsigned long long) * 2 * (n < 4096 ? n : 4096)) != cudaSuccess)
+    return -1;
+  return cudaMemcpyFromSymbol(misc, g_rel_misc, sizeof(unsigned long long) * 2) == cudaSuccess ? 0 : -1;
+}
 extern "C" int vlr_debug_scan_trace(unsigned long long* out, int n) {
   return cudaMemcpyFromSymbol(out, g_scan_trace, sizeof(unsigned long long) * 6 * (n < 1024 ? n : 1024)) == cudaSuccess
              ? 0 : -1;
