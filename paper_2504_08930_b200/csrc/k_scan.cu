@@ -640,7 +640,8 @@ constexpr unsigned long long kClaim = 1ull << 63;
 // timing variant: per query the globaltimer ns of its flag store and who released it (1 merger, 2 rest);
 // [0] = first k_release_rest CTA start, [1] = merger end
 __device__ unsigned long long g_rel_trace[4096][2];
-__device__ unsigned long long g_rel_misc[2];
+__device__ unsigned long long g_rel_misc[4];  // [2] stamp before the fork, [3] stamp after the join
+__global__ void k_stamp(int i) { g_rel_misc[i] = globaltimer_ns(); }
 #endif
 __device__ __forceinline__ bool rel_claim(const ScanArgs& a, int q, int lane) {
   unsigned long long old = 0;
@@ -913,11 +914,11 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
 
 #ifdef VLR_SCAN_TRACE
 extern "C" int vlr_debug_rel_trace(unsigned long long* out, int n, unsigned long long* misc) {
-  const unsigned long long init[2] = {~0ull, 0ull};
+  const unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
   if (!out) return cudaMemcpyToSymbol(g_rel_misc, init, sizeof(init)) == cudaSuccess ? 0 : -1;  // reset
   if (cudaMemcpyFromSymbol(out, g_rel_trace, sizeof(unsigned long long) * 2 * (n < 4096 ? n : 4096)) != cudaSuccess)
     return -1;
-  return cudaMemcpyFromSymbol(misc, g_rel_misc, sizeof(unsigned long long) * 2) == cudaSuccess ? 0 : -1;
+  return cudaMemcpyFromSymbol(misc, g_rel_misc, sizeof(unsigned long long) * 4) == cudaSuccess ? 0 : -1;
 }
 extern "C" int vlr_debug_scan_trace(unsigned long long* out, int n) {
   return cudaMemcpyFromSymbol(out, g_scan_trace, sizeof(unsigned long long) * 6 * (n < 1024 ? n : 1024)) == cudaSuccess
@@ -1009,6 +1010,9 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
     if (e != cudaSuccess) return e;
     if ((e = ensure_smem((const void*)k_release_merge, (size_t)a.nq)) != cudaSuccess) return e;
     if ((e = ensure_smem((const void*)k_release_rest, 0)) != cudaSuccess) return e;
+#ifdef VLR_SCAN_TRACE
+    k_stamp<<<1, 1, 0, s>>>(2);
+#endif
     // fork: the merger CTA runs concurrently with the scan on a second stream, joined back before return
     e = cudaEventRecord(rel->fork, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(rel->stream, rel->fork, 0);
@@ -1029,6 +1033,9 @@ cudaError_t launch_scan(const DeviceIndex& ix, const Workspace& ws, int nq, int 
     }
     if (e == cudaSuccess) e = cudaEventRecord(rel->join, rel->stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, rel->join, 0);
+#ifdef VLR_SCAN_TRACE
+    k_stamp<<<1, 1, 0, s>>>(3);
+#endif
     return e;
   }
   return launch_scan_k(ix, a, G, s);

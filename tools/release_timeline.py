@@ -57,7 +57,7 @@ def main():
         assert L.vlr_debug_scan_trace(t.ctypes.data, 147) == 0
         t = t.astype(np.int64)
         r = np.zeros((nq, 2), np.uint64)
-        misc = np.zeros(2, np.uint64)
+        misc = np.zeros(4, np.uint64)
         assert L.vlr_debug_rel_trace(r.ctypes.data, nq, misc.ctypes.data) == 0
         r = r.astype(np.int64)
         misc = misc.astype(np.int64)
@@ -69,6 +69,7 @@ def main():
             out["release"].append({
                 "scan_end_us": [float(end.min()), float(np.median(end)), float(end.max())],
                 "rest_start_us": float((misc[0] - t0) / 1e3), "merger_end_us": float((misc[1] - t0) / 1e3),
+                "before_fork_us": float((misc[2] - t0) / 1e3), "after_join_us": float((misc[3] - t0) / 1e3),
                 "release_us": {"p10": float(np.percentile(rel, 10)), "p50": float(np.percentile(rel, 50)),
                                "p90": float(np.percentile(rel, 90)), "p99": float(np.percentile(rel, 99)),
                                "max": float(rel.max())},
