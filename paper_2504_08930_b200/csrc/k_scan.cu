@@ -759,11 +759,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
   __shared__ __align__(8) uint64_t mbar;
   __shared__ long long s_it;
   __shared__ long long s_ng;
-  __shared__ int s_z, s_qa, s_qb;
+  __shared__ int s_z, s_qa, s_qb, s_q;
   __shared__ long long s_g0, s_g1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = gridDim.x, c = blockIdx.x;
-  const int Z = REL ? a.waves : 1;
   const uint32_t lut_bytes = a.lut_bytes;
   if (threadIdx.x == 0) {
     mbar_init(&mbar, 1);
@@ -783,11 +782,18 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
     __syncthreads();
   }
   auto zcur = [&]() -> int { return *reinterpret_cast<volatile int*>(&s_z); };
-  for (int z1 = 0; z1 < Z; ++z1) {
-    if constexpr (REL) __syncthreads();  // s_z of the previous wave written
-    const int z = REL ? zcur() : z1;
-    const int i_lo = (REL ? (int)((long long)z * a.nq / Z) : a.q_lo) * a.np;
-    const int i_hi = (REL ? (int)((long long)(z + 1) * a.nq / Z) : a.q_hi) * a.np;
+  // REL: the wave loop's counter is s_z and its bound the kernel parameter, so no register is live across
+  // the scan loop for them (a register counter made the MP = 128 REL loop spill)
+  for (int z1 = 0;; ++z1) {
+    if constexpr (REL) {
+      __syncthreads();  // s_z of the previous wave written
+      if (zcur() >= a.waves) break;
+    } else {
+      if (z1 > 0) break;
+    }
+    const int z = REL ? zcur() : 0;
+    const int i_lo = (REL ? (int)((long long)z * a.nq / a.waves) : a.q_lo) * a.np;
+    const int i_hi = (REL ? (int)((long long)(z + 1) * a.nq / a.waves) : a.q_hi) * a.np;
     const long long WL = a.item_off[i_lo], WH = a.item_off[i_hi];
     const long long g0 = WL + (long long)c * (WH - WL) / G, g1 = WL + (long long)(c + 1) * (WH - WL) / G;
     if constexpr (REL) {
@@ -849,8 +855,11 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
         for (uint32_t off = 0; off < lut_bytes; off += 32768u)
           bulk_g2s(smem + off, src + off, lut_bytes - off < 32768u ? lut_bytes - off : 32768u, &mbar);
       }
-      if constexpr (REL) {  // segment length through shared memory: nothing extra stays live across the scan loop
-        if (threadIdx.x == 0) s_ng = seg_end - g;
+      if constexpr (REL) {  // segment length and query through shared memory: nothing extra stays live across
+        if (threadIdx.x == 0) {  // the scan loop
+          s_ng = seg_end - g;
+          s_q = q;
+        }
       }
 #ifdef VLR_SCAN_TRACE
       const unsigned long long tw0 = globaltimer_ns();
@@ -889,13 +898,15 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
         grp_finish<MP, NB, EXP, DUMP>(B, a, lutc, lane4, lane, bd, bid, thr, gn - WL);
         gg = gm;
       }
-      const long long slot = ((long long)(c + q) + (long long)(REL ? zcur() - 1 : 0) * G) * kScanWarps * a.k + warp * a.k;
+      // REL: q comes back from shared memory (no register live across the scan loop for it)
+      const int qs = REL ? *reinterpret_cast<volatile int*>(&s_q) : q;
+      const long long slot = ((long long)(c + qs) + (long long)(REL ? zcur() - 1 : 0) * G) * kScanWarps * a.k + warp * a.k;
       if (!DUMP && lane < a.k) {  // REL: released by thread 0's fence after the barrier (rel_segment_done)
         a.pdist[slot + lane] = bd;
         a.pid[slot + lane] = bid;
       }
       __syncthreads();  // every warp is done with this LUT
-      if constexpr (REL) rel_segment_done(a, q, s_ng);
+      if constexpr (REL) rel_segment_done(a, qs, s_ng);
     }
   }
 #ifdef VLR_SCAN_TRACE
