@@ -752,9 +752,6 @@ __global__ void __launch_bounds__(512) k_release_rest(ScanArgs a, int G) {
 // timing variant (tools/scan_trace.py): per CTA start, end, LUT-wait ns, segments, smid, groups
 __device__ unsigned long long g_scan_trace[1024][6];
 #endif
-#ifndef VLR_SCAN_SMEMQ
-#define VLR_SCAN_SMEMQ 0  // variant: the plain scan also keeps the segment's query in shared memory
-#endif
 template <int MP, int NB, int EXP, bool REL = false, bool DUMP = false>
 __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
   pdl_entry();  // PDL: wait for the previous kernel in the stream, then let the next one launch
@@ -858,8 +855,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
         for (uint32_t off = 0; off < lut_bytes; off += 32768u)
           bulk_g2s(smem + off, src + off, lut_bytes - off < 32768u ? lut_bytes - off : 32768u, &mbar);
       }
-      if constexpr (REL || VLR_SCAN_SMEMQ) {  // segment length and query through shared memory: nothing extra
-        if (threadIdx.x == 0) {                // stays live across the scan loop
+      if constexpr (REL) {  // segment length and query through shared memory: nothing extra stays live across
+        if (threadIdx.x == 0) {  // the scan loop
           s_ng = seg_end - g;
           s_q = q;
         }
@@ -901,9 +898,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(ScanArgs a) {
         grp_finish<MP, NB, EXP, DUMP>(B, a, lutc, lane4, lane, bd, bid, thr, gn - WL);
         gg = gm;
       }
-      // REL (and VLR_SCAN_SMEMQ builds): q comes back from shared memory (no register live across the scan
-      // loop for it)
-      const int qs = (REL || VLR_SCAN_SMEMQ) ? *reinterpret_cast<volatile int*>(&s_q) : q;
+      // REL: q comes back from shared memory (no register live across the scan loop for it; the same for the
+      // plain scan measured slower: 1.562 vs 1.530 ms at C4, profiles/r02/scan_ab_smemq_aa.jsonl)
+      const int qs = REL ? *reinterpret_cast<volatile int*>(&s_q) : q;
       const long long slot = ((long long)(c + qs) + (long long)(REL ? zcur() - 1 : 0) * G) * kScanWarps * a.k + warp * a.k;
       if (!DUMP && lane < a.k) {  // REL: released by thread 0's fence after the barrier (rel_segment_done)
         a.pdist[slot + lane] = bd;
