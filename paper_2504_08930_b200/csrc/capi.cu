@@ -1000,7 +1000,9 @@ static vlr_status search_locked(vlr_index* h, const float* Q, int32_t nq, int32_
   }
   int slot = slot_in;
   if (slot < 0 && (st = acquire_slot(h, nq, np, k, s, &slot)) != VLR_OK) return st;
-  pdl_for_search(h->nslots == 1);
+  // PDL only for eager launches without pipelining: captured into a CUDA graph, the programmatic edges
+  // measured slower (B = 256 graph replay p50 1.85 -> 2.17 ms)
+  pdl_for_search(h->nslots == 1 && !capturing(s));
   if (slot_out) *slot_out = slot;
   Workspace& w = h->wsl[slot];
   st = take_status(w, " (detected in a previous search on this handle)");
