@@ -108,7 +108,7 @@ __global__ void k_negative(const int64_t* ids, long long n, int32_t* flag) {
 
 static void free_ws(Workspace& w) {
   void* ps[] = {w.qnorm, w.qsq, w.qf16, w.qf16t, w.qinv, w.dt, w.gmin, w.cand, w.ncand, w.exact, w.x1, w.x1_all, w.x2, w.x2_all, w.dump, w.bound, w.probes, w.term1, w.plocal, w.item_off, w.item_local, w.qtot, w.qdone, w.lut,
-                w.pdist, w.pid, w.send, w.recv, w.d_q, w.d_ids, w.d_dist, w.d_miss, w.d_probes, w.status};
+                w.pdist, w.pid, w.send, w.recv, w.d_q, w.d_q2, w.d_ids, w.d_dist, w.d_miss, w.d_probes, w.status};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (w.h_status) cudaFreeHost(w.h_status);
@@ -179,6 +179,7 @@ static vlr_status ensure_ws(vlr_index* h, int slot, int nq, int np, int k) {
     VLR_CUDA_TRY(dalloc(reinterpret_cast<Packed**>(&w.recv), nqs * ck * ix.world));
   }
   VLR_CUDA_TRY(dalloc(&w.d_q, nqs * ix.d));
+  VLR_CUDA_TRY(dalloc(&w.d_q2, nqs * ix.d));
   VLR_CUDA_TRY(dalloc(&w.d_ids, nqs * ck));
   VLR_CUDA_TRY(dalloc(&w.d_dist, nqs * ck));
   VLR_CUDA_TRY(dalloc(&w.d_miss, nqs * cnp));
@@ -689,8 +690,10 @@ void vlr_index_free(vlr_index* h) {
   for (auto& row : h->ev)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
+  if (h->h2d_stream) cudaStreamDestroy(h->h2d_stream);
   for (auto& r : h->res) {
-    cudaEvent_t evs[] = {r.done, r.lut_fork, r.lut_join, r.rel_fork, r.rel_join};
+    cudaEvent_t evs[] = {r.done, r.lut_fork, r.lut_join, r.rel_fork, r.rel_join, r.q_ready[0], r.q_ready[1],
+                         r.q_free[0], r.q_free[1]};
     for (cudaEvent_t e : evs)
       if (e) cudaEventDestroy(e);
     if (r.lut_stream) cudaStreamDestroy(r.lut_stream);
@@ -1250,10 +1253,33 @@ static vlr_status search_host_impl(vlr_index* h, const float* hQ, int32_t nq, in
     if (st != VLR_OK) return st;
     if ((st = acquire_slot(h, nq, np, k, s, &slot)) != VLR_OK) return st;
     Workspace& w = h->wsl[slot];
-    VLR_CUDA_TRY(cudaMemcpyAsync(w.d_q, hQ, sizeof(float) * nq * h->ix.d, cudaMemcpyHostToDevice, s));
-    st = search_locked(h, w.d_q, nq, nprobe, k, w.d_ids, w.d_dist, w.d_miss, h_probes ? w.d_probes : nullptr, stream,
+    // the queries go through one of two staging buffers, copied on the handle's H2D stream: the copy of
+    // batch i+1 overlaps batch i's kernels (stream capture: the copy stays on `stream`)
+    auto& r = h->res[slot];
+    const int qi = r.qbuf;
+    r.qbuf ^= 1;
+    float* dq = qi ? w.d_q2 : w.d_q;
+    const size_t qbytes = sizeof(float) * nq * h->ix.d;
+    if (capturing(s)) {
+      VLR_CUDA_TRY(cudaMemcpyAsync(dq, hQ, qbytes, cudaMemcpyHostToDevice, s));
+    } else {
+      if (!h->h2d_stream) VLR_CUDA_TRY(cudaStreamCreateWithFlags(&h->h2d_stream, cudaStreamNonBlocking));
+      if (!r.q_ready[qi]) {
+        VLR_CUDA_TRY(cudaEventCreateWithFlags(&r.q_ready[qi], cudaEventDisableTiming));
+        VLR_CUDA_TRY(cudaEventCreateWithFlags(&r.q_free[qi], cudaEventDisableTiming));
+      }
+      if (r.q_used[qi]) VLR_CUDA_TRY(cudaStreamWaitEvent(h->h2d_stream, r.q_free[qi], 0));  // its last reader
+      VLR_CUDA_TRY(cudaMemcpyAsync(dq, hQ, qbytes, cudaMemcpyHostToDevice, h->h2d_stream));
+      VLR_CUDA_TRY(cudaEventRecord(r.q_ready[qi], h->h2d_stream));
+      VLR_CUDA_TRY(cudaStreamWaitEvent(s, r.q_ready[qi], 0));
+    }
+    st = search_locked(h, dq, nq, nprobe, k, w.d_ids, w.d_dist, w.d_miss, h_probes ? w.d_probes : nullptr, stream,
                        nullptr, slot);
     if (st != VLR_OK) return st;
+    if (!capturing(s)) {  // every kernel of the search has read dq once `stream` passes this point
+      VLR_CUDA_TRY(cudaEventRecord(r.q_free[qi], s));
+      r.q_used[qi] = true;
+    }
     VLR_CUDA_TRY(cudaMemcpyAsync(h_ids, w.d_ids, sizeof(int64_t) * nq * k, cudaMemcpyDeviceToHost, s));
     VLR_CUDA_TRY(cudaMemcpyAsync(h_dist, w.d_dist, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, s));
     VLR_CUDA_TRY(cudaMemcpyAsync(h_miss, w.d_miss, (size_t)nq * np, cudaMemcpyDeviceToHost, s));

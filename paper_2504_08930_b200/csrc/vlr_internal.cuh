@@ -143,7 +143,8 @@ struct Workspace {
   void* send = nullptr;        // [nq][k] 16-byte entries (world > 1)
   void* recv = nullptr;        // [world][nq][k]
   float* h_stage = nullptr;    // pinned staging for vlr_search_host (queries)
-  float* d_q = nullptr;        // device queries for vlr_search_host
+  float* d_q = nullptr;        // device queries for vlr_search_host (two buffers: d_q, d_q2, used in turn so the
+  float* d_q2 = nullptr;       // H2D copy of the next batch overlaps this one's kernels)
   int64_t* d_ids = nullptr;
   float* d_dist = nullptr;
   uint8_t* d_miss = nullptr;
@@ -172,7 +173,13 @@ struct vlr_index {
     // NEXT-4 merger stream + fork/join events (created on first use)
     cudaStream_t rel_stream = nullptr;
     cudaEvent_t rel_fork = nullptr, rel_join = nullptr;
+    // vlr_search_host*: query staging buffer i (d_q / d_q2) filled on h2d_stream (q_ready[i]) and free again
+    // once its search has read it (q_free[i], recorded on the search stream)
+    cudaEvent_t q_ready[2] = {}, q_free[2] = {};
+    bool q_used[2] = {};
+    int qbuf = 0;
   } res[kSlots];
+  cudaStream_t h2d_stream = nullptr;  // host -> device query copies of vlr_search_host* (overlap the search)
   int nslots = 1;
   int scan_reserve = 0;      // SMs the scan's persistent grid leaves free (vlr_set_pipeline)
   uint64_t seq = 0;          // searches started (slot = seq % nslots)
