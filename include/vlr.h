@@ -248,13 +248,16 @@ int32_t vlr_merge_ready(int32_t n_shards, const uint32_t* const* ready, uint32_t
 int32_t vlr_wait_ready(const uint32_t* ready, int32_t nq, uint32_t epoch, int64_t* out_t_ns, int64_t timeout_us);
 
 /* vlr_search_host without the final synchronisation (serving pipelines):
- * the H2D copy, the search and the D2H copies are enqueued on `stream` and
- * the call returns; h_* outputs are valid once `stream` has completed this
- * work (cudaStreamSynchronize / an event). Back-to-back calls on one stream
- * are safe (stream order protects the handle's staging buffers) and keep the
- * GPU busy across batches. h_queries and the outputs must be pinned host
+ * the search and the D2H copies are enqueued on `stream`, the H2D copy of the
+ * queries on a handle-owned copy stream into one of two staging buffers used
+ * in turn (events order it after the previous reader of that buffer and
+ * before the search), and the call returns; h_* outputs are valid once
+ * `stream` has completed this work (cudaStreamSynchronize / an event).
+ * Back-to-back calls keep the GPU busy across batches: batch i+1's H2D copy
+ * overlaps batch i's kernels. h_queries and the outputs must be pinned host
  * memory (pageable memory makes the copies synchronous) and stay valid until
- * completion. A non-finite query is reported by the next call on the handle. */
+ * completion. Under stream capture the copy stays on `stream`. A non-finite
+ * query is reported by the next call on the handle. */
 vlr_status vlr_search_host_async(vlr_index* idx, const float* h_queries, int32_t nq, int32_t nprobe, int32_t k,
                                  int64_t* h_ids, float* h_dist, uint8_t* h_miss, int32_t* h_probes, void* stream);
 
